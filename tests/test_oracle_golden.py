@@ -1,0 +1,108 @@
+"""Pin the CPU oracle against the reference's own outputs (golden fixtures made
+by tests/golden/make_golden.py from the real `cutbench`), and pin its U3
+extension with the dense-unitary oracle and the cut identities."""
+import numpy as np
+import pytest
+
+from conftest import golden_cases, golden_tables
+from oracle import cutbench_oracle as orc
+
+
+@pytest.mark.parametrize("key", golden_cases())
+def test_oracle_uncut_matches_reference(golden, key):
+    q = int(golden[f"{key}/q"])
+    k, a, b = golden[f"{key}/kinds"], golden[f"{key}/qa"], golden[f"{key}/qb"]
+    amps = orc.simulate(q, k, a, b)
+    assert np.abs(amps - golden[f"{key}/uncut"]).max() < 1e-12
+
+
+@pytest.mark.parametrize("key", golden_cases())
+def test_oracle_cut_tables_and_merge_match_reference(golden, key):
+    q, n = int(golden[f"{key}/q"]), int(golden[f"{key}/n"])
+    k, a, b = golden[f"{key}/kinds"], golden[f"{key}/qa"], golden[f"{key}/qb"]
+    prm = np.zeros((len(k), 3))
+    sizes = [q // n] * n
+    bgs, counts, c_i = orc.plan(k, a, b, sizes)
+    assert [bg[0] for bg in bgs] == list(golden[f"{key}/positions"])
+    assert c_i == list(golden[f"{key}/c_i"])
+    c_total = sum(counts)
+    tab = orc.merge_table(n, bgs, c_total)
+    assert np.array_equal(tab, golden[f"{key}/merge_table"])
+    co = orc.coefficients(c_total)
+    assert np.abs(co - golden[f"{key}/coeffs"]).max() == 0.0
+    states = []
+    for seg in range(n):
+        vs = orc.segment_variants(k, a, b, prm, sizes, bgs, seg)
+        assert np.array_equal(vs[0][0], golden[f"{key}/seg{seg}/kinds"])
+        assert np.array_equal(vs[0][1], golden[f"{key}/seg{seg}/qa"])
+        assert np.array_equal(vs[0][2], golden[f"{key}/seg{seg}/qb"])
+        st = np.stack([orc.simulate(sizes[seg], *v) for v in vs])
+        assert np.abs(st - golden[f"{key}/seg{seg}/states"]).max() < 1e-12
+        states.append(list(st))
+    merged = orc.merge(states, tab, co)
+    assert np.abs(merged - golden[f"{key}/merged"]).max() < 1e-12
+
+
+@pytest.mark.parametrize("key", golden_tables())
+def test_oracle_generator_and_tables_match_reference_full_size(golden, key):
+    q, d, n, c, seed = (int(v) for v in golden[f"{key}/spec"])
+    k, a, b, _ = orc.brickwall(q, d, n, c, seed, shadow=True)
+    assert len(k) == int(golden[f"{key}/G"])
+    bgs, counts, c_i = orc.plan(k, a, b, [q // n] * n)
+    assert [bg[0] for bg in bgs] == list(golden[f"{key}/positions"])
+    assert c_i == list(golden[f"{key}/c_i"])
+    assert np.array_equal(orc.merge_table(n, bgs, sum(counts)), golden[f"{key}/merge_table"])
+
+
+def test_brickwall_sizes_match_survey():
+    # G per config. q=34 is 502 by layer counting
+    # (340 U3 + 5x16 + 5x16 brick CZ + 2 cuts); the survey's 504 is an
+    # arithmetic slip, and the reference agrees with 502 (golden table_cfg5_q34).
+    expect = {(12, 4, 2, 1): 69, (20, 10, 2, 2): 292, (30, 10, 2, 2): 442, (30, 10, 3, 4): 439,
+              (32, 10, 4, 4): 464, (34, 10, 2, 2): 502}
+    for (q, d, n, c), g in expect.items():
+        k, _, _, _ = orc.brickwall(q, d, n, c, 0)
+        assert len(k) == g
+
+
+@pytest.mark.parametrize("q,d,n,c,seed", [(4, 3, 2, 1, 0), (6, 4, 2, 2, 1), (6, 3, 3, 2, 2),
+                                          (8, 3, 4, 3, 3), (9, 4, 3, 3, 4)])
+def test_u3_engine_matches_dense_unitary(q, d, n, c, seed):
+    k, a, b, p = orc.brickwall(q, d, n, c, seed)
+    assert np.abs(orc.simulate(q, k, a, b, p) - orc.dense_simulate(q, k, a, b, p)).max() < 1e-12
+
+
+@pytest.mark.parametrize("q,d,n,c,seed", [(8, 4, 2, 2, 0), (9, 4, 3, 4, 1), (8, 5, 4, 4, 2),
+                                          (10, 6, 2, 3, 3)])
+def test_u3_cut_equals_uncut(q, d, n, c, seed):
+    k, a, b, p = orc.brickwall(q, d, n, c, seed)
+    merged, _, _, _ = orc.cut_pipeline(q, k, a, b, p, n)
+    uncut = orc.simulate(q, k, a, b, p)
+    assert np.abs(merged - uncut).max() < 1e-10
+    fid = abs(np.vdot(uncut, merged)) ** 2 / (np.vdot(merged, merged).real * np.vdot(uncut, uncut).real)
+    assert 1 - fid < 1e-12
+
+
+def test_u3_linearity_identity():
+    # reference tests/test_engine.py:144-168, with a U3 dressing
+    k, a, b, p = orc.brickwall(4, 3, 2, 1, 7)
+    pos = int(np.flatnonzero((k == orc.CZ) & (a == 1) & (b == 2))[0])
+
+    def variant(term):
+        mid = orc.SDG if term else orc.S
+        kk = np.concatenate([k[:pos], [mid, mid], k[pos + 1:]]).astype(np.uint8)
+        aa = np.concatenate([a[:pos], [1, 2], a[pos + 1:]])
+        bb = np.concatenate([b[:pos], [-1, -1], b[pos + 1:]])
+        pp = np.concatenate([p[:pos], np.zeros((2, 3)), p[pos + 1:]])
+        return orc.simulate(4, kk, aa, bb, pp)
+
+    combo = orc.COEFF_TERM0 * variant(0) + orc.COEFF_TERM1 * variant(1)
+    assert np.abs(combo - orc.simulate(4, k, a, b, p)).max() < 1e-12
+
+
+def test_sample_amplitudes_matches_merge():
+    k, a, b, p = orc.brickwall(9, 4, 3, 4, 5)
+    merged, states, tab, co = orc.cut_pipeline(9, k, a, b, p, 3)
+    idx = np.array([0, 1, 77, 300, 511])
+    got = orc.sample_amplitudes(states, tab, co, [3, 3, 3], idx)
+    assert np.abs(got - merged[idx]).max() < 1e-14
