@@ -1,0 +1,376 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 circuit-cutting path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one pass of the cut pipeline over the BASELINE cfg4a circuit
+(q=30, d=10, n=2 (15|15), c_total=2, seeded U3 brick-wall, complex128):
+host preprocess (plan_cut + decompose) -> batched subcircuit simulation
+(sm_100a sweep kernel) -> chain merge writing the 16 GiB state once
+(sm_100a merge kernel). ``value`` = 2^30 amplitudes x steps / device time
+with the output resident in HBM; ``e2e`` = the same through the public API
+delivering the state into pinned HOST memory (device->host copy in the
+timed region). Multi-GPU (torchrun): the output is sharded by its high
+amplitude bits, subcircuit variants are split across ranks and all-gathered
+over NCCL; value is whole-job (strong scaling, total work fixed).
+
+``--impl reference`` times the reference algorithm's CPU implementation
+(the C restatement of the reference numba kernels in oracle/, all host
+threads) on a bounded sample of the same workload, extrapolated to the
+same metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "End-to-end cut-sim amplitudes/s at q=30; merge % of HBM roofline; stage ms"
+UNIT = "amplitudes/s"
+WORKLOAD = "cfg4a"
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def load_traffic():
+    """dram bytes read+write per merge launch from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return d.get("merge_kernel", {}).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._thr = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                vals = [v.strip() for v in out.stdout.strip().split(",")]
+                if len(vals) == 6:
+                    self.samples.append(vals)
+            except (OSError, subprocess.SubprocessError):
+                return
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._thr = threading.Thread(target=self._run, daemon=True)
+        self._thr.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._thr:
+            self._thr.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm: the C restatement of the reference kernels (oracle/)
+# ---------------------------------------------------------------------------
+def cpu_sample(spec, threads: int, row_fraction: float):
+    """Time preprocess + all subcircuit simulations + a row sample of the merge
+    with the reference's algorithm on the host; extrapolate to the full step."""
+    from oracle import cutbench_oracle as orc
+    from oracle import oracle_c
+    from paper_2603_01443_b200.generators import build_brickwall
+
+    circ = build_brickwall(spec)
+    k, qa, qb, p = circ.kinds, circ.qa, circ.qb, circ.params
+    q, n = spec.q, spec.n
+    sizes = [q // n] * n
+    t0 = time.perf_counter()
+    bgs, counts, _ = orc.plan(k, qa, qb, sizes)
+    variants = [orc.segment_variants(k, qa, qb, p, sizes, bgs, s) for s in range(n)]
+    tab = orc.merge_table(n, bgs, sum(counts))
+    co = orc.coefficients(sum(counts))
+    t_pre = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    states = [[oracle_c.simulate(sizes[s], *v, threads=threads) for v in variants[s]] for s in range(n)]
+    t_sub = time.perf_counter() - t0
+    rows_total = 1 << sizes[1]
+    rows = max(1, int(rows_total * row_fraction))
+    _acc, t_m = oracle_c.merge_rows(states, tab, co, (0, rows), threads=threads)
+    t_merge = t_m * rows_total / rows
+    return {"t_pre": t_pre, "t_sub": t_sub, "t_merge": t_merge,
+            "value": (1 << q) / (t_pre + t_sub + t_merge), "rows": rows, "rows_total": rows_total}
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    from oracle import oracle_c
+    from paper_2603_01443_b200.generators import BASELINE_CONFIGS
+
+    spec = BASELINE_CONFIGS[WORKLOAD]
+    threads = oracle_c.max_threads() if args.threads <= 0 else args.threads
+    frac = args.row_fraction
+    for _ in range(args.warmup):
+        cpu_sample(spec, threads, frac / 8)
+    vals, steps = [], []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        r = cpu_sample(spec, threads, frac)
+        vals.append(r["value"])
+        steps.append(r)
+    wall = time.perf_counter() - t0
+    value = float(np.mean(vals))
+    ms = 1e3 * (1 << spec.q) / value
+    sample = (f"per step: full preprocess + all {sum(1 << c for c in [spec.c_total] * spec.n)} "
+              f"subcircuit states + merge rows [0, {steps[0]['rows']}) of {steps[0]['rows_total']} "
+              f"(fraction {frac}); merge time extrapolated by row count")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{WORKLOAD}: q=30 d=10 n=2 c_total=2 seed=0 (U3 brick-wall)",
+                   "q": spec.q, "n": spec.n, "c_total": spec.c_total, "d": spec.d},
+        "stage_ms": {"pre": 1e3 * np.mean([s["t_pre"] for s in steps]),
+                     "sub": 1e3 * np.mean([s["t_sub"] for s in steps]),
+                     "merge": 1e3 * np.mean([s["t_merge"] for s in steps])},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": sample, "wall_s": wall},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+
+    import paper_2603_01443_b200 as cb
+    from paper_2603_01443_b200 import _native
+    from paper_2603_01443_b200.generators import BASELINE_CONFIGS
+    from paper_2603_01443_b200.merging import merge_chain_device
+    from paper_2603_01443_b200.parallel import run_cut_sharded
+    from paper_2603_01443_b200.pipeline import preprocess, run_cut_to_host, simulate_segments
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    spec = BASELINE_CONFIGS[WORKLOAD]
+    circ = cb.build_brickwall(spec)
+    q = spec.q
+    total = 1 << q
+    stream = torch.cuda.current_stream()
+    peak, peak_src = load_peaks()
+
+    # shard geometry and preallocated output / workspace
+    prep0 = preprocess(circ, spec.n)
+    ws_bytes, bond, qlow = prep0.chain.plan()
+    from paper_2603_01443_b200.parallel import shard_range
+
+    begin, end = shard_range(q, world, rank, qlow)
+    out = torch.empty(end - begin, dtype=torch.complex128, device="cuda")
+    workspace = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device="cuda")
+
+    merge_ms = []
+
+    def step(record=False):
+        if world == 1:
+            prep = preprocess(circ, spec.n)
+            batches = simulate_segments(prep)
+            if record:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            merge_chain_device(prep.chain, batches, out=out, out_range=(begin, end), workspace=workspace)
+            if record:
+                e1.record(stream)
+                merge_ms.append((e0, e1))
+        else:
+            if record:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+            res, _ = run_cut_sharded(circ, spec.n, rank=rank, world=world, out=out)
+            del res
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = _native.launch_count()
+    ev_start = torch.cuda.Event(enable_timing=True)
+    ev_end = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        ev_start.record(stream)
+        for _ in range(args.steps):
+            step(record=True)
+        ev_end.record(stream)
+        torch.cuda.synchronize()
+    launches = _native.launch_count() - launches0
+    elapsed = ev_start.elapsed_time(ev_end) / 1e3
+    if dist:
+        tt = torch.tensor([elapsed], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        elapsed = float(tt.item())
+        dist.barrier()
+    torch.cuda.synchronize()
+    value = total * args.steps / elapsed
+    ms_per_step = 1e3 * elapsed / args.steps
+
+    # stage breakdown (separate, synchronised pass; not the headline)
+    times = cb.StageTimes()
+    stage = {"pre": None, "sub": None, "merge": None}
+    if world == 1:
+        acc = {"pre": [], "sub": [], "merge": []}
+        for _ in range(3):
+            cb.run_cut(circ, spec.n, out=out, workspace=workspace, timers=times)
+            acc["pre"].append(times.pre)
+            acc["sub"].append(times.sub)
+            acc["merge"].append(times.merge)
+        stage = {k: 1e3 * float(np.median(v)) for k, v in acc.items()}
+
+    # roofline of the dominant kernel (merge) from the timed region
+    roofline = None
+    if merge_ms:
+        dur = float(np.mean([a.elapsed_time(b) for a, b in merge_ms])) / 1e3
+        fams = prep0.subs.segments
+        in_bytes = sum(f.num_variants * (1 << f.num_qubits) * 16 for f in fams)
+        alg = 16 * (end - begin) + in_bytes
+        achieved = alg / dur / 1e9
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "traffic": load_traffic(), "kernel": "merge_kernel",
+                    "algorithmic_bytes_per_launch": alg, "avg_launch_ms": dur * 1e3,
+                    "peak_source": peak_src}
+
+    # e2e through the public API into pinned host memory (N=1)
+    e2e = None
+    if world == 1 and not args.no_e2e:
+        host = torch.empty(total, dtype=torch.complex128, pin_memory=True)
+        bufs = [torch.empty(total // 8, dtype=torch.complex128, device="cuda") for _ in range(2)]
+        del out
+        torch.cuda.empty_cache()
+        for _ in range(max(1, min(args.warmup, 2))):
+            run_cut_to_host(circ, spec.n, host, buffers=bufs, workspace=workspace)
+        torch.cuda.synchronize()
+        e_steps = max(1, min(args.steps, args.e2e_steps))
+        t0 = time.perf_counter()
+        for _ in range(e_steps):
+            run_cut_to_host(circ, spec.n, host, buffers=bufs, workspace=workspace)
+        torch.cuda.synchronize()
+        t_e2e = (time.perf_counter() - t0) / e_steps
+        g_bytes = int(sum(a.nbytes for a in (circ.kinds, circ.qa, circ.qb, circ.params)))
+        e2e = {"value": total / t_e2e, "unit": UNIT, "h2d_bytes_per_step": g_bytes,
+               "d2h_bytes_per_step": total * 16, "ms_per_step": t_e2e * 1e3, "steps": e_steps,
+               "path": "run_cut_to_host: chunked merge overlapped with D2H into pinned host memory"}
+        del host, bufs
+
+    # CPU baseline (the oracle port, 1 thread = the reference's protocol), rank 0, N=1
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        try:
+            r = cpu_sample(spec, 1, args.row_fraction)
+            cpu = {"value": r["value"], "unit": UNIT, "cores": 1, "kind": "port",
+                   "sample": (f"oracle C port (reference loop structure), 1 thread: full preprocess, all "
+                              f"subcircuit states, merge rows [0,{r['rows']}) of {r['rows_total']} "
+                              f"extrapolated"),
+                   "stage_ms": {"pre": r["t_pre"] * 1e3, "sub": r["t_sub"] * 1e3,
+                                "merge": r["t_merge"] * 1e3},
+                   "host_cpus": os.cpu_count()}
+        except Exception as exc:  # noqa: BLE001  (baseline is informational)
+            cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "port", "sample": f"failed: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded U3 brick-wall, SURVEY.md §8(d)); output resident in HBM",
+            "config": {"workload": f"{WORKLOAD}: q=30 d=10 n=2 (15|15) c_total=2 seed=0 complex128",
+                       "q": q, "n": spec.n, "c_total": spec.c_total, "d": spec.d, "bond": bond,
+                       "parallelism": f"output-shard{world}",
+                       "l2": "no flush: each step writes the 16 GiB output (>> 126 MB L2)"},
+            "stage_ms": stage,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clocks.summary(),
+            "gpu_launches": launches,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--threads", type=int, default=0, help="reference arm host threads (0 = all)")
+    ap.add_argument("--row-fraction", type=float, default=1 / 16,
+                    help="merge rows sampled by the CPU legs")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,134 @@
+/*
+ * libcutsim — C-ABI of the B200 (sm_100a) circuit-cutting state-vector path.
+ *
+ * The reference (`cutbench`, /root/reference/pkg/src/cutbench) is a Python +
+ * numba package with no FFI; its internal compute seam is two numba kernels
+ * called from Python:
+ *     engine._run_gates(amps, kinds, qa, qb, start, stop)   engine.py:122-139
+ *     merging._axpy_outer(acc, hi, lo, alpha)               merging.py:86-94
+ * driven by simulate() (engine.py:158-168) and merge() (merging.py:156-186).
+ * Each entry point below states which of those it replaces. A ctypes binding
+ * is the reference-side integration.
+ *
+ * Conventions (identical to the reference): amplitudes are complex128
+ * interleaved (re, im) little-endian (or complex64 with dtype CS_C64), index
+ * order with qubit j = bit j (qubit 0 = LSB); segment 0 on the low bits; gate
+ * kind codes H=0 X=1 T=2 S=3 Sdg=4 CX=5 CZ=6 (+ U3=7 with params[g] = theta,
+ * phi, lambda); CX/CZ first qubit = control.
+ *
+ * Memory: every state pointer is caller-owned device memory (e.g. a torch
+ * tensor's data_ptr()); the library never allocates or frees caller memory.
+ * All calls are asynchronous on `stream` (a cudaStream_t, NULL = legacy
+ * default stream) except the reductions, which synchronise the stream to
+ * return a host value. Every function returns CS_OK (0) or an error code;
+ * cs_last_error() gives the thread's last message.
+ */
+#ifndef CUTSIM_H
+#define CUTSIM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CS_OK 0
+#define CS_ERR_INVALID 1
+#define CS_ERR_CAPACITY 2
+#define CS_ERR_CUDA 3
+#define CS_ERR_NCCL 4
+#define CS_ERR_INTERNAL 5
+#define CS_ERR_NODEVICE 6
+
+#define CS_C128 0
+#define CS_C64 1
+
+int cs_version(void);
+const char* cs_last_error(void);
+int cs_device_count(int32_t* count);
+
+/* Options: "tile_bits" (multi-sweep tile, default 12 for c128),
+ * "low_bits" (contiguous low qubits per tile, default 5), "fuse" (1q gate
+ * fusion, default 1), "threads" (0 = auto), "merge_streaming" (evict-first
+ * output stores, default 1), "merge_iters" (0 = auto). */
+int cs_set_option(const char* key, int64_t value);
+int64_t cs_get_option(const char* key);
+
+/* Kernels launched by this library since load (bench `gpu_launches`). */
+int64_t cs_launch_count(void);
+
+/* Set every state of a batch to the basis state |index>.
+ * Replaces StateVec.zero_state (engine.py:47-51). */
+int cs_init_basis(void* states, int32_t nq, int64_t n_states, int64_t index, int32_t dtype,
+                  void* stream);
+
+/* Apply a gate table to a batch of n_states states of nq qubits (state v at
+ * states + v * state_stride amplitudes). slots may be NULL; slots[g] >= 0
+ * marks an S gate that is Sdg for states whose variant id
+ * (variant_base + v) has bit slots[g] set — one template serves all cut
+ * variants of a segment. init_zero != 0 starts from |0..0> without reading.
+ * Replaces _run_gates (engine.py:122-139) over the per-variant simulate()
+ * loop (harness.py:136-139) and the variant tables of cutting.py:237-247. */
+int cs_sim_batch(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int64_t* qb,
+                 const double* params, const int32_t* slots, int64_t n_gates, void* states,
+                 int64_t n_states, int64_t state_stride, uint64_t variant_base, int32_t init_zero,
+                 int32_t dtype, void* stream);
+
+/* Host-only: the sweep schedule cs_sim_batch would run, as JSON. tile_bits
+ * <= 0 uses the current option. Writes up to buflen bytes, *needed = full
+ * length + 1. */
+int cs_sweep_plan_json(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int64_t* qb,
+                       const double* params, const int32_t* slots, int64_t n_gates,
+                       int32_t tile_bits, int32_t dtype, char* buf, int64_t buflen, int64_t* needed);
+
+/* out[s][h - row_begin][l] (+)= sum_{t<K} coef[s,t] * hi[hidx[s,t]][h] * lo[lidx[s,t]][l]
+ * for h in [row_begin, row_end), l in [0, lo_len); hi states have hi_len
+ * amplitudes, lo states lo_len (a power of two); slot s of out starts at
+ * out + s * out_slot_stride amplitudes. hidx/lidx/coef are HOST arrays of
+ * S*K (coef: 2*S*K doubles, (re, im)). accumulate != 0 adds into out.
+ * Replaces _axpy_outer/_outer_into/_iadd and the per-term loop
+ * (merging.py:86-186) with one write-once pass per output. */
+int cs_merge_terms(int32_t S, int32_t K, const int32_t* hidx, const int32_t* lidx,
+                   const double* coef, const void* hi, int64_t hi_len, const void* lo,
+                   int64_t lo_len, int64_t row_begin, int64_t row_end, void* out,
+                   int64_t out_slot_stride, int32_t accumulate, int32_t dtype, void* stream);
+
+/* Plan of the chain-contracted merge (host only). Segments 0..n-1 (segment 0
+ * on the low bits) with seg_nq[j] qubits hold 2^{seg_ncuts[j]} states each;
+ * seg_cut_ids lists, per segment and concatenated, the global cut ids
+ * adjacent to it in circuit order (local variant bit k = k-th id); cut c sits
+ * on boundary cut_boundary[c]; term_coef = {t0.re, t0.im, t1.re, t1.im}.
+ * This is exactly the reference merge table r_i(m) (cutting.py:251-263) and
+ * alpha_m (cutting.py:266-272). force_bond < 0 picks the bond by cost. */
+int cs_merge_chain_plan(int32_t n, const int32_t* seg_nq, const int32_t* seg_ncuts,
+                        const int32_t* seg_cut_ids, int32_t c_total, const int32_t* cut_boundary,
+                        const double* term_coef, int32_t force_bond, int32_t dtype,
+                        int64_t* workspace_bytes, int32_t* bond, int32_t* q_low);
+
+/* Full-state reconstruction sum_m alpha_m psi_{n-1}^{r(m)} (x) ... (x) psi_0^{r(m)}
+ * for output amplitudes [out_begin, out_end) (multiples of 2^{q_low}; out
+ * points at amplitude out_begin) — the shard a GPU owns. seg_states[j] is a
+ * device pointer to segment j's 2^{seg_ncuts[j]} x 2^{seg_nq[j]} states.
+ * Replaces merge() (merging.py:156-186). */
+int cs_merge_chain(int32_t n, const int32_t* seg_nq, const void* const* seg_states,
+                   const int32_t* seg_ncuts, const int32_t* seg_cut_ids, int32_t c_total,
+                   const int32_t* cut_boundary, const double* term_coef, int32_t force_bond,
+                   int64_t out_begin, int64_t out_end, void* out, void* workspace,
+                   int64_t workspace_bytes, int32_t dtype, void* stream);
+
+/* Device reductions (synchronise `stream`). */
+int cs_maxabsdiff(const void* a, const void* b, int64_t n, int32_t dtype, double* result,
+                  void* stream);
+int cs_maxabs(const void* a, int64_t n, int32_t dtype, double* result, void* stream);
+/* result[0..1] = sum conj(a) * b */
+int cs_inner(const void* a, const void* b, int64_t n, int32_t dtype, double* result, void* stream);
+
+/* out[i] = state[idx[i]] (idx, out: device pointers). */
+int cs_gather(const void* state, const int64_t* idx, int64_t m, void* out, int32_t dtype,
+              void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CUTSIM_H */

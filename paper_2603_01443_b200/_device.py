@@ -1,0 +1,90 @@
+"""Device plumbing: PyTorch is used only to own CUDA memory and streams.
+
+Tensors are allocated through torch's caching allocator and handed to the
+C-ABI as raw pointers with the current torch stream. Nothing here computes.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native
+from .errors import CapacityError, NativeUnavailableError, ValidationError
+
+_torch = None
+
+
+def torch():
+    global _torch
+    if _torch is None:
+        import torch as _t  # noqa: PLC0415  (heavy import, done lazily)
+
+        _torch = _t
+    return _torch
+
+
+def require_cuda():
+    t = torch()
+    if not t.cuda.is_available():
+        raise NativeUnavailableError(
+            "no CUDA device is visible; the cut pipeline runs only on the sm_100a kernels "
+            "(there is no CPU fallback)"
+        )
+    _native.load()
+    return t
+
+
+def code_of(dtype) -> int:
+    dt = np.dtype(dtype)
+    if dt == np.complex128:
+        return _native.CS_C128
+    if dt == np.complex64:
+        return _native.CS_C64
+    raise ValidationError(f"dtype must be complex128 or complex64, got {dt}")
+
+
+def torch_dtype(dtype):
+    t = torch()
+    return t.complex128 if np.dtype(dtype) == np.complex128 else t.complex64
+
+
+def stream_ptr(stream=None) -> int:
+    t = torch()
+    s = stream if stream is not None else t.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def empty(n_states: int, nq: int, dtype=np.complex128, check_memory=True):
+    """Uninitialised device batch [n_states, 2^nq]."""
+    t = require_cuda()
+    nbytes = n_states * (1 << nq) * np.dtype(dtype).itemsize
+    if check_memory:
+        free, _total = t.cuda.mem_get_info()
+        cached = t.cuda.memory_reserved() - t.cuda.memory_allocated()
+        if nbytes > free + cached:
+            raise CapacityError(
+                f"{n_states} state(s) of {nq} qubits need {nbytes / 2**30:.2f} GiB; "
+                f"{(free + cached) / 2**30:.2f} GiB free on the device"
+            )
+    return t.empty((n_states, 1 << nq), dtype=torch_dtype(dtype), device="cuda")
+
+
+def empty_shape(shape, dtype=np.complex128):
+    """Uninitialised device tensor of an arbitrary shape (no capacity check)."""
+    t = require_cuda()
+    return t.empty(shape, dtype=torch_dtype(dtype), device="cuda")
+
+
+def from_host(arr: np.ndarray, dtype=None):
+    t = require_cuda()
+    a = np.ascontiguousarray(arr, dtype=dtype or arr.dtype)
+    return t.from_numpy(a).to("cuda", non_blocking=False)
+
+
+def to_host(tensor, out: np.ndarray | None = None) -> np.ndarray:
+    t = torch()
+    tc = tensor.detach()
+    if out is not None:
+        host = t.from_numpy(out.reshape(-1))
+        host.copy_(tc.reshape(-1))
+        return out
+    return tc.cpu().numpy()

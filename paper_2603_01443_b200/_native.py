@@ -1,0 +1,165 @@
+"""ctypes binding of libcutsim.so (the sm_100a C-ABI declared in include/cutsim.h).
+
+There is no CPU fallback: if the library or a CUDA device is missing, every
+compute entry point raises ``NativeUnavailableError``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+from .errors import (
+    CapacityError,
+    CutbenchError,
+    DeviceError,
+    NativeUnavailableError,
+    ValidationError,
+)
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libcutsim.so")
+
+CS_C128 = 0
+CS_C64 = 1
+
+_ERRORS = {
+    1: ValidationError,
+    2: CapacityError,
+    3: DeviceError,
+    4: DeviceError,
+    5: CutbenchError,
+    6: NativeUnavailableError,
+}
+
+_i32, _i64, _u64, _vp, _dp = (ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_void_p,
+                              ctypes.POINTER(ctypes.c_double))
+
+# name -> (restype, argtypes); exactly the functions include/cutsim.h declares
+SIGNATURES = {
+    "cs_version": (ctypes.c_int, []),
+    "cs_last_error": (ctypes.c_char_p, []),
+    "cs_device_count": (ctypes.c_int, [_vp]),
+    "cs_set_option": (ctypes.c_int, [ctypes.c_char_p, _i64]),
+    "cs_get_option": (_i64, [ctypes.c_char_p]),
+    "cs_launch_count": (_i64, []),
+    "cs_init_basis": (ctypes.c_int, [_vp, _i32, _i64, _i64, _i32, _vp]),
+    "cs_sim_batch": (ctypes.c_int, [_i32, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _i64, _i64, _u64, _i32,
+                                    _i32, _vp]),
+    "cs_sweep_plan_json": (ctypes.c_int, [_i32, _vp, _vp, _vp, _vp, _vp, _i64, _i32, _i32, _vp, _i64,
+                                          _vp]),
+    "cs_merge_terms": (ctypes.c_int, [_i32, _i32, _vp, _vp, _vp, _vp, _i64, _vp, _i64, _i64, _i64,
+                                      _vp, _i64, _i32, _i32, _vp]),
+    "cs_merge_chain_plan": (ctypes.c_int, [_i32, _vp, _vp, _vp, _i32, _vp, _vp, _i32, _i32, _vp, _vp,
+                                           _vp]),
+    "cs_merge_chain": (ctypes.c_int, [_i32, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _i32, _i64, _i64, _vp,
+                                      _vp, _i64, _i32, _vp]),
+    "cs_maxabsdiff": (ctypes.c_int, [_vp, _vp, _i64, _i32, _vp, _vp]),
+    "cs_maxabs": (ctypes.c_int, [_vp, _i64, _i32, _vp, _vp]),
+    "cs_inner": (ctypes.c_int, [_vp, _vp, _i64, _i32, _vp, _vp]),
+    "cs_gather": (ctypes.c_int, [_vp, _vp, _i64, _vp, _i32, _vp]),
+}
+
+_lock = threading.Lock()
+_lib = None
+_load_error = None
+
+
+def load() -> ctypes.CDLL:
+    """Load (once) and type the library; raise NativeUnavailableError if absent."""
+    global _lib, _load_error
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise NativeUnavailableError(
+                f"{LIB_PATH} is not built; run __graft_entry__.build() (nvcc, sm_100a). "
+                "This package has no CPU fallback."
+            )
+        try:
+            lib = ctypes.CDLL(LIB_PATH)
+        except OSError as exc:
+            _load_error = exc
+            raise NativeUnavailableError(f"cannot load {LIB_PATH}: {exc}") from exc
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def last_error() -> str:
+    msg = load().cs_last_error()
+    return msg.decode() if msg else ""
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        exc = _ERRORS.get(int(rc), CutbenchError)
+        raise exc(f"{what}: {last_error()}")
+
+
+def ptr(arr) -> int:
+    """Address of a numpy array (must stay alive across the call) or None."""
+    if arr is None:
+        return None
+    return arr.ctypes.data
+
+
+def c_i32(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+def c_i64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.int64)
+
+
+def c_f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def set_option(key: str, value: int) -> None:
+    check(load().cs_set_option(key.encode(), int(value)), f"cs_set_option({key})")
+
+
+def get_option(key: str) -> int:
+    return int(load().cs_get_option(key.encode()))
+
+
+def launch_count() -> int:
+    return int(load().cs_launch_count())
+
+
+def sweep_plan_json(nq, table, slots=None, tile_bits=0, dtype=CS_C128) -> str:
+    """Host-only: the sweep schedule of a gate table (no GPU needed)."""
+    lib = load()
+    k = np.ascontiguousarray(table.kinds, dtype=np.uint8)
+    qa, qb, prm = c_i64(table.qa), c_i64(table.qb), c_f64(table.params)
+    sl = c_i32(slots) if slots is not None else None
+    need = np.zeros(1, dtype=np.int64)
+    check(lib.cs_sweep_plan_json(nq, ptr(k), ptr(qa), ptr(qb), ptr(prm), ptr(sl), len(k), tile_bits,
+                                 dtype, None, 0, ptr(need)), "cs_sweep_plan_json")
+    buf = ctypes.create_string_buffer(int(need[0]))
+    check(lib.cs_sweep_plan_json(nq, ptr(k), ptr(qa), ptr(qb), ptr(prm), ptr(sl), len(k), tile_bits,
+                                 dtype, buf, int(need[0]), ptr(need)), "cs_sweep_plan_json")
+    return buf.value.decode()
+
+
+def chain_plan(n, seg_nq, seg_ncuts, seg_cut_ids, c_total, cut_boundary, term_coef,
+               force_bond=-1, dtype=CS_C128):
+    """Host-only: (workspace_bytes, bond, q_low) of the chain-contracted merge."""
+    lib = load()
+    a_nq, a_nc, a_ids = c_i32(seg_nq), c_i32(seg_ncuts), c_i32(seg_cut_ids if len(seg_cut_ids) else [0])
+    a_b = c_i32(cut_boundary if len(cut_boundary) else [0])
+    a_t = c_f64(term_coef)
+    ws = np.zeros(1, np.int64)
+    bond = np.zeros(1, np.int32)
+    qlow = np.zeros(1, np.int32)
+    check(lib.cs_merge_chain_plan(n, ptr(a_nq), ptr(a_nc), ptr(a_ids), c_total, ptr(a_b), ptr(a_t),
+                                  force_bond, dtype, ptr(ws), ptr(bond), ptr(qlow)),
+          "cs_merge_chain_plan")
+    return int(ws[0]), int(bond[0]), int(qlow[0])

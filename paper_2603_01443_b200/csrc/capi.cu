@@ -1,0 +1,495 @@
+// extern "C" entry points of libcutsim (see include/cutsim.h for the contract
+// and the reference interfaces each one replaces).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/cutsim.h"
+#include "ops.hpp"
+#include "plan.hpp"
+
+namespace cutsim {
+size_t sweep_smem_bytes(int tile_bits, int low_bits, int dtype);
+cudaError_t launch_sweep(const SweepParams& p, uint32_t n_tiles, uint32_t n_states, int threads,
+                         cudaStream_t stream, int dtype);
+cudaError_t launch_merge(const MergeParams& p, int K, dim3 grid, int threads, size_t smem, bool wide,
+                         cudaStream_t stream, int dtype);
+int merge_cols_per_thread(int K);
+cudaError_t launch_init_basis(void* states, int64_t len, int64_t n_states, int64_t index, int dtype,
+                              cudaStream_t stream);
+cudaError_t launch_reduce(const void* a, const void* b, int64_t n, int mode, int dtype, double2* scratch,
+                          cudaStream_t stream);
+int reduce_scratch_elems();
+cudaError_t launch_gather(const void* state, const int64_t* idx, int64_t m, void* out, int dtype,
+                          cudaStream_t stream);
+}  // namespace cutsim
+
+using namespace cutsim;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<int64_t> g_launches{0};
+
+struct Options {
+  int64_t tile_bits_c128 = 12;
+  int64_t tile_bits_c64 = 13;
+  int64_t tile_bits = 0;  // 0 = per-dtype default
+  int64_t low_bits = 5;
+  int64_t fuse = 1;
+  int64_t threads = 0;
+  int64_t merge_streaming = 1;
+  int64_t merge_iters = 0;
+} g_opt;
+std::mutex g_opt_mu;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(CS_ERR_CUDA, std::string(where) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")");
+}
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+inline size_t elem_bytes(int dtype) { return dtype == CS_C128 ? 16 : 8; }
+
+bool valid_dtype(int dtype) { return dtype == CS_C128 || dtype == CS_C64; }
+
+int single_tile_max(int dtype) { return dtype == CS_C128 ? 13 : 14; }
+
+int multi_tile_bits(int dtype) {
+  if (g_opt.tile_bits > 0) return int(g_opt.tile_bits);
+  return int(dtype == CS_C128 ? g_opt.tile_bits_c128 : g_opt.tile_bits_c64);
+}
+
+struct ScratchCache {
+  std::mutex mu;
+  std::vector<double2*> per_device;
+} g_scratch;
+
+double2* reduce_scratch(int* err) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) {
+    *err = cuda_fail(e, "cudaGetDevice");
+    return nullptr;
+  }
+  std::lock_guard<std::mutex> lk(g_scratch.mu);
+  if (int(g_scratch.per_device.size()) <= dev) g_scratch.per_device.resize(size_t(dev) + 1, nullptr);
+  if (!g_scratch.per_device[size_t(dev)]) {
+    double2* p = nullptr;
+    e = cudaMalloc(&p, sizeof(double2) * size_t(reduce_scratch_elems()));
+    if (e != cudaSuccess) {
+      *err = cuda_fail(e, "cudaMalloc(reduce scratch)");
+      return nullptr;
+    }
+    g_scratch.per_device[size_t(dev)] = p;
+  }
+  return g_scratch.per_device[size_t(dev)];
+}
+
+std::vector<Sweep> build_schedule(int nq, const uint8_t* kinds, const int64_t* qa, const int64_t* qb,
+                                  const double* params, const int32_t* slots, int64_t n_gates, int tile_bits,
+                                  int dtype) {
+  std::vector<LOp> ops = lower_gates(nq, kinds, qa, qb, params, slots, n_gates);
+  if (g_opt.fuse) ops = fuse_ops(ops);
+  int T = nq <= single_tile_max(dtype) ? nq : (tile_bits > 0 ? tile_bits : multi_tile_bits(dtype));
+  T = std::min(T, nq);
+  return schedule_sweeps(ops, nq, T, int(g_opt.low_bits));
+}
+
+// Launch one merge_terms problem whose K is one instantiated width.
+int merge_launch_one(int S, int Kc, const int32_t* hidx, const int32_t* lidx, const double* coef,
+                     int64_t stride_terms, const void* hi, int64_t hi_len, const void* lo, int64_t lo_len,
+                     int64_t row_begin, int64_t row_end, void* out, int64_t out_slot_stride, int accumulate,
+                     int dtype, cudaStream_t stream) {
+  // stride_terms: distance between consecutive slots' term lists in hidx/lidx
+  const int threads = 256;
+  const int CC = merge_cols_per_thread(Kc);
+  const int64_t C = int64_t(threads) * CC;
+  const int64_t W = lo_len;
+  const bool wide = W >= C;
+  const int64_t cols = wide ? C : W;
+  const int64_t rows_per_iter = wide ? 1 : C / W;
+  const size_t eb = elem_bytes(dtype);
+  const int64_t nrows = row_end - row_begin;
+  int64_t iters = g_opt.merge_iters > 0 ? g_opt.merge_iters
+                                        : std::max<int64_t>(1, (256 * 1024) / int64_t(C * int64_t(eb)));
+  const int64_t smem_cap = 32 * 1024;
+  iters = std::min<int64_t>(iters, std::max<int64_t>(1, smem_cap / (rows_per_iter * Kc * int64_t(eb))));
+  iters = std::min<int64_t>(iters, (nrows + rows_per_iter - 1) / rows_per_iter);
+  iters = std::max<int64_t>(iters, 1);
+  const int64_t rows_cta = iters * rows_per_iter;
+  const size_t smem = size_t(rows_cta) * size_t(Kc) * eb;
+  int log_w = 0;
+  while ((int64_t(1) << log_w) < W) ++log_w;
+  int log_cols = 0;
+  while ((int64_t(1) << log_cols) < cols) ++log_cols;
+
+  const int slots_per_launch = std::max(1, kMaxMergeTerms / Kc);
+  static MergeParams p;  // large; filled per launch (launch copies it)
+  static std::mutex pm;
+  std::lock_guard<std::mutex> lk(pm);
+  for (int s0 = 0; s0 < S; s0 += slots_per_launch) {
+    const int sc = std::min(slots_per_launch, S - s0);
+    std::memset(&p, 0, offsetof(MergeParams, hidx));
+    p.hi = hi;
+    p.lo = lo;
+    p.out = static_cast<char*>(out) + size_t(s0) * size_t(out_slot_stride) * eb;
+    p.hi_len = hi_len;
+    p.lo_len = lo_len;
+    p.out_slot_stride = out_slot_stride;
+    p.log_w = log_w;
+    p.S = sc;
+    p.K = Kc;
+    p.accumulate = accumulate;
+    p.cols = int32_t(cols);
+    p.log_cols = log_cols;
+    p.rows_per_iter = int32_t(rows_per_iter);
+    p.iters = int32_t(iters);
+    p.streaming = int32_t(g_opt.merge_streaming);
+    for (int s = 0; s < sc; ++s)
+      for (int t = 0; t < Kc; ++t) {
+        const int64_t src = int64_t(s0 + s) * stride_terms + t;
+        p.hidx[s * Kc + t] = hidx[src];
+        p.lidx[s * Kc + t] = lidx[src];
+        p.coef[2 * (s * Kc + t)] = coef[2 * src];
+        p.coef[2 * (s * Kc + t) + 1] = coef[2 * src + 1];
+      }
+    // row chunks so that grid.y stays within limits
+    const int64_t max_rows_per_launch = rows_cta * 65535;
+    for (int64_t r0 = row_begin; r0 < row_end; r0 += max_rows_per_launch) {
+      const int64_t r1 = std::min(row_end, r0 + max_rows_per_launch);
+      p.row_begin = r0;
+      p.row_end = r1;
+      char* base_out = static_cast<char*>(out) + size_t(s0) * size_t(out_slot_stride) * eb;
+      p.out = base_out + size_t(r0 - row_begin) * size_t(W) * eb;
+      dim3 grid(unsigned(wide ? W / C : 1), unsigned((r1 - r0 + rows_cta - 1) / rows_cta), unsigned(sc));
+      cudaError_t e = launch_merge(p, Kc, grid, threads, smem, wide, stream, dtype);
+      g_launches.fetch_add(1);
+      if (e != cudaSuccess) return cuda_fail(e, "merge_kernel launch");
+    }
+  }
+  return CS_OK;
+}
+
+int merge_terms_impl(int S, int K, const int32_t* hidx, const int32_t* lidx, const double* coef,
+                     const void* hi, int64_t hi_len, const void* lo, int64_t lo_len, int64_t row_begin,
+                     int64_t row_end, void* out, int64_t out_slot_stride, int accumulate, int dtype,
+                     cudaStream_t stream) {
+  if (!valid_dtype(dtype)) return fail(CS_ERR_INVALID, "dtype must be CS_C128 or CS_C64");
+  if (S < 1 || K < 0) return fail(CS_ERR_INVALID, "merge needs S >= 1 and K >= 0");
+  if (lo_len < 1 || (lo_len & (lo_len - 1))) return fail(CS_ERR_INVALID, "lo_len must be a power of two");
+  if (hi_len < 1 || row_begin < 0 || row_end > hi_len || row_begin > row_end)
+    return fail(CS_ERR_INVALID, "row range outside [0, hi_len]");
+  if (S > 1 && out_slot_stride < (row_end - row_begin) * lo_len)
+    return fail(CS_ERR_INVALID, "out_slot_stride smaller than one slot");
+  if (!out || (K > 0 && (!hi || !lo))) return fail(CS_ERR_INVALID, "null device pointer");
+  if (row_end == row_begin) return CS_OK;
+  const size_t eb = elem_bytes(dtype);
+  if (K == 0) {
+    if (accumulate) return CS_OK;
+    for (int s = 0; s < S; ++s) {
+      cudaError_t e = cudaMemsetAsync(static_cast<char*>(out) + size_t(s) * size_t(out_slot_stride) * eb, 0,
+                                      size_t(row_end - row_begin) * size_t(lo_len) * eb, stream);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
+    }
+    return CS_OK;
+  }
+  // split K into instantiated chunk widths {16, 8, 4, 2, 1}
+  int t0 = 0;
+  int acc = accumulate;
+  while (t0 < K) {
+    int rem = K - t0;
+    int kc = rem >= 16 ? 16 : rem >= 8 ? 8 : rem >= 4 ? 4 : rem >= 2 ? 2 : 1;
+    int rc = merge_launch_one(S, kc, hidx + t0, lidx + t0, coef + 2 * t0, K, hi, hi_len, lo, lo_len, row_begin,
+                              row_end, out, out_slot_stride, acc, dtype, stream);
+    if (rc != CS_OK) return rc;
+    t0 += kc;
+    acc = 1;
+  }
+  return CS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int cs_version(void) { return 10000; }
+
+const char* cs_last_error(void) { return g_err.c_str(); }
+
+int cs_device_count(int32_t* count) {
+  int c = 0;
+  cudaError_t e = cudaGetDeviceCount(&c);
+  if (e != cudaSuccess) {
+    *count = 0;
+    return fail(CS_ERR_NODEVICE, std::string("no CUDA device: ") + cudaGetErrorString(e));
+  }
+  *count = c;
+  return CS_OK;
+}
+
+int cs_set_option(const char* key, int64_t value) {
+  std::lock_guard<std::mutex> lk(g_opt_mu);
+  const std::string k(key ? key : "");
+  if (k == "tile_bits") {
+    if (value != 0 && (value < 2 || value > 13)) return fail(CS_ERR_INVALID, "tile_bits must be 0 or in [2, 13]");
+    g_opt.tile_bits = value;
+  } else if (k == "low_bits") {
+    if (value < 1 || value > 12) return fail(CS_ERR_INVALID, "low_bits must be in [1, 12]");
+    g_opt.low_bits = value;
+  } else if (k == "fuse") {
+    g_opt.fuse = value ? 1 : 0;
+  } else if (k == "threads") {
+    if (value != 0 && (value < 32 || value > 1024 || (value & 31)))
+      return fail(CS_ERR_INVALID, "threads must be 0 or a multiple of 32 in [32, 1024]");
+    g_opt.threads = value;
+  } else if (k == "merge_streaming") {
+    g_opt.merge_streaming = value ? 1 : 0;
+  } else if (k == "merge_iters") {
+    if (value < 0 || value > 4096) return fail(CS_ERR_INVALID, "merge_iters out of range");
+    g_opt.merge_iters = value;
+  } else {
+    return fail(CS_ERR_INVALID, "unknown option '" + k + "'");
+  }
+  return CS_OK;
+}
+
+int64_t cs_get_option(const char* key) {
+  const std::string k(key ? key : "");
+  if (k == "tile_bits") return g_opt.tile_bits;
+  if (k == "low_bits") return g_opt.low_bits;
+  if (k == "fuse") return g_opt.fuse;
+  if (k == "threads") return g_opt.threads;
+  if (k == "merge_streaming") return g_opt.merge_streaming;
+  if (k == "merge_iters") return g_opt.merge_iters;
+  return -1;
+}
+
+int64_t cs_launch_count(void) { return g_launches.load(); }
+
+int cs_init_basis(void* states, int32_t nq, int64_t n_states, int64_t index, int32_t dtype, void* stream) {
+  if (!valid_dtype(dtype)) return fail(CS_ERR_INVALID, "dtype must be CS_C128 or CS_C64");
+  if (nq < 0 || nq > 62) return fail(CS_ERR_INVALID, "qubit count out of range");
+  if (!states || n_states < 1) return fail(CS_ERR_INVALID, "empty state batch");
+  if (index < 0 || index >= (int64_t(1) << nq)) return fail(CS_ERR_INVALID, "basis index out of range");
+  cudaError_t e = launch_init_basis(states, int64_t(1) << nq, n_states, index, dtype, as_stream(stream));
+  g_launches.fetch_add(1);
+  return e == cudaSuccess ? CS_OK : cuda_fail(e, "init_basis launch");
+}
+
+int cs_sim_batch(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int64_t* qb, const double* params,
+                 const int32_t* slots, int64_t n_gates, void* states, int64_t n_states, int64_t state_stride,
+                 uint64_t variant_base, int32_t init_zero, int32_t dtype, void* stream) {
+  if (!valid_dtype(dtype)) return fail(CS_ERR_INVALID, "dtype must be CS_C128 or CS_C64");
+  if (nq < 0 || nq > 62) return fail(CS_ERR_INVALID, "qubit count out of range");
+  if (!states || n_states < 1) return fail(CS_ERR_INVALID, "empty state batch");
+  if (state_stride < (int64_t(1) << nq)) return fail(CS_ERR_INVALID, "state_stride smaller than 2^nq");
+  if (n_gates < 0 || (n_gates > 0 && (!kinds || !qa || !qb))) return fail(CS_ERR_INVALID, "bad gate table");
+  cudaStream_t st = as_stream(stream);
+  if (nq == 0) {
+    if (!init_zero) return CS_OK;
+    return cs_init_basis(states, 0, n_states, 0, dtype, stream);
+  }
+  std::vector<Sweep> sweeps;
+  try {
+    sweeps = build_schedule(nq, kinds, qa, qb, params, slots, n_gates, 0, dtype);
+  } catch (const PlanError& pe) {
+    return fail(pe.code, pe.msg);
+  }
+  static SweepParams p;
+  static std::mutex pm;
+  std::lock_guard<std::mutex> lk(pm);
+  bool first = true;
+  for (const Sweep& sw : sweeps) {
+    const int T = sw.tile_bits;
+    if (sw.hq.size() > size_t(kMaxTileBits) || sw.oq.size() > 64)
+      return fail(CS_ERR_INTERNAL, "sweep geometry exceeds the kernel limits");
+    const uint32_t n_tiles = uint32_t(1) << (nq - T);
+    // chunk the entries without splitting a slotted pair
+    size_t i0 = 0;
+    do {
+      size_t i1 = i0;
+      while (i1 < sw.entries.size()) {
+        const size_t w = sw.entries[i1].slot >= 0 ? 2 : 1;
+        if (i1 + w - i0 > size_t(kMaxOpsPerLaunch)) break;
+        i1 += w;
+      }
+      std::memset(&p, 0, offsetof(SweepParams, ops));
+      p.nq = nq;
+      p.tile_bits = T;
+      p.low_bits = sw.low_bits;
+      p.n_high = int32_t(sw.hq.size());
+      p.n_out = int32_t(sw.oq.size());
+      for (size_t j = 0; j < sw.hq.size() && j < size_t(kMaxTileBits); ++j) p.hq[j] = int8_t(sw.hq[j]);
+      for (size_t j = 0; j < sw.oq.size() && j < 64; ++j) p.oq[j] = int8_t(sw.oq[j]);
+      p.n_ops = int32_t(i1 - i0);
+      if (i1 > i0) std::memcpy(p.ops, sw.entries.data() + i0, sizeof(SweepOp) * (i1 - i0));
+      p.init_basis = (first && init_zero) ? 1 : 0;
+      p.store = 1;
+      p.stride = state_stride;
+      int threads = int(g_opt.threads);
+      if (threads == 0) {
+        const int64_t ctas = int64_t(n_tiles) * n_states;
+        threads = ctas < 2 * 148 ? 1024 : 256;
+      }
+      const int max_useful = std::max(32, 1 << std::max(0, T - 1));
+      threads = std::min(threads, (max_useful + 31) / 32 * 32);
+      for (int64_t v0 = 0; v0 < n_states; v0 += 65535) {
+        const int64_t vc = std::min<int64_t>(65535, n_states - v0);
+        p.states = static_cast<char*>(states) + size_t(v0) * size_t(state_stride) * elem_bytes(dtype);
+        p.variant_base = variant_base + uint64_t(v0);
+        cudaError_t e = launch_sweep(p, n_tiles, uint32_t(vc), threads, st, dtype);
+        g_launches.fetch_add(1);
+        if (e != cudaSuccess) return cuda_fail(e, "sweep_kernel launch");
+      }
+      first = false;
+      i0 = i1;
+    } while (i0 < sw.entries.size());
+  }
+  return CS_OK;
+}
+
+int cs_sweep_plan_json(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int64_t* qb,
+                       const double* params, const int32_t* slots, int64_t n_gates, int32_t tile_bits,
+                       int32_t dtype, char* buf, int64_t buflen, int64_t* needed) {
+  if (!valid_dtype(dtype)) return fail(CS_ERR_INVALID, "dtype must be CS_C128 or CS_C64");
+  if (nq < 1 || nq > 62) return fail(CS_ERR_INVALID, "qubit count out of range");
+  std::string js;
+  try {
+    js = sweeps_to_json(build_schedule(nq, kinds, qa, qb, params, slots, n_gates, tile_bits, dtype), nq);
+  } catch (const PlanError& pe) {
+    return fail(pe.code, pe.msg);
+  }
+  if (needed) *needed = int64_t(js.size()) + 1;
+  if (buf && buflen > 0) {
+    const size_t n = std::min(size_t(buflen - 1), js.size());
+    std::memcpy(buf, js.data(), n);
+    buf[n] = 0;
+  }
+  return CS_OK;
+}
+
+int cs_merge_terms(int32_t S, int32_t K, const int32_t* hidx, const int32_t* lidx, const double* coef,
+                   const void* hi, int64_t hi_len, const void* lo, int64_t lo_len, int64_t row_begin,
+                   int64_t row_end, void* out, int64_t out_slot_stride, int32_t accumulate, int32_t dtype,
+                   void* stream) {
+  return merge_terms_impl(S, K, hidx, lidx, coef, hi, hi_len, lo, lo_len, row_begin, row_end, out,
+                          out_slot_stride, accumulate, dtype, as_stream(stream));
+}
+
+int cs_merge_chain_plan(int32_t n, const int32_t* seg_nq, const int32_t* seg_ncuts, const int32_t* seg_cut_ids,
+                        int32_t c_total, const int32_t* cut_boundary, const double* term_coef, int32_t force_bond,
+                        int32_t dtype, int64_t* workspace_bytes, int32_t* bond, int32_t* q_low) {
+  if (!valid_dtype(dtype)) return fail(CS_ERR_INVALID, "dtype must be CS_C128 or CS_C64");
+  ChainPlan plan;
+  PlanError err{0, ""};
+  if (!plan_chain(n, seg_nq, seg_ncuts, seg_cut_ids, c_total, cut_boundary, term_coef, force_bond, &plan, &err))
+    return fail(err.code, err.msg);
+  int64_t bytes = 0;
+  for (int64_t a : plan.buf_amps) bytes += (a * int64_t(elem_bytes(dtype)) + 255) / 256 * 256;
+  if (workspace_bytes) *workspace_bytes = bytes;
+  if (bond) *bond = plan.bond;
+  if (q_low) *q_low = plan.q_low;
+  return CS_OK;
+}
+
+int cs_merge_chain(int32_t n, const int32_t* seg_nq, const void* const* seg_states, const int32_t* seg_ncuts,
+                   const int32_t* seg_cut_ids, int32_t c_total, const int32_t* cut_boundary, const double* term_coef,
+                   int32_t force_bond, int64_t out_begin, int64_t out_end, void* out, void* workspace,
+                   int64_t workspace_bytes, int32_t dtype, void* stream) {
+  if (!valid_dtype(dtype)) return fail(CS_ERR_INVALID, "dtype must be CS_C128 or CS_C64");
+  ChainPlan plan;
+  PlanError err{0, ""};
+  if (!plan_chain(n, seg_nq, seg_ncuts, seg_cut_ids, c_total, cut_boundary, term_coef, force_bond, &plan, &err))
+    return fail(err.code, err.msg);
+  const size_t eb = elem_bytes(dtype);
+  std::vector<const void*> bufs(size_t(n) + plan.buf_amps.size(), nullptr);
+  for (int j = 0; j < n; ++j) {
+    if (!seg_states[j]) return fail(CS_ERR_INVALID, "null segment state pointer");
+    bufs[size_t(j)] = seg_states[j];
+  }
+  int64_t off = 0;
+  for (size_t b = 0; b < plan.buf_amps.size(); ++b) {
+    const int64_t bytes = (plan.buf_amps[b] * int64_t(eb) + 255) / 256 * 256;
+    if (off + bytes > workspace_bytes || !workspace)
+      return fail(CS_ERR_INVALID, "merge workspace too small (query cs_merge_chain_plan)");
+    bufs[size_t(n) + b] = static_cast<char*>(workspace) + off;
+    off += bytes;
+  }
+  const int64_t total = int64_t(1) << (plan.q_low + 0);
+  (void)total;
+  const int64_t unit = int64_t(1) << plan.q_low;
+  if (out_begin < 0 || out_end < out_begin || (out_begin % unit) || (out_end % unit))
+    return fail(CS_ERR_INVALID, "output range must be aligned to 2^q_low = " + std::to_string(unit) + " amplitudes");
+  cudaStream_t st = as_stream(stream);
+  for (const MergeStep& s : plan.steps) {
+    const void* hi = bufs[size_t(s.hi_buf)];
+    const void* lo = bufs[size_t(s.lo_buf)];
+    int rc;
+    if (s.final_step) {
+      const int64_t r0 = out_begin / unit, r1 = out_end / unit;
+      if (r1 > s.hi_len) return fail(CS_ERR_INVALID, "output range beyond the state");
+      rc = merge_terms_impl(1, s.K, s.hidx.data(), s.lidx.data(), s.coef.data(), hi, s.hi_len, lo, s.lo_len, r0,
+                            r1, out, (r1 - r0) * s.lo_len, 0, dtype, st);
+    } else {
+      void* dst = const_cast<void*>(bufs[size_t(s.out_buf)]);
+      rc = merge_terms_impl(s.S, s.K, s.hidx.data(), s.lidx.data(), s.coef.data(), hi, s.hi_len, lo, s.lo_len, 0,
+                            s.hi_len, dst, s.hi_len * s.lo_len, 0, dtype, st);
+    }
+    if (rc != CS_OK) return rc;
+  }
+  return CS_OK;
+}
+
+static int reduce_common(const void* a, const void* b, int64_t n, int mode, int32_t dtype, double* result,
+                         void* stream) {
+  if (!valid_dtype(dtype)) return fail(CS_ERR_INVALID, "dtype must be CS_C128 or CS_C64");
+  if (!a || (mode != 2 && !b) || n < 0 || !result) return fail(CS_ERR_INVALID, "bad reduction arguments");
+  int err = CS_OK;
+  double2* scratch = reduce_scratch(&err);
+  if (!scratch) return err;
+  cudaStream_t st = as_stream(stream);
+  cudaError_t e = launch_reduce(a, b ? b : a, n, mode, dtype, scratch, st);
+  g_launches.fetch_add(2);
+  if (e != cudaSuccess) return cuda_fail(e, "reduce launch");
+  double2 host;
+  e = cudaMemcpyAsync(&host, scratch + reduce_scratch_elems() - 1, sizeof(double2), cudaMemcpyDeviceToHost, st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync(reduce)");
+  e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize(reduce)");
+  result[0] = host.x;
+  if (mode == 1) result[1] = host.y;
+  return CS_OK;
+}
+
+int cs_maxabsdiff(const void* a, const void* b, int64_t n, int32_t dtype, double* result, void* stream) {
+  return reduce_common(a, b, n, 0, dtype, result, stream);
+}
+
+int cs_maxabs(const void* a, int64_t n, int32_t dtype, double* result, void* stream) {
+  return reduce_common(a, nullptr, n, 2, dtype, result, stream);
+}
+
+int cs_inner(const void* a, const void* b, int64_t n, int32_t dtype, double* result, void* stream) {
+  return reduce_common(a, b, n, 1, dtype, result, stream);
+}
+
+int cs_gather(const void* state, const int64_t* idx, int64_t m, void* out, int32_t dtype, void* stream) {
+  if (!valid_dtype(dtype)) return fail(CS_ERR_INVALID, "dtype must be CS_C128 or CS_C64");
+  if (m == 0) return CS_OK;
+  if (!state || !idx || !out || m < 0) return fail(CS_ERR_INVALID, "bad gather arguments");
+  cudaError_t e = launch_gather(state, idx, m, out, dtype, as_stream(stream));
+  g_launches.fetch_add(1);
+  return e == cudaSuccess ? CS_OK : cuda_fail(e, "gather launch");
+}
+
+}  // extern "C"

@@ -1,0 +1,471 @@
+// sm_100a kernels of libcutsim: the gate-sweep kernel (subcircuit batches and
+// the uncut simulator), the merge-terms kernel (full-state reconstruction, the
+// HBM-write-bound hot op), basis init and deterministic device reductions.
+//
+// Reference seams replaced (paths under /root/reference/pkg/src/cutbench):
+//   sweep_kernel  <- engine.py:62-139  (_k_h/_k_x/_k_phase/_k_cx/_k_cz, _run_gates)
+//   merge_kernel  <- merging.py:86-110 (_axpy_outer/_outer_into/_iadd) and the
+//                    per-term loop merging.py:161-186, as one write-once pass
+//   init_basis    <- engine.py:47-51   (StateVec.zero_state)
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <type_traits>
+
+#include "ops.hpp"
+
+namespace cutsim {
+
+template <typename R>
+using vec2_t = typename std::conditional<std::is_same<R, double>::value, double2, float2>::type;
+
+template <typename R>
+__device__ __forceinline__ vec2_t<R> cmul(vec2_t<R> a, R br, R bi) {
+  vec2_t<R> r;
+  r.x = a.x * br - a.y * bi;
+  r.y = a.x * bi + a.y * br;
+  return r;
+}
+
+// acc += a * b (complex), four fused multiply-adds
+template <typename R>
+__device__ __forceinline__ void cfma(vec2_t<R>& acc, vec2_t<R> a, vec2_t<R> b) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(-a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(a.y, b.x, acc.y);
+}
+
+// ---------------------------------------------------------------------------
+// Gate sweep: one CTA owns one tile of 2^T amplitudes of one state (local
+// bits [0,L) = qubits [0,L), bits [L,T) = qubits hq[], the tile id scattered
+// over the remaining qubits oq[]). The tile is staged in shared memory, every
+// op of the launch is applied there, and the tile is written back once.
+// ---------------------------------------------------------------------------
+template <typename R>
+__global__ void __launch_bounds__(1024) sweep_kernel(const __grid_constant__ SweepParams p) {
+  using V = vec2_t<R>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  V* s = reinterpret_cast<V*>(smem_raw);
+  const int T = p.tile_bits;
+  const int L = p.low_bits;
+  const uint32_t n = 1u << T;
+  const uint32_t nchunks = 1u << (T - L);
+  const uint32_t lowmask = (1u << L) - 1u;
+  int64_t* chunkoff = reinterpret_cast<int64_t*>(smem_raw + sizeof(V) * size_t(n));
+  const uint32_t tid = threadIdx.x;
+  const uint32_t bd = blockDim.x;
+
+  uint64_t base = 0;
+  {
+    const uint64_t tile = blockIdx.x;
+    for (int j = 0; j < p.n_out; ++j)
+      if ((tile >> j) & 1ull) base |= 1ull << p.oq[j];
+  }
+  const uint64_t variant = p.variant_base + blockIdx.y;
+  V* st = reinterpret_cast<V*>(p.states) + int64_t(blockIdx.y) * p.stride;
+
+  for (uint32_t c = tid; c < nchunks; c += bd) {
+    int64_t off = 0;
+    for (int j = 0; j < p.n_high; ++j)
+      if ((c >> j) & 1u) off |= int64_t(1) << p.hq[j];
+    chunkoff[c] = off;
+  }
+  __syncthreads();
+
+  if (p.init_basis) {
+    for (uint32_t e = tid; e < n; e += bd) {
+      V z;
+      z.x = (base == 0 && e == 0) ? R(1) : R(0);
+      z.y = R(0);
+      s[e] = z;
+    }
+  } else {
+    for (uint32_t e = tid; e < n; e += bd)
+      s[e] = st[int64_t(base) + chunkoff[e >> L] + (e & lowmask)];
+  }
+  __syncthreads();
+
+  const uint32_t half = n >> 1;
+  int i = 0;
+  while (i < p.n_ops) {
+    const SweepOp& op = p.ops[i];
+    if (op.type == OP_PHASE) {
+      int j = i;
+      while (j < p.n_ops && p.ops[j].type == OP_PHASE) j += (p.ops[j].slot >= 0) ? 2 : 1;
+      for (uint32_t e = tid; e < n; e += bd) {
+        R pr = R(1), pi = R(0);
+        bool hit = false;
+        for (int k = i; k < j;) {
+          const SweepOp& o = p.ops[k];
+          const SweepOp* src = &o;
+          int step = 1;
+          if (o.slot >= 0) {
+            src = &p.ops[k + int((variant >> o.slot) & 1ull)];
+            step = 2;
+          }
+          if ((e & o.lmask) == o.lmask && (base & o.omask) == o.omask) {
+            const R qr = R(src->m[0]), qi = R(src->m[1]);
+            const R nr = pr * qr - pi * qi;
+            pi = pr * qi + pi * qr;
+            pr = nr;
+            hit = true;
+          }
+          k += step;
+        }
+        if (hit) s[e] = cmul<R>(s[e], pr, pi);
+      }
+      __syncthreads();
+      i = j;
+      continue;
+    }
+    // OP_DENSE
+    const SweepOp* src = &op;
+    int step = 1;
+    if (op.slot >= 0) {
+      src = &p.ops[i + int((variant >> op.slot) & 1ull)];
+      step = 2;
+    }
+    if ((base & op.omask) == op.omask) {
+      const R m00r = R(src->m[0]), m00i = R(src->m[1]), m01r = R(src->m[2]), m01i = R(src->m[3]);
+      const R m10r = R(src->m[4]), m10i = R(src->m[5]), m11r = R(src->m[6]), m11i = R(src->m[7]);
+      const int t = op.target;
+      const uint32_t lm = op.lmask;
+      const uint32_t below = (1u << t) - 1u;
+      for (uint32_t k = tid; k < half; k += bd) {
+        const uint32_t e0 = ((k & ~below) << 1) | (k & below);
+        if ((e0 & lm) != lm) continue;
+        const uint32_t e1 = e0 | (1u << t);
+        const V a = s[e0];
+        const V b = s[e1];
+        V u, w;
+        u.x = m00r * a.x - m00i * a.y + m01r * b.x - m01i * b.y;
+        u.y = m00r * a.y + m00i * a.x + m01r * b.y + m01i * b.x;
+        w.x = m10r * a.x - m10i * a.y + m11r * b.x - m11i * b.y;
+        w.y = m10r * a.y + m10i * a.x + m11r * b.y + m11i * b.x;
+        s[e0] = u;
+        s[e1] = w;
+      }
+    }
+    __syncthreads();
+    i += step;
+  }
+
+  for (uint32_t e = tid; e < n; e += bd)
+    st[int64_t(base) + chunkoff[e >> L] + (e & lowmask)] = s[e];
+}
+
+// ---------------------------------------------------------------------------
+// merge_terms: out[s][h][l] (+)= sum_t coef[s,t] * hi[hidx[s,t]][h] * lo[lidx[s,t]][l]
+// A CTA owns `iters` row groups x C columns; each thread keeps its CC columns
+// of every lo term in registers (read once), the CTA's rows of coef*hi are
+// staged in shared memory, and every output amplitude is written exactly once
+// with a warp-contiguous 16-byte streaming store — no zero-fill, no
+// read-modify-write (the reference zero-fills and then does one RMW pass per
+// term, merging.py:117,94).
+// ---------------------------------------------------------------------------
+template <typename R, int K, int CC, bool WIDE>
+__global__ void __launch_bounds__(256) merge_kernel(const __grid_constant__ MergeParams p) {
+  using V = vec2_t<R>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  V* bs = reinterpret_cast<V*>(smem_raw);
+  const int sl = blockIdx.z;
+  const int bd = blockDim.x;
+  const int tid = threadIdx.x;
+  const int64_t W = p.lo_len;
+  const int64_t rows_cta = int64_t(p.iters) * p.rows_per_iter;
+  const int64_t row0 = p.row_begin + int64_t(blockIdx.y) * rows_cta;
+  const int32_t* hidx = p.hidx + sl * K;
+  const int32_t* lidx = p.lidx + sl * K;
+  const double* coef = p.coef + 2 * sl * K;
+  const V* hi = reinterpret_cast<const V*>(p.hi);
+  const V* lo = reinterpret_cast<const V*>(p.lo);
+
+  // stage coef * hi for this CTA's rows
+  for (int idx = tid; idx < rows_cta * K; idx += bd) {
+    const int r = idx / K;
+    const int t = idx - r * K;
+    const int64_t h = row0 + r;
+    V b;
+    b.x = R(0);
+    b.y = R(0);
+    if (h < p.row_end) {
+      const V hv = __ldg(hi + int64_t(hidx[t]) * p.hi_len + h);
+      b = cmul<R>(hv, R(coef[2 * t]), R(coef[2 * t + 1]));
+    }
+    bs[idx] = b;
+  }
+
+  V a[K][CC];
+  int64_t col[CC];
+  int rsub[CC];
+#pragma unroll
+  for (int j = 0; j < CC; ++j) {
+    const int flat = tid + j * bd;
+    if (WIDE) {
+      col[j] = int64_t(blockIdx.x) * (int64_t(bd) * CC) + flat;
+      rsub[j] = 0;
+    } else {
+      col[j] = flat & (p.cols - 1);
+      rsub[j] = flat >> p.log_cols;
+    }
+#pragma unroll
+    for (int t = 0; t < K; ++t) a[t][j] = __ldg(lo + int64_t(lidx[t]) * W + col[j]);
+  }
+  __syncthreads();
+
+  V* out = reinterpret_cast<V*>(p.out) + int64_t(sl) * p.out_slot_stride;
+  for (int i = 0; i < p.iters; ++i) {
+    if (WIDE) {
+      const int r = i;
+      const int64_t h = row0 + r;
+      if (h >= p.row_end) break;
+      V b[K];
+#pragma unroll
+      for (int t = 0; t < K; ++t) b[t] = bs[r * K + t];
+      const int64_t obase = (h - p.row_begin) * W;
+#pragma unroll
+      for (int j = 0; j < CC; ++j) {
+        V acc;
+        acc.x = R(0);
+        acc.y = R(0);
+#pragma unroll
+        for (int t = 0; t < K; ++t) cfma<R>(acc, b[t], a[t][j]);
+        V* dst = out + obase + col[j];
+        if (p.accumulate) {
+          const V prev = *dst;
+          acc.x += prev.x;
+          acc.y += prev.y;
+        }
+        if (p.streaming) __stcs(dst, acc);
+        else *dst = acc;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < CC; ++j) {
+        const int r = i * p.rows_per_iter + rsub[j];
+        const int64_t h = row0 + r;
+        if (h >= p.row_end) continue;
+        V acc;
+        acc.x = R(0);
+        acc.y = R(0);
+#pragma unroll
+        for (int t = 0; t < K; ++t) cfma<R>(acc, bs[r * K + t], a[t][j]);
+        V* dst = out + (h - p.row_begin) * W + col[j];
+        if (p.accumulate) {
+          const V prev = *dst;
+          acc.x += prev.x;
+          acc.y += prev.y;
+        }
+        if (p.streaming) __stcs(dst, acc);
+        else *dst = acc;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// small utilities
+// ---------------------------------------------------------------------------
+template <typename R>
+__global__ void init_basis_kernel(vec2_t<R>* states, int64_t len, int64_t n_states, int64_t index) {
+  const int64_t total = len * n_states;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    vec2_t<R> z;
+    z.x = ((i % len) == index) ? R(1) : R(0);
+    z.y = R(0);
+    states[i] = z;
+  }
+}
+
+// Deterministic two-pass reductions: per-block partials, then one block.
+// mode 0: max |a - b|; mode 1: sum conj(a) * b (re, im); mode 2: max |a|
+template <typename R>
+__global__ void reduce_pass1(const vec2_t<R>* a, const vec2_t<R>* b, int64_t n, int mode,
+                             double2* partial) {
+  __shared__ double sx[256], sy[256];
+  double x = 0.0, y = 0.0;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const double ar = a[i].x, ai = a[i].y;
+    if (mode == 0) {
+      const double dr = ar - double(b[i].x), di = ai - double(b[i].y);
+      x = fmax(x, sqrt(dr * dr + di * di));
+    } else if (mode == 1) {
+      const double br = b[i].x, bi = b[i].y;
+      x += ar * br + ai * bi;
+      y += ar * bi - ai * br;
+    } else {
+      x = fmax(x, sqrt(ar * ar + ai * ai));
+    }
+  }
+  sx[threadIdx.x] = x;
+  sy[threadIdx.x] = y;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      if (mode == 1) {
+        sx[threadIdx.x] += sx[threadIdx.x + w];
+        sy[threadIdx.x] += sy[threadIdx.x + w];
+      } else {
+        sx[threadIdx.x] = fmax(sx[threadIdx.x], sx[threadIdx.x + w]);
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = make_double2(sx[0], sy[0]);
+}
+
+__global__ void reduce_pass2(const double2* partial, int n, int mode, double2* result) {
+  __shared__ double sx[256], sy[256];
+  double x = 0.0, y = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    if (mode == 1) {
+      x += partial[i].x;
+      y += partial[i].y;
+    } else {
+      x = fmax(x, partial[i].x);
+    }
+  }
+  sx[threadIdx.x] = x;
+  sy[threadIdx.x] = y;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      if (mode == 1) {
+        sx[threadIdx.x] += sx[threadIdx.x + w];
+        sy[threadIdx.x] += sy[threadIdx.x + w];
+      } else {
+        sx[threadIdx.x] = fmax(sx[threadIdx.x], sx[threadIdx.x + w]);
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *result = make_double2(sx[0], sy[0]);
+}
+
+template <typename R>
+__global__ void gather_kernel(const vec2_t<R>* state, const int64_t* idx, int64_t m, vec2_t<R>* out) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < m;
+       i += int64_t(gridDim.x) * blockDim.x)
+    out[i] = state[idx[i]];
+}
+
+// ---------------------------------------------------------------------------
+// launchers (host)
+// ---------------------------------------------------------------------------
+size_t sweep_smem_bytes(int tile_bits, int low_bits, int dtype) {
+  const size_t elem = dtype == 0 ? sizeof(double2) : sizeof(float2);
+  return (size_t(1) << tile_bits) * elem + (size_t(1) << (tile_bits - low_bits)) * sizeof(int64_t);
+}
+
+template <typename R>
+static cudaError_t launch_sweep_t(const SweepParams& p, uint32_t n_tiles, uint32_t n_states,
+                                  int threads, cudaStream_t stream) {
+  const size_t smem = sweep_smem_bytes(p.tile_bits, p.low_bits, std::is_same<R, double>::value ? 0 : 1);
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(sweep_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(smem));
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  dim3 grid(n_tiles, n_states, 1);
+  sweep_kernel<R><<<grid, threads, smem, stream>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sweep(const SweepParams& p, uint32_t n_tiles, uint32_t n_states, int threads,
+                         cudaStream_t stream, int dtype) {
+  return dtype == 0 ? launch_sweep_t<double>(p, n_tiles, n_states, threads, stream)
+                    : launch_sweep_t<float>(p, n_tiles, n_states, threads, stream);
+}
+
+template <typename R, int K, int CC>
+static cudaError_t launch_merge_kc(const MergeParams& p, dim3 grid, int threads, size_t smem,
+                                   bool wide, cudaStream_t stream) {
+  if (wide) {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(merge_kernel<R, K, CC, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(smem));
+    merge_kernel<R, K, CC, true><<<grid, threads, smem, stream>>>(p);
+  } else {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(merge_kernel<R, K, CC, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(smem));
+    merge_kernel<R, K, CC, false><<<grid, threads, smem, stream>>>(p);
+  }
+  return cudaGetLastError();
+}
+
+int merge_cols_per_thread(int K) { return K <= 4 ? 4 : (K == 8 ? 2 : 1); }
+
+template <typename R>
+static cudaError_t launch_merge_t(const MergeParams& p, int K, dim3 grid, int threads, size_t smem,
+                                  bool wide, cudaStream_t stream) {
+  switch (K) {
+    case 1: return launch_merge_kc<R, 1, 4>(p, grid, threads, smem, wide, stream);
+    case 2: return launch_merge_kc<R, 2, 4>(p, grid, threads, smem, wide, stream);
+    case 4: return launch_merge_kc<R, 4, 4>(p, grid, threads, smem, wide, stream);
+    case 8: return launch_merge_kc<R, 8, 2>(p, grid, threads, smem, wide, stream);
+    case 16: return launch_merge_kc<R, 16, 1>(p, grid, threads, smem, wide, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_merge(const MergeParams& p, int K, dim3 grid, int threads, size_t smem, bool wide,
+                         cudaStream_t stream, int dtype) {
+  return dtype == 0 ? launch_merge_t<double>(p, K, grid, threads, smem, wide, stream)
+                    : launch_merge_t<float>(p, K, grid, threads, smem, wide, stream);
+}
+
+cudaError_t launch_init_basis(void* states, int64_t len, int64_t n_states, int64_t index, int dtype,
+                              cudaStream_t stream) {
+  const int64_t total = len * n_states;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  if (blocks < 1) blocks = 1;
+  if (dtype == 0)
+    init_basis_kernel<double><<<unsigned(blocks), 256, 0, stream>>>(static_cast<double2*>(states), len,
+                                                                    n_states, index);
+  else
+    init_basis_kernel<float><<<unsigned(blocks), 256, 0, stream>>>(static_cast<float2*>(states), len,
+                                                                   n_states, index);
+  return cudaGetLastError();
+}
+
+constexpr int kReduceBlocks = 148 * 4;
+
+cudaError_t launch_reduce(const void* a, const void* b, int64_t n, int mode, int dtype, double2* scratch,
+                          cudaStream_t stream) {
+  // scratch: kReduceBlocks partials followed by one result
+  if (dtype == 0)
+    reduce_pass1<double><<<kReduceBlocks, 256, 0, stream>>>(static_cast<const double2*>(a),
+                                                            static_cast<const double2*>(b), n, mode,
+                                                            scratch);
+  else
+    reduce_pass1<float><<<kReduceBlocks, 256, 0, stream>>>(static_cast<const float2*>(a),
+                                                           static_cast<const float2*>(b), n, mode,
+                                                           scratch);
+  reduce_pass2<<<1, 256, 0, stream>>>(scratch, kReduceBlocks, mode, scratch + kReduceBlocks);
+  return cudaGetLastError();
+}
+
+int reduce_scratch_elems() { return kReduceBlocks + 1; }
+
+cudaError_t launch_gather(const void* state, const int64_t* idx, int64_t m, void* out, int dtype,
+                          cudaStream_t stream) {
+  int64_t blocks = (m + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks < 1) blocks = 1;
+  if (dtype == 0)
+    gather_kernel<double><<<unsigned(blocks), 256, 0, stream>>>(static_cast<const double2*>(state), idx, m,
+                                                                static_cast<double2*>(out));
+  else
+    gather_kernel<float><<<unsigned(blocks), 256, 0, stream>>>(static_cast<const float2*>(state), idx, m,
+                                                               static_cast<float2*>(out));
+  return cudaGetLastError();
+}
+
+}  // namespace cutsim

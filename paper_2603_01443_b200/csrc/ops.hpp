@@ -1,0 +1,81 @@
+// Shared host/device structures of libcutsim (sm_100a).
+//
+// The gate program the kernels execute is a list of two op types, lowered on
+// the host from the reference's packed gate table (kinds/qa/qb, reference
+// engine.py:122-139) plus this build's U3 params and cut-slot column:
+//   OP_DENSE : 2x2 complex matrix on one target qubit, optionally controlled
+//              (H, X, U3, CX, and fused runs of 1q gates);
+//   OP_PHASE : multiply every amplitude whose index has all `mask` bits set by
+//              a complex phase (T, S, Sdg, CZ and fused diagonal runs).
+// An op with slot >= 0 is a *cut slot*: the variant id's bit `slot` selects
+// between this entry (bit 0 -> S side) and the next entry (bit 1 -> Sdg side),
+// which is how one template table serves every subcircuit variant
+// (reference cutting.py:237-247 patches a kind byte; we select a matrix).
+#pragma once
+#include <cstdint>
+
+namespace cutsim {
+
+enum : int16_t { OP_DENSE = 0, OP_PHASE = 1 };
+
+// One op as seen by a sweep kernel. Masks are split into the bits that live
+// inside the tile (lmask, tile-local positions) and the bits that select the
+// tile (omask, global qubit positions, constant over a tile).
+struct SweepOp {
+  uint32_t lmask;     // DENSE: local control bits; PHASE: local phase bits
+  int16_t type;
+  int16_t target;     // DENSE: tile-local target bit
+  uint64_t omask;     // outside-tile qubits that must be 1 for the op to act
+  int32_t slot;       // -1, or cut bit choosing this entry (0) / next entry (1)
+  int32_t pad;
+  double m[8];        // DENSE: m00 m01 m10 m11 as (re,im); PHASE: m[0..1]
+};
+static_assert(sizeof(SweepOp) == 88, "SweepOp layout");
+
+constexpr int kMaxTileBits = 14;
+constexpr int kMaxOpsPerLaunch = 352;  // keeps SweepParams under the 32 KiB param limit
+
+struct SweepParams {
+  void* states;             // batch of states, state v at states + v * stride
+  int64_t stride;           // amplitudes between consecutive states
+  uint64_t variant_base;    // variant id of state 0 of this launch
+  int32_t nq;               // qubits per state
+  int32_t tile_bits;        // T
+  int32_t low_bits;         // L: local bits [0, L) are qubits [0, L)
+  int32_t n_high;           // T - L local bits mapped to qubits hq[]
+  int32_t n_out;            // nq - T outside qubits, tile id bit j -> oq[j]
+  int32_t n_ops;
+  int32_t init_basis;       // 1: ignore memory, start from |0..0>
+  int32_t store;            // 0: keep result in smem only (never used), 1: write back
+  int8_t hq[kMaxTileBits];
+  int8_t oq[64];
+  SweepOp ops[kMaxOpsPerLaunch];
+};
+static_assert(sizeof(SweepParams) <= 32760, "kernel parameter limit");
+
+// merge_terms: out[s][h - row_begin][l] (+)= sum_t coef[s,t] hi[hidx[s,t]][h] lo[lidx[s,t]][l]
+constexpr int kMaxMergeTerms = 1024;
+
+struct MergeParams {
+  const void* hi;           // [n_hi][hi_len]
+  const void* lo;           // [n_lo][lo_len]
+  void* out;                // slot s at out + s * out_slot_stride; row h at (h - row_begin) * W
+  int64_t hi_len;           // amplitudes per hi state (= rows)
+  int64_t lo_len;           // W = amplitudes per lo state (= columns)
+  int64_t row_begin, row_end;
+  int64_t out_slot_stride;
+  int32_t log_w;
+  int32_t S, K;             // slots, terms per slot
+  int32_t accumulate;       // 0: overwrite, 1: add into out
+  int32_t cols;             // min(W, C) columns covered by one row group
+  int32_t log_cols;
+  int32_t rows_per_iter;    // C / cols
+  int32_t iters;            // row groups per CTA
+  int32_t streaming;        // st.global.cs for the output
+  int32_t hidx[kMaxMergeTerms];
+  int32_t lidx[kMaxMergeTerms];
+  double coef[2 * kMaxMergeTerms];
+};
+static_assert(sizeof(MergeParams) <= 32760, "kernel parameter limit");
+
+}  // namespace cutsim

@@ -1,0 +1,516 @@
+// Host-side planning for libcutsim. See plan.hpp.
+//
+// lower_gates   <- reference engine.py:122-139 (kind dispatch) + engine.py:26-27
+//                  (H constant, T phase) + this build's U3 and cut slots
+// schedule_*    <- no reference analogue (the reference applies one gate per
+//                  full pass, engine.py:142-155); this is the B200 tiling
+// plan_chain    <- reference merging.py:156-186 + cutting.py:251-272, refactored
+//                  as a chain tensor-network contraction
+#include "plan.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <sstream>
+
+#include "capi_codes.hpp"
+
+namespace cutsim {
+
+namespace {
+
+constexpr double kSqrtHalf = 0.7071067811865475244;
+
+inline int popcount64(uint64_t v) { return __builtin_popcountll(v); }
+inline int ctz64(uint64_t v) { return __builtin_ctzll(v); }
+
+void set2(double* m, double a, double b, double c, double d, double e, double f, double g, double h) {
+  m[0] = a; m[1] = b; m[2] = c; m[3] = d; m[4] = e; m[5] = f; m[6] = g; m[7] = h;
+}
+
+// C = A * B for 2x2 complex matrices stored as (re, im) row-major
+void matmul2(const double* A, const double* B, double* C) {
+  double out[8];
+  for (int r = 0; r < 2; ++r)
+    for (int c = 0; c < 2; ++c) {
+      double re = 0, im = 0;
+      for (int k = 0; k < 2; ++k) {
+        const double ar = A[2 * (2 * r + k)], ai = A[2 * (2 * r + k) + 1];
+        const double br = B[2 * (2 * k + c)], bi = B[2 * (2 * k + c) + 1];
+        re += ar * br - ai * bi;
+        im += ar * bi + ai * br;
+      }
+      out[2 * (2 * r + c)] = re;
+      out[2 * (2 * r + c) + 1] = im;
+    }
+  for (int i = 0; i < 8; ++i) C[i] = out[i];
+}
+
+bool is_single(const LOp& o) {
+  return (o.type == OP_DENSE && o.mask == 0) || (o.type == OP_PHASE && popcount64(o.mask) == 1);
+}
+
+int single_qubit(const LOp& o) { return o.type == OP_DENSE ? o.target : ctz64(o.mask); }
+
+void as_matrix(const LOp& o, int bit, double* M) {
+  const double* src = (o.slot >= 0 && bit) ? o.alt : o.m;
+  if (o.type == OP_DENSE) {
+    for (int i = 0; i < 8; ++i) M[i] = src[i];
+  } else {
+    set2(M, 1, 0, 0, 0, 0, 0, src[0], src[1]);
+  }
+}
+
+uint64_t qubit_mask(const LOp& o) {
+  return o.type == OP_DENSE ? (o.mask | (1ull << o.target)) : o.mask;
+}
+
+}  // namespace
+
+std::vector<LOp> lower_gates(int nq, const uint8_t* kinds, const int64_t* qa, const int64_t* qb,
+                             const double* params, const int32_t* slots, int64_t n_gates) {
+  std::vector<LOp> ops;
+  ops.reserve(size_t(n_gates));
+  for (int64_t g = 0; g < n_gates; ++g) {
+    const int k = kinds[g];
+    const int64_t a = qa[g];
+    LOp o;
+    const bool two = (k == 5 || k == 6);
+    if (k > 7) throw PlanError{CS_ERR_INVALID, "unknown gate kind code " + std::to_string(k) +
+                                                   " at position " + std::to_string(g)};
+    if (a < 0 || a >= nq)
+      throw PlanError{CS_ERR_INVALID, "gate at position " + std::to_string(g) + " acts on qubit " +
+                                          std::to_string(a) + " outside [0, " + std::to_string(nq) + ")"};
+    if (two) {
+      const int64_t b = qb[g];
+      if (b < 0 || b >= nq || b == a)
+        throw PlanError{CS_ERR_INVALID, "two-qubit gate at position " + std::to_string(g) +
+                                            " has invalid second qubit " + std::to_string(b)};
+    }
+    const int slot = slots ? slots[g] : -1;
+    if (slot >= 0 && k != 3 && k != 4)
+      throw PlanError{CS_ERR_INVALID, "cut slot on a gate that is not S/Sdg at position " + std::to_string(g)};
+    if (slot > 62) throw PlanError{CS_ERR_INVALID, "cut slot index too large"};
+    switch (k) {
+      case 0:  // H (engine.py:62-70)
+        o.type = OP_DENSE;
+        o.target = int(a);
+        set2(o.m, kSqrtHalf, 0, kSqrtHalf, 0, kSqrtHalf, 0, -kSqrtHalf, 0);
+        break;
+      case 1:  // X (engine.py:73-80)
+        o.type = OP_DENSE;
+        o.target = int(a);
+        set2(o.m, 0, 0, 1, 0, 1, 0, 0, 0);
+        break;
+      case 2:  // T: diag(1, (sqrt(1/2), sqrt(1/2))) (engine.py:27,131)
+        o.type = OP_PHASE;
+        o.mask = 1ull << a;
+        o.m[0] = kSqrtHalf;
+        o.m[1] = kSqrtHalf;
+        break;
+      case 3:  // S = diag(1, +i); slot bit 1 -> Sdg (cutting.py:237-247)
+      case 4:  // Sdg = diag(1, -i)
+        o.type = OP_PHASE;
+        o.mask = 1ull << a;
+        if (slot >= 0) {
+          o.slot = slot;
+          o.m[0] = 0; o.m[1] = 1;
+          o.alt[0] = 0; o.alt[1] = -1;
+        } else {
+          o.m[0] = 0;
+          o.m[1] = (k == 3) ? 1.0 : -1.0;
+        }
+        break;
+      case 5:  // CX: X on target where control = 1 (engine.py:92-107)
+        o.type = OP_DENSE;
+        o.target = int(qb[g]);
+        o.mask = 1ull << a;
+        set2(o.m, 0, 0, 1, 0, 1, 0, 0, 0);
+        break;
+      case 6:  // CZ: negate |11> (engine.py:110-119)
+        o.type = OP_PHASE;
+        o.mask = (1ull << a) | (1ull << qb[g]);
+        o.m[0] = -1;
+        o.m[1] = 0;
+        break;
+      case 7: {  // U3 (OpenQASM-2 u3)
+        const double th = params[3 * g], ph = params[3 * g + 1], la = params[3 * g + 2];
+        if (!std::isfinite(th) || !std::isfinite(ph) || !std::isfinite(la))
+          throw PlanError{CS_ERR_INVALID, "non-finite U3 parameter at position " + std::to_string(g)};
+        const double c = std::cos(th / 2), s = std::sin(th / 2);
+        o.type = OP_DENSE;
+        o.target = int(a);
+        set2(o.m, c, 0, -std::cos(la) * s, -std::sin(la) * s, std::cos(ph) * s, std::sin(ph) * s,
+             std::cos(ph + la) * c, std::sin(ph + la) * c);
+        break;
+      }
+      default:
+        break;
+    }
+    ops.push_back(o);
+  }
+  return ops;
+}
+
+std::vector<LOp> fuse_ops(const std::vector<LOp>& ops) {
+  std::vector<LOp> out;
+  out.reserve(ops.size());
+  int last[64];
+  for (int i = 0; i < 64; ++i) last[i] = -1;
+  for (const LOp& op : ops) {
+    if (is_single(op)) {
+      const int q = single_qubit(op);
+      if (last[q] >= 0) {
+        LOp& prev = out[size_t(last[q])];
+        if (prev.slot < 0 || op.slot < 0 || prev.slot == op.slot) {
+          LOp f;
+          f.slot = std::max(prev.slot, op.slot);
+          double A[8], B[8];
+          as_matrix(op, 0, A);
+          as_matrix(prev, 0, B);
+          double M0[8], M1[8];
+          matmul2(A, B, M0);
+          as_matrix(op, 1, A);
+          as_matrix(prev, 1, B);
+          matmul2(A, B, M1);
+          if (prev.type == OP_PHASE && op.type == OP_PHASE) {
+            f.type = OP_PHASE;
+            f.mask = 1ull << q;
+            f.m[0] = M0[6]; f.m[1] = M0[7];
+            f.alt[0] = M1[6]; f.alt[1] = M1[7];
+          } else {
+            f.type = OP_DENSE;
+            f.target = q;
+            f.mask = 0;
+            for (int i = 0; i < 8; ++i) { f.m[i] = M0[i]; f.alt[i] = M1[i]; }
+          }
+          if (f.slot < 0)
+            for (int i = 0; i < 8; ++i) f.alt[i] = 0;
+          prev = f;
+          continue;
+        }
+      }
+      out.push_back(op);
+      last[q] = int(out.size()) - 1;
+    } else {
+      out.push_back(op);
+      uint64_t qm = qubit_mask(op);
+      while (qm) {
+        last[ctz64(qm)] = -1;
+        qm &= qm - 1;
+      }
+    }
+  }
+  return out;
+}
+
+static void emit_entries(const LOp& op, const int* local_pos, Sweep& sw) {
+  SweepOp e{};
+  e.type = op.type;
+  e.slot = op.slot;
+  uint64_t mm = op.mask;
+  while (mm) {
+    const int q = ctz64(mm);
+    mm &= mm - 1;
+    if (local_pos[q] >= 0) e.lmask |= 1u << local_pos[q];
+    else e.omask |= 1ull << q;
+  }
+  e.target = op.type == OP_DENSE ? int16_t(local_pos[op.target]) : int16_t(-1);
+  for (int i = 0; i < 8; ++i) e.m[i] = op.m[i];
+  sw.entries.push_back(e);
+  if (op.slot >= 0) {
+    for (int i = 0; i < 8; ++i) e.m[i] = op.alt[i];
+    sw.entries.push_back(e);
+  }
+}
+
+std::vector<Sweep> schedule_sweeps(const std::vector<LOp>& ops, int nq, int tile_bits, int low_bits) {
+  std::vector<Sweep> sweeps;
+  if (nq <= tile_bits) {
+    Sweep sw;
+    sw.tile_bits = nq;
+    sw.low_bits = nq;
+    int local_pos[64];
+    for (int q = 0; q < 64; ++q) local_pos[q] = q < nq ? q : -1;
+    for (const LOp& op : ops) emit_entries(op, local_pos, sw);
+    sweeps.push_back(std::move(sw));
+    return sweeps;
+  }
+  const int T = tile_bits;
+  const int L = std::max(1, std::min(low_bits, T - 1));
+  std::vector<int> pending(ops.size());
+  for (size_t i = 0; i < ops.size(); ++i) pending[i] = int(i);
+  bool first = true;
+  while (!pending.empty() || first) {
+    first = false;
+    bool inset[64] = {false};
+    for (int q = 0; q < L; ++q) inset[q] = true;
+    int room = T - L;
+    uint64_t blocked_dense = 0, blocked_phase = 0;
+    std::vector<int> run, deferred;
+    for (int idx : pending) {
+      const LOp& op = ops[size_t(idx)];
+      const uint64_t qm = qubit_mask(op);
+      if (op.type == OP_PHASE) {
+        if (qm & blocked_dense) {
+          blocked_phase |= qm;
+          deferred.push_back(idx);
+        } else {
+          run.push_back(idx);
+        }
+        continue;
+      }
+      if (qm & (blocked_dense | blocked_phase)) {
+        blocked_dense |= qm;
+        deferred.push_back(idx);
+      } else if (inset[op.target]) {
+        run.push_back(idx);
+      } else if (room > 0) {
+        inset[op.target] = true;
+        --room;
+        run.push_back(idx);
+      } else {
+        blocked_dense |= qm;
+        deferred.push_back(idx);
+      }
+    }
+    Sweep sw;
+    sw.tile_bits = T;
+    sw.low_bits = L;
+    for (int q = L; q < nq; ++q)
+      if (inset[q]) sw.hq.push_back(q);
+    for (int q = L; q < nq && int(sw.hq.size()) < T - L; ++q)
+      if (!inset[q]) {
+        inset[q] = true;
+        sw.hq.push_back(q);
+      }
+    std::sort(sw.hq.begin(), sw.hq.end());
+    for (int q = L; q < nq; ++q)
+      if (!inset[q]) sw.oq.push_back(q);
+    int local_pos[64];
+    for (int q = 0; q < 64; ++q) local_pos[q] = -1;
+    for (int q = 0; q < L; ++q) local_pos[q] = q;
+    for (size_t j = 0; j < sw.hq.size(); ++j) local_pos[sw.hq[j]] = L + int(j);
+    for (int idx : run) emit_entries(ops[size_t(idx)], local_pos, sw);
+    sweeps.push_back(std::move(sw));
+    pending.swap(deferred);
+  }
+  return sweeps;
+}
+
+std::string sweeps_to_json(const std::vector<Sweep>& sweeps, int nq) {
+  std::ostringstream os;
+  os.precision(17);
+  os << "{\"nq\":" << nq << ",\"sweeps\":[";
+  for (size_t s = 0; s < sweeps.size(); ++s) {
+    const Sweep& sw = sweeps[s];
+    if (s) os << ",";
+    os << "{\"T\":" << sw.tile_bits << ",\"L\":" << sw.low_bits << ",\"hq\":[";
+    for (size_t i = 0; i < sw.hq.size(); ++i) os << (i ? "," : "") << sw.hq[i];
+    os << "],\"oq\":[";
+    for (size_t i = 0; i < sw.oq.size(); ++i) os << (i ? "," : "") << sw.oq[i];
+    os << "],\"entries\":[";
+    for (size_t i = 0; i < sw.entries.size(); ++i) {
+      const SweepOp& e = sw.entries[i];
+      os << (i ? "," : "") << "{\"type\":" << e.type << ",\"target\":" << e.target
+         << ",\"lmask\":" << e.lmask << ",\"omask\":" << e.omask << ",\"slot\":" << e.slot << ",\"m\":[";
+      for (int k = 0; k < 8; ++k) os << (k ? "," : "") << e.m[k];
+      os << "]}";
+    }
+    os << "]}";
+  }
+  os << "]}";
+  return os.str();
+}
+
+// ---------------------------------------------------------------------------
+// chain contraction plan
+// ---------------------------------------------------------------------------
+bool plan_chain(int n, const int32_t* seg_nq, const int32_t* seg_ncuts, const int32_t* seg_cut_ids,
+                int c_total, const int32_t* cut_boundary, const double* term_coef, int force_bond,
+                ChainPlan* out, PlanError* err) {
+  if (n < 2) {
+    *err = {CS_ERR_INVALID, "merging needs at least 2 segments"};
+    return false;
+  }
+  if (c_total < 0 || c_total > 40) {
+    *err = {CS_ERR_INVALID, "c_total out of range"};
+    return false;
+  }
+  // cuts per boundary, and each cut's index within its boundary
+  std::vector<std::vector<int>> bcuts(size_t(n - 1));
+  std::vector<int> index_in_boundary(size_t(c_total), -1);
+  for (int c = 0; c < c_total; ++c) {
+    const int b = cut_boundary[c];
+    if (b < 0 || b >= n - 1) {
+      *err = {CS_ERR_INVALID, "cut " + std::to_string(c) + " on invalid boundary " + std::to_string(b)};
+      return false;
+    }
+    index_in_boundary[size_t(c)] = int(bcuts[size_t(b)].size());
+    bcuts[size_t(b)].push_back(c);
+  }
+  int total_q = 0;
+  std::vector<int> offs(size_t(n) + 1, 0);
+  for (int j = 0; j < n; ++j) {
+    if (seg_nq[j] < 1 || seg_nq[j] > 40) {
+      *err = {CS_ERR_INVALID, "segment qubit count out of range"};
+      return false;
+    }
+    total_q += seg_nq[j];
+    offs[size_t(j) + 1] = offs[size_t(j)] + seg_ncuts[j];
+    const int expect = (j > 0 ? int(bcuts[size_t(j - 1)].size()) : 0) + (j < n - 1 ? int(bcuts[size_t(j)].size()) : 0);
+    if (seg_ncuts[j] != expect) {
+      *err = {CS_ERR_INVALID, "segment " + std::to_string(j) + " lists " + std::to_string(seg_ncuts[j]) +
+                                  " adjacent cuts, boundaries imply " + std::to_string(expect)};
+      return false;
+    }
+    for (int lb = 0; lb < seg_ncuts[j]; ++lb) {
+      const int c = seg_cut_ids[offs[size_t(j)] + lb];
+      if (c < 0 || c >= c_total || (cut_boundary[c] != j - 1 && cut_boundary[c] != j)) {
+        *err = {CS_ERR_INVALID, "segment " + std::to_string(j) + " lists a non-adjacent cut"};
+        return false;
+      }
+    }
+  }
+  if (total_q > 62) {
+    *err = {CS_ERR_CAPACITY, "total qubit count exceeds 62"};
+    return false;
+  }
+  auto cb = [&](int b) { return int(bcuts[size_t(b)].size()); };
+  // r_j(x, y): local variant index of segment j for bond bits x (boundary j-1), y (boundary j)
+  auto variant_of = [&](int j, int64_t x, int64_t y) {
+    int64_t r = 0;
+    for (int lb = 0; lb < seg_ncuts[j]; ++lb) {
+      const int c = seg_cut_ids[offs[size_t(j)] + lb];
+      const int pos = index_in_boundary[size_t(c)];
+      const int64_t bit = (cut_boundary[c] == j - 1) ? ((x >> pos) & 1) : ((y >> pos) & 1);
+      r |= bit << lb;
+    }
+    return int32_t(r);
+  };
+  auto alpha = [&](int64_t bits, int count, double* re, double* im) {
+    double ar = 1, ai = 0;
+    for (int a = 0; a < count; ++a) {
+      const double* t = term_coef + 2 * ((bits >> a) & 1);
+      const double nr = ar * t[0] - ai * t[1];
+      ai = ar * t[1] + ai * t[0];
+      ar = nr;
+    }
+    *re = ar;
+    *im = ai;
+  };
+  // bond choice: minimise modelled time of the final product + intermediates
+  const double bw = 6.5e12, f64 = 3.5e13;
+  auto step_cost = [&](double out_amps, double terms) {
+    return std::max(out_amps * 16.0 / bw, out_amps * terms * 8.0 / f64);
+  };
+  int best = 0;
+  double best_cost = 1e300;
+  for (int k = 0; k < n - 1; ++k) {
+    double cost = step_cost(std::ldexp(1.0, total_q), std::ldexp(1.0, cb(k)));
+    int ql = 0;
+    for (int j = 0; j <= k; ++j) {
+      ql += seg_nq[j];
+      if (j >= 1) cost += step_cost(std::ldexp(1.0, ql + cb(j)), std::ldexp(1.0, cb(j - 1)));
+    }
+    int qr = 0;
+    for (int j = n - 1; j > k; --j) {
+      qr += seg_nq[j];
+      if (j <= n - 2) cost += step_cost(std::ldexp(1.0, qr + cb(j - 1)), std::ldexp(1.0, cb(j)));
+    }
+    if (cost < best_cost * (1 - 1e-9)) {
+      best_cost = cost;
+      best = k;
+    }
+  }
+  if (force_bond >= 0) {
+    if (force_bond > n - 2) {
+      *err = {CS_ERR_INVALID, "forced bond out of range"};
+      return false;
+    }
+    best = force_bond;
+  }
+  const int k = best;
+  ChainPlan plan;
+  plan.bond = k;
+  auto new_buf = [&](int64_t amps) {
+    plan.buf_amps.push_back(amps);
+    return n + int(plan.buf_amps.size()) - 1;
+  };
+  // left side: L_0 = segment 0, L_j = sum_x alpha(x) psi_j[r_j(x,y)] (x) L_{j-1}[x]
+  int lbuf = 0;
+  int64_t llen = int64_t(1) << seg_nq[0];
+  for (int j = 1; j <= k; ++j) {
+    MergeStep st;
+    st.S = 1 << cb(j);
+    st.K = 1 << cb(j - 1);
+    st.hi_buf = j;
+    st.lo_buf = lbuf;
+    st.hi_len = int64_t(1) << seg_nq[j];
+    st.lo_len = llen;
+    st.out_buf = new_buf(int64_t(st.S) * st.hi_len * st.lo_len);
+    for (int64_t y = 0; y < st.S; ++y)
+      for (int64_t x = 0; x < st.K; ++x) {
+        st.hidx.push_back(variant_of(j, x, y));
+        st.lidx.push_back(int32_t(x));
+        double re, im;
+        alpha(x, cb(j - 1), &re, &im);
+        st.coef.push_back(re);
+        st.coef.push_back(im);
+      }
+    lbuf = st.out_buf;
+    llen = st.hi_len * st.lo_len;
+    plan.steps.push_back(std::move(st));
+  }
+  // right side: R_{n-1} = segment n-1, R_j[x] = sum_y alpha(y) R_{j+1}[y] (x) psi_j[r_j(x,y)]
+  int rbuf = n - 1;
+  int64_t rlen = int64_t(1) << seg_nq[n - 1];
+  for (int j = n - 2; j > k; --j) {
+    MergeStep st;
+    st.S = 1 << cb(j - 1);
+    st.K = 1 << cb(j);
+    st.hi_buf = rbuf;
+    st.lo_buf = j;
+    st.hi_len = rlen;
+    st.lo_len = int64_t(1) << seg_nq[j];
+    st.out_buf = new_buf(int64_t(st.S) * st.hi_len * st.lo_len);
+    for (int64_t x = 0; x < st.S; ++x)
+      for (int64_t y = 0; y < st.K; ++y) {
+        st.hidx.push_back(int32_t(y));
+        st.lidx.push_back(variant_of(j, x, y));
+        double re, im;
+        alpha(y, cb(j), &re, &im);
+        st.coef.push_back(re);
+        st.coef.push_back(im);
+      }
+    rbuf = st.out_buf;
+    rlen = st.hi_len * st.lo_len;
+    plan.steps.push_back(std::move(st));
+  }
+  // final product across bond k
+  MergeStep fin;
+  fin.final_step = true;
+  fin.S = 1;
+  fin.K = 1 << cb(k);
+  fin.hi_buf = rbuf;
+  fin.lo_buf = lbuf;
+  fin.hi_len = rlen;
+  fin.lo_len = llen;
+  fin.out_buf = -1;
+  for (int64_t z = 0; z < fin.K; ++z) {
+    fin.hidx.push_back(int32_t(z));
+    fin.lidx.push_back(int32_t(z));
+    double re, im;
+    alpha(z, cb(k), &re, &im);
+    fin.coef.push_back(re);
+    fin.coef.push_back(im);
+  }
+  plan.steps.push_back(std::move(fin));
+  int ql = 0;
+  for (int j = 0; j <= k; ++j) ql += seg_nq[j];
+  plan.q_low = ql;
+  *out = std::move(plan);
+  return true;
+}
+
+}  // namespace cutsim

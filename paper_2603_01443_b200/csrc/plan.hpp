@@ -1,0 +1,72 @@
+// Host-side planning of libcutsim (pure C++, no CUDA): gate lowering and
+// fusion, sweep scheduling for tiled state vectors, and the chain-contraction
+// plan of the merge.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "ops.hpp"
+
+namespace cutsim {
+
+struct PlanError {
+  int code;  // CS_ERR_*
+  std::string msg;
+};
+
+// One lowered op on global qubits. Slotted ops carry both alternatives.
+struct LOp {
+  int16_t type = OP_DENSE;
+  int target = -1;        // DENSE target qubit
+  uint64_t mask = 0;      // DENSE: control qubits; PHASE: phase qubits
+  int slot = -1;
+  double m[8] = {0};      // bit-0 alternative (or the only one)
+  double alt[8] = {0};    // bit-1 alternative when slot >= 0
+};
+
+// Lower the packed table (reference kinds 0..6, U3 = 7) into ops.
+// slots may be null; slots[g] >= 0 marks an S gate that becomes Sdg for
+// variant bit slots[g] = 1.
+std::vector<LOp> lower_gates(int nq, const uint8_t* kinds, const int64_t* qa, const int64_t* qb,
+                             const double* params, const int32_t* slots, int64_t n_gates);
+
+// Merge runs of single-qubit ops on the same qubit (no intervening op on it).
+std::vector<LOp> fuse_ops(const std::vector<LOp>& ops);
+
+struct Sweep {
+  int tile_bits = 0, low_bits = 0;
+  std::vector<int> hq;           // qubits of local bits [L, T)
+  std::vector<int> oq;           // qubits selected by the tile id
+  std::vector<SweepOp> entries;  // slotted ops take two consecutive entries
+};
+
+// Greedy tiling: every sweep holds the low qubits [0, L) plus up to T - L
+// more qubits chosen in order of first need; it absorbs every op whose
+// non-diagonal target is in the tile and that commutes with all deferred ops.
+std::vector<Sweep> schedule_sweeps(const std::vector<LOp>& ops, int nq, int tile_bits, int low_bits);
+
+std::string sweeps_to_json(const std::vector<Sweep>& sweeps, int nq);
+
+// ---- merge chain -----------------------------------------------------------
+struct MergeStep {
+  int hi_buf, lo_buf, out_buf;  // buffer ids: 0..n-1 segment states, n.. workspace
+  int64_t hi_len, lo_len;
+  int S, K;
+  std::vector<int32_t> hidx, lidx;  // S*K
+  std::vector<double> coef;         // 2*S*K
+  bool final_step = false;
+};
+
+struct ChainPlan {
+  int bond = 0;
+  int q_low = 0;                      // qubits of the low (L) side of the final product
+  std::vector<int64_t> buf_amps;      // workspace buffers (amplitudes), ids n..
+  std::vector<MergeStep> steps;
+};
+
+bool plan_chain(int n, const int32_t* seg_nq, const int32_t* seg_ncuts, const int32_t* seg_cut_ids,
+                int c_total, const int32_t* cut_boundary, const double* term_coef, int force_bond,
+                ChainPlan* out, PlanError* err);
+
+}  // namespace cutsim

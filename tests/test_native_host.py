@@ -1,0 +1,193 @@
+"""CPU checks of the native library's host side (no kernels are launched):
+the C-ABI loads and exports every symbol include/cutsim.h declares; the gate
+lowering, fusion and sweep scheduling (executed here by a numpy interpreter of
+the exported schedule) reproduce the oracle; the chain-merge planner picks
+the documented bonds and validates its input."""
+import json
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+from oracle import cutbench_oracle as orc
+from paper_2603_01443_b200 import _native
+from paper_2603_01443_b200 import circuits as C
+from paper_2603_01443_b200 import cutting as K
+from paper_2603_01443_b200 import generators as G
+from paper_2603_01443_b200.errors import NativeUnavailableError, ValidationError
+
+HEADER = os.path.join(ROOT, "include", "cutsim.h")
+
+pytestmark = pytest.mark.skipif(not os.path.exists(_native.LIB_PATH),
+                                reason="libcutsim.so not built (run __graft_entry__.build())")
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[\w\s\*]+?\b(cs_\w+)\s*\(", text, re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _native.load()
+    decl = declared_symbols()
+    assert len(decl) >= 14
+    for name in decl:
+        assert hasattr(lib, name), name
+    assert set(decl) == set(_native.SIGNATURES), "ctypes table and header disagree"
+    assert lib.cs_version() >= 10000
+
+
+def test_options_round_trip_and_errors():
+    old = _native.get_option("tile_bits")
+    _native.set_option("tile_bits", 10)
+    assert _native.get_option("tile_bits") == 10
+    _native.set_option("tile_bits", old)
+    with pytest.raises(ValidationError):
+        _native.set_option("tile_bits", 40)
+    with pytest.raises(ValidationError):
+        _native.set_option("no_such_option", 1)
+    assert "unknown option" in _native.last_error()
+
+
+def execute_schedule(plan, nq, variant=0):
+    """Interpret the exported sweep schedule on a full numpy state."""
+    amps = orc.zero_state(nq)
+    idx = np.arange(1 << nq, dtype=np.int64)
+    for sw in plan["sweeps"]:
+        L, hq = sw["L"], sw["hq"]
+        glob = list(range(L)) + list(hq)
+        ents = sw["entries"]
+        i = 0
+        while i < len(ents):
+            e = ents[i]
+            src = e
+            step = 1
+            if e["slot"] >= 0:
+                src = ents[i + ((variant >> e["slot"]) & 1)]
+                step = 2
+            mask = e["omask"]
+            for p in range(32):
+                if (e["lmask"] >> p) & 1:
+                    mask |= 1 << glob[p]
+            m = np.array(src["m"]).reshape(4, 2)
+            m = m[:, 0] + 1j * m[:, 1]
+            sel = (idx & mask) == mask
+            if e["type"] == 1:
+                amps[sel] *= m[0]
+            else:
+                t = glob[e["target"]]
+                zero = sel & (((idx >> t) & 1) == 0)
+                i0 = idx[zero]
+                i1 = i0 | (1 << t)
+                a, b = amps[i0].copy(), amps[i1].copy()
+                amps[i0] = m[0] * a + m[1] * b
+                amps[i1] = m[2] * a + m[3] * b
+            i += step
+    return amps
+
+
+@pytest.mark.parametrize("tile_bits", [4, 6, 12])
+@pytest.mark.parametrize("q,d,n,c,seed", [(9, 4, 3, 4, 1), (10, 5, 2, 3, 0), (14, 3, 2, 2, 2)])
+def test_schedule_reproduces_oracle_uncut(q, d, n, c, seed, tile_bits):
+    circ = G.build_brickwall(G.BrickwallSpec(q, d, n, c, seed))
+    plan = json.loads(_native.sweep_plan_json(q, circ.table, tile_bits=tile_bits))
+    T = plan["sweeps"][0]["T"]
+    assert T == (q if q <= 13 else tile_bits)
+    got = execute_schedule(plan, q)
+    ref = orc.simulate(q, circ.kinds, circ.qa, circ.qb, circ.params)
+    assert np.abs(got - ref).max() < 1e-12
+
+
+@pytest.mark.parametrize("key", ["stair_q8_n4_b2", "stair_q6_n2_b3", "shadow_q9_d4_n3_c4_s3",
+                                 "padded_q6_n2_b1_p1"])
+def test_schedule_of_variant_templates_matches_reference_states(golden, key):
+    q, n = int(golden[f"{key}/q"]), int(golden[f"{key}/n"])
+    circ = C.Circuit.from_table(q, C.GateTable(golden[f"{key}/kinds"], golden[f"{key}/qa"],
+                                               golden[f"{key}/qb"]))
+    subs = K.decompose(circ, K.plan_cut(circ, n))
+    for fam in subs.segments:
+        for tb in (2, 3, 0):
+            plan = json.loads(_native.sweep_plan_json(fam.num_qubits, fam.template, fam.slots,
+                                                      tile_bits=tb))
+            ref = golden[f"{key}/seg{fam.segment}/states"]
+            for v in range(fam.num_variants):
+                got = execute_schedule(plan, fam.num_qubits, v)
+                assert np.abs(got - ref[v]).max() < 1e-12
+
+
+def test_depth_padded_fusion_collapses_pad():
+    circ = C.build_depth_padded(C.BenchmarkSpec(q=6, n=2, blocks=1, depth_pad_exponent=3))
+    plan = json.loads(_native.sweep_plan_json(6, circ.table))
+    n_entries = sum(len(s["entries"]) for s in plan["sweeps"])
+    assert circ.gate_count > 2000 and n_entries < 60
+    got = execute_schedule(plan, 6)
+    ref = orc.simulate(6, circ.kinds, circ.qa, circ.qb)
+    assert np.abs(got - ref).max() < 1e-10
+
+
+def test_uncut_q30_schedule_is_compact():
+    circ = G.build_brickwall(G.BASELINE_CONFIGS["cfg4a"])
+    plan = json.loads(_native.sweep_plan_json(30, circ.table))
+    sweeps = plan["sweeps"]
+    ops = sum(len(s["entries"]) for s in sweeps)
+    # edge qubits skip the odd-layer CZ, so their U3 pairs fuse
+    assert ops < circ.gate_count
+    assert len(sweeps) <= 40
+
+
+def test_lowering_rejects_bad_tables():
+    bad = C.GateTable(np.array([9], np.uint8), np.array([0]), np.array([-1]))
+    with pytest.raises(ValidationError):
+        _native.sweep_plan_json(2, bad)
+    out_of_range = C.GateTable(np.array([0], np.uint8), np.array([5]), np.array([-1]))
+    with pytest.raises(ValidationError):
+        _native.sweep_plan_json(2, out_of_range)
+    slot_on_h = C.GateTable(np.array([0], np.uint8), np.array([0]), np.array([-1]))
+    with pytest.raises(ValidationError):
+        _native.sweep_plan_json(2, slot_on_h, np.array([0], np.int32))
+
+
+def _chain(spec):
+    circ = G.build_brickwall(spec)
+    from paper_2603_01443_b200.merging import ChainSpec
+
+    return ChainSpec.from_plan(K.plan_cut(circ, spec.n))
+
+
+@pytest.mark.parametrize("name,bond,qlow,ws", [
+    ("cfg4a", 0, 15, 0),
+    ("cfg5_q34_n2_c2", 0, 17, 0),
+    ("cfg5_q32_n4_c4", 1, 16, 2 * 2 * (1 << 16) * 16),   # middle bond: rank 2
+])
+def test_chain_plan_bonds(name, bond, qlow, ws):
+    ch = _chain(G.BASELINE_CONFIGS[name])
+    got_ws, got_bond, got_qlow = ch.plan()
+    assert (got_bond, got_qlow) == (bond, qlow)
+    assert got_ws == ws
+
+
+def test_chain_plan_cfg4b_rank4_and_small_workspace():
+    ch = _chain(G.BASELINE_CONFIGS["cfg4b"])
+    ws, bond, qlow = ch.plan()
+    assert bond in (0, 1)
+    assert ws == 4 * (1 << 20) * 16  # one 2^20-amplitude intermediate per bond value
+
+
+def test_chain_plan_validation():
+    with pytest.raises(ValidationError):
+        _native.chain_plan(2, [3, 3], [1, 2], [0, 0, 1], 1, [0], [0.5, -0.5, 0.5, 0.5])
+    with pytest.raises(ValidationError):
+        _native.chain_plan(1, [3], [0], [], 0, [], [0.5, -0.5, 0.5, 0.5])
+
+
+def test_compute_entry_points_fail_loudly_without_gpu():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2603_01443_b200 import engine
+
+    with pytest.raises(NativeUnavailableError):
+        engine.simulate(C.Circuit(2, [C.h(0)]))
