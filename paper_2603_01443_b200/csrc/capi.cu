@@ -5,7 +5,9 @@
 #include <algorithm>
 #include <atomic>
 #include <cstring>
+#include <memory>
 #include <mutex>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -95,14 +97,53 @@ double2* reduce_scratch(int* err) {
   return g_scratch.per_device[size_t(dev)];
 }
 
-std::vector<Sweep> build_schedule(int nq, const uint8_t* kinds, const int64_t* qa, const int64_t* qb,
-                                  const double* params, const int32_t* slots, int64_t n_gates, int tile_bits,
-                                  int dtype) {
+int choose_tile_bits(int nq, int64_t n_states, int tile_bits, int dtype) {
+  if (nq <= single_tile_max(dtype)) return nq;
+  if (tile_bits > 0) return std::min(tile_bits, nq);
+  if (g_opt.tile_bits > 0) return std::min(int(g_opt.tile_bits), nq);
+  const int dflt = multi_tile_bits(dtype);
+  if (n_states > 1) {
+    // small batches of mid-size states (cut variants): shrink the tile until
+    // the grid covers the chip twice (the states are L2-resident anyway)
+    const int64_t want = (2 * 148 + n_states - 1) / n_states;
+    int lg = 0;
+    while ((int64_t(1) << lg) < want) ++lg;
+    return std::max(9, std::min(dflt, nq - lg));
+  }
+  return dflt;
+}
+
+std::mutex g_cache_mu;
+std::unordered_map<std::string, std::shared_ptr<const std::vector<Sweep>>> g_cache;
+
+// Lowered, fused and scheduled program for a gate table; cached by content.
+std::shared_ptr<const std::vector<Sweep>> build_schedule(int nq, const uint8_t* kinds, const int64_t* qa,
+                                                         const int64_t* qb, const double* params,
+                                                         const int32_t* slots, int64_t n_gates, int64_t n_states,
+                                                         int tile_bits, int dtype) {
+  const int T = choose_tile_bits(nq, n_states, tile_bits, dtype);
+  const int L = (T == nq) ? nq : std::max(3, std::min(int(g_opt.low_bits), T - 6));
+  std::string key;
+  key.reserve(size_t(n_gates) * 45 + 32);
+  const int32_t hdr[5] = {nq, T, L, int32_t(g_opt.fuse), slots ? 1 : 0};
+  key.append(reinterpret_cast<const char*>(hdr), sizeof(hdr));
+  key.append(reinterpret_cast<const char*>(kinds), size_t(n_gates));
+  key.append(reinterpret_cast<const char*>(qa), size_t(n_gates) * 8);
+  key.append(reinterpret_cast<const char*>(qb), size_t(n_gates) * 8);
+  if (params) key.append(reinterpret_cast<const char*>(params), size_t(n_gates) * 24);
+  if (slots) key.append(reinterpret_cast<const char*>(slots), size_t(n_gates) * 4);
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    auto it = g_cache.find(key);
+    if (it != g_cache.end()) return it->second;
+  }
   std::vector<LOp> ops = lower_gates(nq, kinds, qa, qb, params, slots, n_gates);
   if (g_opt.fuse) ops = fuse_ops(ops);
-  int T = nq <= single_tile_max(dtype) ? nq : (tile_bits > 0 ? tile_bits : multi_tile_bits(dtype));
-  T = std::min(T, nq);
-  return schedule_sweeps(ops, nq, T, int(g_opt.low_bits));
+  auto prog = std::make_shared<const std::vector<Sweep>>(schedule_sweeps(ops, nq, T, L));
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  if (g_cache.size() >= 256) g_cache.clear();
+  g_cache.emplace(std::move(key), prog);
+  return prog;
 }
 
 // Launch one merge_terms problem whose K is one instantiated width.
@@ -249,8 +290,8 @@ int cs_set_option(const char* key, int64_t value) {
   } else if (k == "fuse") {
     g_opt.fuse = value ? 1 : 0;
   } else if (k == "threads") {
-    if (value != 0 && (value < 32 || value > 1024 || (value & 31)))
-      return fail(CS_ERR_INVALID, "threads must be 0 or a multiple of 32 in [32, 1024]");
+    if (value != 0 && (value < 32 || value > 256 || (value & 31)))
+      return fail(CS_ERR_INVALID, "threads must be 0 or a multiple of 32 in [32, 256]");
     g_opt.threads = value;
   } else if (k == "merge_streaming") {
     g_opt.merge_streaming = value ? 1 : 0;
@@ -299,12 +340,13 @@ int cs_sim_batch(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int6
     if (!init_zero) return CS_OK;
     return cs_init_basis(states, 0, n_states, 0, dtype, stream);
   }
-  std::vector<Sweep> sweeps;
+  std::shared_ptr<const std::vector<Sweep>> prog;
   try {
-    sweeps = build_schedule(nq, kinds, qa, qb, params, slots, n_gates, 0, dtype);
+    prog = build_schedule(nq, kinds, qa, qb, params, slots, n_gates, n_states, 0, dtype);
   } catch (const PlanError& pe) {
     return fail(pe.code, pe.msg);
   }
+  const std::vector<Sweep>& sweeps = *prog;
   static SweepParams p;
   static std::mutex pm;
   std::lock_guard<std::mutex> lk(pm);
@@ -337,12 +379,8 @@ int cs_sim_batch(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int6
       p.store = 1;
       p.stride = state_stride;
       int threads = int(g_opt.threads);
-      if (threads == 0) {
-        const int64_t ctas = int64_t(n_tiles) * n_states;
-        threads = ctas < 2 * 148 ? 1024 : 256;
-      }
-      const int max_useful = std::max(32, 1 << std::max(0, T - 1));
-      threads = std::min(threads, (max_useful + 31) / 32 * 32);
+      if (threads == 0) threads = std::max(32, std::min(256, 1 << std::max(0, T - 2)));
+      threads = std::min(threads, 256);
       for (int64_t v0 = 0; v0 < n_states; v0 += 65535) {
         const int64_t vc = std::min<int64_t>(65535, n_states - v0);
         p.states = static_cast<char*>(states) + size_t(v0) * size_t(state_stride) * elem_bytes(dtype);
@@ -365,7 +403,7 @@ int cs_sweep_plan_json(int32_t nq, const uint8_t* kinds, const int64_t* qa, cons
   if (nq < 1 || nq > 62) return fail(CS_ERR_INVALID, "qubit count out of range");
   std::string js;
   try {
-    js = sweeps_to_json(build_schedule(nq, kinds, qa, qb, params, slots, n_gates, tile_bits, dtype), nq);
+    js = sweeps_to_json(*build_schedule(nq, kinds, qa, qb, params, slots, n_gates, 1, tile_bits, dtype), nq);
   } catch (const PlanError& pe) {
     return fail(pe.code, pe.msg);
   }

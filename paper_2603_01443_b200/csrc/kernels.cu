@@ -9,7 +9,9 @@
 //   init_basis    <- engine.py:47-51   (StateVec.zero_state)
 #include <cuda_runtime.h>
 
+#include <cstddef>
 #include <cstdint>
+#include <cstring>
 #include <type_traits>
 
 #include "ops.hpp"
@@ -41,9 +43,103 @@ __device__ __forceinline__ void cfma(vec2_t<R>& acc, vec2_t<R> a, vec2_t<R> b) {
 // bits [0,L) = qubits [0,L), bits [L,T) = qubits hq[], the tile id scattered
 // over the remaining qubits oq[]). The tile is staged in shared memory, every
 // op of the launch is applied there, and the tile is written back once.
+//
+// Dense ops come in register groups of up to 4 commuting ops on distinct
+// qubits: each thread loads the 2^k amplitudes of one k-qubit cell into
+// registers, applies all k 2x2 matrices, and stores once — k times less
+// shared-memory traffic and k-1 fewer barriers than op-by-op. Shared memory
+// is XOR-swizzled on 16-byte granules so the cell strides (2^t elements) do
+// not collide on banks.
 // ---------------------------------------------------------------------------
-template <typename R>
-__global__ void __launch_bounds__(1024) sweep_kernel(const __grid_constant__ SweepParams p) {
+__device__ __forceinline__ uint32_t swz(uint32_t e) {
+  uint32_t x = e >> 3;
+  x ^= (x >> 3) ^ (x >> 6) ^ (x >> 9);
+  return e ^ (x & 7u);
+}
+
+template <typename R, int K, class P>
+__device__ __forceinline__ int apply_group(vec2_t<R>* s, const P& p, int i0, uint64_t base, uint64_t variant,
+                                           int T, uint32_t tid, uint32_t bd) {
+  using V = vec2_t<R>;
+  int tgt[K];
+  uint32_t lm[K];
+  bool act[K];
+  int src[K];
+  int j = i0;
+#pragma unroll
+  for (int g = 0; g < K; ++g) {
+    const SweepOp& o = p.ops[j];
+    int step = 1;
+    src[g] = j;
+    if (o.slot >= 0) {
+      src[g] = j + int((variant >> o.slot) & 1ull);
+      step = 2;
+    }
+    tgt[g] = o.target;
+    lm[g] = o.lmask;
+    act[g] = (base & o.omask) == o.omask;
+    j += step;
+  }
+  int srt[K];
+#pragma unroll
+  for (int g = 0; g < K; ++g) srt[g] = tgt[g];
+#pragma unroll
+  for (int a = 1; a < K; ++a)
+#pragma unroll
+    for (int b = a; b > 0; --b)
+      if (srt[b] < srt[b - 1]) {
+        const int t = srt[b];
+        srt[b] = srt[b - 1];
+        srt[b - 1] = t;
+      }
+  uint32_t off[1 << K];
+#pragma unroll
+  for (int i = 0; i < (1 << K); ++i) {
+    uint32_t o = 0;
+#pragma unroll
+    for (int g = 0; g < K; ++g)
+      if ((i >> g) & 1) o |= 1u << tgt[g];
+    off[i] = o;
+  }
+  const uint32_t cells = 1u << (T - K);
+  for (uint32_t c = tid; c < cells; c += bd) {
+    uint32_t e = c;
+#pragma unroll
+    for (int g = 0; g < K; ++g) {
+      const uint32_t b = (1u << srt[g]) - 1u;
+      e = ((e & ~b) << 1) | (e & b);
+    }
+    V v[1 << K];
+#pragma unroll
+    for (int i = 0; i < (1 << K); ++i) v[i] = s[swz(e | off[i])];
+#pragma unroll
+    for (int g = 0; g < K; ++g) {
+      if (!act[g] || (e & lm[g]) != lm[g]) continue;
+      const double* m = p.ops[src[g]].m;
+      const R m00r = R(m[0]), m00i = R(m[1]), m01r = R(m[2]), m01i = R(m[3]);
+      const R m10r = R(m[4]), m10i = R(m[5]), m11r = R(m[6]), m11i = R(m[7]);
+#pragma unroll
+      for (int i = 0; i < (1 << K); ++i) {
+        if ((i >> g) & 1) continue;
+        const V a = v[i];
+        const V b = v[i | (1 << g)];
+        V u, w;
+        u.x = m00r * a.x - m00i * a.y + m01r * b.x - m01i * b.y;
+        u.y = m00r * a.y + m00i * a.x + m01r * b.y + m01i * b.x;
+        w.x = m10r * a.x - m10i * a.y + m11r * b.x - m11i * b.y;
+        w.y = m10r * a.y + m10i * a.x + m11r * b.y + m11i * b.x;
+        v[i] = u;
+        v[i | (1 << g)] = w;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < (1 << K); ++i) s[swz(e | off[i])] = v[i];
+  }
+  return j;
+}
+
+template <typename R, int CAP>
+__global__ void __launch_bounds__(256, 2) sweep_kernel(const __grid_constant__ SweepParamsT<CAP> p) {
   using V = vec2_t<R>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   V* s = reinterpret_cast<V*>(smem_raw);
@@ -78,15 +174,14 @@ __global__ void __launch_bounds__(1024) sweep_kernel(const __grid_constant__ Swe
       V z;
       z.x = (base == 0 && e == 0) ? R(1) : R(0);
       z.y = R(0);
-      s[e] = z;
+      s[swz(e)] = z;
     }
   } else {
     for (uint32_t e = tid; e < n; e += bd)
-      s[e] = st[int64_t(base) + chunkoff[e >> L] + (e & lowmask)];
+      s[swz(e)] = st[int64_t(base) + chunkoff[e >> L] + (e & lowmask)];
   }
   __syncthreads();
 
-  const uint32_t half = n >> 1;
   int i = 0;
   while (i < p.n_ops) {
     const SweepOp& op = p.ops[i];
@@ -98,14 +193,14 @@ __global__ void __launch_bounds__(1024) sweep_kernel(const __grid_constant__ Swe
         bool hit = false;
         for (int k = i; k < j;) {
           const SweepOp& o = p.ops[k];
-          const SweepOp* src = &o;
+          int sel = k;
           int step = 1;
           if (o.slot >= 0) {
-            src = &p.ops[k + int((variant >> o.slot) & 1ull)];
+            sel = k + int((variant >> o.slot) & 1ull);
             step = 2;
           }
           if ((e & o.lmask) == o.lmask && (base & o.omask) == o.omask) {
-            const R qr = R(src->m[0]), qi = R(src->m[1]);
+            const R qr = R(p.ops[sel].m[0]), qi = R(p.ops[sel].m[1]);
             const R nr = pr * qr - pi * qi;
             pi = pr * qi + pi * qr;
             pr = nr;
@@ -113,46 +208,26 @@ __global__ void __launch_bounds__(1024) sweep_kernel(const __grid_constant__ Swe
           }
           k += step;
         }
-        if (hit) s[e] = cmul<R>(s[e], pr, pi);
+        if (hit) {
+          const uint32_t a = swz(e);
+          s[a] = cmul<R>(s[a], pr, pi);
+        }
       }
       __syncthreads();
       i = j;
       continue;
     }
-    // OP_DENSE
-    const SweepOp* src = &op;
-    int step = 1;
-    if (op.slot >= 0) {
-      src = &p.ops[i + int((variant >> op.slot) & 1ull)];
-      step = 2;
-    }
-    if ((base & op.omask) == op.omask) {
-      const R m00r = R(src->m[0]), m00i = R(src->m[1]), m01r = R(src->m[2]), m01i = R(src->m[3]);
-      const R m10r = R(src->m[4]), m10i = R(src->m[5]), m11r = R(src->m[6]), m11i = R(src->m[7]);
-      const int t = op.target;
-      const uint32_t lm = op.lmask;
-      const uint32_t below = (1u << t) - 1u;
-      for (uint32_t k = tid; k < half; k += bd) {
-        const uint32_t e0 = ((k & ~below) << 1) | (k & below);
-        if ((e0 & lm) != lm) continue;
-        const uint32_t e1 = e0 | (1u << t);
-        const V a = s[e0];
-        const V b = s[e1];
-        V u, w;
-        u.x = m00r * a.x - m00i * a.y + m01r * b.x - m01i * b.y;
-        u.y = m00r * a.y + m00i * a.x + m01r * b.y + m01i * b.x;
-        w.x = m10r * a.x - m10i * a.y + m11r * b.x - m11i * b.y;
-        w.y = m10r * a.y + m10i * a.x + m11r * b.y + m11i * b.x;
-        s[e0] = u;
-        s[e1] = w;
-      }
+    switch (op.gsize) {
+      case 4: i = apply_group<R, 4>(s, p, i, base, variant, T, tid, bd); break;
+      case 3: i = apply_group<R, 3>(s, p, i, base, variant, T, tid, bd); break;
+      case 2: i = apply_group<R, 2>(s, p, i, base, variant, T, tid, bd); break;
+      default: i = apply_group<R, 1>(s, p, i, base, variant, T, tid, bd); break;
     }
     __syncthreads();
-    i += step;
   }
 
   for (uint32_t e = tid; e < n; e += bd)
-    st[int64_t(base) + chunkoff[e >> L] + (e & lowmask)] = s[e];
+    st[int64_t(base) + chunkoff[e >> L] + (e & lowmask)] = s[swz(e)];
 }
 
 // ---------------------------------------------------------------------------
@@ -360,20 +435,32 @@ size_t sweep_smem_bytes(int tile_bits, int low_bits, int dtype) {
   return (size_t(1) << tile_bits) * elem + (size_t(1) << (tile_bits - low_bits)) * sizeof(int64_t);
 }
 
-template <typename R>
-static cudaError_t launch_sweep_t(const SweepParams& p, uint32_t n_tiles, uint32_t n_states,
-                                  int threads, cudaStream_t stream) {
-  const size_t smem = sweep_smem_bytes(p.tile_bits, p.low_bits, std::is_same<R, double>::value ? 0 : 1);
+template <typename R, int CAP>
+static cudaError_t launch_sweep_cap(const SweepParamsT<CAP>& p, uint32_t n_tiles, uint32_t n_states, int threads,
+                                    size_t smem, cudaStream_t stream) {
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(sweep_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(sweep_kernel<R, CAP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(smem));
     if (e != cudaSuccess) return e;
     configured = smem;
   }
   dim3 grid(n_tiles, n_states, 1);
-  sweep_kernel<R><<<grid, threads, smem, stream>>>(p);
+  sweep_kernel<R, CAP><<<grid, threads, smem, stream>>>(p);
   return cudaGetLastError();
+}
+
+template <typename R>
+static cudaError_t launch_sweep_t(const SweepParams& p, uint32_t n_tiles, uint32_t n_states, int threads,
+                                  cudaStream_t stream) {
+  const size_t smem = sweep_smem_bytes(p.tile_bits, p.low_bits, std::is_same<R, double>::value ? 0 : 1);
+  if (p.n_ops <= kSmallOps) {
+    static SweepParamsSmall ps;  // launch copies it; callers hold capi's lock
+    std::memcpy(&ps, &p, offsetof(SweepParams, ops));
+    std::memcpy(ps.ops, p.ops, sizeof(SweepOp) * size_t(p.n_ops));
+    return launch_sweep_cap<R, kSmallOps>(ps, n_tiles, n_states, threads, smem, stream);
+  }
+  return launch_sweep_cap<R, kMaxOpsPerLaunch>(p, n_tiles, n_states, threads, smem, stream);
 }
 
 cudaError_t launch_sweep(const SweepParams& p, uint32_t n_tiles, uint32_t n_states, int threads,

@@ -27,15 +27,18 @@ struct SweepOp {
   int16_t target;     // DENSE: tile-local target bit
   uint64_t omask;     // outside-tile qubits that must be 1 for the op to act
   int32_t slot;       // -1, or cut bit choosing this entry (0) / next entry (1)
-  int32_t pad;
+  int32_t gsize;      // DENSE, first op of a register group: ops in the group (1..4)
   double m[8];        // DENSE: m00 m01 m10 m11 as (re,im); PHASE: m[0..1]
 };
 static_assert(sizeof(SweepOp) == 88, "SweepOp layout");
 
 constexpr int kMaxTileBits = 14;
+constexpr int kMaxGroup = 4;           // dense ops applied together in registers
 constexpr int kMaxOpsPerLaunch = 352;  // keeps SweepParams under the 32 KiB param limit
+constexpr int kSmallOps = 40;          // small-program launch (about 4 KiB of params)
 
-struct SweepParams {
+template <int CAP>
+struct SweepParamsT {
   void* states;             // batch of states, state v at states + v * stride
   int64_t stride;           // amplitudes between consecutive states
   uint64_t variant_base;    // variant id of state 0 of this launch
@@ -49,8 +52,10 @@ struct SweepParams {
   int32_t store;            // 0: keep result in smem only (never used), 1: write back
   int8_t hq[kMaxTileBits];
   int8_t oq[64];
-  SweepOp ops[kMaxOpsPerLaunch];
+  SweepOp ops[CAP];
 };
+using SweepParams = SweepParamsT<kMaxOpsPerLaunch>;
+using SweepParamsSmall = SweepParamsT<kSmallOps>;
 static_assert(sizeof(SweepParams) <= 32760, "kernel parameter limit");
 
 // merge_terms: out[s][h - row_begin][l] (+)= sum_t coef[s,t] hi[hidx[s,t]][h] lo[lidx[s,t]][l]

@@ -204,10 +204,11 @@ std::vector<LOp> fuse_ops(const std::vector<LOp>& ops) {
   return out;
 }
 
-static void emit_entries(const LOp& op, const int* local_pos, Sweep& sw) {
+static void emit_entries(const LOp& op, const int* local_pos, Sweep& sw, int gsize) {
   SweepOp e{};
   e.type = op.type;
   e.slot = op.slot;
+  e.gsize = gsize;
   uint64_t mm = op.mask;
   while (mm) {
     const int q = ctz64(mm);
@@ -220,7 +221,33 @@ static void emit_entries(const LOp& op, const int* local_pos, Sweep& sw) {
   sw.entries.push_back(e);
   if (op.slot >= 0) {
     for (int i = 0; i < 8; ++i) e.m[i] = op.alt[i];
+    e.gsize = 0;
     sw.entries.push_back(e);
+  }
+}
+
+// Emit a sweep's ops in order, packing runs of consecutive dense ops with
+// pairwise-disjoint qubits (they commute) into register groups of <= kMaxGroup.
+static void emit_run(const std::vector<LOp>& ops, const std::vector<int>& run, const int* local_pos, Sweep& sw) {
+  size_t a = 0;
+  while (a < run.size()) {
+    const LOp& op = ops[size_t(run[a])];
+    if (op.type != OP_DENSE) {
+      emit_entries(op, local_pos, sw, 0);
+      ++a;
+      continue;
+    }
+    size_t b = a + 1;
+    uint64_t used = qubit_mask(op);
+    while (b < run.size() && int(b - a) < kMaxGroup) {
+      const LOp& o2 = ops[size_t(run[b])];
+      if (o2.type != OP_DENSE || (qubit_mask(o2) & used)) break;
+      used |= qubit_mask(o2);
+      ++b;
+    }
+    for (size_t k = a; k < b; ++k)
+      emit_entries(ops[size_t(run[k])], local_pos, sw, k == a ? int(b - a) : 0);
+    a = b;
   }
 }
 
@@ -232,7 +259,9 @@ std::vector<Sweep> schedule_sweeps(const std::vector<LOp>& ops, int nq, int tile
     sw.low_bits = nq;
     int local_pos[64];
     for (int q = 0; q < 64; ++q) local_pos[q] = q < nq ? q : -1;
-    for (const LOp& op : ops) emit_entries(op, local_pos, sw);
+    std::vector<int> all(ops.size());
+    for (size_t i = 0; i < ops.size(); ++i) all[i] = int(i);
+    emit_run(ops, all, local_pos, sw);
     sweeps.push_back(std::move(sw));
     return sweeps;
   }
@@ -291,7 +320,7 @@ std::vector<Sweep> schedule_sweeps(const std::vector<LOp>& ops, int nq, int tile
     for (int q = 0; q < 64; ++q) local_pos[q] = -1;
     for (int q = 0; q < L; ++q) local_pos[q] = q;
     for (size_t j = 0; j < sw.hq.size(); ++j) local_pos[sw.hq[j]] = L + int(j);
-    for (int idx : run) emit_entries(ops[size_t(idx)], local_pos, sw);
+    emit_run(ops, run, local_pos, sw);
     sweeps.push_back(std::move(sw));
     pending.swap(deferred);
   }
@@ -313,7 +342,8 @@ std::string sweeps_to_json(const std::vector<Sweep>& sweeps, int nq) {
     for (size_t i = 0; i < sw.entries.size(); ++i) {
       const SweepOp& e = sw.entries[i];
       os << (i ? "," : "") << "{\"type\":" << e.type << ",\"target\":" << e.target
-         << ",\"lmask\":" << e.lmask << ",\"omask\":" << e.omask << ",\"slot\":" << e.slot << ",\"m\":[";
+         << ",\"lmask\":" << e.lmask << ",\"omask\":" << e.omask << ",\"slot\":" << e.slot
+         << ",\"gsize\":" << e.gsize << ",\"m\":[";
       for (int k = 0; k < 8; ++k) os << (k ? "," : "") << e.m[k];
       os << "]}";
     }
