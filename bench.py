@@ -281,6 +281,21 @@ def run_ours(args):
             acc["merge"].append(times.merge)
         stage = {k: 1e3 * float(np.median(v)) for k, v in acc.items()}
 
+    # the uncut simulator on the same circuit (the cut-vs-uncut comparison point)
+    uncut_ms = None
+    if world == 1 and not args.no_uncut:
+        cb.simulate(circ)
+        torch.cuda.synchronize()
+        u0 = torch.cuda.Event(enable_timing=True)
+        u1 = torch.cuda.Event(enable_timing=True)
+        u0.record(stream)
+        sv = cb.simulate(circ)
+        u1.record(stream)
+        u1.synchronize()
+        uncut_ms = u0.elapsed_time(u1)
+        del sv
+        torch.cuda.empty_cache()
+
     # roofline of the dominant kernel (merge) from the timed region
     roofline = None
     if merge_ms:
@@ -342,6 +357,7 @@ def run_ours(args):
                        "parallelism": f"output-shard{world}",
                        "l2": "no flush: each step writes the 16 GiB output (>> 126 MB L2)"},
             "stage_ms": stage,
+            "uncut_ms": uncut_ms,
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -366,6 +382,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-uncut", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -57,7 +57,8 @@ def empty(n_states: int, nq: int, dtype=np.complex128, check_memory=True):
     """Uninitialised device batch [n_states, 2^nq]."""
     t = require_cuda()
     nbytes = n_states * (1 << nq) * np.dtype(dtype).itemsize
-    if check_memory:
+    # cudaMemGetInfo costs ~0.5 ms per call: only consult it for big states
+    if check_memory and nbytes >= (1 << 30):
         free, _total = t.cuda.mem_get_info()
         cached = t.cuda.memory_reserved() - t.cuda.memory_allocated()
         if nbytes > free + cached:

@@ -139,7 +139,7 @@ std::shared_ptr<const std::vector<Sweep>> build_schedule(int nq, const uint8_t* 
   }
   std::vector<LOp> ops = lower_gates(nq, kinds, qa, qb, params, slots, n_gates);
   if (g_opt.fuse) ops = fuse_ops(ops);
-  auto prog = std::make_shared<const std::vector<Sweep>>(schedule_sweeps(ops, nq, T, L));
+  auto prog = std::make_shared<const std::vector<Sweep>>(schedule_sweeps(ops, nq, T, L, sweep_max_group(T)));
   std::lock_guard<std::mutex> lk(g_cache_mu);
   if (g_cache.size() >= 256) g_cache.clear();
   g_cache.emplace(std::move(key), prog);
@@ -379,7 +379,7 @@ int cs_sim_batch(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int6
       p.store = 1;
       p.stride = state_stride;
       int threads = int(g_opt.threads);
-      if (threads == 0) threads = std::max(32, std::min(256, 1 << std::max(0, T - 2)));
+      if (threads == 0) threads = sweep_threads(T);
       threads = std::min(threads, 256);
       for (int64_t v0 = 0; v0 < n_states; v0 += 65535) {
         const int64_t vc = std::min<int64_t>(65535, n_states - v0);

@@ -228,7 +228,8 @@ static void emit_entries(const LOp& op, const int* local_pos, Sweep& sw, int gsi
 
 // Emit a sweep's ops in order, packing runs of consecutive dense ops with
 // pairwise-disjoint qubits (they commute) into register groups of <= kMaxGroup.
-static void emit_run(const std::vector<LOp>& ops, const std::vector<int>& run, const int* local_pos, Sweep& sw) {
+static void emit_run(const std::vector<LOp>& ops, const std::vector<int>& run, const int* local_pos, Sweep& sw,
+                     int max_group) {
   size_t a = 0;
   while (a < run.size()) {
     const LOp& op = ops[size_t(run[a])];
@@ -239,7 +240,7 @@ static void emit_run(const std::vector<LOp>& ops, const std::vector<int>& run, c
     }
     size_t b = a + 1;
     uint64_t used = qubit_mask(op);
-    while (b < run.size() && int(b - a) < kMaxGroup) {
+    while (b < run.size() && int(b - a) < max_group) {
       const LOp& o2 = ops[size_t(run[b])];
       if (o2.type != OP_DENSE || (qubit_mask(o2) & used)) break;
       used |= qubit_mask(o2);
@@ -251,7 +252,16 @@ static void emit_run(const std::vector<LOp>& ops, const std::vector<int>& run, c
   }
 }
 
-std::vector<Sweep> schedule_sweeps(const std::vector<LOp>& ops, int nq, int tile_bits, int low_bits) {
+int sweep_threads(int tile_bits) { return std::max(32, std::min(256, 1 << std::max(0, tile_bits - 2))); }
+
+int sweep_max_group(int tile_bits) {
+  int lg = 0;
+  while ((1 << lg) < sweep_threads(tile_bits)) ++lg;
+  return std::max(1, std::min(kMaxGroup, tile_bits - lg));
+}
+
+std::vector<Sweep> schedule_sweeps(const std::vector<LOp>& ops, int nq, int tile_bits, int low_bits,
+                                   int max_group) {
   std::vector<Sweep> sweeps;
   if (nq <= tile_bits) {
     Sweep sw;
@@ -261,7 +271,7 @@ std::vector<Sweep> schedule_sweeps(const std::vector<LOp>& ops, int nq, int tile
     for (int q = 0; q < 64; ++q) local_pos[q] = q < nq ? q : -1;
     std::vector<int> all(ops.size());
     for (size_t i = 0; i < ops.size(); ++i) all[i] = int(i);
-    emit_run(ops, all, local_pos, sw);
+    emit_run(ops, all, local_pos, sw, max_group);
     sweeps.push_back(std::move(sw));
     return sweeps;
   }
@@ -320,7 +330,7 @@ std::vector<Sweep> schedule_sweeps(const std::vector<LOp>& ops, int nq, int tile
     for (int q = 0; q < 64; ++q) local_pos[q] = -1;
     for (int q = 0; q < L; ++q) local_pos[q] = q;
     for (size_t j = 0; j < sw.hq.size(); ++j) local_pos[sw.hq[j]] = L + int(j);
-    emit_run(ops, run, local_pos, sw);
+    emit_run(ops, run, local_pos, sw, max_group);
     sweeps.push_back(std::move(sw));
     pending.swap(deferred);
   }

@@ -44,7 +44,13 @@ struct Sweep {
 // Greedy tiling: every sweep holds the low qubits [0, L) plus up to T - L
 // more qubits chosen in order of first need; it absorbs every op whose
 // non-diagonal target is in the tile and that commutes with all deferred ops.
-std::vector<Sweep> schedule_sweeps(const std::vector<LOp>& ops, int nq, int tile_bits, int low_bits);
+std::vector<Sweep> schedule_sweeps(const std::vector<LOp>& ops, int nq, int tile_bits, int low_bits,
+                                  int max_group = kMaxGroup);
+
+// Threads per CTA of the sweep kernel for a tile of 2^T amplitudes, and the
+// largest register group that still gives every thread a cell.
+int sweep_threads(int tile_bits);
+int sweep_max_group(int tile_bits);
 
 std::string sweeps_to_json(const std::vector<Sweep>& sweeps, int nq);
 

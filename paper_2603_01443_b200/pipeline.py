@@ -53,8 +53,42 @@ def preprocess(circuit: Circuit, n: int) -> Prepared:
 
 
 def simulate_segments(prep: Prepared, *, dtype=np.complex128, max_qubits=DEFAULT_MAX_QUBITS):
-    """Device batches [2^{c_i}, 2^{q_i}] of every segment's variants (t_sub)."""
-    return [simulate_family(f, dtype=dtype, max_qubits=max_qubits) for f in prep.subs.segments]
+    """Device batches [2^{c_i}, 2^{q_i}] of every segment's variants (t_sub).
+
+    Segments are independent, so each family runs on its own side stream
+    (forked from and joined back into the current stream): the short,
+    latency-bound sweep chains of different segments overlap on the GPU."""
+    fams = prep.subs.segments
+    if len(fams) == 1:
+        return [simulate_family(fams[0], dtype=dtype, max_qubits=max_qubits)]
+    t = _device.torch()
+    main = t.cuda.current_stream()
+    fork = t.cuda.Event()
+    fork.record(main)
+    outs, joins = [], []
+    for j, fam in enumerate(fams):
+        s = _side_stream(j)
+        s.wait_event(fork)
+        with t.cuda.stream(s):
+            outs.append(simulate_family(fam, dtype=dtype, max_qubits=max_qubits))
+            ev = t.cuda.Event()
+            ev.record(s)
+        joins.append(ev)
+    for ev, o in zip(joins, outs):
+        main.wait_event(ev)
+        o.record_stream(main)
+    return outs
+
+
+_SIDE_STREAMS: dict = {}
+
+
+def _side_stream(j: int):
+    t = _device.torch()
+    key = (t.cuda.current_device(), j % 4)
+    if key not in _SIDE_STREAMS:
+        _SIDE_STREAMS[key] = t.cuda.Stream()
+    return _SIDE_STREAMS[key]
 
 
 def run_cut(circuit: Circuit, n: int, *, dtype=np.complex128, max_qubits: int = DEFAULT_MAX_QUBITS,
