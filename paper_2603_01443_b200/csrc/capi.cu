@@ -125,7 +125,7 @@ std::shared_ptr<const std::vector<Sweep>> build_schedule(int nq, const uint8_t* 
   const int L = (T == nq) ? nq : std::max(3, std::min(int(g_opt.low_bits), T - 6));
   std::string key;
   key.reserve(size_t(n_gates) * 45 + 32);
-  const int32_t hdr[5] = {nq, T, L, int32_t(g_opt.fuse), slots ? 1 : 0};
+  const int32_t hdr[6] = {nq, T, L, int32_t(g_opt.fuse), slots ? 1 : 0, dtype};
   key.append(reinterpret_cast<const char*>(hdr), sizeof(hdr));
   key.append(reinterpret_cast<const char*>(kinds), size_t(n_gates));
   key.append(reinterpret_cast<const char*>(qa), size_t(n_gates) * 8);
@@ -139,7 +139,9 @@ std::shared_ptr<const std::vector<Sweep>> build_schedule(int nq, const uint8_t* 
   }
   std::vector<LOp> ops = lower_gates(nq, kinds, qa, qb, params, slots, n_gates);
   if (g_opt.fuse) ops = fuse_ops(ops);
-  auto prog = std::make_shared<const std::vector<Sweep>>(schedule_sweeps(ops, nq, T, L, sweep_max_group(T)));
+  // complex128 groups stop at 3 ops (8 complex registers) to keep 2 CTAs/SM
+  const int max_group = std::min(sweep_max_group(T), dtype == CS_C128 ? 3 : kMaxGroup);
+  auto prog = std::make_shared<const std::vector<Sweep>>(schedule_sweeps(ops, nq, T, L, max_group));
   std::lock_guard<std::mutex> lk(g_cache_mu);
   if (g_cache.size() >= 256) g_cache.clear();
   g_cache.emplace(std::move(key), prog);

@@ -138,6 +138,59 @@ __device__ __forceinline__ int apply_group(vec2_t<R>* s, const P& p, int i0, uin
   return j;
 }
 
+// A run of diagonal ops [i0, i1): each thread keeps a chunk of its elements
+// in registers, walks the ops once (uniform loads, tile-constant outside-mask
+// test hoisted), multiplies matching elements (a sign flip for CZ-type -1
+// phases), and stores once — no per-element re-scan of the op list.
+template <typename R, class P>
+__device__ __forceinline__ void apply_phase_run(vec2_t<R>* s, const P& p, int i0, int i1, uint64_t base,
+                                                uint64_t variant, uint32_t n, uint32_t tid, uint32_t bd) {
+  using V = vec2_t<R>;
+  constexpr int CH = 8;
+  for (uint32_t e0 = tid; e0 < n; e0 += bd * CH) {
+    V v[CH];
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      const uint32_t e = e0 + uint32_t(c) * bd;
+      if (e < n) v[c] = s[swz(e)];
+    }
+    for (int k = i0; k < i1;) {
+      const SweepOp& o = p.ops[k];
+      int sel = k;
+      int step = 1;
+      if (o.slot >= 0) {
+        sel = k + int((variant >> o.slot) & 1ull);
+        step = 2;
+      }
+      k += step;
+      if ((base & o.omask) != o.omask) continue;
+      const uint32_t lm = o.lmask;
+      const double qr = p.ops[sel].m[0], qi = p.ops[sel].m[1];
+      if (qi == 0.0 && qr == -1.0) {
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+          const uint32_t e = e0 + uint32_t(c) * bd;
+          if ((e & lm) == lm) {
+            v[c].x = -v[c].x;
+            v[c].y = -v[c].y;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+          const uint32_t e = e0 + uint32_t(c) * bd;
+          if ((e & lm) == lm) v[c] = cmul<R>(v[c], R(qr), R(qi));
+        }
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      const uint32_t e = e0 + uint32_t(c) * bd;
+      if (e < n) s[swz(e)] = v[c];
+    }
+  }
+}
+
 template <typename R, int CAP>
 __global__ void __launch_bounds__(256, 2) sweep_kernel(const __grid_constant__ SweepParamsT<CAP> p) {
   using V = vec2_t<R>;
@@ -188,37 +241,23 @@ __global__ void __launch_bounds__(256, 2) sweep_kernel(const __grid_constant__ S
     if (op.type == OP_PHASE) {
       int j = i;
       while (j < p.n_ops && p.ops[j].type == OP_PHASE) j += (p.ops[j].slot >= 0) ? 2 : 1;
-      for (uint32_t e = tid; e < n; e += bd) {
-        R pr = R(1), pi = R(0);
-        bool hit = false;
-        for (int k = i; k < j;) {
-          const SweepOp& o = p.ops[k];
-          int sel = k;
-          int step = 1;
-          if (o.slot >= 0) {
-            sel = k + int((variant >> o.slot) & 1ull);
-            step = 2;
-          }
-          if ((e & o.lmask) == o.lmask && (base & o.omask) == o.omask) {
-            const R qr = R(p.ops[sel].m[0]), qi = R(p.ops[sel].m[1]);
-            const R nr = pr * qr - pi * qi;
-            pi = pr * qi + pi * qr;
-            pr = nr;
-            hit = true;
-          }
-          k += step;
-        }
-        if (hit) {
-          const uint32_t a = swz(e);
-          s[a] = cmul<R>(s[a], pr, pi);
-        }
-      }
+      apply_phase_run<R>(s, p, i, j, base, variant, n, tid, bd);
       __syncthreads();
       i = j;
       continue;
     }
     switch (op.gsize) {
-      case 4: i = apply_group<R, 4>(s, p, i, base, variant, T, tid, bd); break;
+      case 4:
+        // double: 16 complex registers + matrices exceed the 128-register
+        // budget of 2 CTAs/SM, so a group of 4 runs as 3 + 1
+        if (std::is_same<R, double>::value) {
+          i = apply_group<R, 3>(s, p, i, base, variant, T, tid, bd);
+          __syncthreads();
+          i = apply_group<R, 1>(s, p, i, base, variant, T, tid, bd);
+        } else {
+          i = apply_group<R, 4>(s, p, i, base, variant, T, tid, bd);
+        }
+        break;
       case 3: i = apply_group<R, 3>(s, p, i, base, variant, T, tid, bd); break;
       case 2: i = apply_group<R, 2>(s, p, i, base, variant, T, tid, bd); break;
       default: i = apply_group<R, 1>(s, p, i, base, variant, T, tid, bd); break;
