@@ -16,7 +16,7 @@
 #include "plan.hpp"
 
 namespace cutsim {
-size_t sweep_smem_bytes(int tile_bits, int low_bits, int dtype);
+size_t sweep_smem_bytes(int tile_bits, int low_bits, int dtype, int n_ops);
 cudaError_t launch_sweep(const SweepParams& p, uint32_t n_tiles, uint32_t n_states, int threads,
                          cudaStream_t stream, int dtype);
 cudaError_t launch_merge(const MergeParams& p, int K, dim3 grid, int threads, size_t smem, bool wide,

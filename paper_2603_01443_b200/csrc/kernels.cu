@@ -57,9 +57,9 @@ __device__ __forceinline__ uint32_t swz(uint32_t e) {
   return e ^ (x & 7u);
 }
 
-template <typename R, int K, class P>
-__device__ __forceinline__ int apply_group(vec2_t<R>* s, const P& p, int i0, uint64_t base, uint64_t variant,
-                                           int T, uint32_t tid, uint32_t bd) {
+template <typename R, int K>
+__device__ __forceinline__ int apply_group(vec2_t<R>* s, const SweepOp* ops, int i0, uint64_t base,
+                                           uint64_t variant, int T, uint32_t tid, uint32_t bd) {
   using V = vec2_t<R>;
   int tgt[K];
   uint32_t lm[K];
@@ -68,7 +68,7 @@ __device__ __forceinline__ int apply_group(vec2_t<R>* s, const P& p, int i0, uin
   int j = i0;
 #pragma unroll
   for (int g = 0; g < K; ++g) {
-    const SweepOp& o = p.ops[j];
+    const SweepOp& o = ops[j];
     int step = 1;
     src[g] = j;
     if (o.slot >= 0) {
@@ -115,7 +115,7 @@ __device__ __forceinline__ int apply_group(vec2_t<R>* s, const P& p, int i0, uin
 #pragma unroll
     for (int g = 0; g < K; ++g) {
       if (!act[g] || (e & lm[g]) != lm[g]) continue;
-      const double* m = p.ops[src[g]].m;
+      const double* m = ops[src[g]].m;
       const R m00r = R(m[0]), m00i = R(m[1]), m01r = R(m[2]), m01i = R(m[3]);
       const R m10r = R(m[4]), m10i = R(m[5]), m11r = R(m[6]), m11i = R(m[7]);
 #pragma unroll
@@ -142,8 +142,8 @@ __device__ __forceinline__ int apply_group(vec2_t<R>* s, const P& p, int i0, uin
 // in registers, walks the ops once (uniform loads, tile-constant outside-mask
 // test hoisted), multiplies matching elements (a sign flip for CZ-type -1
 // phases), and stores once — no per-element re-scan of the op list.
-template <typename R, class P>
-__device__ __forceinline__ void apply_phase_run(vec2_t<R>* s, const P& p, int i0, int i1, uint64_t base,
+template <typename R>
+__device__ __forceinline__ void apply_phase_run(vec2_t<R>* s, const SweepOp* ops, int i0, int i1, uint64_t base,
                                                 uint64_t variant, uint32_t n, uint32_t tid, uint32_t bd) {
   using V = vec2_t<R>;
   constexpr int CH = 8;
@@ -155,7 +155,7 @@ __device__ __forceinline__ void apply_phase_run(vec2_t<R>* s, const P& p, int i0
       if (e < n) v[c] = s[swz(e)];
     }
     for (int k = i0; k < i1;) {
-      const SweepOp& o = p.ops[k];
+      const SweepOp& o = ops[k];
       int sel = k;
       int step = 1;
       if (o.slot >= 0) {
@@ -165,7 +165,7 @@ __device__ __forceinline__ void apply_phase_run(vec2_t<R>* s, const P& p, int i0
       k += step;
       if ((base & o.omask) != o.omask) continue;
       const uint32_t lm = o.lmask;
-      const double qr = p.ops[sel].m[0], qi = p.ops[sel].m[1];
+      const double qr = ops[sel].m[0], qi = ops[sel].m[1];
       if (qi == 0.0 && qr == -1.0) {
 #pragma unroll
         for (int c = 0; c < CH; ++c) {
@@ -202,8 +202,19 @@ __global__ void __launch_bounds__(256, 2) sweep_kernel(const __grid_constant__ S
   const uint32_t nchunks = 1u << (T - L);
   const uint32_t lowmask = (1u << L) - 1u;
   int64_t* chunkoff = reinterpret_cast<int64_t*>(smem_raw + sizeof(V) * size_t(n));
+  SweepOp* ops = reinterpret_cast<SweepOp*>(smem_raw + sizeof(V) * size_t(n) + sizeof(int64_t) * size_t(nchunks));
   const uint32_t tid = threadIdx.x;
   const uint32_t bd = blockDim.x;
+  const int n_ops = p.n_ops;
+
+  // stage the op list in shared memory once: per-op reads from the 31 KiB
+  // parameter bank would miss the constant cache at every step
+  {
+    const uint64_t* src = reinterpret_cast<const uint64_t*>(&p.ops[0]);
+    uint64_t* dst = reinterpret_cast<uint64_t*>(ops);
+    const uint32_t words = uint32_t(n_ops) * uint32_t(sizeof(SweepOp) / 8);
+    for (uint32_t w = tid; w < words; w += bd) dst[w] = src[w];
+  }
 
   uint64_t base = 0;
   {
@@ -236,12 +247,12 @@ __global__ void __launch_bounds__(256, 2) sweep_kernel(const __grid_constant__ S
   __syncthreads();
 
   int i = 0;
-  while (i < p.n_ops) {
-    const SweepOp& op = p.ops[i];
+  while (i < n_ops) {
+    const SweepOp& op = ops[i];
     if (op.type == OP_PHASE) {
       int j = i;
-      while (j < p.n_ops && p.ops[j].type == OP_PHASE) j += (p.ops[j].slot >= 0) ? 2 : 1;
-      apply_phase_run<R>(s, p, i, j, base, variant, n, tid, bd);
+      while (j < n_ops && ops[j].type == OP_PHASE) j += (ops[j].slot >= 0) ? 2 : 1;
+      apply_phase_run<R>(s, ops, i, j, base, variant, n, tid, bd);
       __syncthreads();
       i = j;
       continue;
@@ -251,16 +262,16 @@ __global__ void __launch_bounds__(256, 2) sweep_kernel(const __grid_constant__ S
         // double: 16 complex registers + matrices exceed the 128-register
         // budget of 2 CTAs/SM, so a group of 4 runs as 3 + 1
         if (std::is_same<R, double>::value) {
-          i = apply_group<R, 3>(s, p, i, base, variant, T, tid, bd);
+          i = apply_group<R, 3>(s, ops, i, base, variant, T, tid, bd);
           __syncthreads();
-          i = apply_group<R, 1>(s, p, i, base, variant, T, tid, bd);
+          i = apply_group<R, 1>(s, ops, i, base, variant, T, tid, bd);
         } else {
-          i = apply_group<R, 4>(s, p, i, base, variant, T, tid, bd);
+          i = apply_group<R, 4>(s, ops, i, base, variant, T, tid, bd);
         }
         break;
-      case 3: i = apply_group<R, 3>(s, p, i, base, variant, T, tid, bd); break;
-      case 2: i = apply_group<R, 2>(s, p, i, base, variant, T, tid, bd); break;
-      default: i = apply_group<R, 1>(s, p, i, base, variant, T, tid, bd); break;
+      case 3: i = apply_group<R, 3>(s, ops, i, base, variant, T, tid, bd); break;
+      case 2: i = apply_group<R, 2>(s, ops, i, base, variant, T, tid, bd); break;
+      default: i = apply_group<R, 1>(s, ops, i, base, variant, T, tid, bd); break;
     }
     __syncthreads();
   }
@@ -469,9 +480,10 @@ __global__ void gather_kernel(const vec2_t<R>* state, const int64_t* idx, int64_
 // ---------------------------------------------------------------------------
 // launchers (host)
 // ---------------------------------------------------------------------------
-size_t sweep_smem_bytes(int tile_bits, int low_bits, int dtype) {
+size_t sweep_smem_bytes(int tile_bits, int low_bits, int dtype, int n_ops) {
   const size_t elem = dtype == 0 ? sizeof(double2) : sizeof(float2);
-  return (size_t(1) << tile_bits) * elem + (size_t(1) << (tile_bits - low_bits)) * sizeof(int64_t);
+  return (size_t(1) << tile_bits) * elem + (size_t(1) << (tile_bits - low_bits)) * sizeof(int64_t) +
+         size_t(n_ops) * sizeof(SweepOp);
 }
 
 template <typename R, int CAP>
@@ -492,7 +504,7 @@ static cudaError_t launch_sweep_cap(const SweepParamsT<CAP>& p, uint32_t n_tiles
 template <typename R>
 static cudaError_t launch_sweep_t(const SweepParams& p, uint32_t n_tiles, uint32_t n_states, int threads,
                                   cudaStream_t stream) {
-  const size_t smem = sweep_smem_bytes(p.tile_bits, p.low_bits, std::is_same<R, double>::value ? 0 : 1);
+  const size_t smem = sweep_smem_bytes(p.tile_bits, p.low_bits, std::is_same<R, double>::value ? 0 : 1, p.n_ops);
   if (p.n_ops <= kSmallOps) {
     static SweepParamsSmall ps;  // launch copies it; callers hold capi's lock
     std::memcpy(&ps, &p, offsetof(SweepParams, ops));
