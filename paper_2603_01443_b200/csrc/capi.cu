@@ -16,9 +16,9 @@
 #include "plan.hpp"
 
 namespace cutsim {
-size_t sweep_smem_bytes(int tile_bits, int low_bits, int dtype, int n_ops);
-cudaError_t launch_sweep(const SweepParams& p, uint32_t n_tiles, uint32_t n_states, int threads,
-                         cudaStream_t stream, int dtype);
+size_t sweep_smem_bytes(int tile_bits, int low_bits, int dtype, int n_ops, int vb);
+cudaError_t launch_sweep(const SweepParams& p, uint32_t n_tiles, int vb, int threads, cudaStream_t stream,
+                         int dtype);
 cudaError_t launch_merge(const MergeParams& p, int K, dim3 grid, int threads, size_t smem, bool wide,
                          cudaStream_t stream, int dtype);
 int merge_cols_per_thread(int K);
@@ -47,6 +47,7 @@ struct Options {
   int64_t threads = 0;
   int64_t merge_streaming = 1;
   int64_t merge_iters = 0;
+  int64_t vb = 0;  // states per CTA in a variant batch (0 = auto)
 } g_opt;
 std::mutex g_opt_mu;
 
@@ -63,8 +64,6 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 inline size_t elem_bytes(int dtype) { return dtype == CS_C128 ? 16 : 8; }
 
 bool valid_dtype(int dtype) { return dtype == CS_C128 || dtype == CS_C64; }
-
-int single_tile_max(int dtype) { return dtype == CS_C128 ? 13 : 14; }
 
 int multi_tile_bits(int dtype) {
   if (g_opt.tile_bits > 0) return int(g_opt.tile_bits);
@@ -97,18 +96,38 @@ double2* reduce_scratch(int* err) {
   return g_scratch.per_device[size_t(dev)];
 }
 
+int choose_vb(int64_t n_states) {
+  if (g_opt.vb > 0) return int(std::min<int64_t>(g_opt.vb, 4));
+  // measured (tools/tune_sub.py): 2 states per CTA beats 1 and 4 for cut variants
+  return n_states >= 2 ? 2 : 1;
+}
+
+int group_budget(int vb, int dtype) {
+  const int values = (dtype == CS_C128 ? 8 : 16) / vb;
+  return values >= 16 ? 4 : values >= 8 ? 3 : values >= 4 ? 2 : 1;
+}
+
+int single_tile_max_vb(int dtype, int vb) {
+  // the tile of vb states must fit shared memory next to the op list
+  int t = dtype == CS_C128 ? 13 : 14;
+  while (t > 6 && ((size_t(1) << t) * (dtype == CS_C128 ? 16 : 8) * size_t(vb)) > size_t(128 * 1024)) --t;
+  return t;
+}
+
 int choose_tile_bits(int nq, int64_t n_states, int tile_bits, int dtype) {
-  if (nq <= single_tile_max(dtype)) return nq;
+  const int vb = choose_vb(n_states);
+  if (nq <= single_tile_max_vb(dtype, vb)) return nq;
   if (tile_bits > 0) return std::min(tile_bits, nq);
   if (g_opt.tile_bits > 0) return std::min(int(g_opt.tile_bits), nq);
   const int dflt = multi_tile_bits(dtype);
   if (n_states > 1) {
     // small batches of mid-size states (cut variants): shrink the tile until
-    // the grid covers the chip twice (the states are L2-resident anyway)
-    const int64_t want = (2 * 148 + n_states - 1) / n_states;
+    // the grid covers the chip (the states are L2-resident anyway)
+    const int64_t groups = (n_states + vb - 1) / vb;
+    const int64_t want = (148 + groups - 1) / groups;
     int lg = 0;
     while ((int64_t(1) << lg) < want) ++lg;
-    return std::max(9, std::min(dflt, nq - lg));
+    return std::max(9, std::min(std::min(dflt, single_tile_max_vb(dtype, vb)), nq - lg));
   }
   return dflt;
 }
@@ -123,9 +142,10 @@ std::shared_ptr<const std::vector<Sweep>> build_schedule(int nq, const uint8_t* 
                                                          int tile_bits, int dtype) {
   const int T = choose_tile_bits(nq, n_states, tile_bits, dtype);
   const int L = (T == nq) ? nq : std::max(3, std::min(int(g_opt.low_bits), T - 6));
+  const int vb = choose_vb(n_states);
   std::string key;
   key.reserve(size_t(n_gates) * 45 + 32);
-  const int32_t hdr[6] = {nq, T, L, int32_t(g_opt.fuse), slots ? 1 : 0, dtype};
+  const int32_t hdr[7] = {nq, T, L, int32_t(g_opt.fuse), slots ? 1 : 0, dtype, vb};
   key.append(reinterpret_cast<const char*>(hdr), sizeof(hdr));
   key.append(reinterpret_cast<const char*>(kinds), size_t(n_gates));
   key.append(reinterpret_cast<const char*>(qa), size_t(n_gates) * 8);
@@ -139,8 +159,8 @@ std::shared_ptr<const std::vector<Sweep>> build_schedule(int nq, const uint8_t* 
   }
   std::vector<LOp> ops = lower_gates(nq, kinds, qa, qb, params, slots, n_gates);
   if (g_opt.fuse) ops = fuse_ops(ops);
-  // complex128 groups stop at 3 ops (8 complex registers) to keep 2 CTAs/SM
-  const int max_group = std::min(sweep_max_group(T), dtype == CS_C128 ? 3 : kMaxGroup);
+  // register groups hold 2^k x vb complex values: 8 (c128) / 16 (c64) per thread
+  const int max_group = std::min(sweep_max_group(T), group_budget(vb, dtype));
   auto prog = std::make_shared<const std::vector<Sweep>>(schedule_sweeps(ops, nq, T, L, max_group));
   std::lock_guard<std::mutex> lk(g_cache_mu);
   if (g_cache.size() >= 256) g_cache.clear();
@@ -300,6 +320,9 @@ int cs_set_option(const char* key, int64_t value) {
   } else if (k == "merge_iters") {
     if (value < 0 || value > 4096) return fail(CS_ERR_INVALID, "merge_iters out of range");
     g_opt.merge_iters = value;
+  } else if (k == "vb") {
+    if (value < 0 || value > 4 || value == 3) return fail(CS_ERR_INVALID, "vb must be 0, 1, 2 or 4");
+    g_opt.vb = value;
   } else {
     return fail(CS_ERR_INVALID, "unknown option '" + k + "'");
   }
@@ -314,6 +337,7 @@ int64_t cs_get_option(const char* key) {
   if (k == "threads") return g_opt.threads;
   if (k == "merge_streaming") return g_opt.merge_streaming;
   if (k == "merge_iters") return g_opt.merge_iters;
+  if (k == "vb") return g_opt.vb;
   return -1;
 }
 
@@ -378,7 +402,6 @@ int cs_sim_batch(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int6
       p.n_ops = int32_t(i1 - i0);
       if (i1 > i0) std::memcpy(p.ops, sw.entries.data() + i0, sizeof(SweepOp) * (i1 - i0));
       p.init_basis = (first && init_zero) ? 1 : 0;
-      p.store = 1;
       p.stride = state_stride;
       int threads = int(g_opt.threads);
       if (threads == 0) threads = sweep_threads(T);
@@ -387,7 +410,8 @@ int cs_sim_batch(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int6
         const int64_t vc = std::min<int64_t>(65535, n_states - v0);
         p.states = static_cast<char*>(states) + size_t(v0) * size_t(state_stride) * elem_bytes(dtype);
         p.variant_base = variant_base + uint64_t(v0);
-        cudaError_t e = launch_sweep(p, n_tiles, uint32_t(vc), threads, st, dtype);
+        p.n_states = int32_t(vc);
+        cudaError_t e = launch_sweep(p, n_tiles, choose_vb(n_states), threads, st, dtype);
         g_launches.fetch_add(1);
         if (e != cudaSuccess) return cuda_fail(e, "sweep_kernel launch");
       }

@@ -57,28 +57,40 @@ __device__ __forceinline__ uint32_t swz(uint32_t e) {
   return e ^ (x & 7u);
 }
 
-template <typename R, int K>
+template <typename R>
+__device__ __forceinline__ void apply2x2(vec2_t<R>& a, vec2_t<R>& b, const double* m) {
+  const R m00r = R(m[0]), m00i = R(m[1]), m01r = R(m[2]), m01i = R(m[3]);
+  const R m10r = R(m[4]), m10i = R(m[5]), m11r = R(m[6]), m11i = R(m[7]);
+  vec2_t<R> u, w;
+  u.x = m00r * a.x - m00i * a.y + m01r * b.x - m01i * b.y;
+  u.y = m00r * a.y + m00i * a.x + m01r * b.y + m01i * b.x;
+  w.x = m10r * a.x - m10i * a.y + m11r * b.x - m11i * b.y;
+  w.y = m10r * a.y + m10i * a.x + m11r * b.y + m11i * b.x;
+  a = u;
+  b = w;
+}
+
+// One register group of K commuting dense ops for the VB states this CTA
+// holds (shared memory layout: element e of state b at swz(e) * VB + b).
+template <typename R, int K, int VB>
 __device__ __forceinline__ int apply_group(vec2_t<R>* s, const SweepOp* ops, int i0, uint64_t base,
-                                           uint64_t variant, int T, uint32_t tid, uint32_t bd) {
+                                           uint64_t variant0, int T, uint32_t tid, uint32_t bd) {
   using V = vec2_t<R>;
   int tgt[K];
   uint32_t lm[K];
   bool act[K];
-  int src[K];
+  int first[K];
+  int slot[K];
   int j = i0;
 #pragma unroll
   for (int g = 0; g < K; ++g) {
     const SweepOp& o = ops[j];
-    int step = 1;
-    src[g] = j;
-    if (o.slot >= 0) {
-      src[g] = j + int((variant >> o.slot) & 1ull);
-      step = 2;
-    }
+    first[g] = j;
+    slot[g] = o.slot;
     tgt[g] = o.target;
     lm[g] = o.lmask;
     act[g] = (base & o.omask) == o.omask;
-    j += step;
+    j += (o.slot >= 0) ? 2 : 1;
   }
   int srt[K];
 #pragma unroll
@@ -109,89 +121,122 @@ __device__ __forceinline__ int apply_group(vec2_t<R>* s, const SweepOp* ops, int
       const uint32_t b = (1u << srt[g]) - 1u;
       e = ((e & ~b) << 1) | (e & b);
     }
-    V v[1 << K];
+    V v[1 << K][VB];
 #pragma unroll
-    for (int i = 0; i < (1 << K); ++i) v[i] = s[swz(e | off[i])];
+    for (int i = 0; i < (1 << K); ++i) {
+      const uint32_t a = swz(e | off[i]) * VB;
+#pragma unroll
+      for (int b = 0; b < VB; ++b) v[i][b] = s[a + b];
+    }
 #pragma unroll
     for (int g = 0; g < K; ++g) {
       if (!act[g] || (e & lm[g]) != lm[g]) continue;
-      const double* m = ops[src[g]].m;
-      const R m00r = R(m[0]), m00i = R(m[1]), m01r = R(m[2]), m01i = R(m[3]);
-      const R m10r = R(m[4]), m10i = R(m[5]), m11r = R(m[6]), m11i = R(m[7]);
+      if (slot[g] < 0) {
+        const double* m = ops[first[g]].m;
 #pragma unroll
-      for (int i = 0; i < (1 << K); ++i) {
-        if ((i >> g) & 1) continue;
-        const V a = v[i];
-        const V b = v[i | (1 << g)];
-        V u, w;
-        u.x = m00r * a.x - m00i * a.y + m01r * b.x - m01i * b.y;
-        u.y = m00r * a.y + m00i * a.x + m01r * b.y + m01i * b.x;
-        w.x = m10r * a.x - m10i * a.y + m11r * b.x - m11i * b.y;
-        w.y = m10r * a.y + m10i * a.x + m11r * b.y + m11i * b.x;
-        v[i] = u;
-        v[i | (1 << g)] = w;
+        for (int i = 0; i < (1 << K); ++i) {
+          if ((i >> g) & 1) continue;
+#pragma unroll
+          for (int b = 0; b < VB; ++b) apply2x2<R>(v[i][b], v[i | (1 << g)][b], m);
+        }
+      } else {
+#pragma unroll
+        for (int b = 0; b < VB; ++b) {
+          const double* m = ops[first[g] + int(((variant0 + b) >> slot[g]) & 1ull)].m;
+#pragma unroll
+          for (int i = 0; i < (1 << K); ++i) {
+            if ((i >> g) & 1) continue;
+            apply2x2<R>(v[i][b], v[i | (1 << g)][b], m);
+          }
+        }
       }
     }
 #pragma unroll
-    for (int i = 0; i < (1 << K); ++i) s[swz(e | off[i])] = v[i];
+    for (int i = 0; i < (1 << K); ++i) {
+      const uint32_t a = swz(e | off[i]) * VB;
+#pragma unroll
+      for (int b = 0; b < VB; ++b) s[a + b] = v[i][b];
+    }
   }
   return j;
 }
 
 // A run of diagonal ops [i0, i1): each thread keeps a chunk of its elements
-// in registers, walks the ops once (uniform loads, tile-constant outside-mask
-// test hoisted), multiplies matching elements (a sign flip for CZ-type -1
-// phases), and stores once — no per-element re-scan of the op list.
-template <typename R>
+// (all VB states) in registers, walks the ops once (uniform loads, the
+// tile-constant outside-mask test hoisted), multiplies matching elements (a
+// sign flip for CZ-type -1 phases), and stores once.
+template <typename R, int VB>
 __device__ __forceinline__ void apply_phase_run(vec2_t<R>* s, const SweepOp* ops, int i0, int i1, uint64_t base,
-                                                uint64_t variant, uint32_t n, uint32_t tid, uint32_t bd) {
+                                                uint64_t variant0, uint32_t n, uint32_t tid, uint32_t bd) {
   using V = vec2_t<R>;
-  constexpr int CH = 8;
+  constexpr int CH = VB >= 4 ? 2 : (VB == 2 ? 4 : 8);
   for (uint32_t e0 = tid; e0 < n; e0 += bd * CH) {
-    V v[CH];
+    V v[CH][VB];
 #pragma unroll
     for (int c = 0; c < CH; ++c) {
       const uint32_t e = e0 + uint32_t(c) * bd;
-      if (e < n) v[c] = s[swz(e)];
+      if (e < n) {
+#pragma unroll
+        for (int b = 0; b < VB; ++b) v[c][b] = s[swz(e) * VB + b];
+      }
     }
     for (int k = i0; k < i1;) {
       const SweepOp& o = ops[k];
-      int sel = k;
-      int step = 1;
-      if (o.slot >= 0) {
-        sel = k + int((variant >> o.slot) & 1ull);
-        step = 2;
-      }
-      k += step;
+      const int sl = o.slot;
+      const int here = k;
+      k += (sl >= 0) ? 2 : 1;
       if ((base & o.omask) != o.omask) continue;
       const uint32_t lm = o.lmask;
-      const double qr = ops[sel].m[0], qi = ops[sel].m[1];
-      if (qi == 0.0 && qr == -1.0) {
+      if (sl < 0) {
+        const double qr = o.m[0], qi = o.m[1];
+        if (qi == 0.0 && qr == -1.0) {
 #pragma unroll
-        for (int c = 0; c < CH; ++c) {
-          const uint32_t e = e0 + uint32_t(c) * bd;
-          if ((e & lm) == lm) {
-            v[c].x = -v[c].x;
-            v[c].y = -v[c].y;
+          for (int c = 0; c < CH; ++c) {
+            const uint32_t e = e0 + uint32_t(c) * bd;
+            if ((e & lm) == lm) {
+#pragma unroll
+              for (int b = 0; b < VB; ++b) {
+                v[c][b].x = -v[c][b].x;
+                v[c][b].y = -v[c][b].y;
+              }
+            }
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < CH; ++c) {
+            const uint32_t e = e0 + uint32_t(c) * bd;
+            if ((e & lm) == lm) {
+#pragma unroll
+              for (int b = 0; b < VB; ++b) v[c][b] = cmul<R>(v[c][b], R(qr), R(qi));
+            }
           }
         }
       } else {
 #pragma unroll
-        for (int c = 0; c < CH; ++c) {
-          const uint32_t e = e0 + uint32_t(c) * bd;
-          if ((e & lm) == lm) v[c] = cmul<R>(v[c], R(qr), R(qi));
+        for (int b = 0; b < VB; ++b) {
+          const double* q = ops[here + int(((variant0 + b) >> sl) & 1ull)].m;
+          const R qr = R(q[0]), qi = R(q[1]);
+#pragma unroll
+          for (int c = 0; c < CH; ++c) {
+            const uint32_t e = e0 + uint32_t(c) * bd;
+            if ((e & lm) == lm) v[c][b] = cmul<R>(v[c][b], qr, qi);
+          }
         }
       }
     }
 #pragma unroll
     for (int c = 0; c < CH; ++c) {
       const uint32_t e = e0 + uint32_t(c) * bd;
-      if (e < n) s[swz(e)] = v[c];
+      if (e < n) {
+#pragma unroll
+        for (int b = 0; b < VB; ++b) s[swz(e) * VB + b] = v[c][b];
+      }
     }
   }
 }
 
-template <typename R, int CAP>
+// One CTA = one tile of VB consecutive states of the batch.
+template <typename R, int CAP, int VB>
 __global__ void __launch_bounds__(256, 2) sweep_kernel(const __grid_constant__ SweepParamsT<CAP> p) {
   using V = vec2_t<R>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -201,14 +246,14 @@ __global__ void __launch_bounds__(256, 2) sweep_kernel(const __grid_constant__ S
   const uint32_t n = 1u << T;
   const uint32_t nchunks = 1u << (T - L);
   const uint32_t lowmask = (1u << L) - 1u;
-  int64_t* chunkoff = reinterpret_cast<int64_t*>(smem_raw + sizeof(V) * size_t(n));
-  SweepOp* ops = reinterpret_cast<SweepOp*>(smem_raw + sizeof(V) * size_t(n) + sizeof(int64_t) * size_t(nchunks));
+  int64_t* chunkoff = reinterpret_cast<int64_t*>(smem_raw + sizeof(V) * size_t(n) * VB);
+  SweepOp* ops = reinterpret_cast<SweepOp*>(smem_raw + sizeof(V) * size_t(n) * VB + sizeof(int64_t) * size_t(nchunks));
   const uint32_t tid = threadIdx.x;
   const uint32_t bd = blockDim.x;
   const int n_ops = p.n_ops;
 
-  // stage the op list in shared memory once: per-op reads from the 31 KiB
-  // parameter bank would miss the constant cache at every step
+  // stage the op list in shared memory once (uniform reads from the 31 KiB
+  // parameter bank would miss the constant cache at every step)
   {
     const uint64_t* src = reinterpret_cast<const uint64_t*>(&p.ops[0]);
     uint64_t* dst = reinterpret_cast<uint64_t*>(ops);
@@ -222,8 +267,10 @@ __global__ void __launch_bounds__(256, 2) sweep_kernel(const __grid_constant__ S
     for (int j = 0; j < p.n_out; ++j)
       if ((tile >> j) & 1ull) base |= 1ull << p.oq[j];
   }
-  const uint64_t variant = p.variant_base + blockIdx.y;
-  V* st = reinterpret_cast<V*>(p.states) + int64_t(blockIdx.y) * p.stride;
+  const int v0 = int(blockIdx.y) * VB;
+  const uint64_t variant0 = p.variant_base + uint64_t(v0);
+  V* st = reinterpret_cast<V*>(p.states) + int64_t(v0) * p.stride;
+  const int nvalid = min(VB, p.n_states - v0);
 
   for (uint32_t c = tid; c < nchunks; c += bd) {
     int64_t off = 0;
@@ -238,11 +285,21 @@ __global__ void __launch_bounds__(256, 2) sweep_kernel(const __grid_constant__ S
       V z;
       z.x = (base == 0 && e == 0) ? R(1) : R(0);
       z.y = R(0);
-      s[swz(e)] = z;
+#pragma unroll
+      for (int b = 0; b < VB; ++b) s[swz(e) * VB + b] = z;
     }
   } else {
-    for (uint32_t e = tid; e < n; e += bd)
-      s[swz(e)] = st[int64_t(base) + chunkoff[e >> L] + (e & lowmask)];
+    for (uint32_t e = tid; e < n; e += bd) {
+      const int64_t g = int64_t(base) + chunkoff[e >> L] + (e & lowmask);
+#pragma unroll
+      for (int b = 0; b < VB; ++b) {
+        V z;
+        z.x = R(0);
+        z.y = R(0);
+        if (b < nvalid) z = st[int64_t(b) * p.stride + g];
+        s[swz(e) * VB + b] = z;
+      }
+    }
   }
   __syncthreads();
 
@@ -252,32 +309,39 @@ __global__ void __launch_bounds__(256, 2) sweep_kernel(const __grid_constant__ S
     if (op.type == OP_PHASE) {
       int j = i;
       while (j < n_ops && ops[j].type == OP_PHASE) j += (ops[j].slot >= 0) ? 2 : 1;
-      apply_phase_run<R>(s, ops, i, j, base, variant, n, tid, bd);
+      apply_phase_run<R, VB>(s, ops, i, j, base, variant0, n, tid, bd);
       __syncthreads();
       i = j;
       continue;
     }
-    switch (op.gsize) {
-      case 4:
-        // double: 16 complex registers + matrices exceed the 128-register
-        // budget of 2 CTAs/SM, so a group of 4 runs as 3 + 1
-        if (std::is_same<R, double>::value) {
-          i = apply_group<R, 3>(s, ops, i, base, variant, T, tid, bd);
-          __syncthreads();
-          i = apply_group<R, 1>(s, ops, i, base, variant, T, tid, bd);
-        } else {
-          i = apply_group<R, 4>(s, ops, i, base, variant, T, tid, bd);
-        }
-        break;
-      case 3: i = apply_group<R, 3>(s, ops, i, base, variant, T, tid, bd); break;
-      case 2: i = apply_group<R, 2>(s, ops, i, base, variant, T, tid, bd); break;
-      default: i = apply_group<R, 1>(s, ops, i, base, variant, T, tid, bd); break;
+    // register budget: 8 (double) / 16 (float) complex values per thread
+    constexpr int kBudget = std::is_same<R, double>::value ? 8 : 16;
+    constexpr int KMAX = (kBudget / VB) >= 16 ? 4 : (kBudget / VB) >= 8 ? 3 : (kBudget / VB) >= 4 ? 2 : 1;
+    int left = op.gsize > 0 ? op.gsize : 1;
+    while (left > 0) {
+      const int k = left < KMAX ? left : KMAX;
+      if constexpr (KMAX >= 4) {
+        if (k == 4) i = apply_group<R, 4, VB>(s, ops, i, base, variant0, T, tid, bd);
+      }
+      if constexpr (KMAX >= 3) {
+        if (k == 3) i = apply_group<R, 3, VB>(s, ops, i, base, variant0, T, tid, bd);
+      }
+      if constexpr (KMAX >= 2) {
+        if (k == 2) i = apply_group<R, 2, VB>(s, ops, i, base, variant0, T, tid, bd);
+      }
+      if (k == 1) i = apply_group<R, 1, VB>(s, ops, i, base, variant0, T, tid, bd);
+      left -= k;
+      if (left > 0) __syncthreads();
     }
     __syncthreads();
   }
 
-  for (uint32_t e = tid; e < n; e += bd)
-    st[int64_t(base) + chunkoff[e >> L] + (e & lowmask)] = s[swz(e)];
+  for (uint32_t e = tid; e < n; e += bd) {
+    const int64_t g = int64_t(base) + chunkoff[e >> L] + (e & lowmask);
+#pragma unroll
+    for (int b = 0; b < VB; ++b)
+      if (b < nvalid) st[int64_t(b) * p.stride + g] = s[swz(e) * VB + b];
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -480,44 +544,55 @@ __global__ void gather_kernel(const vec2_t<R>* state, const int64_t* idx, int64_
 // ---------------------------------------------------------------------------
 // launchers (host)
 // ---------------------------------------------------------------------------
-size_t sweep_smem_bytes(int tile_bits, int low_bits, int dtype, int n_ops) {
+size_t sweep_smem_bytes(int tile_bits, int low_bits, int dtype, int n_ops, int vb) {
   const size_t elem = dtype == 0 ? sizeof(double2) : sizeof(float2);
-  return (size_t(1) << tile_bits) * elem + (size_t(1) << (tile_bits - low_bits)) * sizeof(int64_t) +
+  return (size_t(1) << tile_bits) * elem * size_t(vb) + (size_t(1) << (tile_bits - low_bits)) * sizeof(int64_t) +
          size_t(n_ops) * sizeof(SweepOp);
 }
 
-template <typename R, int CAP>
-static cudaError_t launch_sweep_cap(const SweepParamsT<CAP>& p, uint32_t n_tiles, uint32_t n_states, int threads,
+template <typename R, int CAP, int VB>
+static cudaError_t launch_sweep_cap(const SweepParamsT<CAP>& p, uint32_t n_tiles, uint32_t n_groups, int threads,
                                     size_t smem, cudaStream_t stream) {
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(sweep_kernel<R, CAP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(sweep_kernel<R, CAP, VB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(smem));
     if (e != cudaSuccess) return e;
     configured = smem;
   }
-  dim3 grid(n_tiles, n_states, 1);
-  sweep_kernel<R, CAP><<<grid, threads, smem, stream>>>(p);
+  dim3 grid(n_tiles, n_groups, 1);
+  sweep_kernel<R, CAP, VB><<<grid, threads, smem, stream>>>(p);
   return cudaGetLastError();
 }
 
+template <typename R, int CAP>
+static cudaError_t launch_sweep_vb(const SweepParamsT<CAP>& p, uint32_t n_tiles, int vb, int threads,
+                                   cudaStream_t stream) {
+  const int dt = std::is_same<R, double>::value ? 0 : 1;
+  const size_t smem = sweep_smem_bytes(p.tile_bits, p.low_bits, dt, p.n_ops, vb);
+  const uint32_t groups = uint32_t((p.n_states + vb - 1) / vb);
+  switch (vb) {
+    case 4: return launch_sweep_cap<R, CAP, 4>(p, n_tiles, groups, threads, smem, stream);
+    case 2: return launch_sweep_cap<R, CAP, 2>(p, n_tiles, groups, threads, smem, stream);
+    default: return launch_sweep_cap<R, CAP, 1>(p, n_tiles, groups, threads, smem, stream);
+  }
+}
+
 template <typename R>
-static cudaError_t launch_sweep_t(const SweepParams& p, uint32_t n_tiles, uint32_t n_states, int threads,
-                                  cudaStream_t stream) {
-  const size_t smem = sweep_smem_bytes(p.tile_bits, p.low_bits, std::is_same<R, double>::value ? 0 : 1, p.n_ops);
+static cudaError_t launch_sweep_t(const SweepParams& p, uint32_t n_tiles, int vb, int threads, cudaStream_t stream) {
   if (p.n_ops <= kSmallOps) {
     static SweepParamsSmall ps;  // launch copies it; callers hold capi's lock
     std::memcpy(&ps, &p, offsetof(SweepParams, ops));
     std::memcpy(ps.ops, p.ops, sizeof(SweepOp) * size_t(p.n_ops));
-    return launch_sweep_cap<R, kSmallOps>(ps, n_tiles, n_states, threads, smem, stream);
+    return launch_sweep_vb<R, kSmallOps>(ps, n_tiles, vb, threads, stream);
   }
-  return launch_sweep_cap<R, kMaxOpsPerLaunch>(p, n_tiles, n_states, threads, smem, stream);
+  return launch_sweep_vb<R, kMaxOpsPerLaunch>(p, n_tiles, vb, threads, stream);
 }
 
-cudaError_t launch_sweep(const SweepParams& p, uint32_t n_tiles, uint32_t n_states, int threads,
-                         cudaStream_t stream, int dtype) {
-  return dtype == 0 ? launch_sweep_t<double>(p, n_tiles, n_states, threads, stream)
-                    : launch_sweep_t<float>(p, n_tiles, n_states, threads, stream);
+cudaError_t launch_sweep(const SweepParams& p, uint32_t n_tiles, int vb, int threads, cudaStream_t stream,
+                         int dtype) {
+  return dtype == 0 ? launch_sweep_t<double>(p, n_tiles, vb, threads, stream)
+                    : launch_sweep_t<float>(p, n_tiles, vb, threads, stream);
 }
 
 template <typename R, int K, int CC>

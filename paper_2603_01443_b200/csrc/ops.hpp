@@ -49,7 +49,7 @@ struct SweepParamsT {
   int32_t n_out;            // nq - T outside qubits, tile id bit j -> oq[j]
   int32_t n_ops;
   int32_t init_basis;       // 1: ignore memory, start from |0..0>
-  int32_t store;            // 0: keep result in smem only (never used), 1: write back
+  int32_t n_states;         // states in this launch (CTA group y holds VB of them)
   int8_t hq[kMaxTileBits];
   int8_t oq[64];
   SweepOp ops[CAP];

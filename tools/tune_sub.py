@@ -1,6 +1,5 @@
-"""Time the batched subcircuit stage under different tile/thread settings."""
+"""Time the batched subcircuit stage under different tile/vb settings."""
 import sys
-import time
 
 import torch
 
@@ -27,15 +26,15 @@ for name in sys.argv[1:] or ["cfg4a", "cfg2", "cfg5_q32_n2_c2", "cfg4b"]:
     spec = cb.BASELINE_CONFIGS[name]
     circ = cb.build_brickwall(spec)
     prep = preprocess(circ, spec.n)
-    for tb in (0, 9, 10, 11, 12):
-        for th in (0, 64, 128, 256):
+    for tb in (0, 8, 9, 10, 11):
+        for vb in (0, 1, 2, 4):
             _native.set_option("tile_bits", tb)
-            _native.set_option("threads", th)
+            _native.set_option("vb", vb)
             try:
                 ms = timeit(lambda: simulate_segments(prep))
             except Exception as exc:  # noqa: BLE001
-                print(name, tb, th, "ERR", exc)
+                print(name, tb, vb, "ERR", exc)
                 continue
-            print(f"{name} tile_bits={tb} threads={th}: {ms*1e3:.1f} us")
+            print(f"{name} tile_bits={tb} vb={vb}: {ms*1e3:.1f} us", flush=True)
     _native.set_option("tile_bits", 0)
-    _native.set_option("threads", 0)
+    _native.set_option("vb", 0)
