@@ -304,3 +304,32 @@ def test_q30_cfg4b_three_way(cb):
     uncut = cb.simulate(circ)
     assert engine.max_abs_diff(cut, uncut) < TOL
     del cut, uncut
+
+
+def test_q34_shard_sampled_vs_oracle(cb):
+    """One GPU's share of the 8-GPU q=34 job (rows [0, 2^17/8)) against the
+    oracle's sampled amplitudes sum_m alpha_m prod_i psi_i[x_i]."""
+    import torch
+
+    from paper_2603_01443_b200.merging import merge_chain_device
+    from paper_2603_01443_b200.parallel import shard_range
+    from paper_2603_01443_b200.pipeline import preprocess, simulate_segments
+
+    spec = cb.BASELINE_CONFIGS["cfg5_q34_n2_c2"]
+    circ = cb.build_brickwall(spec)
+    prep = preprocess(circ, 2)
+    for rank in (0, 5):
+        begin, end = shard_range(34, 8, rank, 17)
+        out = merge_chain_device(prep.chain, simulate_segments(prep), out_range=(begin, end))
+        k, qa, qb, p = circ.kinds, circ.qa, circ.qb, circ.params
+        sizes = [17, 17]
+        bgs, counts, _ = orc.plan(k, qa, qb, sizes)
+        states = [[orc.simulate(17, *v) for v in orc.segment_variants(k, qa, qb, p, sizes, bgs, s)]
+                  for s in range(2)]
+        idx = np.random.default_rng(rank).integers(begin, end, size=2048)
+        want = orc.sample_amplitudes(states, orc.merge_table(2, bgs, sum(counts)),
+                                     orc.coefficients(sum(counts)), sizes, idx)
+        got = out[torch.as_tensor(idx - begin, device="cuda")].cpu().numpy()
+        assert np.abs(got - want).max() < TOL
+        del out
+        torch.cuda.empty_cache()
