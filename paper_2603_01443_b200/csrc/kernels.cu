@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(256, 2) sweep_kernel(const __grid_constant__ S
 // term, merging.py:117,94).
 // ---------------------------------------------------------------------------
 template <typename R, int K, int CC, bool WIDE>
-__global__ void __launch_bounds__(256) merge_kernel(const __grid_constant__ MergeParams p) {
+__global__ void __launch_bounds__(256, 2) merge_kernel(const __grid_constant__ MergeParams p) {
   using V = vec2_t<R>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   V* bs = reinterpret_cast<V*>(smem_raw);
@@ -406,28 +406,49 @@ __global__ void __launch_bounds__(256) merge_kernel(const __grid_constant__ Merg
   V* out = reinterpret_cast<V*>(p.out) + int64_t(sl) * p.out_slot_stride;
   for (int i = 0; i < p.iters; ++i) {
     if (WIDE) {
-      const int r = i;
-      const int64_t h = row0 + r;
-      if (h >= p.row_end) break;
-      V b[K];
+      // RR rows at a time share the register-resident lo columns; each output
+      // sums its K terms in two interleaved accumulators (even / odd t) so the
+      // FP64 dependency chains are K long instead of 2K
+      constexpr int RR = K == 8 ? 2 : 1;
+      const int r0 = i;
+      i += RR - 1;
+      V b[RR][K];
 #pragma unroll
-      for (int t = 0; t < K; ++t) b[t] = bs[r * K + t];
-      const int64_t obase = (h - p.row_begin) * W;
+      for (int rr = 0; rr < RR; ++rr)
 #pragma unroll
-      for (int j = 0; j < CC; ++j) {
-        V acc;
-        acc.x = R(0);
-        acc.y = R(0);
-#pragma unroll
-        for (int t = 0; t < K; ++t) cfma<R>(acc, b[t], a[t][j]);
-        V* dst = out + obase + col[j];
-        if (p.accumulate) {
-          const V prev = *dst;
-          acc.x += prev.x;
-          acc.y += prev.y;
+        for (int t = 0; t < K; ++t) {
+          const int r = r0 + rr < rows_cta ? r0 + rr : r0;
+          b[rr][t] = bs[r * K + t];
         }
-        if (p.streaming) __stcs(dst, acc);
-        else *dst = acc;
+#pragma unroll
+      for (int rr = 0; rr < RR; ++rr) {
+        const int64_t h = row0 + r0 + rr;
+        if (r0 + rr >= p.iters || h >= p.row_end) break;
+        const int64_t obase = (h - p.row_begin) * W;
+#pragma unroll
+        for (int j = 0; j < CC; ++j) {
+          V acc0, acc1;
+          acc0.x = R(0);
+          acc0.y = R(0);
+          acc1.x = R(0);
+          acc1.y = R(0);
+#pragma unroll
+          for (int t = 0; t < K; t += 2) {
+            cfma<R>(acc0, b[rr][t], a[t][j]);
+            if (t + 1 < K) cfma<R>(acc1, b[rr][t + 1], a[t + 1][j]);
+          }
+          V acc;
+          acc.x = acc0.x + acc1.x;
+          acc.y = acc0.y + acc1.y;
+          V* dst = out + obase + col[j];
+          if (p.accumulate) {
+            const V prev = *dst;
+            acc.x += prev.x;
+            acc.y += prev.y;
+          }
+          if (p.streaming) __stcs(dst, acc);
+          else *dst = acc;
+        }
       }
     } else {
 #pragma unroll
