@@ -16,6 +16,7 @@
 #include "plan.hpp"
 
 namespace cutsim {
+extern int g_sweep_minb;
 size_t sweep_smem_bytes(int tile_bits, int low_bits, int dtype, int n_ops, int vb);
 cudaError_t launch_sweep(const SweepParams& p, uint32_t n_tiles, int vb, int threads, cudaStream_t stream,
                          int dtype);
@@ -103,7 +104,8 @@ int choose_vb(int64_t n_states) {
 }
 
 int group_budget(int vb, int dtype) {
-  const int values = (dtype == CS_C128 ? 8 : 16) / vb;
+  const int minb = vb == 1 ? g_sweep_minb : 2;
+  const int values = (dtype == CS_C128 ? 8 : 16) * 2 / minb / vb;
   return values >= 16 ? 4 : values >= 8 ? 3 : values >= 4 ? 2 : 1;
 }
 
@@ -145,7 +147,7 @@ std::shared_ptr<const std::vector<Sweep>> build_schedule(int nq, const uint8_t* 
   const int vb = choose_vb(n_states);
   std::string key;
   key.reserve(size_t(n_gates) * 45 + 32);
-  const int32_t hdr[7] = {nq, T, L, int32_t(g_opt.fuse), slots ? 1 : 0, dtype, vb};
+  const int32_t hdr[8] = {nq, T, L, int32_t(g_opt.fuse), slots ? 1 : 0, dtype, vb, g_sweep_minb};
   key.append(reinterpret_cast<const char*>(hdr), sizeof(hdr));
   key.append(reinterpret_cast<const char*>(kinds), size_t(n_gates));
   key.append(reinterpret_cast<const char*>(qa), size_t(n_gates) * 8);
@@ -320,6 +322,9 @@ int cs_set_option(const char* key, int64_t value) {
   } else if (k == "merge_iters") {
     if (value < 0 || value > 4096) return fail(CS_ERR_INVALID, "merge_iters out of range");
     g_opt.merge_iters = value;
+  } else if (k == "sweep_minb") {
+    if (value < 2 || value > 4) return fail(CS_ERR_INVALID, "sweep_minb must be 2, 3 or 4");
+    g_sweep_minb = int(value);
   } else if (k == "vb") {
     if (value < 0 || value > 4 || value == 3) return fail(CS_ERR_INVALID, "vb must be 0, 1, 2 or 4");
     g_opt.vb = value;
@@ -338,6 +343,7 @@ int64_t cs_get_option(const char* key) {
   if (k == "merge_streaming") return g_opt.merge_streaming;
   if (k == "merge_iters") return g_opt.merge_iters;
   if (k == "vb") return g_opt.vb;
+  if (k == "sweep_minb") return g_sweep_minb;
   return -1;
 }
 

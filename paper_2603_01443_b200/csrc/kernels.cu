@@ -236,8 +236,8 @@ __device__ __forceinline__ void apply_phase_run(vec2_t<R>* s, const SweepOp* ops
 }
 
 // One CTA = one tile of VB consecutive states of the batch.
-template <typename R, int CAP, int VB>
-__global__ void __launch_bounds__(256, 2) sweep_kernel(const __grid_constant__ SweepParamsT<CAP> p) {
+template <typename R, int CAP, int VB, int MINB>
+__global__ void __launch_bounds__(256, MINB) sweep_kernel(const __grid_constant__ SweepParamsT<CAP> p) {
   using V = vec2_t<R>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   V* s = reinterpret_cast<V*>(smem_raw);
@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(256, 2) sweep_kernel(const __grid_constant__ S
       continue;
     }
     // register budget: 8 (double) / 16 (float) complex values per thread
-    constexpr int kBudget = std::is_same<R, double>::value ? 8 : 16;
+    constexpr int kBudget = (std::is_same<R, double>::value ? 8 : 16) * 2 / MINB;
     constexpr int KMAX = (kBudget / VB) >= 16 ? 4 : (kBudget / VB) >= 8 ? 3 : (kBudget / VB) >= 4 ? 2 : 1;
     int left = op.gsize > 0 ? op.gsize : 1;
     while (left > 0) {
@@ -571,20 +571,22 @@ size_t sweep_smem_bytes(int tile_bits, int low_bits, int dtype, int n_ops, int v
          size_t(n_ops) * sizeof(SweepOp);
 }
 
-template <typename R, int CAP, int VB>
+template <typename R, int CAP, int VB, int MINB>
 static cudaError_t launch_sweep_cap(const SweepParamsT<CAP>& p, uint32_t n_tiles, uint32_t n_groups, int threads,
                                     size_t smem, cudaStream_t stream) {
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(sweep_kernel<R, CAP, VB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(smem));
+    cudaError_t e = cudaFuncSetAttribute(sweep_kernel<R, CAP, VB, MINB>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     configured = smem;
   }
   dim3 grid(n_tiles, n_groups, 1);
-  sweep_kernel<R, CAP, VB><<<grid, threads, smem, stream>>>(p);
+  sweep_kernel<R, CAP, VB, MINB><<<grid, threads, smem, stream>>>(p);
   return cudaGetLastError();
 }
+
+int g_sweep_minb = 2;  // CTAs per SM the big-grid (uncut) sweep kernel is compiled for
 
 template <typename R, int CAP>
 static cudaError_t launch_sweep_vb(const SweepParamsT<CAP>& p, uint32_t n_tiles, int vb, int threads,
@@ -593,9 +595,12 @@ static cudaError_t launch_sweep_vb(const SweepParamsT<CAP>& p, uint32_t n_tiles,
   const size_t smem = sweep_smem_bytes(p.tile_bits, p.low_bits, dt, p.n_ops, vb);
   const uint32_t groups = uint32_t((p.n_states + vb - 1) / vb);
   switch (vb) {
-    case 4: return launch_sweep_cap<R, CAP, 4>(p, n_tiles, groups, threads, smem, stream);
-    case 2: return launch_sweep_cap<R, CAP, 2>(p, n_tiles, groups, threads, smem, stream);
-    default: return launch_sweep_cap<R, CAP, 1>(p, n_tiles, groups, threads, smem, stream);
+    case 4: return launch_sweep_cap<R, CAP, 4, 2>(p, n_tiles, groups, threads, smem, stream);
+    case 2: return launch_sweep_cap<R, CAP, 2, 2>(p, n_tiles, groups, threads, smem, stream);
+    default:
+      if (g_sweep_minb >= 4) return launch_sweep_cap<R, CAP, 1, 4>(p, n_tiles, groups, threads, smem, stream);
+      if (g_sweep_minb == 3) return launch_sweep_cap<R, CAP, 1, 3>(p, n_tiles, groups, threads, smem, stream);
+      return launch_sweep_cap<R, CAP, 1, 2>(p, n_tiles, groups, threads, smem, stream);
   }
 }
 
