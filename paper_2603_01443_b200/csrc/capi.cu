@@ -20,6 +20,8 @@ extern int g_sweep_minb;
 size_t sweep_smem_bytes(int tile_bits, int low_bits, int dtype, int n_ops, int vb);
 cudaError_t launch_sweep(const SweepParams& p, uint32_t n_tiles, int vb, int threads, cudaStream_t stream,
                          int dtype);
+cudaError_t launch_rsweep(const RegParams& p, int rb, uint32_t n_tiles, uint32_t n_states, cudaStream_t stream,
+                          int dtype);
 cudaError_t launch_merge(const MergeParams& p, int K, dim3 grid, int threads, size_t smem, bool wide,
                          cudaStream_t stream, int dtype);
 int merge_cols_per_thread(int K);
@@ -49,6 +51,8 @@ struct Options {
   int64_t merge_streaming = 1;
   int64_t merge_iters = 0;
   int64_t vb = 0;  // states per CTA in a variant batch (0 = auto)
+  int64_t engine = 1;      // 1: register-tile kernel (rsweep), 0: shared-memory tile kernel (sweep)
+  int64_t plan_json = 0;   // cs_sweep_plan_json: 0 sweeps, 1 register programs
 } g_opt;
 std::mutex g_opt_mu;
 
@@ -98,6 +102,7 @@ double2* reduce_scratch(int* err) {
 }
 
 int choose_vb(int64_t n_states) {
+  if (g_opt.engine == 1) return 1;
   if (g_opt.vb > 0) return int(std::min<int64_t>(g_opt.vb, 4));
   // measured (tools/tune_sub.py): 2 states per CTA beats 1 and 4 for cut variants
   return n_states >= 2 ? 2 : 1;
@@ -110,7 +115,9 @@ int group_budget(int vb, int dtype) {
 }
 
 int single_tile_max_vb(int dtype, int vb) {
-  // the tile of vb states must fit shared memory next to the op list
+  // the tile of vb states must fit shared memory next to the op list; the
+  // register kernel runs at most 512 threads x 16 amplitudes
+  if (g_opt.engine == 1) return 13;
   int t = dtype == CS_C128 ? 13 : 14;
   while (t > 6 && ((size_t(1) << t) * (dtype == CS_C128 ? 16 : 8) * size_t(vb)) > size_t(128 * 1024)) --t;
   return t;
@@ -134,11 +141,51 @@ int choose_tile_bits(int nq, int64_t n_states, int tile_bits, int dtype) {
   return dflt;
 }
 
+struct Launch {
+  int sweep = 0;
+  std::vector<SweepOp> entries;  // engine 0
+  std::vector<RegOp> reg;        // engine 1
+};
+struct Program {
+  std::vector<Sweep> sweeps;
+  std::vector<Launch> launches;
+  int engine = 1;
+};
+
 std::mutex g_cache_mu;
-std::unordered_map<std::string, std::shared_ptr<const std::vector<Sweep>>> g_cache;
+std::unordered_map<std::string, std::shared_ptr<const Program>> g_cache;
+
+// Split each sweep's entries into launches that fit the kernel parameter
+// block (never splitting a slotted pair); the register kernel's chunks are
+// smaller because its REMAPs add entries.
+void build_launches(Program& prog) {
+  const size_t cap = prog.engine == 1 ? 170 : size_t(kMaxOpsPerLaunch);
+  for (size_t s = 0; s < prog.sweeps.size(); ++s) {
+    const Sweep& sw = prog.sweeps[s];
+    size_t i0 = 0;
+    do {
+      size_t i1 = i0;
+      while (i1 < sw.entries.size()) {
+        const size_t w = sw.entries[i1].slot >= 0 ? 2 : 1;
+        if (i1 + w - i0 > cap) break;
+        i1 += w;
+      }
+      Launch l;
+      l.sweep = int(s);
+      l.entries.assign(sw.entries.begin() + long(i0), sw.entries.begin() + long(i1));
+      if (prog.engine == 1) {
+        Sweep part = sw;
+        part.entries = l.entries;
+        l.reg = reg_program(part, reg_bits_for(sw.tile_bits));
+      }
+      prog.launches.push_back(std::move(l));
+      i0 = i1;
+    } while (i0 < sw.entries.size());
+  }
+}
 
 // Lowered, fused and scheduled program for a gate table; cached by content.
-std::shared_ptr<const std::vector<Sweep>> build_schedule(int nq, const uint8_t* kinds, const int64_t* qa,
+std::shared_ptr<const Program> build_schedule(int nq, const uint8_t* kinds, const int64_t* qa,
                                                          const int64_t* qb, const double* params,
                                                          const int32_t* slots, int64_t n_gates, int64_t n_states,
                                                          int tile_bits, int dtype) {
@@ -147,7 +194,8 @@ std::shared_ptr<const std::vector<Sweep>> build_schedule(int nq, const uint8_t* 
   const int vb = choose_vb(n_states);
   std::string key;
   key.reserve(size_t(n_gates) * 45 + 32);
-  const int32_t hdr[8] = {nq, T, L, int32_t(g_opt.fuse), slots ? 1 : 0, dtype, vb, g_sweep_minb};
+  const int32_t hdr[9] = {nq, T, L, int32_t(g_opt.fuse), slots ? 1 : 0, dtype, vb, g_sweep_minb,
+                          int32_t(g_opt.engine)};
   key.append(reinterpret_cast<const char*>(hdr), sizeof(hdr));
   key.append(reinterpret_cast<const char*>(kinds), size_t(n_gates));
   key.append(reinterpret_cast<const char*>(qa), size_t(n_gates) * 8);
@@ -163,7 +211,11 @@ std::shared_ptr<const std::vector<Sweep>> build_schedule(int nq, const uint8_t* 
   if (g_opt.fuse) ops = fuse_ops(ops);
   // register groups hold 2^k x vb complex values: 8 (c128) / 16 (c64) per thread
   const int max_group = std::min(sweep_max_group(T), group_budget(vb, dtype));
-  auto prog = std::make_shared<const std::vector<Sweep>>(schedule_sweeps(ops, nq, T, L, max_group));
+  auto built = std::make_shared<Program>();
+  built->engine = int(g_opt.engine);
+  built->sweeps = schedule_sweeps(ops, nq, T, L, max_group);
+  build_launches(*built);
+  std::shared_ptr<const Program> prog = built;
   std::lock_guard<std::mutex> lk(g_cache_mu);
   if (g_cache.size() >= 256) g_cache.clear();
   g_cache.emplace(std::move(key), prog);
@@ -325,6 +377,11 @@ int cs_set_option(const char* key, int64_t value) {
   } else if (k == "sweep_minb") {
     if (value < 2 || value > 4) return fail(CS_ERR_INVALID, "sweep_minb must be 2, 3 or 4");
     g_sweep_minb = int(value);
+  } else if (k == "engine") {
+    if (value != 0 && value != 1) return fail(CS_ERR_INVALID, "engine must be 0 or 1");
+    g_opt.engine = value;
+  } else if (k == "plan_json") {
+    g_opt.plan_json = value ? 1 : 0;
   } else if (k == "vb") {
     if (value < 0 || value > 4 || value == 3) return fail(CS_ERR_INVALID, "vb must be 0, 1, 2 or 4");
     g_opt.vb = value;
@@ -343,6 +400,8 @@ int64_t cs_get_option(const char* key) {
   if (k == "merge_streaming") return g_opt.merge_streaming;
   if (k == "merge_iters") return g_opt.merge_iters;
   if (k == "vb") return g_opt.vb;
+  if (k == "engine") return g_opt.engine;
+  if (k == "plan_json") return g_opt.plan_json;
   if (k == "sweep_minb") return g_sweep_minb;
   return -1;
 }
@@ -372,58 +431,69 @@ int cs_sim_batch(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int6
     if (!init_zero) return CS_OK;
     return cs_init_basis(states, 0, n_states, 0, dtype, stream);
   }
-  std::shared_ptr<const std::vector<Sweep>> prog;
+  std::shared_ptr<const Program> prog;
   try {
     prog = build_schedule(nq, kinds, qa, qb, params, slots, n_gates, n_states, 0, dtype);
   } catch (const PlanError& pe) {
     return fail(pe.code, pe.msg);
   }
-  const std::vector<Sweep>& sweeps = *prog;
   static SweepParams p;
+  static RegParams rp;
   static std::mutex pm;
   std::lock_guard<std::mutex> lk(pm);
   bool first = true;
-  for (const Sweep& sw : sweeps) {
+  for (const Launch& ln : prog->launches) {
+    const Sweep& sw = prog->sweeps[size_t(ln.sweep)];
     const int T = sw.tile_bits;
     if (sw.hq.size() > size_t(kMaxTileBits) || sw.oq.size() > 64)
       return fail(CS_ERR_INTERNAL, "sweep geometry exceeds the kernel limits");
     const uint32_t n_tiles = uint32_t(1) << (nq - T);
-    // chunk the entries without splitting a slotted pair
-    size_t i0 = 0;
-    do {
-      size_t i1 = i0;
-      while (i1 < sw.entries.size()) {
-        const size_t w = sw.entries[i1].slot >= 0 ? 2 : 1;
-        if (i1 + w - i0 > size_t(kMaxOpsPerLaunch)) break;
-        i1 += w;
-      }
-      std::memset(&p, 0, offsetof(SweepParams, ops));
-      p.nq = nq;
-      p.tile_bits = T;
-      p.low_bits = sw.low_bits;
-      p.n_high = int32_t(sw.hq.size());
-      p.n_out = int32_t(sw.oq.size());
-      for (size_t j = 0; j < sw.hq.size() && j < size_t(kMaxTileBits); ++j) p.hq[j] = int8_t(sw.hq[j]);
-      for (size_t j = 0; j < sw.oq.size() && j < 64; ++j) p.oq[j] = int8_t(sw.oq[j]);
-      p.n_ops = int32_t(i1 - i0);
-      if (i1 > i0) std::memcpy(p.ops, sw.entries.data() + i0, sizeof(SweepOp) * (i1 - i0));
-      p.init_basis = (first && init_zero) ? 1 : 0;
-      p.stride = state_stride;
-      int threads = int(g_opt.threads);
-      if (threads == 0) threads = sweep_threads(T);
-      threads = std::min(threads, 256);
-      for (int64_t v0 = 0; v0 < n_states; v0 += 65535) {
-        const int64_t vc = std::min<int64_t>(65535, n_states - v0);
-        p.states = static_cast<char*>(states) + size_t(v0) * size_t(state_stride) * elem_bytes(dtype);
+    for (int64_t v0 = 0; v0 < n_states; v0 += 65535) {
+      const int64_t vc = std::min<int64_t>(65535, n_states - v0);
+      void* sp = static_cast<char*>(states) + size_t(v0) * size_t(state_stride) * elem_bytes(dtype);
+      cudaError_t e;
+      if (prog->engine == 1) {
+        if (ln.reg.size() > size_t(kMaxOpsPerLaunch)) return fail(CS_ERR_INTERNAL, "register program too long");
+        std::memset(&rp, 0, offsetof(RegParams, ops));
+        rp.states = sp;
+        rp.stride = state_stride;
+        rp.variant_base = variant_base + uint64_t(v0);
+        rp.tile_bits = T;
+        rp.low_bits = sw.low_bits;
+        rp.n_high = int32_t(sw.hq.size());
+        rp.n_out = int32_t(sw.oq.size());
+        rp.n_ops = int32_t(ln.reg.size());
+        rp.init_basis = (first && init_zero) ? 1 : 0;
+        rp.n_states = int32_t(vc);
+        for (size_t j = 0; j < sw.hq.size() && j < size_t(kMaxTileBits); ++j) rp.hq[j] = int8_t(sw.hq[j]);
+        for (size_t j = 0; j < sw.oq.size() && j < 64; ++j) rp.oq[j] = int8_t(sw.oq[j]);
+        if (!ln.reg.empty()) std::memcpy(rp.ops, ln.reg.data(), sizeof(RegOp) * ln.reg.size());
+        e = launch_rsweep(rp, reg_bits_for(T), n_tiles, uint32_t(vc), st, dtype);
+      } else {
+        std::memset(&p, 0, offsetof(SweepParams, ops));
+        p.nq = nq;
+        p.tile_bits = T;
+        p.low_bits = sw.low_bits;
+        p.n_high = int32_t(sw.hq.size());
+        p.n_out = int32_t(sw.oq.size());
+        for (size_t j = 0; j < sw.hq.size() && j < size_t(kMaxTileBits); ++j) p.hq[j] = int8_t(sw.hq[j]);
+        for (size_t j = 0; j < sw.oq.size() && j < 64; ++j) p.oq[j] = int8_t(sw.oq[j]);
+        p.n_ops = int32_t(ln.entries.size());
+        if (!ln.entries.empty()) std::memcpy(p.ops, ln.entries.data(), sizeof(SweepOp) * ln.entries.size());
+        p.init_basis = (first && init_zero) ? 1 : 0;
+        p.stride = state_stride;
+        int threads = int(g_opt.threads);
+        if (threads == 0) threads = sweep_threads(T);
+        threads = std::min(threads, 256);
+        p.states = sp;
         p.variant_base = variant_base + uint64_t(v0);
         p.n_states = int32_t(vc);
-        cudaError_t e = launch_sweep(p, n_tiles, choose_vb(n_states), threads, st, dtype);
-        g_launches.fetch_add(1);
-        if (e != cudaSuccess) return cuda_fail(e, "sweep_kernel launch");
+        e = launch_sweep(p, n_tiles, choose_vb(n_states), threads, st, dtype);
       }
-      first = false;
-      i0 = i1;
-    } while (i0 < sw.entries.size());
+      g_launches.fetch_add(1);
+      if (e != cudaSuccess) return cuda_fail(e, "sweep kernel launch");
+    }
+    first = false;
   }
   return CS_OK;
 }
@@ -435,7 +505,8 @@ int cs_sweep_plan_json(int32_t nq, const uint8_t* kinds, const int64_t* qa, cons
   if (nq < 1 || nq > 62) return fail(CS_ERR_INVALID, "qubit count out of range");
   std::string js;
   try {
-    js = sweeps_to_json(*build_schedule(nq, kinds, qa, qb, params, slots, n_gates, 1, tile_bits, dtype), nq);
+    auto prog = build_schedule(nq, kinds, qa, qb, params, slots, n_gates, 1, tile_bits, dtype);
+    js = g_opt.plan_json ? reg_programs_to_json(prog->sweeps, nq) : sweeps_to_json(prog->sweeps, nq);
   } catch (const PlanError& pe) {
     return fail(pe.code, pe.msg);
   }

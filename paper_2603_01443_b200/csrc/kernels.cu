@@ -345,6 +345,151 @@ __global__ void __launch_bounds__(256, MINB) sweep_kernel(const __grid_constant_
 }
 
 // ---------------------------------------------------------------------------
+// Register-tile sweep: the same tile geometry as sweep_kernel, but the tile
+// lives in registers (2^RB amplitudes per thread). Dense gates on register
+// bits run entirely in registers — no shared-memory traffic, no barrier;
+// diagonal gates test thread/register masks; a REMAP (two barriers, one
+// swizzled shared-memory transpose) brings the next gates' targets into the
+// register bits. The host chooses the remaps (plan.cpp: reg_program).
+// ---------------------------------------------------------------------------
+template <typename R, int RB>
+__device__ __forceinline__ void reg_dense(vec2_t<R> (&v)[1 << RB], int k, uint32_t rmask, const double* m) {
+#pragma unroll
+  for (int kk = 0; kk < RB; ++kk) {
+    if (kk != k) continue;
+#pragma unroll
+    for (int j = 0; j < (1 << RB); ++j) {
+      if ((j >> kk) & 1) continue;
+      if ((uint32_t(j) & rmask) != rmask) continue;
+      apply2x2<R>(v[j], v[j | (1 << kk)], m);
+    }
+  }
+}
+
+template <typename R, int RB, int CAP>
+__global__ void __launch_bounds__(512) rsweep_kernel(const __grid_constant__ RegParamsT<CAP> p) {
+  using V = vec2_t<R>;
+  constexpr int NR = 1 << RB;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  V* s = reinterpret_cast<V*>(smem_raw);
+  const int T = p.tile_bits;
+  const int L = p.low_bits;
+  const uint32_t n = 1u << T;
+  const uint32_t nchunks = 1u << (T - L);
+  const uint32_t lowmask = (1u << L) - 1u;
+  int64_t* chunkoff = reinterpret_cast<int64_t*>(smem_raw + sizeof(V) * size_t(n));
+  RegOp* ops = reinterpret_cast<RegOp*>(smem_raw + sizeof(V) * size_t(n) + sizeof(int64_t) * size_t(nchunks));
+  const uint32_t tid = threadIdx.x;
+  const uint32_t bd = blockDim.x;  // = 2^(T - RB)
+  const int n_ops = p.n_ops;
+  {
+    const uint64_t* src = reinterpret_cast<const uint64_t*>(&p.ops[0]);
+    uint64_t* dst = reinterpret_cast<uint64_t*>(ops);
+    const uint32_t words = uint32_t(n_ops) * uint32_t(sizeof(RegOp) / 8);
+    for (uint32_t w = tid; w < words; w += bd) dst[w] = src[w];
+  }
+  uint64_t base = 0;
+  {
+    const uint64_t tile = blockIdx.x;
+    for (int j = 0; j < p.n_out; ++j)
+      if ((tile >> j) & 1ull) base |= 1ull << p.oq[j];
+  }
+  const uint64_t variant = p.variant_base + blockIdx.y;
+  V* st = reinterpret_cast<V*>(p.states) + int64_t(blockIdx.y) * p.stride;
+  for (uint32_t c = tid; c < nchunks; c += bd) {
+    int64_t off = 0;
+    for (int j = 0; j < p.n_high; ++j)
+      if ((c >> j) & 1u) off |= int64_t(1) << p.hq[j];
+    chunkoff[c] = off;
+  }
+  __syncthreads();
+
+  // canonical mapping: register bits = top RB tile bits, so element
+  // e = tid + j * bd and consecutive threads touch consecutive addresses
+  V v[NR];
+#pragma unroll
+  for (int j = 0; j < NR; ++j) {
+    const uint32_t e = tid + uint32_t(j) * bd;
+    if (p.init_basis) {
+      v[j].x = (base == 0 && e == 0) ? R(1) : R(0);
+      v[j].y = R(0);
+    } else {
+      v[j] = st[int64_t(base) + chunkoff[e >> L] + (e & lowmask)];
+    }
+  }
+  // current mapping: thread part of the element index and register offsets
+  uint32_t tpart = tid;
+  uint32_t roff[NR];
+#pragma unroll
+  for (int j = 0; j < NR; ++j) roff[j] = uint32_t(j) * bd;
+
+  for (int i = 0; i < n_ops;) {
+    const RegOp& op = ops[i];
+    if (op.kind == ROP_REMAP) {
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < NR; ++j) s[swz(tpart | roff[j])] = v[j];
+      // new mapping: register bit k -> tile bit rpos[k]; thread bits fill the rest
+      uint32_t rmaskbits = 0;
+#pragma unroll
+      for (int k = 0; k < RB; ++k) rmaskbits |= 1u << op.rpos[k];
+      uint32_t tp = 0;
+      {
+        uint32_t t = tid;
+        for (int b = 0; b < T; ++b) {
+          if ((rmaskbits >> b) & 1u) continue;
+          tp |= (t & 1u) << b;
+          t >>= 1;
+        }
+      }
+      tpart = tp;
+#pragma unroll
+      for (int j = 0; j < NR; ++j) {
+        uint32_t o = 0;
+#pragma unroll
+        for (int k = 0; k < RB; ++k)
+          if ((j >> k) & 1) o |= 1u << op.rpos[k];
+        roff[j] = o;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < NR; ++j) v[j] = s[swz(tpart | roff[j])];
+      ++i;
+      continue;
+    }
+    const int step = op.slot >= 0 ? 2 : 1;
+    const RegOp& src = op.slot >= 0 ? ops[i + int((variant >> op.slot) & 1ull)] : op;
+    if ((base & op.omask) == op.omask && (tid & op.tmask) == op.tmask) {
+      if (op.kind == ROP_DENSE) {
+        reg_dense<R, RB>(v, op.k, op.rmask, src.m);
+      } else {
+        const double qr = src.m[0], qi = src.m[1];
+        const uint32_t rm = op.rmask;
+        if (qi == 0.0 && qr == -1.0) {
+#pragma unroll
+          for (int j = 0; j < NR; ++j)
+            if ((uint32_t(j) & rm) == rm) {
+              v[j].x = -v[j].x;
+              v[j].y = -v[j].y;
+            }
+        } else {
+#pragma unroll
+          for (int j = 0; j < NR; ++j)
+            if ((uint32_t(j) & rm) == rm) v[j] = cmul<R>(v[j], R(qr), R(qi));
+        }
+      }
+    }
+    i += step;
+  }
+
+#pragma unroll
+  for (int j = 0; j < NR; ++j) {
+    const uint32_t e = tid + uint32_t(j) * bd;
+    st[int64_t(base) + chunkoff[e >> L] + (e & lowmask)] = v[j];
+  }
+}
+
+// ---------------------------------------------------------------------------
 // merge_terms: out[s][h][l] (+)= sum_t coef[s,t] * hi[hidx[s,t]][h] * lo[lidx[s,t]][l]
 // A CTA owns `iters` row groups x C columns; each thread keeps its CC columns
 // of every lo term in registers (read once), the CTA's rows of coef*hi are
@@ -619,6 +764,59 @@ cudaError_t launch_sweep(const SweepParams& p, uint32_t n_tiles, int vb, int thr
                          int dtype) {
   return dtype == 0 ? launch_sweep_t<double>(p, n_tiles, vb, threads, stream)
                     : launch_sweep_t<float>(p, n_tiles, vb, threads, stream);
+}
+
+size_t rsweep_smem_bytes(int tile_bits, int low_bits, int dtype, int n_ops) {
+  const size_t elem = dtype == 0 ? sizeof(double2) : sizeof(float2);
+  return (size_t(1) << tile_bits) * elem + (size_t(1) << (tile_bits - low_bits)) * sizeof(int64_t) +
+         size_t(n_ops) * sizeof(RegOp);
+}
+
+template <typename R, int RB, int CAP>
+static cudaError_t launch_rsweep_rb(const RegParamsT<CAP>& p, uint32_t n_tiles, uint32_t n_states,
+                                    cudaStream_t stream) {
+  const int dt = std::is_same<R, double>::value ? 0 : 1;
+  const size_t smem = rsweep_smem_bytes(p.tile_bits, p.low_bits, dt, p.n_ops);
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(rsweep_kernel<R, RB, CAP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(smem));
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  const int threads = 1 << (p.tile_bits - RB);
+  dim3 grid(n_tiles, n_states, 1);
+  rsweep_kernel<R, RB, CAP><<<grid, threads, smem, stream>>>(p);
+  return cudaGetLastError();
+}
+
+template <typename R, int CAP>
+static cudaError_t launch_rsweep_cap(const RegParamsT<CAP>& p, int rb, uint32_t n_tiles, uint32_t n_states,
+                                     cudaStream_t stream) {
+  switch (rb) {
+    case 1: return launch_rsweep_rb<R, 1, CAP>(p, n_tiles, n_states, stream);
+    case 2: return launch_rsweep_rb<R, 2, CAP>(p, n_tiles, n_states, stream);
+    case 3: return launch_rsweep_rb<R, 3, CAP>(p, n_tiles, n_states, stream);
+    default: return launch_rsweep_rb<R, 4, CAP>(p, n_tiles, n_states, stream);
+  }
+}
+
+template <typename R>
+static cudaError_t launch_rsweep_t(const RegParams& p, int rb, uint32_t n_tiles, uint32_t n_states,
+                                   cudaStream_t stream) {
+  if (p.n_ops <= kSmallOps) {
+    static RegParamsSmall ps;  // launch copies it; callers hold capi's lock
+    std::memcpy(&ps, &p, offsetof(RegParams, ops));
+    std::memcpy(ps.ops, p.ops, sizeof(RegOp) * size_t(p.n_ops));
+    return launch_rsweep_cap<R, kSmallOps>(ps, rb, n_tiles, n_states, stream);
+  }
+  return launch_rsweep_cap<R, kMaxOpsPerLaunch>(p, rb, n_tiles, n_states, stream);
+}
+
+cudaError_t launch_rsweep(const RegParams& p, int rb, uint32_t n_tiles, uint32_t n_states, cudaStream_t stream,
+                          int dtype) {
+  return dtype == 0 ? launch_rsweep_t<double>(p, rb, n_tiles, n_states, stream)
+                    : launch_rsweep_t<float>(p, rb, n_tiles, n_states, stream);
 }
 
 template <typename R, int K, int CC>

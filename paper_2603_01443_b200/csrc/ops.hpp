@@ -58,6 +58,39 @@ using SweepParams = SweepParamsT<kMaxOpsPerLaunch>;
 using SweepParamsSmall = SweepParamsT<kSmallOps>;
 static_assert(sizeof(SweepParams) <= 32760, "kernel parameter limit");
 
+// Register-tile program (rsweep_kernel): the tile's 2^T amplitudes live in
+// registers, 2^RB per thread; register bit k of a thread's amplitude index is
+// tile bit rpos[k] of the current mapping, the thread index bits are the other
+// tile bits in ascending order. Gates act on register bits only; REMAP
+// changes which tile bits are register bits (one shared-memory transpose).
+enum : uint8_t { ROP_DENSE = 0, ROP_PHASE = 1, ROP_REMAP = 2 };
+
+struct RegOp {
+  uint8_t kind;
+  uint8_t k;          // DENSE: target register bit
+  int16_t slot;       // -1, or cut bit choosing this entry (0) / next entry (1)
+  uint32_t tmask;     // thread-index bits that must be 1 (controls / phase bits)
+  uint32_t rmask;     // register-index bits that must be 1
+  uint8_t rpos[4];    // REMAP: tile bit of each register bit
+  uint64_t omask;     // outside-tile qubits that must be 1
+  double m[8];
+};
+static_assert(sizeof(RegOp) == 88, "RegOp layout");
+
+template <int CAP>
+struct RegParamsT {
+  void* states;
+  int64_t stride;
+  uint64_t variant_base;
+  int32_t tile_bits, low_bits, n_high, n_out, n_ops, init_basis, n_states, pad;
+  int8_t hq[kMaxTileBits];
+  int8_t oq[64];
+  RegOp ops[CAP];
+};
+using RegParams = RegParamsT<kMaxOpsPerLaunch>;
+using RegParamsSmall = RegParamsT<kSmallOps>;
+static_assert(sizeof(RegParams) <= 32760, "kernel parameter limit");
+
 // merge_terms: out[s][h - row_begin][l] (+)= sum_t coef[s,t] hi[hidx[s,t]][h] lo[lidx[s,t]][l]
 constexpr int kMaxMergeTerms = 1024;
 

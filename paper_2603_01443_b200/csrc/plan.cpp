@@ -364,6 +364,144 @@ std::string sweeps_to_json(const std::vector<Sweep>& sweeps, int nq) {
 }
 
 // ---------------------------------------------------------------------------
+// register-tile lowering
+// ---------------------------------------------------------------------------
+int reg_bits_for(int tile_bits) {
+  if (tile_bits <= 2) return std::max(1, tile_bits);
+  return std::max(2, std::min(4, tile_bits - 8));
+}
+
+namespace {
+
+struct Mapping {
+  int T = 0, RB = 0;
+  int rpos[4] = {0, 0, 0, 0};
+  int reg_of[32];     // tile bit -> register bit or -1
+  int thread_of[32];  // tile bit -> thread bit or -1
+  void build() {
+    for (int b = 0; b < 32; ++b) reg_of[b] = thread_of[b] = -1;
+    for (int k = 0; k < RB; ++k) reg_of[rpos[k]] = k;
+    int m = 0;
+    for (int b = 0; b < T; ++b)
+      if (reg_of[b] < 0) thread_of[b] = m++;
+  }
+  void split(uint32_t lmask, uint32_t* tmask, uint32_t* rmask) const {
+    *tmask = 0;
+    *rmask = 0;
+    for (int b = 0; b < T; ++b)
+      if ((lmask >> b) & 1u) {
+        if (reg_of[b] >= 0) *rmask |= 1u << reg_of[b];
+        else *tmask |= 1u << thread_of[b];
+      }
+  }
+  bool canonical() const {
+    for (int k = 0; k < RB; ++k)
+      if (rpos[k] != T - RB + k) return false;
+    return true;
+  }
+};
+
+void push_remap(std::vector<RegOp>& out, Mapping& map, const int* want) {
+  RegOp r{};
+  r.kind = ROP_REMAP;
+  r.slot = -1;
+  for (int k = 0; k < map.RB; ++k) {
+    map.rpos[k] = want[k];
+    r.rpos[k] = uint8_t(want[k]);
+  }
+  map.build();
+  out.push_back(r);
+}
+
+}  // namespace
+
+std::vector<RegOp> reg_program(const Sweep& sw, int RB) {
+  RB = std::max(1, std::min(RB, 4));
+  const int T = sw.tile_bits;
+  Mapping map;
+  map.T = T;
+  map.RB = RB;
+  for (int k = 0; k < RB; ++k) map.rpos[k] = T - RB + k;
+  map.build();
+  std::vector<RegOp> out;
+  const auto& E = sw.entries;
+  for (size_t i = 0; i < E.size();) {
+    const SweepOp& e = E[i];
+    const size_t w = e.slot >= 0 ? 2 : 1;
+    if (e.type == OP_DENSE && map.reg_of[e.target] < 0) {
+      // new register set: this target and the next distinct dense targets
+      int want[4];
+      int n = 0;
+      for (size_t j = i; j < E.size() && n < RB; j += (E[j].slot >= 0 ? 2 : 1)) {
+        if (E[j].type != OP_DENSE) continue;
+        bool dup = false;
+        for (int a = 0; a < n; ++a) dup |= want[a] == E[j].target;
+        if (!dup) want[n++] = E[j].target;
+      }
+      for (int k = 0; k < RB && n < RB; ++k) {  // keep current register bits
+        bool dup = false;
+        for (int a = 0; a < n; ++a) dup |= want[a] == map.rpos[k];
+        if (!dup) want[n++] = map.rpos[k];
+      }
+      for (int b = 0; b < T && n < RB; ++b) {
+        bool dup = false;
+        for (int a = 0; a < n; ++a) dup |= want[a] == b;
+        if (!dup) want[n++] = b;
+      }
+      for (int a = 1; a < RB; ++a)  // insertion sort (RB <= 4)
+        for (int b = a; b > 0 && want[b] < want[b - 1]; --b) std::swap(want[b], want[b - 1]);
+      push_remap(out, map, want);
+    }
+    for (size_t j = 0; j < w; ++j) {
+      const SweepOp& x = E[i + j];
+      RegOp r{};
+      r.kind = x.type == OP_DENSE ? ROP_DENSE : ROP_PHASE;
+      r.slot = int16_t(x.slot);
+      r.k = x.type == OP_DENSE ? uint8_t(map.reg_of[x.target]) : 0;
+      map.split(x.lmask, &r.tmask, &r.rmask);
+      r.omask = x.omask;
+      for (int q = 0; q < 8; ++q) r.m[q] = x.m[q];
+      out.push_back(r);
+    }
+    i += w;
+  }
+  if (!map.canonical()) {
+    int want[4];
+    for (int k = 0; k < RB; ++k) want[k] = T - RB + k;
+    push_remap(out, map, want);
+  }
+  return out;
+}
+
+std::string reg_programs_to_json(const std::vector<Sweep>& sweeps, int nq) {
+  std::ostringstream os;
+  os.precision(17);
+  os << "{\"nq\":" << nq << ",\"sweeps\":[";
+  for (size_t s = 0; s < sweeps.size(); ++s) {
+    const Sweep& sw = sweeps[s];
+    const int RB = reg_bits_for(sw.tile_bits);
+    const std::vector<RegOp> prog = reg_program(sw, RB);
+    if (s) os << ",";
+    os << "{\"T\":" << sw.tile_bits << ",\"L\":" << sw.low_bits << ",\"RB\":" << RB << ",\"hq\":[";
+    for (size_t i = 0; i < sw.hq.size(); ++i) os << (i ? "," : "") << sw.hq[i];
+    os << "],\"oq\":[";
+    for (size_t i = 0; i < sw.oq.size(); ++i) os << (i ? "," : "") << sw.oq[i];
+    os << "],\"ops\":[";
+    for (size_t i = 0; i < prog.size(); ++i) {
+      const RegOp& r = prog[i];
+      os << (i ? "," : "") << "{\"kind\":" << int(r.kind) << ",\"k\":" << int(r.k) << ",\"slot\":" << r.slot
+         << ",\"tmask\":" << r.tmask << ",\"rmask\":" << r.rmask << ",\"omask\":" << r.omask << ",\"rpos\":["
+         << int(r.rpos[0]) << "," << int(r.rpos[1]) << "," << int(r.rpos[2]) << "," << int(r.rpos[3]) << "],\"m\":[";
+      for (int k = 0; k < 8; ++k) os << (k ? "," : "") << r.m[k];
+      os << "]}";
+    }
+    os << "]}";
+  }
+  os << "]}";
+  return os.str();
+}
+
+// ---------------------------------------------------------------------------
 // chain contraction plan
 // ---------------------------------------------------------------------------
 bool plan_chain(int n, const int32_t* seg_nq, const int32_t* seg_ncuts, const int32_t* seg_cut_ids,

@@ -54,6 +54,13 @@ int sweep_max_group(int tile_bits);
 
 std::string sweeps_to_json(const std::vector<Sweep>& sweeps, int nq);
 
+// Register-tile lowering of one sweep: register bits per thread for a tile of
+// 2^T amplitudes, and the op list translated to register coordinates with the
+// REMAPs it needs (ends in the canonical mapping, register bits = top bits).
+int reg_bits_for(int tile_bits);
+std::vector<RegOp> reg_program(const Sweep& sw, int reg_bits);
+std::string reg_programs_to_json(const std::vector<Sweep>& sweeps, int nq);
+
 // ---- merge chain -----------------------------------------------------------
 struct MergeStep {
   int hi_buf, lo_buf, out_buf;  // buffer ids: 0..n-1 segment states, n.. workspace

@@ -191,3 +191,85 @@ def test_compute_entry_points_fail_loudly_without_gpu():
 
     with pytest.raises(NativeUnavailableError):
         engine.simulate(C.Circuit(2, [C.h(0)]))
+
+
+def execute_reg_programs(plan, nq, variant=0):
+    """Interpret the register-tile programs (rsweep kernel input) on a full
+    numpy state: tile bit b is qubit b (< L) or hq[b - L]; register bit k is
+    tile bit rpos[k]; thread-index bit m is the m-th non-register tile bit."""
+    amps = orc.zero_state(nq)
+    idx = np.arange(1 << nq, dtype=np.int64)
+    for sw in plan["sweeps"]:
+        T, L, RB = sw["T"], sw["L"], sw["RB"]
+        glob = list(range(L)) + list(sw["hq"])
+        rpos = [T - RB + k for k in range(RB)]
+        ops = sw["ops"]
+        i = 0
+        while i < len(ops):
+            op = ops[i]
+            if op["kind"] == 2:
+                rpos = op["rpos"][:RB]
+                i += 1
+                continue
+            src, step = op, 1
+            if op["slot"] >= 0:
+                src = ops[i + ((variant >> op["slot"]) & 1)]
+                step = 2
+            tbits = [b for b in range(T) if b not in rpos]
+            mask = op["omask"]
+            for m in range(32):
+                if (op["tmask"] >> m) & 1:
+                    mask |= 1 << glob[tbits[m]]
+            for k in range(RB):
+                if (op["rmask"] >> k) & 1:
+                    mask |= 1 << glob[rpos[k]]
+            mm = np.array(src["m"]).reshape(4, 2)
+            mm = mm[:, 0] + 1j * mm[:, 1]
+            sel = (idx & mask) == mask
+            if op["kind"] == 1:
+                amps[sel] *= mm[0]
+            else:
+                t = glob[rpos[op["k"]]]
+                zero = sel & (((idx >> t) & 1) == 0)
+                i0 = idx[zero]
+                i1 = i0 | (1 << t)
+                a, b = amps[i0].copy(), amps[i1].copy()
+                amps[i0] = mm[0] * a + mm[1] * b
+                amps[i1] = mm[2] * a + mm[3] * b
+            i += step
+        assert rpos == [T - RB + k for k in range(RB)], "program must end in the canonical mapping"
+    return amps
+
+
+def _reg_plan(nq, table, slots=None, tile_bits=0):
+    _native.set_option("plan_json", 1)
+    try:
+        return json.loads(_native.sweep_plan_json(nq, table, slots, tile_bits=tile_bits))
+    finally:
+        _native.set_option("plan_json", 0)
+
+
+@pytest.mark.parametrize("tile_bits", [4, 6, 9, 12])
+@pytest.mark.parametrize("q,d,n,c,seed", [(9, 4, 3, 4, 1), (14, 3, 2, 2, 2), (16, 3, 4, 3, 5)])
+def test_register_programs_reproduce_oracle(q, d, n, c, seed, tile_bits):
+    circ = G.build_brickwall(G.BrickwallSpec(q, d, n, c, seed))
+    plan = _reg_plan(q, circ.table, tile_bits=tile_bits)
+    got = execute_reg_programs(plan, q)
+    ref = orc.simulate(q, circ.kinds, circ.qa, circ.qb, circ.params)
+    assert np.abs(got - ref).max() < 1e-12
+
+
+@pytest.mark.parametrize("key", ["stair_q8_n4_b2", "stair_q6_n2_b3", "shadow_q9_d4_n3_c4_s3",
+                                 "stair_q12_n3_b1"])
+def test_register_programs_of_variant_templates(golden, key):
+    q, n = int(golden[f"{key}/q"]), int(golden[f"{key}/n"])
+    circ = C.Circuit.from_table(q, C.GateTable(golden[f"{key}/kinds"], golden[f"{key}/qa"],
+                                               golden[f"{key}/qb"]))
+    subs = K.decompose(circ, K.plan_cut(circ, n))
+    for fam in subs.segments:
+        for tb in (2, 3, 0):
+            plan = _reg_plan(fam.num_qubits, fam.template, fam.slots, tile_bits=tb)
+            ref = golden[f"{key}/seg{fam.segment}/states"]
+            for v in range(fam.num_variants):
+                got = execute_reg_programs(plan, fam.num_qubits, v)
+                assert np.abs(got - ref[v]).max() < 1e-12
