@@ -25,6 +25,9 @@ cudaError_t launch_rsweep(const RegParams& p, int rb, uint32_t n_tiles, uint32_t
 cudaError_t launch_merge(const MergeParams& p, int K, dim3 grid, int threads, size_t smem, bool wide,
                          cudaStream_t stream, int dtype);
 int merge_cols_per_thread(int K);
+cudaError_t launch_merge_dmma(const MergeParams& p, int K, dim3 grid, int threads, size_t smem,
+                              cudaStream_t stream);
+int merge_dmma_cols_per_warp(int K);
 cudaError_t launch_init_basis(void* states, int64_t len, int64_t n_states, int64_t index, int dtype,
                               cudaStream_t stream);
 cudaError_t launch_reduce(const void* a, const void* b, int64_t n, int mode, int dtype, double2* scratch,
@@ -51,6 +54,7 @@ struct Options {
   int64_t merge_streaming = 1;
   int64_t merge_iters = 0;
   int64_t vb = 0;  // states per CTA in a variant batch (0 = auto)
+  int64_t merge_dmma = 1;  // FP64 tensor-core merge for K = 8, 16 (complex128)
   int64_t engine = 1;      // 1: register-tile kernel (rsweep), 0: shared-memory tile kernel (sweep)
   int64_t plan_json = 0;   // cs_sweep_plan_json: 0 sweeps, 1 register programs
 } g_opt;
@@ -222,6 +226,11 @@ std::shared_ptr<const Program> build_schedule(int nq, const uint8_t* kinds, cons
   return prog;
 }
 
+bool dmma_eligible(int K, int dtype, int64_t lo_len) {
+  return g_opt.merge_dmma && dtype == CS_C128 && (K == 8 || K == 16 || K == 32 || K == 64) &&
+         lo_len >= merge_dmma_cols_per_warp(K);
+}
+
 // Launch one merge_terms problem whose K is one instantiated width.
 int merge_launch_one(int S, int Kc, const int32_t* hidx, const int32_t* lidx, const double* coef,
                      int64_t stride_terms, const void* hi, int64_t hi_len, const void* lo, int64_t lo_len,
@@ -229,6 +238,65 @@ int merge_launch_one(int S, int Kc, const int32_t* hidx, const int32_t* lidx, co
                      int dtype, cudaStream_t stream) {
   // stride_terms: distance between consecutive slots' term lists in hidx/lidx
   const int threads = 256;
+  const size_t eb0 = elem_bytes(dtype);
+  if (dmma_eligible(Kc, dtype, lo_len)) {
+    // tensor-core path: 8 warps over ncg column groups of (16, 8 or 4)
+    // complex columns; a CTA spans >= 128 columns so row staging is amortised
+    const int64_t cw = merge_dmma_cols_per_warp(Kc);
+    const int64_t ncg = std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(8, 256 / cw), lo_len / cw));
+    const int64_t C = cw * ncg;
+    const int64_t nrows = row_end - row_begin;
+    const int RS = 2 * Kc + 4;
+    const int64_t rbg = 8 / (merge_dmma_cols_per_warp(Kc) / 4);  // row blocks processed together
+    int64_t iters = std::max<int64_t>(1, std::min<int64_t>((96 * 1024) / (8 * RS * 8), (nrows + 7) / 8));
+    iters = std::min<int64_t>(iters, 64);
+    // keep at least two CTAs per SM for small products
+    const int64_t col_blocks = std::max<int64_t>(1, lo_len / C);
+    iters = std::min<int64_t>(iters, std::max<int64_t>(1, ((nrows + 7) / 8) * col_blocks * S / (2 * 148)));
+    iters = std::max<int64_t>(rbg, iters / rbg * rbg);
+    const int64_t rows_cta = iters * 8;
+    const size_t smem = size_t(rows_cta) * size_t(RS) * sizeof(double);
+    const int slots_per_launch = std::max(1, kMaxMergeTerms / Kc);
+    static MergeParams pd;
+    static std::mutex pdm;
+    std::lock_guard<std::mutex> lk(pdm);
+    for (int s0 = 0; s0 < S; s0 += slots_per_launch) {
+      const int sc = std::min(slots_per_launch, S - s0);
+      std::memset(&pd, 0, offsetof(MergeParams, hidx));
+      pd.hi = hi;
+      pd.lo = lo;
+      pd.hi_len = hi_len;
+      pd.lo_len = lo_len;
+      pd.out_slot_stride = out_slot_stride;
+      pd.S = sc;
+      pd.K = Kc;
+      pd.accumulate = accumulate;
+      pd.iters = int32_t(iters);
+      pd.cols = int32_t(ncg);
+      pd.streaming = int32_t(g_opt.merge_streaming);
+      for (int s = 0; s < sc; ++s)
+        for (int t = 0; t < Kc; ++t) {
+          const int64_t src = int64_t(s0 + s) * stride_terms + t;
+          pd.hidx[s * Kc + t] = hidx[src];
+          pd.lidx[s * Kc + t] = lidx[src];
+          pd.coef[2 * (s * Kc + t)] = coef[2 * src];
+          pd.coef[2 * (s * Kc + t) + 1] = coef[2 * src + 1];
+        }
+      const int64_t max_rows_per_launch = rows_cta * 65535;
+      for (int64_t r0 = row_begin; r0 < row_end; r0 += max_rows_per_launch) {
+        const int64_t r1 = std::min(row_end, r0 + max_rows_per_launch);
+        pd.row_begin = r0;
+        pd.row_end = r1;
+        char* base_out = static_cast<char*>(out) + size_t(s0) * size_t(out_slot_stride) * eb0;
+        pd.out = base_out + size_t(r0 - row_begin) * size_t(lo_len) * eb0;
+        dim3 grid(unsigned(lo_len / C), unsigned((r1 - r0 + rows_cta - 1) / rows_cta), unsigned(sc));
+        cudaError_t e = launch_merge_dmma(pd, Kc, grid, threads, smem, stream);
+        g_launches.fetch_add(1);
+        if (e != cudaSuccess) return cuda_fail(e, "merge_dmma_kernel launch");
+      }
+    }
+    return CS_OK;
+  }
   const int CC = merge_cols_per_thread(Kc);
   const int64_t C = int64_t(threads) * CC;
   const int64_t W = lo_len;
@@ -320,12 +388,15 @@ int merge_terms_impl(int S, int K, const int32_t* hidx, const int32_t* lidx, con
     }
     return CS_OK;
   }
-  // split K into instantiated chunk widths {16, 8, 4, 2, 1}
+  // split K into instantiated chunk widths: {64, 32} on the tensor-core path,
+  // then {16, 8, 4, 2, 1}
   int t0 = 0;
   int acc = accumulate;
   while (t0 < K) {
     int rem = K - t0;
     int kc = rem >= 16 ? 16 : rem >= 8 ? 8 : rem >= 4 ? 4 : rem >= 2 ? 2 : 1;
+    if (rem >= 64 && dmma_eligible(64, dtype, lo_len)) kc = 64;
+    else if (rem >= 32 && dmma_eligible(32, dtype, lo_len)) kc = 32;
     int rc = merge_launch_one(S, kc, hidx + t0, lidx + t0, coef + 2 * t0, K, hi, hi_len, lo, lo_len, row_begin,
                               row_end, out, out_slot_stride, acc, dtype, stream);
     if (rc != CS_OK) return rc;
@@ -377,6 +448,8 @@ int cs_set_option(const char* key, int64_t value) {
   } else if (k == "sweep_minb") {
     if (value < 2 || value > 4) return fail(CS_ERR_INVALID, "sweep_minb must be 2, 3 or 4");
     g_sweep_minb = int(value);
+  } else if (k == "merge_dmma") {
+    g_opt.merge_dmma = value ? 1 : 0;
   } else if (k == "engine") {
     if (value != 0 && value != 1) return fail(CS_ERR_INVALID, "engine must be 0 or 1");
     g_opt.engine = value;
@@ -401,6 +474,7 @@ int64_t cs_get_option(const char* key) {
   if (k == "merge_iters") return g_opt.merge_iters;
   if (k == "vb") return g_opt.vb;
   if (k == "engine") return g_opt.engine;
+  if (k == "merge_dmma") return g_opt.merge_dmma;
   if (k == "plan_json") return g_opt.plan_json;
   if (k == "sweep_minb") return g_sweep_minb;
   return -1;

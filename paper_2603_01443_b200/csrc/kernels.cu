@@ -620,6 +620,154 @@ __global__ void __launch_bounds__(256, 2) merge_kernel(const __grid_constant__ M
 }
 
 // ---------------------------------------------------------------------------
+// merge_dmma_kernel: the same product for complex128 with K = 8 or 16 terms,
+// where 4 FMA per term per amplitude make the DFMA version FP64-issue-bound.
+// Written as a real GEMM on the FP64 tensor path (mma.sync m8n8k4 f64):
+//   out[h][2l+v] = sum_k Bc[h][k] * Ac[k][2l+v],  k = 2t+u (2K real terms)
+//   Bc[h][2t+u]   = (re, im)[u] of coef_t * hi_t[h]   (the staged rows)
+//   Ac[2t][2l+v]  = (re, im)[v] of lo_t[l];  Ac[2t+1][2l] = -im, [2l+1] = re
+// so an accumulator fragment (row, real cols 2c, 2c+1) is exactly one complex
+// output and is stored as one 16-byte evict-first store. Each warp owns 8 rows
+// x 4*NT complex columns per row block; its Ac fragments stay in registers.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <int KT, int NT>
+__global__ void __launch_bounds__(256, 2) merge_dmma_kernel(const __grid_constant__ MergeParams p) {
+  constexpr int KR = 2 * KT;          // real inner dimension
+  constexpr int KS = KR / 4;          // mma k-steps
+  constexpr int RS = KR + 4;          // padded smem row stride (doubles): conflict-free A fragments
+  constexpr int COLS_W = 4 * NT;      // complex columns per warp
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* bsd = reinterpret_cast<double*>(smem_raw);
+  const int sl = blockIdx.z;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  const int nwarps = blockDim.x >> 5;
+  const int64_t W = p.lo_len;
+  const int rows_cta = p.iters * 8;
+  const int64_t row0 = p.row_begin + int64_t(blockIdx.y) * rows_cta;
+  const int32_t* hidx = p.hidx + sl * KT;
+  const int32_t* lidx = p.lidx + sl * KT;
+  const double* coef = p.coef + 2 * sl * KT;
+  const double2* hi = reinterpret_cast<const double2*>(p.hi);
+  const double2* lo = reinterpret_cast<const double2*>(p.lo);
+
+  for (int idx = tid; idx < rows_cta * KT; idx += blockDim.x) {
+    const int r = idx / KT;
+    const int t = idx - r * KT;
+    const int64_t h = row0 + r;
+    double2 b = make_double2(0.0, 0.0);
+    if (h < p.row_end) {
+      const double2 hv = __ldg(hi + int64_t(hidx[t]) * p.hi_len + h);
+      const double cr = coef[2 * t], ci = coef[2 * t + 1];
+      b.x = hv.x * cr - hv.y * ci;
+      b.y = hv.x * ci + hv.y * cr;
+    }
+    bsd[r * RS + 2 * t] = b.x;
+    bsd[r * RS + 2 * t + 1] = b.y;
+  }
+
+  __syncthreads();
+  double2* out = reinterpret_cast<double2*>(p.out) + int64_t(sl) * p.out_slot_stride;
+  const int arow = lane >> 2;
+  const int acol = lane & 3;
+  // RB row blocks at once: NT * RB independent accumulator chains per warp
+  // hide the latency of the dependent m8n8k4 accumulation
+  constexpr int RB = 8 / NT;
+  // the CTA spans p.cols column groups of COLS_W complex columns; warps take
+  // them round-robin and reuse the staged rows for each
+  const int ncg = p.cols;
+  for (int cg = warp; cg < ncg; cg += nwarps) {
+    const int64_t col_w = (int64_t(blockIdx.x) * ncg + cg) * COLS_W;
+    // B-operand fragments: lane holds Ac[k = s*4 + (lane&3)][n = lane>>2] of n-tile j
+    double bop[NT][KS];
+    {
+      const int n = lane >> 2;
+      const int v = n & 1;
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        const int64_t l = col_w + j * 4 + (n >> 1);
+#pragma unroll
+        for (int s2 = 0; s2 < KS; ++s2) {
+          const int k = s2 * 4 + (lane & 3);
+          const int t = k >> 1;
+          const int u = k & 1;
+          const double2 a = __ldg(lo + int64_t(lidx[t]) * W + l);
+          bop[j][s2] = u == 0 ? (v == 0 ? a.x : a.y) : (v == 0 ? -a.y : a.x);
+        }
+      }
+    }
+    for (int rb0 = 0; rb0 < p.iters; rb0 += RB) {
+      double acc[RB][NT][2];
+#pragma unroll
+      for (int r = 0; r < RB; ++r)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) acc[r][j][0] = acc[r][j][1] = 0.0;
+#pragma unroll
+      for (int s2 = 0; s2 < KS; ++s2) {
+#pragma unroll
+        for (int r = 0; r < RB; ++r) {
+          const double a = bsd[((rb0 + r) * 8 + arow) * RS + s2 * 4 + acol];
+#pragma unroll
+          for (int j = 0; j < NT; ++j) dmma884(acc[r][j][0], acc[r][j][1], a, bop[j][s2]);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < RB; ++r) {
+        const int64_t h = row0 + (rb0 + r) * 8 + arow;
+        if (rb0 + r >= p.iters || h >= p.row_end) continue;
+        double2* dst = out + (h - p.row_begin) * W + col_w + acol;
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          double2 v = make_double2(acc[r][j][0], acc[r][j][1]);
+          if (p.accumulate) {
+            const double2 prev = dst[j * 4];
+            v.x += prev.x;
+            v.y += prev.y;
+          }
+          if (p.streaming) __stcs(dst + j * 4, v);
+          else dst[j * 4] = v;
+        }
+      }
+    }
+  }
+}
+
+template <int KT, int NT>
+static cudaError_t launch_dmma_kt(const MergeParams& p, dim3 grid, int threads, size_t smem, cudaStream_t stream) {
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(merge_dmma_kernel<KT, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(smem));
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  merge_dmma_kernel<KT, NT><<<grid, threads, smem, stream>>>(p);
+  return cudaGetLastError();
+}
+
+// complex columns per warp for each instantiated K (register budget of the
+// B-operand fragments: NT * K / 2 doubles per thread)
+int merge_dmma_cols_per_warp(int K) { return K <= 16 ? 16 : (K == 32 ? 8 : 4); }
+
+cudaError_t launch_merge_dmma(const MergeParams& p, int K, dim3 grid, int threads, size_t smem,
+                              cudaStream_t stream) {
+  switch (K) {
+    case 8: return launch_dmma_kt<8, 4>(p, grid, threads, smem, stream);
+    case 16: return launch_dmma_kt<16, 4>(p, grid, threads, smem, stream);
+    case 32: return launch_dmma_kt<32, 2>(p, grid, threads, smem, stream);
+    case 64: return launch_dmma_kt<64, 1>(p, grid, threads, smem, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // small utilities
 // ---------------------------------------------------------------------------
 template <typename R>
