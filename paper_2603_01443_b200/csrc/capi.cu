@@ -163,7 +163,7 @@ std::unordered_map<std::string, std::shared_ptr<const Program>> g_cache;
 // block (never splitting a slotted pair); the register kernel's chunks are
 // smaller because its REMAPs add entries.
 void build_launches(Program& prog) {
-  const size_t cap = prog.engine == 1 ? 170 : size_t(kMaxOpsPerLaunch);
+  const size_t cap = prog.engine == 1 ? size_t(kMaxRegOps / 2 - 4) : size_t(kMaxOpsPerLaunch);
   for (size_t s = 0; s < prog.sweeps.size(); ++s) {
     const Sweep& sw = prog.sweeps[s];
     size_t i0 = 0;
@@ -527,7 +527,7 @@ int cs_sim_batch(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int6
       void* sp = static_cast<char*>(states) + size_t(v0) * size_t(state_stride) * elem_bytes(dtype);
       cudaError_t e;
       if (prog->engine == 1) {
-        if (ln.reg.size() > size_t(kMaxOpsPerLaunch)) return fail(CS_ERR_INTERNAL, "register program too long");
+        if (ln.reg.size() > size_t(kMaxRegOps)) return fail(CS_ERR_INTERNAL, "register program too long");
         std::memset(&rp, 0, offsetof(RegParams, ops));
         rp.states = sp;
         rp.stride = state_stride;

@@ -354,14 +354,25 @@ __global__ void __launch_bounds__(256, MINB) sweep_kernel(const __grid_constant_
 // ---------------------------------------------------------------------------
 template <typename R, int RB>
 __device__ __forceinline__ void reg_dense(vec2_t<R> (&v)[1 << RB], int k, uint32_t rmask, const double* m) {
+  const double2 q0 = reinterpret_cast<const double2*>(m)[0];
+  const double2 q1 = reinterpret_cast<const double2*>(m)[1];
+  const double2 q2 = reinterpret_cast<const double2*>(m)[2];
+  const double2 q3 = reinterpret_cast<const double2*>(m)[3];
+  const double mm[8] = {q0.x, q0.y, q1.x, q1.y, q2.x, q2.y, q3.x, q3.y};
 #pragma unroll
   for (int kk = 0; kk < RB; ++kk) {
     if (kk != k) continue;
+    if (rmask == 0) {
 #pragma unroll
-    for (int j = 0; j < (1 << RB); ++j) {
-      if ((j >> kk) & 1) continue;
-      if ((uint32_t(j) & rmask) != rmask) continue;
-      apply2x2<R>(v[j], v[j | (1 << kk)], m);
+      for (int j = 0; j < (1 << RB); ++j)
+        if (!((j >> kk) & 1)) apply2x2<R>(v[j], v[j | (1 << kk)], mm);
+    } else {
+#pragma unroll
+      for (int j = 0; j < (1 << RB); ++j) {
+        if ((j >> kk) & 1) continue;
+        if ((uint32_t(j) & rmask) != rmask) continue;
+        apply2x2<R>(v[j], v[j | (1 << kk)], mm);
+      }
     }
   }
 }
@@ -378,7 +389,7 @@ __global__ void __launch_bounds__(512) rsweep_kernel(const __grid_constant__ Reg
   const uint32_t nchunks = 1u << (T - L);
   const uint32_t lowmask = (1u << L) - 1u;
   int64_t* chunkoff = reinterpret_cast<int64_t*>(smem_raw + sizeof(V) * size_t(n));
-  RegOp* ops = reinterpret_cast<RegOp*>(smem_raw + sizeof(V) * size_t(n) + sizeof(int64_t) * size_t(nchunks));
+  RegOp* ops = reinterpret_cast<RegOp*>(smem_raw + ((sizeof(V) * size_t(n) + sizeof(int64_t) * size_t(nchunks) + 15) & ~size_t(15)));
   const uint32_t tid = threadIdx.x;
   const uint32_t bd = blockDim.x;  // = 2^(T - RB)
   const int n_ops = p.n_ops;
@@ -433,16 +444,16 @@ __global__ void __launch_bounds__(512) rsweep_kernel(const __grid_constant__ Reg
       uint32_t rmaskbits = 0;
 #pragma unroll
       for (int k = 0; k < RB; ++k) rmaskbits |= 1u << op.rpos[k];
-      uint32_t tp = 0;
-      {
-        uint32_t t = tid;
-        for (int b = 0; b < T; ++b) {
-          if ((rmaskbits >> b) & 1u) continue;
-          tp |= (t & 1u) << b;
-          t >>= 1;
-        }
+      // thread bits fill the non-register tile bits in ascending order:
+      // insert a zero at each (ascending) register position
+      uint32_t tp = tid;
+#pragma unroll
+      for (int k = 0; k < RB; ++k) {
+        const uint32_t below = (1u << op.rpos[k]) - 1u;
+        tp = ((tp & ~below) << 1) | (tp & below);
       }
       tpart = tp;
+      (void)rmaskbits;
 #pragma unroll
       for (int j = 0; j < NR; ++j) {
         uint32_t o = 0;
@@ -916,8 +927,8 @@ cudaError_t launch_sweep(const SweepParams& p, uint32_t n_tiles, int vb, int thr
 
 size_t rsweep_smem_bytes(int tile_bits, int low_bits, int dtype, int n_ops) {
   const size_t elem = dtype == 0 ? sizeof(double2) : sizeof(float2);
-  return (size_t(1) << tile_bits) * elem + (size_t(1) << (tile_bits - low_bits)) * sizeof(int64_t) +
-         size_t(n_ops) * sizeof(RegOp);
+  const size_t head = (size_t(1) << tile_bits) * elem + (size_t(1) << (tile_bits - low_bits)) * sizeof(int64_t);
+  return ((head + 15) & ~size_t(15)) + size_t(n_ops) * sizeof(RegOp);
 }
 
 template <typename R, int RB, int CAP>
@@ -958,7 +969,7 @@ static cudaError_t launch_rsweep_t(const RegParams& p, int rb, uint32_t n_tiles,
     std::memcpy(ps.ops, p.ops, sizeof(RegOp) * size_t(p.n_ops));
     return launch_rsweep_cap<R, kSmallOps>(ps, rb, n_tiles, n_states, stream);
   }
-  return launch_rsweep_cap<R, kMaxOpsPerLaunch>(p, rb, n_tiles, n_states, stream);
+  return launch_rsweep_cap<R, kMaxRegOps>(p, rb, n_tiles, n_states, stream);
 }
 
 cudaError_t launch_rsweep(const RegParams& p, int rb, uint32_t n_tiles, uint32_t n_states, cudaStream_t stream,

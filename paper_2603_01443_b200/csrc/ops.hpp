@@ -65,7 +65,7 @@ static_assert(sizeof(SweepParams) <= 32760, "kernel parameter limit");
 // changes which tile bits are register bits (one shared-memory transpose).
 enum : uint8_t { ROP_DENSE = 0, ROP_PHASE = 1, ROP_REMAP = 2 };
 
-struct RegOp {
+struct alignas(16) RegOp {
   uint8_t kind;
   uint8_t k;          // DENSE: target register bit
   int16_t slot;       // -1, or cut bit choosing this entry (0) / next entry (1)
@@ -73,9 +73,11 @@ struct RegOp {
   uint32_t rmask;     // register-index bits that must be 1
   uint8_t rpos[4];    // REMAP: tile bit of each register bit
   uint64_t omask;     // outside-tile qubits that must be 1
-  double m[8];
+  uint64_t pad;
+  double m[8];        // 16-byte aligned: four 128-bit shared-memory loads
 };
-static_assert(sizeof(RegOp) == 88, "RegOp layout");
+static_assert(sizeof(RegOp) == 96, "RegOp layout");
+constexpr int kMaxRegOps = 320;        // RegParams under the 32 KiB param limit
 
 template <int CAP>
 struct RegParamsT {
@@ -87,7 +89,7 @@ struct RegParamsT {
   int8_t oq[64];
   RegOp ops[CAP];
 };
-using RegParams = RegParamsT<kMaxOpsPerLaunch>;
+using RegParams = RegParamsT<kMaxRegOps>;
 using RegParamsSmall = RegParamsT<kSmallOps>;
 static_assert(sizeof(RegParams) <= 32760, "kernel parameter limit");
 

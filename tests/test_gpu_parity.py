@@ -333,3 +333,15 @@ def test_q34_shard_sampled_vs_oracle(cb):
         assert np.abs(got - want).max() < TOL
         del out
         torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("world,q,d", [(2, 14, 6), (8, 16, 5), (4, 20, 4)])
+def test_distributed_uncut_emulated_on_one_gpu(cb, world, q, d):
+    """The q >= 33 distributed simulator's schedule and per-rank gate tables,
+    all ranks in lockstep on one GPU (exchange = device copy)."""
+    from paper_2603_01443_b200.distributed import simulate_emulated
+
+    circ = cb.build_brickwall(cb.BrickwallSpec(q, d, 2, 2, world))
+    got = simulate_emulated(circ, world).cpu().numpy()
+    ref = orc.simulate(q, circ.kinds, circ.qa, circ.qb, circ.params)
+    assert np.abs(got - ref).max() < TOL
