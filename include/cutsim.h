@@ -50,7 +50,11 @@ int cs_device_count(int32_t* count);
 /* Options: "tile_bits" (multi-sweep tile, default 12 for c128),
  * "low_bits" (contiguous low qubits per tile, default 5), "fuse" (1q gate
  * fusion, default 1), "threads" (0 = auto), "merge_streaming" (evict-first
- * output stores, default 1), "merge_iters" (0 = auto). */
+ * output stores, default 1), "merge_iters" (0 = auto), "merge_dmma" (FP64
+ * tensor-core merge for K = 8..64, default 1), "engine" (1 register-tile
+ * sweep kernel, 0 shared-memory tile kernel), "jit" (0 never, 1 from a
+ * program's second use, 2 always: NVRTC-specialised sweep kernels),
+ * "jit_max_cost", "vb", "sweep_minb", "plan_json" (tuning / testing). */
 int cs_set_option(const char* key, int64_t value);
 int64_t cs_get_option(const char* key);
 
@@ -80,6 +84,13 @@ int cs_sim_batch(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int6
 int cs_sweep_plan_json(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int64_t* qb,
                        const double* params, const int32_t* slots, int64_t n_gates,
                        int32_t tile_bits, int32_t dtype, char* buf, int64_t buflen, int64_t* needed);
+
+/* Host-only self-test of the NVRTC path: schedule the gate table as
+ * cs_sim_batch would, emit the specialised sweep kernels and compile them to
+ * an sm_100a CUBIN (no device needed). *cubin_bytes = CUBIN size. */
+int cs_jit_selftest(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int64_t* qb,
+                    const double* params, const int32_t* slots, int64_t n_gates, int64_t n_states,
+                    int32_t dtype, int64_t* cubin_bytes);
 
 /* out[s][h - row_begin][l] (+)= sum_{t<K} coef[s,t] * hi[hidx[s,t]][h] * lo[lidx[s,t]][l]
  * for h in [row_begin, row_end), l in [0, lo_len); hi states have hi_len

@@ -49,6 +49,7 @@ SIGNATURES = {
                                     _i32, _vp]),
     "cs_sweep_plan_json": (ctypes.c_int, [_i32, _vp, _vp, _vp, _vp, _vp, _i64, _i32, _i32, _vp, _i64,
                                           _vp]),
+    "cs_jit_selftest": (ctypes.c_int, [_i32, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i32, _vp]),
     "cs_merge_terms": (ctypes.c_int, [_i32, _i32, _vp, _vp, _vp, _vp, _i64, _vp, _i64, _i64, _i64,
                                       _vp, _i64, _i32, _i32, _vp]),
     "cs_merge_chain_plan": (ctypes.c_int, [_i32, _vp, _vp, _vp, _i32, _vp, _vp, _i32, _i32, _vp, _vp,
@@ -147,6 +148,18 @@ def sweep_plan_json(nq, table, slots=None, tile_bits=0, dtype=CS_C128) -> str:
     check(lib.cs_sweep_plan_json(nq, ptr(k), ptr(qa), ptr(qb), ptr(prm), ptr(sl), len(k), tile_bits,
                                  dtype, buf, int(need[0]), ptr(need)), "cs_sweep_plan_json")
     return buf.value.decode()
+
+
+def jit_selftest(nq, table, slots=None, n_states=1, dtype=CS_C128) -> int:
+    """Host-only: compile the NVRTC-specialised sweep kernels; CUBIN bytes."""
+    lib = load()
+    k = np.ascontiguousarray(table.kinds, dtype=np.uint8)
+    qa, qb, prm = c_i64(table.qa), c_i64(table.qb), c_f64(table.params)
+    sl = c_i32(slots) if slots is not None else None
+    out = np.zeros(1, np.int64)
+    check(lib.cs_jit_selftest(nq, ptr(k), ptr(qa), ptr(qb), ptr(prm), ptr(sl), len(k), n_states, dtype,
+                              ptr(out)), "cs_jit_selftest")
+    return int(out[0])
 
 
 def chain_plan(n, seg_nq, seg_ncuts, seg_cut_ids, c_total, cut_boundary, term_coef,

@@ -14,6 +14,7 @@
 #include "../../include/cutsim.h"
 #include "ops.hpp"
 #include "plan.hpp"
+#include "jit.hpp"
 
 namespace cutsim {
 extern int g_sweep_minb;
@@ -56,6 +57,8 @@ struct Options {
   int64_t vb = 0;  // states per CTA in a variant batch (0 = auto)
   int64_t merge_dmma = 1;  // FP64 tensor-core merge for K = 8, 16 (complex128)
   int64_t engine = 1;      // 1: register-tile kernel (rsweep), 0: shared-memory tile kernel (sweep)
+  int64_t jit = 0;         // 0 never, 1 from a program's 2nd use, 2 always: NVRTC-specialised sweeps (opt-in: compile ~1-7 s)
+  int64_t jit_max_cost = 40000;  // FP64 instructions per specialised launch (code-size guard)
   int64_t plan_json = 0;   // cs_sweep_plan_json: 0 sweeps, 1 register programs
 } g_opt;
 std::mutex g_opt_mu;
@@ -154,6 +157,11 @@ struct Program {
   std::vector<Sweep> sweeps;
   std::vector<Launch> launches;
   int engine = 1;
+  // NVRTC-specialised kernels, built once the program is hot (jit.cpp)
+  mutable std::mutex jit_mu;
+  mutable std::shared_ptr<JitModule> jit;
+  mutable bool jit_tried = false;
+  mutable std::atomic<int> uses{0};
 };
 
 std::mutex g_cache_mu;
@@ -406,6 +414,31 @@ int merge_terms_impl(int S, int K, const int32_t* hidx, const int32_t* lidx, con
   return CS_OK;
 }
 
+// The program's specialised kernels, compiling them on first demand (engine 1).
+std::shared_ptr<JitModule> program_jit(const Program& prog, int dtype) {
+  if (prog.engine != 1 || g_opt.jit == 0) return nullptr;
+  const int uses = ++prog.uses;
+  if (g_opt.jit == 1 && uses < 2) return nullptr;
+  std::lock_guard<std::mutex> lk(prog.jit_mu);
+  if (prog.jit_tried) return prog.jit;
+  prog.jit_tried = true;
+  std::vector<const Sweep*> sw;
+  std::vector<const std::vector<RegOp>*> rp;
+  bool any = false;
+  for (const Launch& ln : prog.launches) {
+    const Sweep& s = prog.sweeps[size_t(ln.sweep)];
+    sw.push_back(&s);
+    const bool ok = jit_cost(ln.reg, reg_bits_for(s.tile_bits)) <= g_opt.jit_max_cost;
+    rp.push_back(ok ? &ln.reg : nullptr);
+    any |= ok;
+  }
+  if (!any) return nullptr;
+  std::string err;
+  prog.jit = jit_compile(sw, rp, dtype, &err);
+  if (!prog.jit) g_err = "JIT unavailable, using the interpreter kernel: " + err;
+  return prog.jit;
+}
+
 }  // namespace
 
 extern "C" {
@@ -450,6 +483,12 @@ int cs_set_option(const char* key, int64_t value) {
     g_sweep_minb = int(value);
   } else if (k == "merge_dmma") {
     g_opt.merge_dmma = value ? 1 : 0;
+  } else if (k == "jit") {
+    if (value < 0 || value > 2) return fail(CS_ERR_INVALID, "jit must be 0, 1 or 2");
+    g_opt.jit = value;
+  } else if (k == "jit_max_cost") {
+    if (value < 0) return fail(CS_ERR_INVALID, "jit_max_cost must be >= 0");
+    g_opt.jit_max_cost = value;
   } else if (k == "engine") {
     if (value != 0 && value != 1) return fail(CS_ERR_INVALID, "engine must be 0 or 1");
     g_opt.engine = value;
@@ -474,6 +513,8 @@ int64_t cs_get_option(const char* key) {
   if (k == "merge_iters") return g_opt.merge_iters;
   if (k == "vb") return g_opt.vb;
   if (k == "engine") return g_opt.engine;
+  if (k == "jit") return g_opt.jit;
+  if (k == "jit_max_cost") return g_opt.jit_max_cost;
   if (k == "merge_dmma") return g_opt.merge_dmma;
   if (k == "plan_json") return g_opt.plan_json;
   if (k == "sweep_minb") return g_sweep_minb;
@@ -511,12 +552,16 @@ int cs_sim_batch(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int6
   } catch (const PlanError& pe) {
     return fail(pe.code, pe.msg);
   }
+  std::shared_ptr<JitModule> jit = program_jit(*prog, dtype);
   static SweepParams p;
   static RegParams rp;
   static std::mutex pm;
   std::lock_guard<std::mutex> lk(pm);
   bool first = true;
+  size_t li = 0;
   for (const Launch& ln : prog->launches) {
+    const JitKernel* jk = (jit && li < jit->kernels.size() && jit->kernels[li].kernel) ? &jit->kernels[li] : nullptr;
+    ++li;
     const Sweep& sw = prog->sweeps[size_t(ln.sweep)];
     const int T = sw.tile_bits;
     if (sw.hq.size() > size_t(kMaxTileBits) || sw.oq.size() > 64)
@@ -526,7 +571,23 @@ int cs_sim_batch(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int6
       const int64_t vc = std::min<int64_t>(65535, n_states - v0);
       void* sp = static_cast<char*>(states) + size_t(v0) * size_t(state_stride) * elem_bytes(dtype);
       cudaError_t e;
-      if (prog->engine == 1) {
+      if (jk) {
+        void* sp_arg = sp;
+        long long stride_arg = state_stride;
+        unsigned long long vbase_arg = variant_base + uint64_t(v0);
+        int init_arg = (first && init_zero) ? 1 : 0;
+        void* args[] = {&sp_arg, &stride_arg, &vbase_arg, &init_arg};
+        e = cudaSuccess;
+        if (jk->smem > 48 * 1024) {
+          int dev = 0;
+          cudaGetDevice(&dev);
+          e = cudaKernelSetAttributeForDevice(jk->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              int(jk->smem), dev);
+        }
+        if (e == cudaSuccess)
+          e = cudaLaunchKernel(reinterpret_cast<const void*>(jk->kernel), dim3(n_tiles, unsigned(vc), 1),
+                               dim3(unsigned(jk->threads), 1, 1), args, jk->smem, st);
+      } else if (prog->engine == 1) {
         if (ln.reg.size() > size_t(kMaxRegOps)) return fail(CS_ERR_INTERNAL, "register program too long");
         std::memset(&rp, 0, offsetof(RegParams, ops));
         rp.states = sp;
@@ -590,6 +651,31 @@ int cs_sweep_plan_json(int32_t nq, const uint8_t* kinds, const int64_t* qa, cons
     std::memcpy(buf, js.data(), n);
     buf[n] = 0;
   }
+  return CS_OK;
+}
+
+int cs_jit_selftest(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int64_t* qb, const double* params,
+                    const int32_t* slots, int64_t n_gates, int64_t n_states, int32_t dtype, int64_t* cubin_bytes) {
+  if (!valid_dtype(dtype)) return fail(CS_ERR_INVALID, "dtype must be CS_C128 or CS_C64");
+  if (nq < 1 || nq > 62) return fail(CS_ERR_INVALID, "qubit count out of range");
+  std::shared_ptr<const Program> prog;
+  try {
+    prog = build_schedule(nq, kinds, qa, qb, params, slots, n_gates, n_states, 0, dtype);
+  } catch (const PlanError& pe) {
+    return fail(pe.code, pe.msg);
+  }
+  if (prog->engine != 1) return fail(CS_ERR_INVALID, "JIT needs engine 1");
+  std::vector<const Sweep*> sw;
+  std::vector<const std::vector<RegOp>*> rp;
+  for (const Launch& ln : prog->launches) {
+    sw.push_back(&prog->sweeps[size_t(ln.sweep)]);
+    rp.push_back(&ln.reg);
+  }
+  std::vector<char> cubin;
+  std::vector<std::string> names;
+  std::string err;
+  if (!jit_cubin(sw, rp, dtype, &cubin, &names, &err)) return fail(CS_ERR_INTERNAL, err);
+  if (cubin_bytes) *cubin_bytes = int64_t(cubin.size());
   return CS_OK;
 }
 

@@ -1,0 +1,278 @@
+// NVRTC specialisation of register-tile sweep programs.
+//
+// The interpreter kernel (rsweep_kernel) spends ~90 of ~120 instructions per
+// gate on decoding the op record, branching on its masks and moving the
+// matrix into registers; the 32 FP64 instructions of a 2-pair update are the
+// minority. Here each launch of a (hot) program is emitted as straight-line
+// CUDA with the tile geometry, masks, remap index maps and matrices baked in
+// as literals, compiled once to an sm_100a CUBIN with NVRTC and loaded with
+// cudaLibraryLoadData. Semantics are identical to rsweep_kernel (same
+// register mapping, same swizzled transposes, same canonical load/store).
+#include "jit.hpp"
+
+#include <dlfcn.h>
+#include <nvrtc.h>
+
+#include <cstdio>
+#include <mutex>
+#include <sstream>
+
+namespace cutsim {
+
+namespace {
+
+struct Nvrtc {
+  bool ok = false;
+  std::string why;
+  nvrtcResult (*create)(nvrtcProgram*, const char*, const char*, int, const char* const*, const char* const*) = nullptr;
+  nvrtcResult (*compile)(nvrtcProgram, int, const char* const*) = nullptr;
+  nvrtcResult (*cubin_size)(nvrtcProgram, size_t*) = nullptr;
+  nvrtcResult (*cubin)(nvrtcProgram, char*) = nullptr;
+  nvrtcResult (*log_size)(nvrtcProgram, size_t*) = nullptr;
+  nvrtcResult (*log)(nvrtcProgram, char*) = nullptr;
+  nvrtcResult (*destroy)(nvrtcProgram*) = nullptr;
+};
+
+Nvrtc& nvrtc() {
+  static Nvrtc n = [] {
+    Nvrtc r;
+    void* h = dlopen("libnvrtc.so.12", RTLD_NOW | RTLD_LOCAL);
+    if (!h) h = dlopen("libnvrtc.so", RTLD_NOW | RTLD_LOCAL);
+    if (!h) {
+      r.why = "libnvrtc.so.12 not found";
+      return r;
+    }
+    r.create = reinterpret_cast<decltype(r.create)>(dlsym(h, "nvrtcCreateProgram"));
+    r.compile = reinterpret_cast<decltype(r.compile)>(dlsym(h, "nvrtcCompileProgram"));
+    r.cubin_size = reinterpret_cast<decltype(r.cubin_size)>(dlsym(h, "nvrtcGetCUBINSize"));
+    r.cubin = reinterpret_cast<decltype(r.cubin)>(dlsym(h, "nvrtcGetCUBIN"));
+    r.log_size = reinterpret_cast<decltype(r.log_size)>(dlsym(h, "nvrtcGetProgramLogSize"));
+    r.log = reinterpret_cast<decltype(r.log)>(dlsym(h, "nvrtcGetProgramLog"));
+    r.destroy = reinterpret_cast<decltype(r.destroy)>(dlsym(h, "nvrtcDestroyProgram"));
+    r.ok = r.create && r.compile && r.cubin_size && r.cubin && r.log_size && r.log && r.destroy;
+    if (!r.ok) r.why = "libnvrtc lacks the CUBIN entry points";
+    return r;
+  }();
+  return n;
+}
+
+std::string lit(double v) {
+  char b[64];
+  std::snprintf(b, sizeof b, "%a", v);
+  return std::string("R(") + b + ")";
+}
+
+const char* kPrelude = R"(
+#define DEV __device__ __forceinline__
+DEV unsigned swz(unsigned e) { unsigned x = e >> 3; x ^= (x >> 3) ^ (x >> 6) ^ (x >> 9); return e ^ (x & 7u); }
+DEV void ap(V& a, V& b, R m0r, R m0i, R m1r, R m1i, R m2r, R m2i, R m3r, R m3i) {
+  V u, w;
+  u.x = m0r * a.x - m0i * a.y + m1r * b.x - m1i * b.y;
+  u.y = m0r * a.y + m0i * a.x + m1r * b.y + m1i * b.x;
+  w.x = m2r * a.x - m2i * a.y + m3r * b.x - m3i * b.y;
+  w.y = m2r * a.y + m2i * a.x + m3r * b.y + m3i * b.x;
+  a = u; b = w;
+}
+DEV void ph(V& a, R pr, R pi) { const R x = a.x * pr - a.y * pi; a.y = a.x * pi + a.y * pr; a.x = x; }
+DEV void ng(V& a) { a.x = -a.x; a.y = -a.y; }
+)";
+
+}  // namespace
+
+JitModule::~JitModule() {
+  if (lib) cudaLibraryUnload(lib);
+}
+
+int64_t jit_cost(const std::vector<RegOp>& prog, int RB) {
+  const int NR = 1 << RB;
+  int64_t c = 0;
+  for (const RegOp& r : prog) {
+    if (r.kind == ROP_DENSE) {
+      for (int j = 0; j < NR; ++j)
+        if (!((j >> r.k) & 1) && (uint32_t(j) & r.rmask) == r.rmask) c += 16;
+    } else if (r.kind == ROP_PHASE) {
+      for (int j = 0; j < NR; ++j)
+        if ((uint32_t(j) & r.rmask) == r.rmask) c += 4;
+    } else {
+      c += 4 * NR;
+    }
+  }
+  return c;
+}
+
+std::string jit_source(const Sweep& sw, const std::vector<RegOp>& prog, int RB, int dtype, const std::string& name) {
+  const int T = sw.tile_bits;
+  const int L = sw.low_bits;
+  const int NR = 1 << RB;
+  const int BD = 1 << (T - RB);
+  std::ostringstream o;
+  o << "extern \"C\" __global__ void __launch_bounds__(" << BD << ") " << name
+    << "(V* __restrict__ states, long long stride, unsigned long long vbase, int init) {\n";
+  o << "  extern __shared__ __align__(16) unsigned char smraw[];\n";
+  o << "  V* sm = reinterpret_cast<V*>(smraw); (void)sm;\n";
+  o << "  const unsigned tid = threadIdx.x;\n";
+  o << "  const unsigned long long tile = blockIdx.x;\n";
+  o << "  unsigned long long base = 0ull;\n";
+  for (size_t j = 0; j < sw.oq.size(); ++j)
+    o << "  base |= ((tile >> " << j << ") & 1ull) << " << sw.oq[j] << ";\n";
+  o << "  const unsigned long long variant = vbase + blockIdx.y; (void)variant;\n";
+  o << "  V* st = states + (long long)blockIdx.y * stride;\n";
+  auto gidx = [&](int j) {
+    std::ostringstream g;
+    g << "{ const unsigned e = tid + " << (j * BD) << "u; const unsigned c = e >> " << L
+      << "; unsigned long long g = base + (e & " << ((1u << L) - 1u) << "u);";
+    for (size_t i = 0; i < sw.hq.size(); ++i)
+      g << " g |= (unsigned long long)((c >> " << i << ") & 1u) << " << sw.hq[i] << ";";
+    return g.str();
+  };
+  for (int j = 0; j < NR; ++j) o << "  V v" << j << ";\n";
+  for (int j = 0; j < NR; ++j)
+    o << "  " << gidx(j) << " if (init) { v" << j << ".x = (base == 0ull && e == 0u) ? R(1) : R(0); v" << j
+      << ".y = R(0); } else v" << j << " = st[g]; }\n";
+  o << "  unsigned tp = tid; (void)tp;\n";
+  int rpos[4];
+  for (int k = 0; k < RB; ++k) rpos[k] = T - RB + k;
+  auto roff = [&](int j) {
+    uint32_t r = 0;
+    for (int k = 0; k < RB; ++k)
+      if ((j >> k) & 1) r |= 1u << rpos[k];
+    return r;
+  };
+  for (size_t i = 0; i < prog.size();) {
+    const RegOp& op = prog[i];
+    if (op.kind == ROP_REMAP) {
+      o << "  __syncthreads();\n";
+      for (int j = 0; j < NR; ++j) o << "  sm[swz(tp | " << roff(j) << "u)] = v" << j << ";\n";
+      for (int k = 0; k < RB; ++k) rpos[k] = op.rpos[k];
+      o << "  tp = tid;";
+      for (int k = 0; k < RB; ++k)
+        o << " tp = ((tp >> " << rpos[k] << ") << " << (rpos[k] + 1) << ") | (tp & " << ((1u << rpos[k]) - 1u)
+          << "u);";
+      o << "\n  __syncthreads();\n";
+      for (int j = 0; j < NR; ++j) o << "  v" << j << " = sm[swz(tp | " << roff(j) << "u)];\n";
+      ++i;
+      continue;
+    }
+    const bool slotted = op.slot >= 0;
+    const RegOp* alt = slotted ? &prog[i + 1] : nullptr;
+    o << "  {";
+    std::string cond;
+    if (op.omask) cond += "(base & " + std::to_string(op.omask) + "ull) == " + std::to_string(op.omask) + "ull";
+    if (op.tmask) {
+      if (!cond.empty()) cond += " && ";
+      cond += "(tid & " + std::to_string(op.tmask) + "u) == " + std::to_string(op.tmask) + "u";
+    }
+    if (!cond.empty()) o << " if (" << cond << ")";
+    o << " {";
+    std::string m[8];
+    if (slotted) {
+      o << " const bool sb = ((variant >> " << op.slot << ") & 1ull) != 0ull;";
+      for (int q = 0; q < 8; ++q) {
+        o << " const R m" << q << " = sb ? " << lit(alt->m[q]) << " : " << lit(op.m[q]) << ";";
+        m[q] = "m" + std::to_string(q);
+      }
+    } else {
+      for (int q = 0; q < 8; ++q) m[q] = lit(op.m[q]);
+    }
+    if (op.kind == ROP_DENSE) {
+      for (int j = 0; j < NR; ++j) {
+        if ((j >> op.k) & 1) continue;
+        if ((uint32_t(j) & op.rmask) != op.rmask) continue;
+        o << " ap(v" << j << ", v" << (j | (1 << op.k)) << ", " << m[0] << ", " << m[1] << ", " << m[2] << ", "
+          << m[3] << ", " << m[4] << ", " << m[5] << ", " << m[6] << ", " << m[7] << ");";
+      }
+    } else {
+      const bool neg = !slotted && op.m[0] == -1.0 && op.m[1] == 0.0;
+      for (int j = 0; j < NR; ++j) {
+        if ((uint32_t(j) & op.rmask) != op.rmask) continue;
+        if (neg) o << " ng(v" << j << ");";
+        else o << " ph(v" << j << ", " << m[0] << ", " << m[1] << ");";
+      }
+    }
+    o << " } }\n";
+    i += slotted ? 2 : 1;
+  }
+  for (int j = 0; j < NR; ++j) o << "  " << gidx(j) << " st[g] = v" << j << "; }\n";
+  o << "}\n";
+  (void)dtype;
+  return o.str();
+}
+
+bool jit_cubin(const std::vector<const Sweep*>& sweeps, const std::vector<const std::vector<RegOp>*>& progs,
+               int dtype, std::vector<char>* cubin, std::vector<std::string>* names, std::string* err) {
+  Nvrtc& nv = nvrtc();
+  if (!nv.ok) {
+    *err = nv.why;
+    return false;
+  }
+  std::ostringstream src;
+  if (dtype == 0) src << "typedef double R; typedef double2 V;\n";
+  else src << "typedef float R; typedef float2 V;\n";
+  src << kPrelude;
+  names->clear();
+  for (size_t i = 0; i < sweeps.size(); ++i) {
+    if (!progs[i]) {
+      names->emplace_back();
+      continue;
+    }
+    names->push_back("cs_jit_" + std::to_string(i));
+    src << jit_source(*sweeps[i], *progs[i], reg_bits_for(sweeps[i]->tile_bits), dtype, names->back());
+  }
+  const std::string code = src.str();
+  nvrtcProgram prog = nullptr;
+  if (nv.create(&prog, code.c_str(), "cutsim_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
+    *err = "nvrtcCreateProgram failed";
+    return false;
+  }
+  const char* opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-default-device", "--extra-device-vectorization"};
+  const nvrtcResult rc = nv.compile(prog, 4, opts);
+  if (rc != NVRTC_SUCCESS) {
+    size_t n = 0;
+    nv.log_size(prog, &n);
+    std::string log(n, '\0');
+    if (n) nv.log(prog, &log[0]);
+    *err = "NVRTC compile failed: " + log.substr(0, 2000);
+    nv.destroy(&prog);
+    return false;
+  }
+  size_t n = 0;
+  nv.cubin_size(prog, &n);
+  cubin->assign(n, 0);
+  nv.cubin(prog, cubin->data());
+  nv.destroy(&prog);
+  return true;
+}
+
+std::shared_ptr<JitModule> jit_compile(const std::vector<const Sweep*>& sweeps,
+                                       const std::vector<const std::vector<RegOp>*>& progs, int dtype,
+                                       std::string* err) {
+  std::vector<char> cubin;
+  std::vector<std::string> names;
+  if (!jit_cubin(sweeps, progs, dtype, &cubin, &names, err)) return nullptr;
+  auto mod = std::make_shared<JitModule>();
+  cudaError_t e = cudaLibraryLoadData(&mod->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
+  if (e != cudaSuccess) {
+    *err = std::string("cudaLibraryLoadData: ") + cudaGetErrorString(e);
+    mod->lib = nullptr;
+    return nullptr;
+  }
+  mod->kernels.resize(sweeps.size());
+  for (size_t i = 0; i < sweeps.size(); ++i) {
+    if (names[i].empty()) continue;
+    JitKernel& k = mod->kernels[i];
+    e = cudaLibraryGetKernel(&k.kernel, mod->lib, names[i].c_str());
+    if (e != cudaSuccess) {
+      *err = std::string("cudaLibraryGetKernel: ") + cudaGetErrorString(e);
+      return nullptr;
+    }
+    const int T = sweeps[i]->tile_bits;
+    const int RB = reg_bits_for(T);
+    k.threads = 1 << (T - RB);
+    bool remap = false;
+    for (const RegOp& r : *progs[i]) remap |= r.kind == ROP_REMAP;
+    k.smem = remap ? (size_t(1) << T) * (dtype == 0 ? 16 : 8) : 0;
+  }
+  return mod;
+}
+
+}  // namespace cutsim

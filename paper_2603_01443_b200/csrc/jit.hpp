@@ -1,0 +1,48 @@
+// NVRTC specialisation of register-tile sweep programs (see jit.cpp).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "ops.hpp"
+#include "plan.hpp"
+
+namespace cutsim {
+
+// One compiled launch: the kernel handle and its dynamic shared memory.
+struct JitKernel {
+  cudaKernel_t kernel = nullptr;
+  size_t smem = 0;
+  int threads = 0;
+};
+
+struct JitModule {
+  cudaLibrary_t lib = nullptr;
+  std::vector<JitKernel> kernels;  // one per launch, same order as the program's launches
+  ~JitModule();
+};
+
+// CUDA C++ source of one launch: straight-line code for the register program
+// (dense/phase/remap) with the tile geometry, masks, matrices (hex-float
+// literals) and remap index maps baked in.
+std::string jit_source(const Sweep& sw, const std::vector<RegOp>& prog, int reg_bits, int dtype,
+                       const std::string& name);
+
+// Compile every launch of a program into one module (sm_100a CUBIN via
+// NVRTC, loaded with cudaLibraryLoadData). Returns null and sets *err on
+// failure (NVRTC missing, compile error).
+std::shared_ptr<JitModule> jit_compile(const std::vector<const Sweep*>& sweeps,
+                                       const std::vector<const std::vector<RegOp>*>& progs, int dtype,
+                                       std::string* err);
+
+// NVRTC step only (no device needed): the CUBIN and kernel names.
+bool jit_cubin(const std::vector<const Sweep*>& sweeps, const std::vector<const std::vector<RegOp>*>& progs,
+               int dtype, std::vector<char>* cubin, std::vector<std::string>* names, std::string* err);
+
+// FP64 instructions the specialised code would contain (size guard).
+int64_t jit_cost(const std::vector<RegOp>& prog, int reg_bits);
+
+}  // namespace cutsim

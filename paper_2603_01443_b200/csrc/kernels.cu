@@ -353,12 +353,8 @@ __global__ void __launch_bounds__(256, MINB) sweep_kernel(const __grid_constant_
 // register bits. The host chooses the remaps (plan.cpp: reg_program).
 // ---------------------------------------------------------------------------
 template <typename R, int RB>
-__device__ __forceinline__ void reg_dense(vec2_t<R> (&v)[1 << RB], int k, uint32_t rmask, const double* m) {
-  const double2 q0 = reinterpret_cast<const double2*>(m)[0];
-  const double2 q1 = reinterpret_cast<const double2*>(m)[1];
-  const double2 q2 = reinterpret_cast<const double2*>(m)[2];
-  const double2 q3 = reinterpret_cast<const double2*>(m)[3];
-  const double mm[8] = {q0.x, q0.y, q1.x, q1.y, q2.x, q2.y, q3.x, q3.y};
+__device__ __forceinline__ void reg_dense(vec2_t<R> (&v)[1 << RB], int k, uint32_t rmask, const double2 (&q)[4]) {
+  const double mm[8] = {q[0].x, q[0].y, q[1].x, q[1].y, q[2].x, q[2].y, q[3].x, q[3].y};
 #pragma unroll
   for (int kk = 0; kk < RB; ++kk) {
     if (kk != k) continue;
@@ -375,6 +371,16 @@ __device__ __forceinline__ void reg_dense(vec2_t<R> (&v)[1 << RB], int k, uint32
       }
     }
   }
+}
+
+__device__ __forceinline__ void load_op(const RegOp* ops, int i, uint4& hdr, uint64_t& om, double2 (&mat)[4]) {
+  hdr = *reinterpret_cast<const uint4*>(&ops[i]);
+  om = ops[i].omask;
+  const double2* mp = reinterpret_cast<const double2*>(ops[i].m);
+  mat[0] = mp[0];
+  mat[1] = mp[1];
+  mat[2] = mp[2];
+  mat[3] = mp[3];
 }
 
 template <typename R, int RB, int CAP>
@@ -434,48 +440,76 @@ __global__ void __launch_bounds__(512) rsweep_kernel(const __grid_constant__ Reg
 #pragma unroll
   for (int j = 0; j < NR; ++j) roff[j] = uint32_t(j) * bd;
 
+  // software-pipelined op loop: the next op's 16-byte header, outside mask and
+  // matrix are loaded while the current op computes
+  uint4 hdr = make_uint4(0, 0, 0, 0);
+  uint64_t om = 0;
+  double2 mat[4];
+  if (n_ops > 0) load_op(ops, 0, hdr, om, mat);
   for (int i = 0; i < n_ops;) {
-    const RegOp& op = ops[i];
-    if (op.kind == ROP_REMAP) {
+    const int kind = int(hdr.x & 0xffu);
+    const int slot = int(int16_t(hdr.x >> 16));
+    const int next = i + ((kind != ROP_REMAP && slot >= 0) ? 2 : 1);
+    uint4 hdr_n = hdr;
+    uint64_t om_n = 0;
+    double2 mat_n[4];
+    // RB = 4 keeps 16 amplitudes live: prefetch only the header there
+    constexpr bool kPrefetchMatrix = RB <= 3;
+    if (next < n_ops) {
+      if (kPrefetchMatrix) {
+        load_op(ops, next, hdr_n, om_n, mat_n);
+      } else {
+        hdr_n = *reinterpret_cast<const uint4*>(&ops[next]);
+        om_n = ops[next].omask;
+      }
+    }
+    if (kind == ROP_REMAP) {
+      const uint32_t rp = hdr.w;
       __syncthreads();
 #pragma unroll
       for (int j = 0; j < NR; ++j) s[swz(tpart | roff[j])] = v[j];
-      // new mapping: register bit k -> tile bit rpos[k]; thread bits fill the rest
-      uint32_t rmaskbits = 0;
-#pragma unroll
-      for (int k = 0; k < RB; ++k) rmaskbits |= 1u << op.rpos[k];
       // thread bits fill the non-register tile bits in ascending order:
       // insert a zero at each (ascending) register position
       uint32_t tp = tid;
 #pragma unroll
       for (int k = 0; k < RB; ++k) {
-        const uint32_t below = (1u << op.rpos[k]) - 1u;
+        const uint32_t pos = (rp >> (8 * k)) & 0xffu;
+        const uint32_t below = (1u << pos) - 1u;
         tp = ((tp & ~below) << 1) | (tp & below);
       }
       tpart = tp;
-      (void)rmaskbits;
 #pragma unroll
       for (int j = 0; j < NR; ++j) {
         uint32_t o = 0;
 #pragma unroll
         for (int k = 0; k < RB; ++k)
-          if ((j >> k) & 1) o |= 1u << op.rpos[k];
+          if ((j >> k) & 1) o |= 1u << ((rp >> (8 * k)) & 0xffu);
         roff[j] = o;
       }
       __syncthreads();
 #pragma unroll
       for (int j = 0; j < NR; ++j) v[j] = s[swz(tpart | roff[j])];
-      ++i;
-      continue;
-    }
-    const int step = op.slot >= 0 ? 2 : 1;
-    const RegOp& src = op.slot >= 0 ? ops[i + int((variant >> op.slot) & 1ull)] : op;
-    if ((base & op.omask) == op.omask && (tid & op.tmask) == op.tmask) {
-      if (op.kind == ROP_DENSE) {
-        reg_dense<R, RB>(v, op.k, op.rmask, src.m);
+    } else if ((base & om) == om && (tid & hdr.y) == hdr.y) {
+      double2 cur[4] = {mat[0], mat[1], mat[2], mat[3]};
+      if (!kPrefetchMatrix) {
+        const double2* mp = reinterpret_cast<const double2*>(ops[i].m);
+        cur[0] = mp[0];
+        cur[1] = mp[1];
+        cur[2] = mp[2];
+        cur[3] = mp[3];
+      }
+      if (slot >= 0 && ((variant >> slot) & 1ull)) {
+        const double2* mp = reinterpret_cast<const double2*>(ops[i + 1].m);
+        cur[0] = mp[0];
+        cur[1] = mp[1];
+        cur[2] = mp[2];
+        cur[3] = mp[3];
+      }
+      const uint32_t rm = hdr.z;
+      if (kind == ROP_DENSE) {
+        reg_dense<R, RB>(v, int((hdr.x >> 8) & 0xffu), rm, cur);
       } else {
-        const double qr = src.m[0], qi = src.m[1];
-        const uint32_t rm = op.rmask;
+        const double qr = cur[0].x, qi = cur[0].y;
         if (qi == 0.0 && qr == -1.0) {
 #pragma unroll
           for (int j = 0; j < NR; ++j)
@@ -490,7 +524,15 @@ __global__ void __launch_bounds__(512) rsweep_kernel(const __grid_constant__ Reg
         }
       }
     }
-    i += step;
+    hdr = hdr_n;
+    om = om_n;
+    if (kPrefetchMatrix) {
+      mat[0] = mat_n[0];
+      mat[1] = mat_n[1];
+      mat[2] = mat_n[2];
+      mat[3] = mat_n[3];
+    }
+    i = next;
   }
 
 #pragma unroll

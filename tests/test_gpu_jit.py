@@ -1,0 +1,54 @@
+"""NVRTC-specialised sweep kernels (cs_set_option("jit", 2)) against the
+oracle: uncut multi-sweep circuits, cut-variant batches with slots,
+controlled gates, complex64. The host-only NVRTC compile runs on CPU too."""
+import numpy as np
+import pytest
+
+from oracle import cutbench_oracle as orc
+from paper_2603_01443_b200 import _native
+from paper_2603_01443_b200 import circuits as C
+from paper_2603_01443_b200 import generators as G
+from paper_2603_01443_b200.pipeline import preprocess
+
+
+def test_nvrtc_compiles_generated_kernels_on_cpu():
+    circ = G.build_brickwall(G.BrickwallSpec(14, 3, 2, 2, 0))
+    prep = preprocess(circ, 2)
+    fam = prep.subs.segments[0]
+    assert _native.jit_selftest(fam.num_qubits, fam.template, fam.slots, n_states=fam.num_variants) > 1000
+    stair = C.build_staircase(C.BenchmarkSpec(q=14, n=2, blocks=2))
+    assert _native.jit_selftest(14, stair.table, n_states=1) > 1000
+
+
+@pytest.fixture
+def jit_on():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    old = _native.get_option("jit")
+    _native.set_option("jit", 2)
+    yield
+    _native.set_option("jit", old)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("q,d,n,c,seed", [(14, 5, 2, 3, 0), (17, 4, 2, 2, 1), (12, 4, 3, 4, 2)])
+def test_jit_cut_and_uncut_match_oracle(jit_on, q, d, n, c, seed):
+    import paper_2603_01443_b200 as cb
+
+    circ = cb.build_brickwall(cb.BrickwallSpec(q, d, n, c, seed))
+    ref = orc.simulate(q, circ.kinds, circ.qa, circ.qb, circ.params)
+    assert np.abs(cb.simulate(circ).amps - ref).max() < 1e-10
+    assert np.abs(cb.run_cut(circ, n).amps - ref).max() < 1e-10
+
+
+@pytest.mark.gpu
+def test_jit_controlled_gates_and_complex64(jit_on):
+    import paper_2603_01443_b200 as cb
+
+    circ = cb.build_staircase(cb.BenchmarkSpec(q=16, n=2, blocks=2))
+    ref = orc.simulate(16, circ.kinds, circ.qa, circ.qb)
+    assert np.abs(cb.simulate(circ).amps - ref).max() < 1e-10
+    got = cb.simulate(circ, dtype=np.complex64).amps
+    assert np.abs(got - ref).max() < 1e-5

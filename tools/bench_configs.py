@@ -96,6 +96,9 @@ def run(name, shard=1, steps=5):
 
 
 def main():
+    from paper_2603_01443_b200 import _native
+
+    _native.set_option("jit", 2)
     names = sys.argv[1:] or ["cfg1", "cfg2", "cfg4a", "cfg4b", "cfg5_q32_n2_c2", "cfg5_q32_n2_c4",
                              "cfg5_q32_n4_c4", "cfg5_q34_n2_c2_shard8"]
     for name in names:
