@@ -33,7 +33,7 @@ def jit_on():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("q,d,n,c,seed", [(14, 5, 2, 3, 0), (17, 4, 2, 2, 1), (12, 4, 3, 4, 2)])
+@pytest.mark.parametrize("q,d,n,c,seed", [(14, 5, 2, 3, 0), (18, 4, 2, 2, 1), (12, 4, 3, 4, 2)])
 def test_jit_cut_and_uncut_match_oracle(jit_on, q, d, n, c, seed):
     import paper_2603_01443_b200 as cb
 
