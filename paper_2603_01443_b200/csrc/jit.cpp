@@ -178,8 +178,41 @@ std::string jit_source(const Sweep& sw, const std::vector<RegOp>& prog, int RB, 
       for (int j = 0; j < NR; ++j) {
         if ((j >> op.k) & 1) continue;
         if ((uint32_t(j) & op.rmask) != op.rmask) continue;
-        o << " ap(v" << j << ", v" << (j | (1 << op.k)) << ", " << m[0] << ", " << m[1] << ", " << m[2] << ", "
-          << m[3] << ", " << m[4] << ", " << m[5] << ", " << m[6] << ", " << m[7] << ");";
+        const int jb = j | (1 << op.k);
+        if (slotted) {
+          o << " ap(v" << j << ", v" << jb << ", " << m[0] << ", " << m[1] << ", " << m[2] << ", " << m[3] << ", "
+            << m[4] << ", " << m[5] << ", " << m[6] << ", " << m[7] << ");";
+          continue;
+        }
+        // literal matrix: drop the terms whose coefficient is exactly zero
+        // (U3 has a real m00, H/X are real) — fewer FP64 instructions
+        auto comp = [&](int re, int im, const char* ax, const char* ay, const char* bx, const char* by, bool imag) {
+          // imag == false: real part  = m[re]*ax - m[im]*ay + m[re+2]*bx - m[im+2]*by
+          // imag == true : imag part  = m[re]*ay + m[im]*ax + m[re+2]*by + m[im+2]*bx
+          std::string e;
+          auto add = [&](double c, const std::string& cs, const char* v, bool neg) {
+            if (c == 0.0) return;
+            if (!e.empty() || neg) e += neg ? " - " : " + ";
+            e += cs + " * " + v;
+          };
+          if (!imag) {
+            add(op.m[re], m[re], ax, false);
+            add(op.m[im], m[im], ay, true);
+            add(op.m[re + 2], m[re + 2], bx, false);
+            add(op.m[im + 2], m[im + 2], by, true);
+          } else {
+            add(op.m[re], m[re], ay, false);
+            add(op.m[im], m[im], ax, false);
+            add(op.m[re + 2], m[re + 2], by, false);
+            add(op.m[im + 2], m[im + 2], bx, false);
+          }
+          return e.empty() ? std::string("R(0)") : (e[0] == ' ' ? "R(0)" + e : e);
+        };
+        o << " { const V a = v" << j << ", b = v" << jb << ";";
+        o << " v" << j << ".x = " << comp(0, 1, "a.x", "a.y", "b.x", "b.y", false) << ";";
+        o << " v" << j << ".y = " << comp(0, 1, "a.x", "a.y", "b.x", "b.y", true) << ";";
+        o << " v" << jb << ".x = " << comp(4, 5, "a.x", "a.y", "b.x", "b.y", false) << ";";
+        o << " v" << jb << ".y = " << comp(4, 5, "a.x", "a.y", "b.x", "b.y", true) << "; }";
       }
     } else {
       const bool neg = !slotted && op.m[0] == -1.0 && op.m[1] == 0.0;
