@@ -13,9 +13,12 @@
 #include <dlfcn.h>
 #include <nvrtc.h>
 
+#include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <mutex>
 #include <sstream>
+#include <thread>
 
 namespace cutsim {
 
@@ -80,7 +83,8 @@ DEV void ng(V& a) { a.x = -a.x; a.y = -a.y; }
 }  // namespace
 
 JitModule::~JitModule() {
-  if (lib) cudaLibraryUnload(lib);
+  for (cudaLibrary_t l : libs)
+    if (l) cudaLibraryUnload(l);
 }
 
 int64_t jit_cost(const std::vector<RegOp>& prog, int RB) {
@@ -231,27 +235,19 @@ std::string jit_source(const Sweep& sw, const std::vector<RegOp>& prog, int RB, 
   return o.str();
 }
 
-bool jit_cubin(const std::vector<const Sweep*>& sweeps, const std::vector<const std::vector<RegOp>*>& progs,
-               int dtype, std::vector<char>* cubin, std::vector<std::string>* names, std::string* err) {
+namespace {
+
+std::string header(int dtype) {
+  std::string h = dtype == 0 ? "typedef double R; typedef double2 V;\n" : "typedef float R; typedef float2 V;\n";
+  return h + kPrelude;
+}
+
+bool compile_source(const std::string& code, std::vector<char>* cubin, std::string* err) {
   Nvrtc& nv = nvrtc();
   if (!nv.ok) {
     *err = nv.why;
     return false;
   }
-  std::ostringstream src;
-  if (dtype == 0) src << "typedef double R; typedef double2 V;\n";
-  else src << "typedef float R; typedef float2 V;\n";
-  src << kPrelude;
-  names->clear();
-  for (size_t i = 0; i < sweeps.size(); ++i) {
-    if (!progs[i]) {
-      names->emplace_back();
-      continue;
-    }
-    names->push_back("cs_jit_" + std::to_string(i));
-    src << jit_source(*sweeps[i], *progs[i], reg_bits_for(sweeps[i]->tile_bits), dtype, names->back());
-  }
-  const std::string code = src.str();
   nvrtcProgram prog = nullptr;
   if (nv.create(&prog, code.c_str(), "cutsim_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
     *err = "nvrtcCreateProgram failed";
@@ -276,24 +272,68 @@ bool jit_cubin(const std::vector<const Sweep*>& sweeps, const std::vector<const 
   return true;
 }
 
+}  // namespace
+
+bool jit_cubin(const std::vector<const Sweep*>& sweeps, const std::vector<const std::vector<RegOp>*>& progs,
+               int dtype, std::vector<char>* cubin, std::vector<std::string>* names, std::string* err) {
+  std::string code = header(dtype);
+  names->clear();
+  for (size_t i = 0; i < sweeps.size(); ++i) {
+    if (!progs[i]) {
+      names->emplace_back();
+      continue;
+    }
+    names->push_back("cs_jit_" + std::to_string(i));
+    code += jit_source(*sweeps[i], *progs[i], reg_bits_for(sweeps[i]->tile_bits), dtype, names->back());
+  }
+  return compile_source(code, cubin, err);
+}
+
+// One NVRTC program per launch, compiled on parallel host threads (NVRTC is
+// thread-safe), so a 12-sweep program costs about one sweep's compile time.
 std::shared_ptr<JitModule> jit_compile(const std::vector<const Sweep*>& sweeps,
                                        const std::vector<const std::vector<RegOp>*>& progs, int dtype,
                                        std::string* err) {
-  std::vector<char> cubin;
-  std::vector<std::string> names;
-  if (!jit_cubin(sweeps, progs, dtype, &cubin, &names, err)) return nullptr;
+  const size_t n = sweeps.size();
+  std::vector<std::vector<char>> cubins(n);
+  std::vector<std::string> errs(n);
+  std::vector<char> ok(n, 0);
+  std::atomic<size_t> next{0};
+  auto work = [&] {
+    for (size_t i = next++; i < n; i = next++) {
+      if (!progs[i]) {
+        ok[i] = 1;
+        continue;
+      }
+      const std::string code = header(dtype) + jit_source(*sweeps[i], *progs[i], reg_bits_for(sweeps[i]->tile_bits),
+                                                        dtype, "cs_jit_" + std::to_string(i));
+      ok[i] = compile_source(code, &cubins[i], &errs[i]) ? 1 : 0;
+    }
+  };
+  const size_t nt = std::max<size_t>(1, std::min<size_t>(n, std::max(1u, std::thread::hardware_concurrency())));
+  std::vector<std::thread> pool;
+  for (size_t t = 1; t < nt; ++t) pool.emplace_back(work);
+  work();
+  for (auto& th : pool) th.join();
+  for (size_t i = 0; i < n; ++i)
+    if (!ok[i]) {
+      *err = errs[i];
+      return nullptr;
+    }
   auto mod = std::make_shared<JitModule>();
-  cudaError_t e = cudaLibraryLoadData(&mod->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
-  if (e != cudaSuccess) {
-    *err = std::string("cudaLibraryLoadData: ") + cudaGetErrorString(e);
-    mod->lib = nullptr;
-    return nullptr;
-  }
-  mod->kernels.resize(sweeps.size());
-  for (size_t i = 0; i < sweeps.size(); ++i) {
-    if (names[i].empty()) continue;
+  mod->libs.assign(n, nullptr);
+  mod->kernels.resize(n);
+  for (size_t i = 0; i < n; ++i) {
+    if (!progs[i]) continue;
+    cudaError_t e = cudaLibraryLoadData(&mod->libs[i], cubins[i].data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
+    if (e != cudaSuccess) {
+      mod->libs[i] = nullptr;
+      *err = std::string("cudaLibraryLoadData: ") + cudaGetErrorString(e);
+      return nullptr;
+    }
     JitKernel& k = mod->kernels[i];
-    e = cudaLibraryGetKernel(&k.kernel, mod->lib, names[i].c_str());
+    const std::string name = "cs_jit_" + std::to_string(i);
+    e = cudaLibraryGetKernel(&k.kernel, mod->libs[i], name.c_str());
     if (e != cudaSuccess) {
       *err = std::string("cudaLibraryGetKernel: ") + cudaGetErrorString(e);
       return nullptr;

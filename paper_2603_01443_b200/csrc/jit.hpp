@@ -20,7 +20,7 @@ struct JitKernel {
 };
 
 struct JitModule {
-  cudaLibrary_t lib = nullptr;
+  std::vector<cudaLibrary_t> libs;  // one library per compiled launch
   std::vector<JitKernel> kernels;  // one per launch, same order as the program's launches
   ~JitModule();
 };
