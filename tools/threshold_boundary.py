@@ -62,7 +62,7 @@ def main():
     _native.set_option("jit", 2)
     qs = [int(v) for v in (sys.argv[1] if len(sys.argv) > 1 else "16,20,24,28").split(",")]
     ds = [int(v) for v in (sys.argv[2] if len(sys.argv) > 2 else "5,10,20").split(",")]
-    seeds = (0, 1)
+    seeds = (0,)
     print("q,d,c_total,t_cut,t_orig,delta,seeds", flush=True)
     best = {}
     for d in ds:
