@@ -333,3 +333,40 @@ __all__ = [
     "tensor",
 ]
 
+
+
+def dump_shard(shard, prefix, *, rank: int, world: int) -> str:
+    """Per-rank amplitude dump of a sharded state: the reference's format
+    (little-endian float64 (re, im) pairs, engine.py:192-196) for amplitudes
+    [begin, end), plus a JSON manifest written by rank 0. `shard` is a
+    ShardedState or a (num_qubits, begin, end, tensor-or-array) tuple."""
+    import json
+
+    if hasattr(shard, "device"):
+        q, begin, end, data = shard.num_qubits, shard.begin, shard.end, shard.device
+    else:
+        q, begin, end, data = shard
+    arr = data.cpu().numpy() if hasattr(data, "cpu") else np.asarray(data)
+    if arr.shape != (end - begin,):
+        raise ValidationError("shard length does not match its range")
+    path = f"{prefix}.rank{rank}-of-{world}.bin"
+    with open(path, "wb") as fh:
+        fh.write(np.ascontiguousarray(arr, dtype="<c16").tobytes())
+    if rank == 0:
+        with open(f"{prefix}.manifest.json", "w") as fh:
+            json.dump({"num_qubits": q, "world": world, "format": "<c16 (re, im) pairs, index order",
+                       "shards": [f"{prefix}.rank{r}-of-{world}.bin" for r in range(world)]}, fh)
+    return path
+
+
+def load_shards(prefix) -> StateVec:
+    """Reassemble a full host StateVec from dump_shard files."""
+    import json
+
+    with open(f"{prefix}.manifest.json") as fh:
+        man = json.load(fh)
+    parts = []
+    for path in man["shards"]:
+        with open(path, "rb") as fh:
+            parts.append(np.frombuffer(fh.read(), dtype="<c16"))
+    return StateVec(man["num_qubits"], np.concatenate(parts).astype(np.complex128))

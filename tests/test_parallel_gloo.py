@@ -104,3 +104,16 @@ def test_variant_slices_cover_each_variant_once():
                 for sl in variant_slices(counts, world, r):
                     seen += [(sl.segment, v) for v in range(sl.v0, sl.v1)]
             assert sorted(seen) == [(s, v) for s, c in enumerate(counts) for v in range(c)]
+
+
+def test_sharded_dump_round_trip(tmp_path):
+    from paper_2603_01443_b200.engine import dump_shard, load_shards
+
+    full = (np.arange(16) + 1j * np.arange(16)[::-1]).astype(np.complex128)
+    prefix = str(tmp_path / "state")
+    for r in range(4):
+        dump_shard((4, 4 * r, 4 * r + 4, full[4 * r:4 * r + 4]), prefix, rank=r, world=4)
+    back = load_shards(prefix)
+    assert back.num_qubits == 4 and np.array_equal(back.amps, full)
+    raw = open(f"{prefix}.rank1-of-4.bin", "rb").read()
+    assert np.array_equal(np.frombuffer(raw, "<f8"), np.stack([full[4:8].real, full[4:8].imag], 1).ravel())
