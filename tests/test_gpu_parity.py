@@ -345,3 +345,43 @@ def test_distributed_uncut_emulated_on_one_gpu(cb, world, q, d):
     got = simulate_emulated(circ, world).cpu().numpy()
     ref = orc.simulate(q, circ.kinds, circ.qa, circ.qb, circ.params)
     assert np.abs(got - ref).max() < TOL
+
+
+def test_run_cut_to_host_matches_device_state(cb):
+    """The e2e path of bench.py: chunked merge overlapped with D2H into pinned memory."""
+    import torch
+
+    from paper_2603_01443_b200.pipeline import run_cut_to_host
+
+    circ = cb.build_brickwall(cb.BrickwallSpec(20, 6, 2, 2, 3))
+    host = torch.empty(1 << 20, dtype=torch.complex128, pin_memory=True)
+    run_cut_to_host(circ, 2, host, chunks=8)
+    dev = cb.run_cut(circ, 2).amps
+    assert np.array_equal(host.numpy(), dev)
+
+
+def test_sharded_pipeline_over_nccl_world1(cb):
+    """run_cut_sharded through a real NCCL process group (world size 1 on one
+    GPU: the all-gather path runs, no rank waits on another)."""
+    import os
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2603_01443_b200.parallel import run_cut_sharded
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        circ = cb.build_brickwall(cb.BrickwallSpec(18, 5, 3, 4, 2))
+        res, (b, e) = run_cut_sharded(circ, 3, rank=0, world=1)
+        assert (b, e) == (0, 1 << 18)
+        assert np.abs(res.cpu().numpy() - cb.run_cut(circ, 3).amps).max() < 1e-14
+    finally:
+        dist.destroy_process_group()
