@@ -61,30 +61,65 @@ def load_traffic():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled every few ms during the timed
+    region (NVML through nvidia_ml_py; nvidia-smi as a fallback)."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    REASONS = {  # NVML clocks-event-reason bits
+        0x0000000000000004: "sw_power_cap",
+        0x0000000000000008: "hw_slowdown",
+        0x0000000000000020: "sw_thermal_slowdown",
+        0x0000000000000040: "hw_thermal_slowdown",
+        0x0000000000000080: "hw_power_brake_slowdown",
+    }
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, interval: float = 0.005):
         self.index = index
+        self.interval = interval
         self.samples = []
         self._stop = threading.Event()
         self._thr = None
+        self._nvml = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nvml = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001
+            self._nvml = None
+            self.max_mhz = None
+
+    def _sample_nvml(self):
+        nv = self._nvml
+        sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+        try:
+            bits = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+        except AttributeError:
+            bits = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self._h)
+        return sm, bits
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(
-                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                vals = [v.strip() for v in out.stdout.strip().split(",")]
-                if len(vals) == 6:
-                    self.samples.append(vals)
-            except (OSError, subprocess.SubprocessError):
+                if self._nvml is not None:
+                    sm, bits = self._sample_nvml()
+                    self.samples.append((float(sm), [n for b, n in self.REASONS.items() if bits & b]))
+                else:
+                    out = subprocess.run(
+                        ["nvidia-smi", "-i", str(self.index),
+                         "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                         "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits"],
+                        capture_output=True, text=True, timeout=5)
+                    v = [x.strip() for x in out.stdout.strip().split(",")]
+                    if len(v) == 6:
+                        self.max_mhz = float(v[1])
+                        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+                        self.samples.append((float(v[0]), [names[i] for i in range(4) if v[2 + i] == "Active"]))
+            except Exception:  # noqa: BLE001
                 return
-            self._stop.wait(0.2)
+            self._stop.wait(self.interval)
 
     def __enter__(self):
         self._thr = threading.Thread(target=self._run, daemon=True)
@@ -98,13 +133,11 @@ class ClockSampler:
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i] == "Active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"], "samples": 0}
+        sm = [s for s, _ in self.samples]
+        reasons = sorted({r for _, rs in self.samples for r in rs})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(self.samples), "source": "nvml" if self._nvml else "nvidia-smi"}
 
 
 def dist_env():
@@ -241,10 +274,10 @@ def run_ours(args):
                 e1.record(stream)
                 merge_ms.append((e0, e1))
         else:
+            timers = {} if record else None
+            res, _ = run_cut_sharded(circ, spec.n, rank=rank, world=world, out=out, merge_events=timers)
             if record:
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
-            res, _ = run_cut_sharded(circ, spec.n, rank=rank, world=world, out=out)
+                merge_ms.append((timers["start"], timers["end"]))
             del res
 
     for _ in range(args.warmup):

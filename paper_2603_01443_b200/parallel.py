@@ -110,7 +110,7 @@ def _as_complex(t):
 
 
 def run_cut_sharded(circuit, n: int, *, rank: int, world: int, dtype=np.complex128, out=None,
-                    group=None, simulate_slice=None, merge_shard=None, all_gather=None):
+                    group=None, simulate_slice=None, merge_shard=None, all_gather=None, merge_events=None):
     """Cut pipeline on `world` ranks; returns (ShardedState-like tensor, (begin, end)).
 
     simulate_slice(family, v0, v1) -> tensor [v1-v0, 2^q_i] and
@@ -154,8 +154,14 @@ def run_cut_sharded(circuit, n: int, *, rank: int, world: int, dtype=np.complex1
     if merge_shard is None:
         from .merging import merge_chain_device
 
+        if merge_events is not None:
+            merge_events["start"] = torch.cuda.Event(enable_timing=True)
+            merge_events["end"] = torch.cuda.Event(enable_timing=True)
+            merge_events["start"].record()
         res = merge_chain_device(chain, [b.contiguous() for b in batches], dtype=dtype, out=out,
                                  out_range=(begin, end))
+        if merge_events is not None:
+            merge_events["end"].record()
     else:
         res = merge_shard(chain, batches, (begin, end))
     return res, (begin, end)
