@@ -228,9 +228,8 @@ def run_ours(args):
     import paper_2603_01443_b200 as cb
     from paper_2603_01443_b200 import _native
     from paper_2603_01443_b200.generators import BASELINE_CONFIGS
-    from paper_2603_01443_b200.merging import merge_chain_device
     from paper_2603_01443_b200.parallel import run_cut_sharded
-    from paper_2603_01443_b200.pipeline import preprocess, run_cut_to_host, simulate_segments
+    from paper_2603_01443_b200.pipeline import preprocess, run_cut_to_host
 
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
@@ -252,7 +251,8 @@ def run_ours(args):
 
     # shard geometry and preallocated output / workspace
     prep0 = preprocess(circ, spec.n)
-    ws_bytes, bond, qlow = prep0.chain.plan()
+    ws_bytes, qlow, _c = _native.cut_workspace(q, circ.table, [q // spec.n] * spec.n)
+    bond = prep0.chain.plan()[1]
     from paper_2603_01443_b200.parallel import shard_range
 
     begin, end = shard_range(q, world, rank, qlow)
@@ -263,16 +263,13 @@ def run_ours(args):
 
     def step(record=False):
         if world == 1:
-            prep = preprocess(circ, spec.n)
-            batches = simulate_segments(prep)
+            # one native call: C++ preprocess -> batched variant sweeps -> chain merge
+            evs = None
             if record:
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-            merge_chain_device(prep.chain, batches, out=out, out_range=(begin, end), workspace=workspace)
+                evs = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            cb.run_cut(circ, spec.n, out=out, workspace=workspace, events=evs)
             if record:
-                e1.record(stream)
-                merge_ms.append((e0, e1))
+                merge_ms.append((evs[1], evs[2]))
         else:
             timers = {} if record else None
             res, _ = run_cut_sharded(circ, spec.n, rank=rank, world=world, out=out, merge_events=timers)

@@ -39,6 +39,7 @@ extern "C" {
 #define CS_ERR_NCCL 4
 #define CS_ERR_INTERNAL 5
 #define CS_ERR_NODEVICE 6
+#define CS_ERR_TOPOLOGY 7
 
 #define CS_C128 0
 #define CS_C64 1
@@ -126,6 +127,36 @@ int cs_merge_chain(int32_t n, const int32_t* seg_nq, const void* const* seg_stat
                    const int32_t* cut_boundary, const double* term_coef, int32_t force_bond,
                    int64_t out_begin, int64_t out_end, void* out, void* workspace,
                    int64_t workspace_bytes, int32_t dtype, void* stream);
+
+/* ---- the cut pipeline as one call -------------------------------------------
+ * Preprocess (reference plan_cut_sizes + decompose, cutting.py:82-136,
+ * 190-283) on the host in C++, simulate every segment's variant family in
+ * batched sweeps (segments on internal side streams joined back into
+ * `stream`), and write amplitudes [out_begin, out_end) of the reconstructed
+ * state (chain merge) into `out` — the reference's _cut_once
+ * (harness.py:125-145) behind one entry point. seg_sizes has n_seg entries
+ * summing to nq. The variant states and merge intermediates live in the
+ * caller's `workspace` (size from cs_cut_workspace); out_begin/out_end must
+ * be multiples of 2^q_low. stage_events (nullable: 3 cudaEvent_t) are
+ * recorded on `stream` before the subcircuit stage, between it and the merge,
+ * and after the merge (no synchronisation). stage_ms (nullable, 3 doubles)
+ * receives the host preprocess time and the event-timed subcircuit and merge
+ * stages (the call then synchronises `stream`). */
+int cs_cut_workspace(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int64_t* qb,
+                     const double* params, int64_t n_gates, int32_t n_seg, const int32_t* seg_sizes,
+                     int32_t force_bond, int32_t dtype, int64_t* workspace_bytes, int32_t* q_low,
+                     int32_t* c_total);
+int cs_cut_run(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int64_t* qb,
+               const double* params, int64_t n_gates, int32_t n_seg, const int32_t* seg_sizes,
+               int32_t force_bond, int64_t out_begin, int64_t out_end, void* out, void* workspace,
+               int64_t workspace_bytes, int32_t dtype, void* stream, void* const* stage_events,
+               double* stage_ms);
+/* Host-only: the C++ preprocess result as JSON (cuts and per-segment
+ * template tables with their cut slots) — checked against the Python
+ * planner and the reference's golden tables in the CPU tests. */
+int cs_cut_describe_json(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int64_t* qb,
+                         const double* params, int64_t n_gates, int32_t n_seg, const int32_t* seg_sizes,
+                         char* buf, int64_t buflen, int64_t* needed);
 
 /* Device reductions (synchronise `stream`). */
 int cs_maxabsdiff(const void* a, const void* b, int64_t n, int32_t dtype, double* result,

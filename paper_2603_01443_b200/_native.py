@@ -16,6 +16,7 @@ from .errors import (
     CutbenchError,
     DeviceError,
     NativeUnavailableError,
+    UnsupportedTopologyError,
     ValidationError,
 )
 
@@ -31,6 +32,7 @@ _ERRORS = {
     4: DeviceError,
     5: CutbenchError,
     6: NativeUnavailableError,
+    7: UnsupportedTopologyError,
 }
 
 _i32, _i64, _u64, _vp, _dp = (ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_void_p,
@@ -56,6 +58,11 @@ SIGNATURES = {
                                            _vp]),
     "cs_merge_chain": (ctypes.c_int, [_i32, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _i32, _i64, _i64, _vp,
                                       _vp, _i64, _i32, _vp]),
+    "cs_cut_workspace": (ctypes.c_int, [_i32, _vp, _vp, _vp, _vp, _i64, _i32, _vp, _i32, _i32, _vp, _vp,
+                                        _vp]),
+    "cs_cut_run": (ctypes.c_int, [_i32, _vp, _vp, _vp, _vp, _i64, _i32, _vp, _i32, _i64, _i64, _vp, _vp,
+                                  _i64, _i32, _vp, _vp, _vp]),
+    "cs_cut_describe_json": (ctypes.c_int, [_i32, _vp, _vp, _vp, _vp, _i64, _i32, _vp, _vp, _i64, _vp]),
     "cs_maxabsdiff": (ctypes.c_int, [_vp, _vp, _i64, _i32, _vp, _vp]),
     "cs_maxabs": (ctypes.c_int, [_vp, _i64, _i32, _vp, _vp]),
     "cs_inner": (ctypes.c_int, [_vp, _vp, _i64, _i32, _vp, _vp]),
@@ -176,3 +183,36 @@ def chain_plan(n, seg_nq, seg_ncuts, seg_cut_ids, c_total, cut_boundary, term_co
                                   force_bond, dtype, ptr(ws), ptr(bond), ptr(qlow)),
           "cs_merge_chain_plan")
     return int(ws[0]), int(bond[0]), int(qlow[0])
+
+
+def _table_args(table):
+    k = np.ascontiguousarray(table.kinds, dtype=np.uint8)
+    return k, c_i64(table.qa), c_i64(table.qb), c_f64(table.params)
+
+
+def cut_workspace(nq, table, sizes, force_bond=-1, dtype=CS_C128):
+    """Host-only: (workspace_bytes, q_low, c_total) of cs_cut_run."""
+    k, qa, qb, prm = _table_args(table)
+    sz = c_i32(sizes)
+    ws = np.zeros(1, np.int64)
+    ql = np.zeros(1, np.int32)
+    ct = np.zeros(1, np.int32)
+    check(load().cs_cut_workspace(nq, ptr(k), ptr(qa), ptr(qb), ptr(prm), len(k), len(sz), ptr(sz), force_bond,
+                                  dtype, ptr(ws), ptr(ql), ptr(ct)), "cs_cut_workspace")
+    return int(ws[0]), int(ql[0]), int(ct[0])
+
+
+def cut_describe(nq, table, sizes) -> dict:
+    """Host-only: the C++ preprocess (cuts and per-segment templates)."""
+    import json
+
+    lib = load()
+    k, qa, qb, prm = _table_args(table)
+    sz = c_i32(sizes)
+    need = np.zeros(1, np.int64)
+    check(lib.cs_cut_describe_json(nq, ptr(k), ptr(qa), ptr(qb), ptr(prm), len(k), len(sz), ptr(sz), None, 0,
+                                   ptr(need)), "cs_cut_describe_json")
+    buf = ctypes.create_string_buffer(int(need[0]))
+    check(lib.cs_cut_describe_json(nq, ptr(k), ptr(qa), ptr(qb), ptr(prm), len(k), len(sz), ptr(sz), buf,
+                                   int(need[0]), ptr(need)), "cs_cut_describe_json")
+    return json.loads(buf.value.decode())

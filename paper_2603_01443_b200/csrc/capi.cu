@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -439,6 +440,200 @@ std::shared_ptr<JitModule> program_jit(const Program& prog, int dtype) {
   return prog.jit;
 }
 
+int run_program(const Program& prog_ref, int nq, void* states, int64_t n_states, int64_t state_stride,
+                uint64_t variant_base, int init_zero, int dtype, cudaStream_t st) {
+  const Program* prog = &prog_ref;
+  std::shared_ptr<JitModule> jit = program_jit(*prog, dtype);
+  static SweepParams p;
+  static RegParams rp;
+  static std::mutex pm;
+  std::lock_guard<std::mutex> lk(pm);
+  bool first = true;
+  size_t li = 0;
+  for (const Launch& ln : prog->launches) {
+    const JitKernel* jk = (jit && li < jit->kernels.size() && jit->kernels[li].kernel) ? &jit->kernels[li] : nullptr;
+    ++li;
+    const Sweep& sw = prog->sweeps[size_t(ln.sweep)];
+    const int T = sw.tile_bits;
+    if (sw.hq.size() > size_t(kMaxTileBits) || sw.oq.size() > 64)
+      return fail(CS_ERR_INTERNAL, "sweep geometry exceeds the kernel limits");
+    const uint32_t n_tiles = uint32_t(1) << (nq - T);
+    for (int64_t v0 = 0; v0 < n_states; v0 += 65535) {
+      const int64_t vc = std::min<int64_t>(65535, n_states - v0);
+      void* sp = static_cast<char*>(states) + size_t(v0) * size_t(state_stride) * elem_bytes(dtype);
+      cudaError_t e;
+      if (jk) {
+        void* sp_arg = sp;
+        long long stride_arg = state_stride;
+        unsigned long long vbase_arg = variant_base + uint64_t(v0);
+        int init_arg = (first && init_zero) ? 1 : 0;
+        void* args[] = {&sp_arg, &stride_arg, &vbase_arg, &init_arg};
+        e = cudaSuccess;
+        if (jk->smem > 48 * 1024) {
+          int dev = 0;
+          cudaGetDevice(&dev);
+          e = cudaKernelSetAttributeForDevice(jk->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              int(jk->smem), dev);
+        }
+        if (e == cudaSuccess)
+          e = cudaLaunchKernel(reinterpret_cast<const void*>(jk->kernel), dim3(n_tiles, unsigned(vc), 1),
+                               dim3(unsigned(jk->threads), 1, 1), args, jk->smem, st);
+      } else if (prog->engine == 1) {
+        if (ln.reg.size() > size_t(kMaxRegOps)) return fail(CS_ERR_INTERNAL, "register program too long");
+        std::memset(&rp, 0, offsetof(RegParams, ops));
+        rp.states = sp;
+        rp.stride = state_stride;
+        rp.variant_base = variant_base + uint64_t(v0);
+        rp.tile_bits = T;
+        rp.low_bits = sw.low_bits;
+        rp.n_high = int32_t(sw.hq.size());
+        rp.n_out = int32_t(sw.oq.size());
+        rp.n_ops = int32_t(ln.reg.size());
+        rp.init_basis = (first && init_zero) ? 1 : 0;
+        rp.n_states = int32_t(vc);
+        for (size_t j = 0; j < sw.hq.size() && j < size_t(kMaxTileBits); ++j) rp.hq[j] = int8_t(sw.hq[j]);
+        for (size_t j = 0; j < sw.oq.size() && j < 64; ++j) rp.oq[j] = int8_t(sw.oq[j]);
+        if (!ln.reg.empty()) std::memcpy(rp.ops, ln.reg.data(), sizeof(RegOp) * ln.reg.size());
+        e = launch_rsweep(rp, reg_bits_for(T), n_tiles, uint32_t(vc), st, dtype);
+      } else {
+        std::memset(&p, 0, offsetof(SweepParams, ops));
+        p.nq = nq;
+        p.tile_bits = T;
+        p.low_bits = sw.low_bits;
+        p.n_high = int32_t(sw.hq.size());
+        p.n_out = int32_t(sw.oq.size());
+        for (size_t j = 0; j < sw.hq.size() && j < size_t(kMaxTileBits); ++j) p.hq[j] = int8_t(sw.hq[j]);
+        for (size_t j = 0; j < sw.oq.size() && j < 64; ++j) p.oq[j] = int8_t(sw.oq[j]);
+        p.n_ops = int32_t(ln.entries.size());
+        if (!ln.entries.empty()) std::memcpy(p.ops, ln.entries.data(), sizeof(SweepOp) * ln.entries.size());
+        p.init_basis = (first && init_zero) ? 1 : 0;
+        p.stride = state_stride;
+        int threads = int(g_opt.threads);
+        if (threads == 0) threads = sweep_threads(T);
+        threads = std::min(threads, 256);
+        p.states = sp;
+        p.variant_base = variant_base + uint64_t(v0);
+        p.n_states = int32_t(vc);
+        e = launch_sweep(p, n_tiles, choose_vb(n_states), threads, st, dtype);
+      }
+      g_launches.fetch_add(1);
+      if (e != cudaSuccess) return cuda_fail(e, "sweep kernel launch");
+    }
+    first = false;
+  }
+  return CS_OK;
+}
+
+
+int run_chain(const ChainPlan& plan, int n, const void* const* seg_states, int64_t out_begin, int64_t out_end,
+              void* out, void* workspace, int64_t workspace_bytes, int dtype, cudaStream_t st) {
+  const size_t eb = elem_bytes(dtype);
+  std::vector<const void*> bufs(size_t(n) + plan.buf_amps.size(), nullptr);
+  for (int j = 0; j < n; ++j) {
+    if (!seg_states[j]) return fail(CS_ERR_INVALID, "null segment state pointer");
+    bufs[size_t(j)] = seg_states[j];
+  }
+  int64_t off = 0;
+  for (size_t b = 0; b < plan.buf_amps.size(); ++b) {
+    const int64_t bytes = (plan.buf_amps[b] * int64_t(eb) + 255) / 256 * 256;
+    if (off + bytes > workspace_bytes || !workspace)
+      return fail(CS_ERR_INVALID, "merge workspace too small (query cs_merge_chain_plan)");
+    bufs[size_t(n) + b] = static_cast<char*>(workspace) + off;
+    off += bytes;
+  }
+  const int64_t unit = int64_t(1) << plan.q_low;
+  if (out_begin < 0 || out_end < out_begin || (out_begin % unit) || (out_end % unit))
+    return fail(CS_ERR_INVALID, "output range must be aligned to 2^q_low = " + std::to_string(unit) + " amplitudes");
+  for (const MergeStep& s : plan.steps) {
+    const void* hi = bufs[size_t(s.hi_buf)];
+    const void* lo = bufs[size_t(s.lo_buf)];
+    int rc;
+    if (s.final_step) {
+      const int64_t r0 = out_begin / unit, r1 = out_end / unit;
+      if (r1 > s.hi_len) return fail(CS_ERR_INVALID, "output range beyond the state");
+      rc = merge_terms_impl(1, s.K, s.hidx.data(), s.lidx.data(), s.coef.data(), hi, s.hi_len, lo, s.lo_len, r0,
+                            r1, out, (r1 - r0) * s.lo_len, 0, dtype, st);
+    } else {
+      void* dst = const_cast<void*>(bufs[size_t(s.out_buf)]);
+      rc = merge_terms_impl(s.S, s.K, s.hidx.data(), s.lidx.data(), s.coef.data(), hi, s.hi_len, lo, s.lo_len, 0,
+                            s.hi_len, dst, s.hi_len * s.lo_len, 0, dtype, st);
+    }
+    if (rc != CS_OK) return rc;
+  }
+  return CS_OK;
+}
+
+
+
+// ---- the whole cut pipeline behind one call ---------------------------------
+struct CutJob {
+  CutPrep prep;
+  ChainPlan plan;
+  std::vector<int32_t> seg_nq, seg_ncuts, seg_cut_ids;
+  std::vector<int64_t> seg_off;  // workspace byte offsets of the segment batches
+  int64_t chain_off = 0, total_bytes = 0;
+};
+
+const double kTermCoef[4] = {0.5, -0.5, 0.5, 0.5};  // (1-i)/2, (1+i)/2 (reference cutting.py:34-35)
+
+bool cut_job(int nq, const uint8_t* kinds, const int64_t* qa, const int64_t* qb, const double* params,
+             int64_t n_gates, int n_seg, const int32_t* sizes, int force_bond, int dtype, CutJob* job, int* rc) {
+  try {
+    job->prep = cut_prepare(nq, kinds, qa, qb, params, n_gates, n_seg, sizes);
+  } catch (const PlanError& pe) {
+    *rc = fail(pe.code, pe.msg);
+    return false;
+  }
+  const CutPrep& pr = job->prep;
+  for (const SegmentPlan& sp : pr.segs) {
+    job->seg_nq.push_back(sp.nq);
+    job->seg_ncuts.push_back(int32_t(sp.cut_ids.size()));
+    for (int32_t c : sp.cut_ids) job->seg_cut_ids.push_back(c);
+  }
+  PlanError err{0, ""};
+  const int32_t dummy = 0;
+  if (!plan_chain(pr.n, job->seg_nq.data(), job->seg_ncuts.data(),
+                  job->seg_cut_ids.empty() ? &dummy : job->seg_cut_ids.data(), pr.c_total(),
+                  pr.cut_boundary.empty() ? &dummy : pr.cut_boundary.data(), kTermCoef, force_bond, &job->plan,
+                  &err)) {
+    *rc = fail(err.code, err.msg);
+    return false;
+  }
+  const int64_t eb = int64_t(elem_bytes(dtype));
+  int64_t off = 0;
+  for (const SegmentPlan& sp : pr.segs) {
+    if (sp.cut_ids.size() > 30 || sp.nq > 40) {
+      *rc = fail(CS_ERR_CAPACITY, "segment too large for a variant batch");
+      return false;
+    }
+    job->seg_off.push_back(off);
+    off += ((int64_t(1) << (sp.cut_ids.size() + size_t(sp.nq))) * eb + 255) / 256 * 256;
+  }
+  job->chain_off = off;
+  for (int64_t a : job->plan.buf_amps) off += (a * eb + 255) / 256 * 256;
+  job->total_bytes = off;
+  return true;
+}
+
+struct SideStreams {
+  std::mutex mu;
+  std::vector<std::vector<cudaStream_t>> per_device;
+} g_side;
+
+cudaStream_t side_stream(int i) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_side.mu);
+  if (int(g_side.per_device.size()) <= dev) g_side.per_device.resize(size_t(dev) + 1);
+  auto& v = g_side.per_device[size_t(dev)];
+  while (int(v.size()) <= i) {
+    cudaStream_t s = nullptr;
+    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    v.push_back(s);
+  }
+  return v[size_t(i)];
+}
+
 }  // namespace
 
 extern "C" {
@@ -552,85 +747,7 @@ int cs_sim_batch(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int6
   } catch (const PlanError& pe) {
     return fail(pe.code, pe.msg);
   }
-  std::shared_ptr<JitModule> jit = program_jit(*prog, dtype);
-  static SweepParams p;
-  static RegParams rp;
-  static std::mutex pm;
-  std::lock_guard<std::mutex> lk(pm);
-  bool first = true;
-  size_t li = 0;
-  for (const Launch& ln : prog->launches) {
-    const JitKernel* jk = (jit && li < jit->kernels.size() && jit->kernels[li].kernel) ? &jit->kernels[li] : nullptr;
-    ++li;
-    const Sweep& sw = prog->sweeps[size_t(ln.sweep)];
-    const int T = sw.tile_bits;
-    if (sw.hq.size() > size_t(kMaxTileBits) || sw.oq.size() > 64)
-      return fail(CS_ERR_INTERNAL, "sweep geometry exceeds the kernel limits");
-    const uint32_t n_tiles = uint32_t(1) << (nq - T);
-    for (int64_t v0 = 0; v0 < n_states; v0 += 65535) {
-      const int64_t vc = std::min<int64_t>(65535, n_states - v0);
-      void* sp = static_cast<char*>(states) + size_t(v0) * size_t(state_stride) * elem_bytes(dtype);
-      cudaError_t e;
-      if (jk) {
-        void* sp_arg = sp;
-        long long stride_arg = state_stride;
-        unsigned long long vbase_arg = variant_base + uint64_t(v0);
-        int init_arg = (first && init_zero) ? 1 : 0;
-        void* args[] = {&sp_arg, &stride_arg, &vbase_arg, &init_arg};
-        e = cudaSuccess;
-        if (jk->smem > 48 * 1024) {
-          int dev = 0;
-          cudaGetDevice(&dev);
-          e = cudaKernelSetAttributeForDevice(jk->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              int(jk->smem), dev);
-        }
-        if (e == cudaSuccess)
-          e = cudaLaunchKernel(reinterpret_cast<const void*>(jk->kernel), dim3(n_tiles, unsigned(vc), 1),
-                               dim3(unsigned(jk->threads), 1, 1), args, jk->smem, st);
-      } else if (prog->engine == 1) {
-        if (ln.reg.size() > size_t(kMaxRegOps)) return fail(CS_ERR_INTERNAL, "register program too long");
-        std::memset(&rp, 0, offsetof(RegParams, ops));
-        rp.states = sp;
-        rp.stride = state_stride;
-        rp.variant_base = variant_base + uint64_t(v0);
-        rp.tile_bits = T;
-        rp.low_bits = sw.low_bits;
-        rp.n_high = int32_t(sw.hq.size());
-        rp.n_out = int32_t(sw.oq.size());
-        rp.n_ops = int32_t(ln.reg.size());
-        rp.init_basis = (first && init_zero) ? 1 : 0;
-        rp.n_states = int32_t(vc);
-        for (size_t j = 0; j < sw.hq.size() && j < size_t(kMaxTileBits); ++j) rp.hq[j] = int8_t(sw.hq[j]);
-        for (size_t j = 0; j < sw.oq.size() && j < 64; ++j) rp.oq[j] = int8_t(sw.oq[j]);
-        if (!ln.reg.empty()) std::memcpy(rp.ops, ln.reg.data(), sizeof(RegOp) * ln.reg.size());
-        e = launch_rsweep(rp, reg_bits_for(T), n_tiles, uint32_t(vc), st, dtype);
-      } else {
-        std::memset(&p, 0, offsetof(SweepParams, ops));
-        p.nq = nq;
-        p.tile_bits = T;
-        p.low_bits = sw.low_bits;
-        p.n_high = int32_t(sw.hq.size());
-        p.n_out = int32_t(sw.oq.size());
-        for (size_t j = 0; j < sw.hq.size() && j < size_t(kMaxTileBits); ++j) p.hq[j] = int8_t(sw.hq[j]);
-        for (size_t j = 0; j < sw.oq.size() && j < 64; ++j) p.oq[j] = int8_t(sw.oq[j]);
-        p.n_ops = int32_t(ln.entries.size());
-        if (!ln.entries.empty()) std::memcpy(p.ops, ln.entries.data(), sizeof(SweepOp) * ln.entries.size());
-        p.init_basis = (first && init_zero) ? 1 : 0;
-        p.stride = state_stride;
-        int threads = int(g_opt.threads);
-        if (threads == 0) threads = sweep_threads(T);
-        threads = std::min(threads, 256);
-        p.states = sp;
-        p.variant_base = variant_base + uint64_t(v0);
-        p.n_states = int32_t(vc);
-        e = launch_sweep(p, n_tiles, choose_vb(n_states), threads, st, dtype);
-      }
-      g_launches.fetch_add(1);
-      if (e != cudaSuccess) return cuda_fail(e, "sweep kernel launch");
-    }
-    first = false;
-  }
-  return CS_OK;
+  return run_program(*prog, nq, states, n_states, state_stride, variant_base, init_zero, dtype, st);
 }
 
 int cs_sweep_plan_json(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int64_t* qb,
@@ -712,43 +829,125 @@ int cs_merge_chain(int32_t n, const int32_t* seg_nq, const void* const* seg_stat
   PlanError err{0, ""};
   if (!plan_chain(n, seg_nq, seg_ncuts, seg_cut_ids, c_total, cut_boundary, term_coef, force_bond, &plan, &err))
     return fail(err.code, err.msg);
-  const size_t eb = elem_bytes(dtype);
-  std::vector<const void*> bufs(size_t(n) + plan.buf_amps.size(), nullptr);
-  for (int j = 0; j < n; ++j) {
-    if (!seg_states[j]) return fail(CS_ERR_INVALID, "null segment state pointer");
-    bufs[size_t(j)] = seg_states[j];
+  return run_chain(plan, n, seg_states, out_begin, out_end, out, workspace, workspace_bytes, dtype,
+                   as_stream(stream));
+}
+
+
+int cs_cut_workspace(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int64_t* qb, const double* params,
+                     int64_t n_gates, int32_t n_seg, const int32_t* seg_sizes, int32_t force_bond, int32_t dtype,
+                     int64_t* workspace_bytes, int32_t* q_low, int32_t* c_total) {
+  if (!valid_dtype(dtype)) return fail(CS_ERR_INVALID, "dtype must be CS_C128 or CS_C64");
+  if (nq < 2 || nq > 62 || !seg_sizes) return fail(CS_ERR_INVALID, "bad qubit count or segment sizes");
+  CutJob job;
+  int rc = CS_OK;
+  if (!cut_job(nq, kinds, qa, qb, params, n_gates, n_seg, seg_sizes, force_bond, dtype, &job, &rc)) return rc;
+  if (workspace_bytes) *workspace_bytes = job.total_bytes;
+  if (q_low) *q_low = job.plan.q_low;
+  if (c_total) *c_total = job.prep.c_total();
+  return CS_OK;
+}
+
+int cs_cut_describe_json(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int64_t* qb,
+                         const double* params, int64_t n_gates, int32_t n_seg, const int32_t* seg_sizes, char* buf,
+                         int64_t buflen, int64_t* needed) {
+  if (nq < 2 || nq > 62 || !seg_sizes) return fail(CS_ERR_INVALID, "bad qubit count or segment sizes");
+  std::string js;
+  try {
+    js = cut_prep_to_json(cut_prepare(nq, kinds, qa, qb, params, n_gates, n_seg, seg_sizes));
+  } catch (const PlanError& pe) {
+    return fail(pe.code, pe.msg);
   }
-  int64_t off = 0;
-  for (size_t b = 0; b < plan.buf_amps.size(); ++b) {
-    const int64_t bytes = (plan.buf_amps[b] * int64_t(eb) + 255) / 256 * 256;
-    if (off + bytes > workspace_bytes || !workspace)
-      return fail(CS_ERR_INVALID, "merge workspace too small (query cs_merge_chain_plan)");
-    bufs[size_t(n) + b] = static_cast<char*>(workspace) + off;
-    off += bytes;
-  }
-  const int64_t total = int64_t(1) << (plan.q_low + 0);
-  (void)total;
-  const int64_t unit = int64_t(1) << plan.q_low;
-  if (out_begin < 0 || out_end < out_begin || (out_begin % unit) || (out_end % unit))
-    return fail(CS_ERR_INVALID, "output range must be aligned to 2^q_low = " + std::to_string(unit) + " amplitudes");
-  cudaStream_t st = as_stream(stream);
-  for (const MergeStep& s : plan.steps) {
-    const void* hi = bufs[size_t(s.hi_buf)];
-    const void* lo = bufs[size_t(s.lo_buf)];
-    int rc;
-    if (s.final_step) {
-      const int64_t r0 = out_begin / unit, r1 = out_end / unit;
-      if (r1 > s.hi_len) return fail(CS_ERR_INVALID, "output range beyond the state");
-      rc = merge_terms_impl(1, s.K, s.hidx.data(), s.lidx.data(), s.coef.data(), hi, s.hi_len, lo, s.lo_len, r0,
-                            r1, out, (r1 - r0) * s.lo_len, 0, dtype, st);
-    } else {
-      void* dst = const_cast<void*>(bufs[size_t(s.out_buf)]);
-      rc = merge_terms_impl(s.S, s.K, s.hidx.data(), s.lidx.data(), s.coef.data(), hi, s.hi_len, lo, s.lo_len, 0,
-                            s.hi_len, dst, s.hi_len * s.lo_len, 0, dtype, st);
-    }
-    if (rc != CS_OK) return rc;
+  if (needed) *needed = int64_t(js.size()) + 1;
+  if (buf && buflen > 0) {
+    const size_t m = std::min(size_t(buflen - 1), js.size());
+    std::memcpy(buf, js.data(), m);
+    buf[m] = 0;
   }
   return CS_OK;
+}
+
+int cs_cut_run(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int64_t* qb, const double* params,
+               int64_t n_gates, int32_t n_seg, const int32_t* seg_sizes, int32_t force_bond, int64_t out_begin,
+               int64_t out_end, void* out, void* workspace, int64_t workspace_bytes, int32_t dtype, void* stream,
+               void* const* stage_events, double* stage_ms) {
+  if (!valid_dtype(dtype)) return fail(CS_ERR_INVALID, "dtype must be CS_C128 or CS_C64");
+  if (nq < 2 || nq > 62 || !seg_sizes) return fail(CS_ERR_INVALID, "bad qubit count or segment sizes");
+  if (!out) return fail(CS_ERR_INVALID, "null output pointer");
+  const auto t0 = std::chrono::steady_clock::now();
+  CutJob job;
+  int rc = CS_OK;
+  if (!cut_job(nq, kinds, qa, qb, params, n_gates, n_seg, seg_sizes, force_bond, dtype, &job, &rc)) return rc;
+  if (!workspace || workspace_bytes < job.total_bytes)
+    return fail(CS_ERR_INVALID, "cut workspace too small (query cs_cut_workspace)");
+  const CutPrep& pr = job.prep;
+  std::vector<std::shared_ptr<const Program>> progs;
+  try {
+    for (const SegmentPlan& sp : pr.segs)
+      progs.push_back(build_schedule(sp.nq, sp.kinds.data(), sp.qa.data(), sp.qb.data(), sp.params.data(),
+                                     sp.slots.data(), int64_t(sp.kinds.size()),
+                                     int64_t(1) << sp.cut_ids.size(), 0, dtype));
+  } catch (const PlanError& pe) {
+    return fail(pe.code, pe.msg);
+  }
+  for (const auto& pg : progs) program_jit(*pg, dtype);  // compile before any timing
+  const double t_pre = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  cudaStream_t st = as_stream(stream);
+  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  if (stage_events) {
+    for (int i = 0; i < 3; ++i) ev[i] = static_cast<cudaEvent_t>(stage_events[i]);
+  } else if (stage_ms) {
+    for (auto& e : ev) cudaEventCreate(&e);
+  }
+  if (ev[0]) cudaEventRecord(ev[0], st);
+  // batched subcircuit simulation: every segment's variant family at once,
+  // segments on side streams forked from / joined into the caller's stream
+  std::vector<const void*> seg_states;
+  cudaEvent_t fork = nullptr;
+  if (pr.n > 1) {
+    cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
+    cudaEventRecord(fork, st);
+  }
+  for (size_t s = 0; s < pr.segs.size(); ++s) {
+    const SegmentPlan& sp = pr.segs[s];
+    void* states = static_cast<char*>(workspace) + job.seg_off[s];
+    seg_states.push_back(states);
+    const int64_t nv = int64_t(1) << sp.cut_ids.size();
+    cudaStream_t ss = pr.n > 1 ? side_stream(int(s % 4)) : st;
+    if (fork) cudaStreamWaitEvent(ss, fork, 0);
+    rc = run_program(*progs[s], sp.nq, states, nv, int64_t(1) << sp.nq, 0, 1, dtype, ss);
+    if (rc != CS_OK) {
+      if (fork) cudaEventDestroy(fork);
+      return rc;
+    }
+    if (ss != st) {
+      cudaEvent_t done = nullptr;
+      cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
+      cudaEventRecord(done, ss);
+      cudaStreamWaitEvent(st, done, 0);
+      cudaEventDestroy(done);
+    }
+  }
+  if (fork) cudaEventDestroy(fork);
+  if (ev[1]) cudaEventRecord(ev[1], st);
+  rc = run_chain(job.plan, pr.n, seg_states.data(), out_begin, out_end, out,
+                 static_cast<char*>(workspace) + job.chain_off, job.total_bytes - job.chain_off, dtype, st);
+  if (rc != CS_OK) return rc;
+  if (ev[2]) cudaEventRecord(ev[2], st);
+  if (stage_ms) {
+    cudaError_t e = cudaEventSynchronize(ev[2]);
+    float a = 0, b = 0;
+    cudaEventElapsedTime(&a, ev[0], ev[1]);
+    cudaEventElapsedTime(&b, ev[1], ev[2]);
+    if (!stage_events)
+      for (auto& x : ev) cudaEventDestroy(x);
+    if (e != cudaSuccess) return cuda_fail(e, "cut pipeline");
+    stage_ms[0] = t_pre;
+    stage_ms[1] = a;
+    stage_ms[2] = b;
+  }
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? CS_OK : cuda_fail(e, "cut pipeline");
 }
 
 static int reduce_common(const void* a, const void* b, int64_t n, int mode, int32_t dtype, double* result,

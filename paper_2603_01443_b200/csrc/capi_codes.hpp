@@ -8,3 +8,4 @@
 #define CS_ERR_NCCL 4      /* -> DeviceError */
 #define CS_ERR_INTERNAL 5  /* -> CutbenchError */
 #define CS_ERR_NODEVICE 6  /* -> NativeUnavailableError */
+#define CS_ERR_TOPOLOGY 7  /* -> UnsupportedTopologyError */

@@ -502,6 +502,115 @@ std::string reg_programs_to_json(const std::vector<Sweep>& sweeps, int nq) {
 }
 
 // ---------------------------------------------------------------------------
+// cut preprocess
+// ---------------------------------------------------------------------------
+CutPrep cut_prepare(int nq, const uint8_t* kinds, const int64_t* qa, const int64_t* qb, const double* params,
+                    int64_t G, int n, const int32_t* sizes) {
+  if (n < 2) throw PlanError{CS_ERR_INVALID, "segment count must be >= 2, got " + std::to_string(n)};
+  CutPrep prep;
+  prep.n = n;
+  std::vector<int> seg_of;
+  int total = 0;
+  for (int s = 0; s < n; ++s) {
+    if (sizes[s] < 1) throw PlanError{CS_ERR_INVALID, "segment sizes must be >= 1"};
+    prep.sizes.push_back(sizes[s]);
+    for (int k = 0; k < sizes[s]; ++k) seg_of.push_back(s);
+    total += sizes[s];
+  }
+  if (total != nq)
+    throw PlanError{CS_ERR_INVALID, "segment sizes must sum to q=" + std::to_string(nq)};
+  std::vector<int> cut_at(size_t(G), -1);
+  for (int64_t g = 0; g < G; ++g) {
+    const int k = kinds[g];
+    if (k > 7) throw PlanError{CS_ERR_INVALID, "unknown gate kind code " + std::to_string(k)};
+    if (qa[g] < 0 || qa[g] >= nq) throw PlanError{CS_ERR_INVALID, "gate qubit outside the circuit"};
+    if (k != 5 && k != 6) continue;
+    if (qb[g] < 0 || qb[g] >= nq || qb[g] == qa[g]) throw PlanError{CS_ERR_INVALID, "bad two-qubit gate"};
+    const int sa = seg_of[size_t(qa[g])], sb = seg_of[size_t(qb[g])];
+    if (sa == sb) continue;
+    if (std::abs(sa - sb) != 1)
+      throw PlanError{CS_ERR_TOPOLOGY, "gate at position " + std::to_string(g) + " spans non-adjacent segments " +
+                                           std::to_string(sa) + " and " + std::to_string(sb)};
+    cut_at[size_t(g)] = int(prep.cut_pos.size());
+    prep.cut_pos.push_back(g);
+    prep.cut_boundary.push_back(std::min(sa, sb));
+    prep.cut_ctrl.push_back(sa);
+    prep.cut_tgt.push_back(sb);
+  }
+  int first = 0;
+  for (int s = 0; s < n; ++s) {
+    SegmentPlan sp;
+    sp.nq = sizes[s];
+    sp.first = first;
+    auto put = [&](uint8_t k, int64_t a, int64_t b, const double* p, int32_t slot) {
+      sp.kinds.push_back(k);
+      sp.qa.push_back(a);
+      sp.qb.push_back(b);
+      sp.params.push_back(p ? p[0] : 0.0);
+      sp.params.push_back(p ? p[1] : 0.0);
+      sp.params.push_back(p ? p[2] : 0.0);
+      sp.slots.push_back(slot);
+    };
+    for (int64_t g = 0; g < G; ++g) {
+      const int c = cut_at[size_t(g)];
+      if (c >= 0) {
+        // cut: control side gets S/Sdg, target side S/Sdg (CZ) or H,S/Sdg,H (CX)
+        const int32_t bit = int32_t(sp.cut_ids.size());
+        if (prep.cut_ctrl[size_t(c)] == s) {
+          sp.cut_ids.push_back(c);
+          put(3, qa[g] - first, -1, nullptr, bit);
+        } else if (prep.cut_tgt[size_t(c)] == s) {
+          sp.cut_ids.push_back(c);
+          const int64_t lq = qb[g] - first;
+          if (kinds[g] == 5) {
+            put(0, lq, -1, nullptr, -1);
+            put(3, lq, -1, nullptr, bit);
+            put(0, lq, -1, nullptr, -1);
+          } else {
+            put(3, lq, -1, nullptr, bit);
+          }
+        }
+        continue;
+      }
+      if (seg_of[size_t(qa[g])] != s) continue;
+      const bool two = kinds[g] == 5 || kinds[g] == 6;
+      put(kinds[g], qa[g] - first, two ? qb[g] - first : -1, params ? params + 3 * g : nullptr, -1);
+    }
+    first += sizes[s];
+    prep.segs.push_back(std::move(sp));
+  }
+  return prep;
+}
+
+std::string cut_prep_to_json(const CutPrep& prep) {
+  std::ostringstream o;
+  o.precision(17);
+  o << "{\"n\":" << prep.n << ",\"cuts\":[";
+  for (size_t c = 0; c < prep.cut_pos.size(); ++c)
+    o << (c ? "," : "") << "[" << prep.cut_pos[c] << "," << prep.cut_boundary[c] << "," << prep.cut_ctrl[c] << ","
+      << prep.cut_tgt[c] << "]";
+  o << "],\"segments\":[";
+  for (size_t s = 0; s < prep.segs.size(); ++s) {
+    const SegmentPlan& sp = prep.segs[s];
+    o << (s ? "," : "") << "{\"nq\":" << sp.nq << ",\"first\":" << sp.first << ",\"cut_ids\":[";
+    for (size_t i = 0; i < sp.cut_ids.size(); ++i) o << (i ? "," : "") << sp.cut_ids[i];
+    o << "],\"kinds\":[";
+    for (size_t i = 0; i < sp.kinds.size(); ++i) o << (i ? "," : "") << int(sp.kinds[i]);
+    o << "],\"qa\":[";
+    for (size_t i = 0; i < sp.qa.size(); ++i) o << (i ? "," : "") << sp.qa[i];
+    o << "],\"qb\":[";
+    for (size_t i = 0; i < sp.qb.size(); ++i) o << (i ? "," : "") << sp.qb[i];
+    o << "],\"slots\":[";
+    for (size_t i = 0; i < sp.slots.size(); ++i) o << (i ? "," : "") << sp.slots[i];
+    o << "],\"params\":[";
+    for (size_t i = 0; i < sp.params.size(); ++i) o << (i ? "," : "") << sp.params[i];
+    o << "]}";
+  }
+  o << "]}";
+  return o.str();
+}
+
+// ---------------------------------------------------------------------------
 // chain contraction plan
 // ---------------------------------------------------------------------------
 bool plan_chain(int n, const int32_t* seg_nq, const int32_t* seg_ncuts, const int32_t* seg_cut_ids,

@@ -78,6 +78,32 @@ struct ChainPlan {
   std::vector<MergeStep> steps;
 };
 
+// ---- cut preprocess (reference cutting.py:82-136, 190-248) -----------------
+struct SegmentPlan {
+  int nq = 0;
+  int first = 0;
+  std::vector<uint8_t> kinds;
+  std::vector<int64_t> qa, qb;
+  std::vector<double> params;   // 3 per gate
+  std::vector<int32_t> slots;   // cut bit patching the gate, or -1
+  std::vector<int32_t> cut_ids; // adjacent cuts in circuit order (local variant bit = index)
+};
+
+struct CutPrep {
+  int n = 0;
+  std::vector<int32_t> sizes;
+  std::vector<int64_t> cut_pos;
+  std::vector<int32_t> cut_boundary, cut_ctrl, cut_tgt;
+  std::vector<SegmentPlan> segs;
+  int c_total() const { return int(cut_pos.size()); }
+};
+
+// Throws PlanError: CS_ERR_INVALID (bad sizes / table), CS_ERR_TOPOLOGY
+// (a two-qubit gate spans non-adjacent segments).
+CutPrep cut_prepare(int nq, const uint8_t* kinds, const int64_t* qa, const int64_t* qb, const double* params,
+                    int64_t n_gates, int n_seg, const int32_t* sizes);
+std::string cut_prep_to_json(const CutPrep& prep);
+
 bool plan_chain(int n, const int32_t* seg_nq, const int32_t* seg_ncuts, const int32_t* seg_cut_ids,
                 int c_total, const int32_t* cut_boundary, const double* term_coef, int force_bond,
                 ChainPlan* out, PlanError* err);

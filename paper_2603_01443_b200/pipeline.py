@@ -11,6 +11,7 @@ kernel writing the state (or this GPU's shard of it) once.
 """
 from __future__ import annotations
 
+import ctypes
 import time
 from dataclasses import dataclass
 
@@ -91,34 +92,78 @@ def _side_stream(j: int):
     return _SIDE_STREAMS[key]
 
 
+_WORKSPACE: dict = {}
+
+
+def cut_workspace_tensor(nbytes: int):
+    """The per-device workspace of cs_cut_run (grown on demand, reused)."""
+    t = _device.torch()
+    dev = t.cuda.current_device()
+    ws = _WORKSPACE.get(dev)
+    if ws is None or ws.numel() < nbytes:
+        ws = t.empty(max(nbytes, 1), dtype=t.uint8, device="cuda")
+        _WORKSPACE[dev] = ws
+    return ws
+
+
 def run_cut(circuit: Circuit, n: int, *, dtype=np.complex128, max_qubits: int = DEFAULT_MAX_QUBITS,
-            out=None, out_range=None, timers: StageTimes | None = None, workspace=None):
-    """Cut-simulate ``circuit`` into n equal segments; return the merged state
-    (a device StateVec, or a ShardedState when ``out_range`` selects a shard)."""
+            out=None, out_range=None, timers: StageTimes | None = None, workspace=None, sizes=None,
+            force_bond: int = -1, events=None):
+    """Cut-simulate ``circuit`` into n equal segments (or ``sizes``) and return
+    the merged state (a device StateVec, or a ShardedState when ``out_range``
+    selects a shard). One native call (cs_cut_run): C++ preprocess, batched
+    variant sweeps on side streams, chain merge written once into ``out``.
+    ``timers`` synchronises and fills pre/sub/merge; ``events`` (three
+    torch.cuda.Event with timing) are recorded around the two device stages
+    without synchronising. Reference: harness.py:125-145 (cut leg)."""
+    from . import _native
+    from .errors import CapacityError, ValidationError
+
     q = circuit.num_qubits
     check_capacity(q, max_qubits)
+    if sizes is None:
+        if n < 2:
+            raise ValidationError(f"segment count must be >= 2, got {n}")
+        if q % n:
+            raise ValidationError(f"q must be divisible by n: q={q}, n={n}")
+        sizes = (q // n,) * n
     t = _device.require_cuda()
-    stream = t.cuda.current_stream()
+    code = _device.code_of(dtype)
+    ws_bytes, qlow, _c = _native.cut_workspace(q, circuit.table, sizes, force_bond, code)
+    if workspace is None:
+        workspace = cut_workspace_tensor(ws_bytes)
+    begin, end = (0, 1 << q) if out_range is None else tuple(out_range)
+    if not (0 <= begin <= end <= (1 << q)):
+        raise ValidationError(f"output range [{begin}, {end}) outside [0, 2^{q})")
+    if out is None:
+        nbytes = (end - begin) * np.dtype(dtype).itemsize
+        if nbytes >= (1 << 30):
+            free, _ = t.cuda.mem_get_info()
+            slack = t.cuda.memory_reserved() - t.cuda.memory_allocated()
+            if nbytes > free + slack:
+                raise CapacityError(f"state needs {nbytes / 2**30:.2f} GiB; device has "
+                                    f"{(free + slack) / 2**30:.2f} GiB free")
+        out = _device.empty_shape((end - begin,), dtype)
+    k, qa, qb, prm = _native._table_args(circuit.table)
+    sz = _native.c_i32(sizes)
+    stage = np.zeros(3) if timers is not None else None
+    evp = None
+    if events is not None:
+        for ev in events:
+            ev.record()  # materialise the underlying cudaEvent_t
+        evp = (ctypes.c_void_p * 3)(*(ev.cuda_event for ev in events))
+    _native.check(
+        _native.load().cs_cut_run(q, _native.ptr(k), _native.ptr(qa), _native.ptr(qb), _native.ptr(prm), len(k),
+                                  len(sz), _native.ptr(sz), force_bond, begin, end, out.data_ptr(),
+                                  workspace.data_ptr(), workspace.numel(), code, _device.stream_ptr(),
+                                  evp, _native.ptr(stage)),
+        "cs_cut_run",
+    )
     if timers is not None:
-        t0 = time.perf_counter()
-    prep = preprocess(circuit, n)
-    if timers is not None:
-        timers.pre = time.perf_counter() - t0
-        ev = [t.cuda.Event(enable_timing=True) for _ in range(3)]
-        ev[0].record(stream)
-    batches = simulate_segments(prep, dtype=dtype, max_qubits=max_qubits)
-    if timers is not None:
-        ev[1].record(stream)
-    res = merge_chain_device(prep.chain, batches, dtype=dtype, out=out, out_range=out_range,
-                             workspace=workspace)
-    if timers is not None:
-        ev[2].record(stream)
-        ev[2].synchronize()
-        timers.sub = ev[0].elapsed_time(ev[1]) / 1e3
-        timers.merge = ev[1].elapsed_time(ev[2]) / 1e3
-    if out_range is not None and tuple(out_range) != (0, 1 << q):
-        return ShardedState(q, out_range[0], out_range[1], res)
-    return StateVec(q, device=res)
+        timers.pre, timers.sub, timers.merge = (float(v) / 1e3 for v in stage)
+    if (begin, end) != (0, 1 << q):
+        return ShardedState(q, begin, end, out)
+    return StateVec(q, device=out)
 
 
 def cut_simulate(circuit: Circuit, n: int, **kw) -> StateVec:

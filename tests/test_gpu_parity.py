@@ -385,3 +385,52 @@ def test_sharded_pipeline_over_nccl_world1(cb):
         assert np.abs(res.cpu().numpy() - cb.run_cut(circ, 3).amps).max() < 1e-14
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("q,d,sizes,c,seed", [(12, 4, (6, 6), 1, 0), (15, 5, (5, 5, 5), 4, 1),
+                                               (16, 5, (4, 4, 4, 4), 4, 3), (14, 6, (7, 7), 3, 4)])
+def test_one_call_pipeline_equals_stepwise(cb, q, d, sizes, c, seed):
+    """cs_cut_run (C++ preprocess + batched sweeps + chain merge in one call)
+    is bit-identical to the step-by-step Python path and within TOL of the oracle."""
+    from paper_2603_01443_b200.merging import merge_chain_device
+    from paper_2603_01443_b200.pipeline import preprocess, simulate_segments
+
+    n = len(sizes)
+    circ = cb.build_brickwall(cb.BrickwallSpec(q, d, n, c, seed))
+    one = cb.run_cut(circ, n).amps
+    prep = preprocess(circ, n)
+    step = merge_chain_device(prep.chain, simulate_segments(prep)).cpu().numpy()
+    assert np.array_equal(one, step)
+    ref = orc.simulate(q, circ.kinds, circ.qa, circ.qb, circ.params)
+    assert np.abs(one - ref).max() < TOL
+
+
+def test_one_call_pipeline_unequal_sizes_bonds_events(cb):
+    import torch
+
+    from paper_2603_01443_b200.errors import UnsupportedTopologyError, ValidationError
+
+    circ = cb.build_staircase(cb.BenchmarkSpec(q=12, n=3, blocks=3))
+    ref = orc.simulate(12, circ.kinds, circ.qa, circ.qb, circ.params)
+    for sizes in [(3, 4, 5), (6, 6), (2, 5, 5)]:
+        got = cb.run_cut(circ, len(sizes), sizes=sizes).amps
+        assert np.abs(got - ref).max() < TOL
+    circ = cb.build_brickwall(cb.BrickwallSpec(16, 5, 4, 4, 7))
+    ref = orc.simulate(16, circ.kinds, circ.qa, circ.qb, circ.params)
+    for k in range(3):
+        assert np.abs(cb.run_cut(circ, 4, force_bond=k).amps - ref).max() < TOL
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    times = cb.StageTimes()
+    got = cb.run_cut(circ, 4, events=evs, timers=times).amps
+    assert np.abs(got - ref).max() < TOL
+    assert evs[0].elapsed_time(evs[1]) > 0 and evs[1].elapsed_time(evs[2]) > 0
+    assert times.pre > 0 and times.sub > 0 and times.merge > 0
+    with pytest.raises(ValidationError):
+        cb.run_cut(circ, 3)
+    with pytest.raises(UnsupportedTopologyError):
+        from paper_2603_01443_b200 import circuits as C
+
+        cb.run_cut(C.Circuit(3, [C.h(0), C.cx(0, 2)]), 3)
+    with pytest.raises(ValidationError):
+        cb.run_cut(circ, 4, workspace=torch.empty(16, dtype=torch.uint8, device="cuda"),
+                   out=torch.empty(1 << 16, dtype=torch.complex128, device="cuda"))

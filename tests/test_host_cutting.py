@@ -147,3 +147,48 @@ def test_staircase_and_padded_generators_match_oracle():
     c = C.build_depth_padded(C.BenchmarkSpec(q=6, n=2, blocks=1, depth_pad_exponent=2))
     assert c.gate_count == C.build_staircase(C.BenchmarkSpec(q=6, n=2, blocks=1)).gate_count + 200
     assert C.compute_depth(C.Circuit(2, [C.h(0), C.cx(0, 1), C.h(1)])) == 3
+
+
+@pytest.mark.parametrize("key", golden_cases())
+def test_native_preprocess_matches_python_and_reference(golden, key):
+    """cs_cut_run's C++ preprocess == the Python planner (pinned to the reference)."""
+    import os
+
+    from paper_2603_01443_b200 import _native
+
+    if not os.path.exists(_native.LIB_PATH):
+        pytest.skip("libcutsim.so not built")
+    circ = _circuit(golden, key)
+    n = int(golden[f"{key}/n"])
+    q = circ.num_qubits
+    d = _native.cut_describe(q, circ.table, [q // n] * n)
+    plan = K.plan_cut(circ, n)
+    subs = K.decompose(circ, plan)
+    assert [c[0] for c in d["cuts"]] == list(golden[f"{key}/positions"])
+    assert [c[1] for c in d["cuts"]] == list(golden[f"{key}/boundaries"])
+    for fam, seg in zip(subs.segments, d["segments"]):
+        assert np.array_equal(np.array(seg["kinds"], np.uint8), fam.template.kinds)
+        assert np.array_equal(np.array(seg["qa"]), fam.template.qa)
+        assert np.array_equal(np.array(seg["qb"]), fam.template.qb)
+        assert np.array_equal(np.array(seg["slots"]), fam.slots)
+        assert tuple(seg["cut_ids"]) == fam.cut_ids
+
+
+@pytest.mark.parametrize("name", list(G.BASELINE_CONFIGS))
+def test_native_preprocess_full_size_u3(name):
+    import os
+
+    from paper_2603_01443_b200 import _native
+
+    if not os.path.exists(_native.LIB_PATH):
+        pytest.skip("libcutsim.so not built")
+    spec = G.BASELINE_CONFIGS[name]
+    circ = G.build_brickwall(spec)
+    d = _native.cut_describe(spec.q, circ.table, [spec.q // spec.n] * spec.n)
+    subs = K.decompose(circ, K.plan_cut(circ, spec.n))
+    for fam, seg in zip(subs.segments, d["segments"]):
+        assert np.array_equal(np.array(seg["kinds"], np.uint8), fam.template.kinds)
+        assert np.array_equal(np.array(seg["params"]).reshape(-1, 3), fam.template.params)
+        assert np.array_equal(np.array(seg["slots"]), fam.slots)
+    with pytest.raises(UnsupportedTopologyError):
+        _native.cut_describe(3, C.Circuit(3, [C.h(0), C.cx(0, 2)]).table, [1, 1, 1])
