@@ -9,8 +9,8 @@ simulate, delta = (t_cut - t_orig) / t_orig; R repetitions, mean and sample
 std, budgets recorded as "timeout-*" status data.
 
 On the GPU every stage boundary synchronises the device, so each stage time
-is the wall time of its work (kernels included). Sweeps, fits and reports of
-the reference harness are out of scope.
+is the wall time of its work (kernels included). The sweep drivers, the
+boundary fit and the reports built on `measure` live in `sweeps.py`.
 """
 from __future__ import annotations
 
