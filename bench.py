@@ -360,9 +360,24 @@ def run_ours(args):
         torch.cuda.synchronize()
         t_e2e = (time.perf_counter() - t0) / e_steps
         g_bytes = int(sum(a.nbytes for a in (circ.kinds, circ.qa, circ.qb, circ.params)))
+        # the bound of this leg: a plain pinned device->host copy of the same bytes
+        chunk = bufs[0]
+        c0 = torch.cuda.Event(enable_timing=True)
+        c1 = torch.cuda.Event(enable_timing=True)
+        host_view = host[: chunk.numel()]
+        host_view.copy_(chunk, non_blocking=True)
+        c0.record(stream)
+        for _ in range(4):
+            host_view.copy_(chunk, non_blocking=True)
+        c1.record(stream)
+        c1.synchronize()
+        d2h_gbs = 4 * chunk.numel() * 16 / (c0.elapsed_time(c1) / 1e3) / 1e9
         e2e = {"value": total / t_e2e, "unit": UNIT, "h2d_bytes_per_step": g_bytes,
                "d2h_bytes_per_step": total * 16, "ms_per_step": t_e2e * 1e3, "steps": e_steps,
-               "path": "run_cut_to_host: chunked merge overlapped with D2H into pinned host memory"}
+               "path": "run_cut_to_host: chunked merge overlapped with D2H into pinned host memory",
+               "bound": {"kind": "pcie_d2h", "measured_copy_gbs": d2h_gbs,
+                         "achieved_gbs": total * 16 / t_e2e / 1e9,
+                         "frac": total * 16 / t_e2e / 1e9 / d2h_gbs}}
         del host, bufs
 
     # CPU baseline (the oracle port, 1 thread = the reference's protocol), rank 0, N=1
