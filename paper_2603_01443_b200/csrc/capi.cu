@@ -30,6 +30,10 @@ int merge_cols_per_thread(int K);
 cudaError_t launch_merge_dmma(const MergeParams& p, int K, dim3 grid, int threads, size_t smem,
                               cudaStream_t stream);
 int merge_dmma_cols_per_warp(int K);
+cudaError_t launch_merge_dmma3(const MergeParams& p, int K, dim3 grid, int threads, size_t smem,
+                               cudaStream_t stream);
+int merge_dmma3_cols_per_warp(int K);
+int merge_dmma3_row_blocks(int K);
 cudaError_t launch_init_basis(void* states, int64_t len, int64_t n_states, int64_t index, int dtype,
                               cudaStream_t stream);
 cudaError_t launch_reduce(const void* a, const void* b, int64_t n, int mode, int dtype, double2* scratch,
@@ -56,7 +60,7 @@ struct Options {
   int64_t merge_streaming = 1;
   int64_t merge_iters = 0;
   int64_t vb = 0;  // states per CTA in a variant batch (0 = auto)
-  int64_t merge_dmma = 1;  // FP64 tensor-core merge for K = 8, 16 (complex128)
+  int64_t merge_dmma = 2;  // FP64 tensor-core merge: 2 = three-GEMM (3M) for K <= 32, four-GEMM K = 64
   int64_t engine = 1;      // 1: register-tile kernel (rsweep), 0: shared-memory tile kernel (sweep)
   int64_t jit = 0;         // 0 never, 1 from a program's 2nd use, 2 always: NVRTC-specialised sweeps (opt-in: compile ~1-7 s)
   int64_t jit_max_cost = 40000;  // FP64 instructions per specialised launch (code-size guard)
@@ -240,6 +244,13 @@ bool dmma_eligible(int K, int dtype, int64_t lo_len) {
          lo_len >= merge_dmma_cols_per_warp(K);
 }
 
+// merge_dmma = 2: the three-GEMM (3M) tensor-core kernel where it is
+// instantiated (K = 8, 16, 32); K = 64 keeps the four-GEMM kernel
+bool dmma3_eligible(int K, int dtype, int64_t lo_len) {
+  return g_opt.merge_dmma == 2 && dtype == CS_C128 && (K == 8 || K == 16 || K == 32) &&
+         lo_len >= merge_dmma3_cols_per_warp(K);
+}
+
 // Launch one merge_terms problem whose K is one instantiated width.
 int merge_launch_one(int S, int Kc, const int32_t* hidx, const int32_t* lidx, const double* coef,
                      int64_t stride_terms, const void* hi, int64_t hi_len, const void* lo, int64_t lo_len,
@@ -248,15 +259,17 @@ int merge_launch_one(int S, int Kc, const int32_t* hidx, const int32_t* lidx, co
   // stride_terms: distance between consecutive slots' term lists in hidx/lidx
   const int threads = 256;
   const size_t eb0 = elem_bytes(dtype);
-  if (dmma_eligible(Kc, dtype, lo_len)) {
+  const bool m3 = dmma3_eligible(Kc, dtype, lo_len);
+  if (m3 || dmma_eligible(Kc, dtype, lo_len)) {
     // tensor-core path: 8 warps over ncg column groups of (16, 8 or 4)
     // complex columns; a CTA spans >= 128 columns so row staging is amortised
-    const int64_t cw = merge_dmma_cols_per_warp(Kc);
+    const int64_t cw = m3 ? merge_dmma3_cols_per_warp(Kc) : merge_dmma_cols_per_warp(Kc);
     const int64_t ncg = std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(8, 256 / cw), lo_len / cw));
     const int64_t C = cw * ncg;
     const int64_t nrows = row_end - row_begin;
-    const int RS = 2 * Kc + 4;
-    const int64_t rbg = 8 / (merge_dmma_cols_per_warp(Kc) / 4);  // row blocks processed together
+    const int RS = m3 ? 3 * Kc + 4 : 2 * Kc + 4;
+    // row blocks processed together
+    const int64_t rbg = m3 ? merge_dmma3_row_blocks(Kc) : 8 / (merge_dmma_cols_per_warp(Kc) / 4);
     int64_t iters = std::max<int64_t>(1, std::min<int64_t>((96 * 1024) / (8 * RS * 8), (nrows + 7) / 8));
     iters = std::min<int64_t>(iters, 64);
     // keep at least two CTAs per SM for small products
@@ -299,7 +312,8 @@ int merge_launch_one(int S, int Kc, const int32_t* hidx, const int32_t* lidx, co
         char* base_out = static_cast<char*>(out) + size_t(s0) * size_t(out_slot_stride) * eb0;
         pd.out = base_out + size_t(r0 - row_begin) * size_t(lo_len) * eb0;
         dim3 grid(unsigned(lo_len / C), unsigned((r1 - r0 + rows_cta - 1) / rows_cta), unsigned(sc));
-        cudaError_t e = launch_merge_dmma(pd, Kc, grid, threads, smem, stream);
+        cudaError_t e = m3 ? launch_merge_dmma3(pd, Kc, grid, threads, smem, stream)
+                           : launch_merge_dmma(pd, Kc, grid, threads, smem, stream);
         g_launches.fetch_add(1);
         if (e != cudaSuccess) return cuda_fail(e, "merge_dmma_kernel launch");
       }
@@ -677,7 +691,8 @@ int cs_set_option(const char* key, int64_t value) {
     if (value < 2 || value > 4) return fail(CS_ERR_INVALID, "sweep_minb must be 2, 3 or 4");
     g_sweep_minb = int(value);
   } else if (k == "merge_dmma") {
-    g_opt.merge_dmma = value ? 1 : 0;
+    if (value < 0 || value > 2) return fail(CS_ERR_INVALID, "merge_dmma must be 0, 1 or 2");
+    g_opt.merge_dmma = value;
   } else if (k == "jit") {
     if (value < 0 || value > 2) return fail(CS_ERR_INVALID, "jit must be 0, 1 or 2");
     g_opt.jit = value;

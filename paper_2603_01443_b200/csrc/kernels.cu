@@ -792,6 +792,159 @@ __global__ void __launch_bounds__(256, 2) merge_dmma_kernel(const __grid_constan
   }
 }
 
+// ---------------------------------------------------------------------------
+// merge_dmma3_kernel: the complex product with three real GEMMs instead of
+// four (Gauss / "3M"): with B_t = coef_t * hi_t[h] = (br, bi) and
+// A_t = lo_t[l] = (ar, ai),
+//   P1 = sum_t (br + bi) ar,  P2 = sum_t br (ai - ar),  P3 = sum_t bi (ar + ai)
+//   re = P1 - P3,  im = P1 + P2
+// so a complex output costs 3K real FMA on the FP64 tensor path instead of 4K
+// (the merge is FP64-bound for K >= 16). Each m8n8k4 tile is 8 rows x 8
+// complex columns of one of P1..P3; a lane's accumulator pair covers complex
+// columns acol and acol + 4 of the tile (whole-sector stores). The three A
+// operands per term are staged in shared memory ((br+bi) | br | bi row
+// segments, stride 3K+4 doubles: two wavefronts per fragment load), the
+// three B operands per column stay in registers for all of the CTA's rows.
+// Rounding: |error| <= ~K eps (|br|+|bi|)(|ar|+|ai|) per output, far inside
+// the 1e-10 parity bound.
+// ---------------------------------------------------------------------------
+template <int KT, int NT, int RB>
+__global__ void __launch_bounds__(256, 2) merge_dmma3_kernel(const __grid_constant__ MergeParams p) {
+  constexpr int KS = KT / 4;       // mma k-steps per GEMM
+  constexpr int RS = 3 * KT + 4;   // smem row stride (doubles)
+  constexpr int COLS_W = 8 * NT;   // complex columns per warp
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* bsd = reinterpret_cast<double*>(smem_raw);
+  const int sl = blockIdx.z;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  const int nwarps = blockDim.x >> 5;
+  const int64_t W = p.lo_len;
+  const int rows_cta = p.iters * 8;
+  const int64_t row0 = p.row_begin + int64_t(blockIdx.y) * rows_cta;
+  const int32_t* hidx = p.hidx + sl * KT;
+  const int32_t* lidx = p.lidx + sl * KT;
+  const double* coef = p.coef + 2 * sl * KT;
+  const double2* hi = reinterpret_cast<const double2*>(p.hi);
+  const double2* lo = reinterpret_cast<const double2*>(p.lo);
+
+  for (int idx = tid; idx < rows_cta * KT; idx += blockDim.x) {
+    const int r = idx / KT;
+    const int t = idx - r * KT;
+    const int64_t h = row0 + r;
+    double br = 0.0, bi = 0.0;
+    if (h < p.row_end) {
+      const double2 hv = __ldg(hi + int64_t(hidx[t]) * p.hi_len + h);
+      const double cr = coef[2 * t], ci = coef[2 * t + 1];
+      br = hv.x * cr - hv.y * ci;
+      bi = hv.x * ci + hv.y * cr;
+    }
+    double* row = bsd + r * RS;
+    row[t] = br + bi;
+    row[KT + t] = br;
+    row[2 * KT + t] = bi;
+  }
+  __syncthreads();
+
+  double2* out = reinterpret_cast<double2*>(p.out) + int64_t(sl) * p.out_slot_stride;
+  const int arow = lane >> 2;
+  const int acol = lane & 3;
+  const int ncg = p.cols;
+  for (int cg = warp; cg < ncg; cg += nwarps) {
+    const int64_t col_w = (int64_t(blockIdx.x) * ncg + cg) * COLS_W;
+    // B fragments: lane holds X[t = 4s + (lane&3)][n = lane>>2], GEMM column n
+    // being complex column (n>>1) + 4(n&1) of the tile, so that a lane's two
+    // accumulator columns (n = 2 acol + c) are columns acol and acol + 4 and
+    // each store instruction writes 64 contiguous bytes per row (whole sectors)
+    double x0[NT][KS], x1[NT][KS], x2[NT][KS];
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      const int n = lane >> 2;
+      const int64_t l = col_w + 8 * j + (n >> 1) + 4 * (n & 1);
+#pragma unroll
+      for (int s = 0; s < KS; ++s) {
+        const double2 a = __ldg(lo + int64_t(lidx[4 * s + acol]) * W + l);
+        x0[j][s] = a.x;
+        x1[j][s] = a.y - a.x;
+        x2[j][s] = a.x + a.y;
+      }
+    }
+    for (int rb0 = 0; rb0 < p.iters; rb0 += RB) {
+      double acc[RB][NT][3][2];
+#pragma unroll
+      for (int r = 0; r < RB; ++r)
+#pragma unroll
+        for (int j = 0; j < NT; ++j)
+#pragma unroll
+          for (int g = 0; g < 3; ++g) acc[r][j][g][0] = acc[r][j][g][1] = 0.0;
+#pragma unroll
+      for (int s = 0; s < KS; ++s) {
+#pragma unroll
+        for (int r = 0; r < RB; ++r) {
+          const double* row = bsd + ((rb0 + r) * 8 + arow) * RS + 4 * s + acol;
+          const double a0 = row[0], a1 = row[KT], a2 = row[2 * KT];
+#pragma unroll
+          for (int j = 0; j < NT; ++j) {
+            dmma884(acc[r][j][0][0], acc[r][j][0][1], a0, x0[j][s]);
+            dmma884(acc[r][j][1][0], acc[r][j][1][1], a1, x1[j][s]);
+            dmma884(acc[r][j][2][0], acc[r][j][2][1], a2, x2[j][s]);
+          }
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < RB; ++r) {
+        const int64_t h = row0 + (rb0 + r) * 8 + arow;
+        if (rb0 + r >= p.iters || h >= p.row_end) continue;
+        double2* dst = out + (h - p.row_begin) * W + col_w + acol;
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            const double p1 = acc[r][j][0][c];
+            double2 v = make_double2(p1 - acc[r][j][2][c], p1 + acc[r][j][1][c]);
+            double2* d = dst + 8 * j + 4 * c;
+            if (p.accumulate) {
+              const double2 prev = *d;
+              v.x += prev.x;
+              v.y += prev.y;
+            }
+            if (p.streaming) __stcs(d, v);
+            else *d = v;
+          }
+        }
+      }
+    }
+  }
+}
+
+template <int KT, int NT, int RB>
+static cudaError_t launch_dmma3_kt(const MergeParams& p, dim3 grid, int threads, size_t smem, cudaStream_t stream) {
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(merge_dmma3_kernel<KT, NT, RB>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  merge_dmma3_kernel<KT, NT, RB><<<grid, threads, smem, stream>>>(p);
+  return cudaGetLastError();
+}
+
+// 3M kernel geometry per K: complex columns per warp and row blocks per pass
+int merge_dmma3_cols_per_warp(int K) { return K <= 16 ? 16 : 8; }
+int merge_dmma3_row_blocks(int K) { return K <= 16 ? 2 : 4; }
+
+cudaError_t launch_merge_dmma3(const MergeParams& p, int K, dim3 grid, int threads, size_t smem,
+                               cudaStream_t stream) {
+  switch (K) {
+    case 8: return launch_dmma3_kt<8, 2, 2>(p, grid, threads, smem, stream);
+    case 16: return launch_dmma3_kt<16, 2, 2>(p, grid, threads, smem, stream);
+    case 32: return launch_dmma3_kt<32, 1, 4>(p, grid, threads, smem, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 template <int KT, int NT>
 static cudaError_t launch_dmma_kt(const MergeParams& p, dim3 grid, int threads, size_t smem, cudaStream_t stream) {
   static size_t configured = 0;

@@ -40,7 +40,7 @@ CASES = [  # (K, S, H, W, rows)
 ]
 
 
-@pytest.mark.parametrize("dmma", [1, 0])
+@pytest.mark.parametrize("dmma", [2, 1, 0])
 @pytest.mark.parametrize("K,S,H,W,rows", CASES)
 def test_merge_terms_vs_numpy(dev, K, S, H, W, rows, dmma):
     torch, native = dev
