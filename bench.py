@@ -238,6 +238,12 @@ def run_ours(args):
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    comm = None
+    if world > 1:
+        # the pipeline's one exchange goes through libcutsim's NCCL binding
+        from paper_2603_01443_b200.comm import NcclComm
+
+        comm = NcclComm.create(rank, world)
     spec = BASELINE_CONFIGS[WORKLOAD]
     circ = cb.build_brickwall(spec)
     q = spec.q
@@ -272,7 +278,8 @@ def run_ours(args):
                 merge_ms.append((evs[1], evs[2]))
         else:
             timers = {} if record else None
-            res, _ = run_cut_sharded(circ, spec.n, rank=rank, world=world, out=out, merge_events=timers)
+            res, _ = run_cut_sharded(circ, spec.n, rank=rank, world=world, out=out, merge_events=timers,
+                                     comm=comm)
             if record:
                 merge_ms.append((timers["start"], timers["end"]))
             del res

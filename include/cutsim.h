@@ -56,7 +56,8 @@ int cs_device_count(int32_t* count);
  * product, 2 three (3M) for K <= 32; default 2), "engine" (1 register-tile
  * sweep kernel, 0 shared-memory tile kernel), "jit" (0 never, 1 from a
  * program's second use, 2 always: NVRTC-specialised sweep kernels),
- * "jit_max_cost", "vb", "sweep_minb", "plan_json" (tuning / testing). */
+ * "jit_max_cost", "vb", "sweep_minb", "merge_smem_kb", "plan_json" (tuning /
+ * testing). */
 int cs_set_option(const char* key, int64_t value);
 int64_t cs_get_option(const char* key);
 
@@ -169,6 +170,22 @@ int cs_inner(const void* a, const void* b, int64_t n, int32_t dtype, double* res
 /* out[i] = state[idx[i]] (idx, out: device pointers). */
 int cs_gather(const void* state, const int64_t* idx, int64_t m, void* out, int32_t dtype,
               void* stream);
+
+/* Multi-GPU plumbing over NCCL (NVLink / NVSwitch), one process per GPU
+ * (SURVEY.md §8(b) item 6, §8(e)). The reference is single-process, so these
+ * replace no reference symbol; they carry the sharded pipeline's single
+ * exchange (parallel.gather_states) and the distributed simulator's
+ * half-shard swaps (distributed.simulate_distributed). libnccl.so.2 is
+ * dlopen'ed on first use (or from `path` via cs_nccl_load). */
+int cs_nccl_load(const char* path);
+/* rank 0 creates the 128-byte id; the caller distributes it to all ranks */
+int cs_nccl_unique_id(uint8_t* id128);
+int cs_nccl_comm_init(int32_t world, int32_t rank, const uint8_t* id128, int32_t device, void** comm);
+int cs_nccl_comm_destroy(void* comm);
+/* recv[r * bytes_per_rank ...] = rank r's send buffer, for every rank r */
+int cs_allgather_states(void* comm, const void* send, int64_t bytes_per_rank, void* recv, void* stream);
+/* exchange `bytes` with `peer` (grouped ncclSend + ncclRecv) */
+int cs_sendrecv(void* comm, const void* send, void* recv, int64_t bytes, int32_t peer, void* stream);
 
 #ifdef __cplusplus
 }

@@ -67,6 +67,12 @@ SIGNATURES = {
     "cs_maxabs": (ctypes.c_int, [_vp, _i64, _i32, _vp, _vp]),
     "cs_inner": (ctypes.c_int, [_vp, _vp, _i64, _i32, _vp, _vp]),
     "cs_gather": (ctypes.c_int, [_vp, _vp, _i64, _vp, _i32, _vp]),
+    "cs_nccl_load": (ctypes.c_int, [ctypes.c_char_p]),
+    "cs_nccl_unique_id": (ctypes.c_int, [_vp]),
+    "cs_nccl_comm_init": (ctypes.c_int, [_i32, _i32, _vp, _i32, _vp]),
+    "cs_nccl_comm_destroy": (ctypes.c_int, [_vp]),
+    "cs_allgather_states": (ctypes.c_int, [_vp, _vp, _i64, _vp, _vp]),
+    "cs_sendrecv": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i32, _vp]),
 }
 
 _lock = threading.Lock()

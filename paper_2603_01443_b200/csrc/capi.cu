@@ -60,6 +60,7 @@ struct Options {
   int64_t merge_streaming = 1;
   int64_t merge_iters = 0;
   int64_t vb = 0;  // states per CTA in a variant batch (0 = auto)
+  int64_t merge_smem_kb = 96;  // staged-row budget per CTA of the tensor-core merge
   int64_t merge_dmma = 2;  // FP64 tensor-core merge: 2 = three-GEMM (3M) for K <= 32, four-GEMM K = 64
   int64_t engine = 1;      // 1: register-tile kernel (rsweep), 0: shared-memory tile kernel (sweep)
   int64_t jit = 0;         // 0 never, 1 from a program's 2nd use, 2 always: NVRTC-specialised sweeps (opt-in: compile ~1-7 s)
@@ -270,7 +271,8 @@ int merge_launch_one(int S, int Kc, const int32_t* hidx, const int32_t* lidx, co
     const int RS = m3 ? 3 * Kc + 4 : 2 * Kc + 4;
     // row blocks processed together
     const int64_t rbg = m3 ? merge_dmma3_row_blocks(Kc) : 8 / (merge_dmma_cols_per_warp(Kc) / 4);
-    int64_t iters = std::max<int64_t>(1, std::min<int64_t>((96 * 1024) / (8 * RS * 8), (nrows + 7) / 8));
+    int64_t iters = std::max<int64_t>(1, std::min<int64_t>((g_opt.merge_smem_kb * 1024) / (8 * RS * 8),
+                                                           (nrows + 7) / 8));
     iters = std::min<int64_t>(iters, 64);
     // keep at least two CTAs per SM for small products
     const int64_t col_blocks = std::max<int64_t>(1, lo_len / C);
@@ -650,6 +652,11 @@ cudaStream_t side_stream(int i) {
 
 }  // namespace
 
+// error hook for the library's other translation units (comm.cpp)
+namespace cutsim {
+int set_error(int code, const std::string& msg) { return fail(code, msg); }
+}  // namespace cutsim
+
 extern "C" {
 
 int cs_version(void) { return 10000; }
@@ -690,6 +697,9 @@ int cs_set_option(const char* key, int64_t value) {
   } else if (k == "sweep_minb") {
     if (value < 2 || value > 4) return fail(CS_ERR_INVALID, "sweep_minb must be 2, 3 or 4");
     g_sweep_minb = int(value);
+  } else if (k == "merge_smem_kb") {
+    if (value < 8 || value > 112) return fail(CS_ERR_INVALID, "merge_smem_kb must be in [8, 112]");
+    g_opt.merge_smem_kb = value;
   } else if (k == "merge_dmma") {
     if (value < 0 || value > 2) return fail(CS_ERR_INVALID, "merge_dmma must be 0, 1 or 2");
     g_opt.merge_dmma = value;
@@ -726,6 +736,7 @@ int64_t cs_get_option(const char* key) {
   if (k == "jit") return g_opt.jit;
   if (k == "jit_max_cost") return g_opt.jit_max_cost;
   if (k == "merge_dmma") return g_opt.merge_dmma;
+  if (k == "merge_smem_kb") return g_opt.merge_smem_kb;
   if (k == "plan_json") return g_opt.plan_json;
   if (k == "sweep_minb") return g_sweep_minb;
   return -1;

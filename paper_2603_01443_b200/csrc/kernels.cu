@@ -711,19 +711,28 @@ __global__ void __launch_bounds__(256, 2) merge_dmma_kernel(const __grid_constan
   const double2* hi = reinterpret_cast<const double2*>(p.hi);
   const double2* lo = reinterpret_cast<const double2*>(p.lo);
 
-  for (int idx = tid; idx < rows_cta * KT; idx += blockDim.x) {
-    const int r = idx / KT;
-    const int t = idx - r * KT;
-    const int64_t h = row0 + r;
-    double2 b = make_double2(0.0, 0.0);
-    if (h < p.row_end) {
-      const double2 hv = __ldg(hi + int64_t(hidx[t]) * p.hi_len + h);
-      const double cr = coef[2 * t], ci = coef[2 * t + 1];
-      b.x = hv.x * cr - hv.y * ci;
-      b.y = hv.x * ci + hv.y * cr;
+  constexpr int SU = 8;  // staging loads in flight per thread
+  const int nst = rows_cta * KT;
+  for (int base = tid; base < nst; base += SU * int(blockDim.x)) {
+    double2 hv[SU];
+#pragma unroll
+    for (int u = 0; u < SU; ++u) {
+      const int idx = base + u * int(blockDim.x);
+      const int r = idx / KT;
+      const int64_t h = row0 + r;
+      hv[u] = make_double2(0.0, 0.0);
+      if (idx < nst && h < p.row_end) hv[u] = __ldg(hi + int64_t(hidx[idx - r * KT]) * p.hi_len + h);
     }
-    bsd[r * RS + 2 * t] = b.x;
-    bsd[r * RS + 2 * t + 1] = b.y;
+#pragma unroll
+    for (int u = 0; u < SU; ++u) {
+      const int idx = base + u * int(blockDim.x);
+      if (idx >= nst) break;
+      const int r = idx / KT;
+      const int t = idx - r * KT;
+      const double cr = coef[2 * t], ci = coef[2 * t + 1];
+      bsd[r * RS + 2 * t] = hv[u].x * cr - hv[u].y * ci;
+      bsd[r * RS + 2 * t + 1] = hv[u].x * ci + hv[u].y * cr;
+    }
   }
 
   __syncthreads();
@@ -829,21 +838,33 @@ __global__ void __launch_bounds__(256, 2) merge_dmma3_kernel(const __grid_consta
   const double2* hi = reinterpret_cast<const double2*>(p.hi);
   const double2* lo = reinterpret_cast<const double2*>(p.lo);
 
-  for (int idx = tid; idx < rows_cta * KT; idx += blockDim.x) {
-    const int r = idx / KT;
-    const int t = idx - r * KT;
-    const int64_t h = row0 + r;
-    double br = 0.0, bi = 0.0;
-    if (h < p.row_end) {
-      const double2 hv = __ldg(hi + int64_t(hidx[t]) * p.hi_len + h);
-      const double cr = coef[2 * t], ci = coef[2 * t + 1];
-      br = hv.x * cr - hv.y * ci;
-      bi = hv.x * ci + hv.y * cr;
+  // staging: SU independent loads in flight per thread before any use
+  constexpr int SU = 8;
+  const int nst = rows_cta * KT;
+  for (int base = tid; base < nst; base += SU * int(blockDim.x)) {
+    double2 hv[SU];
+#pragma unroll
+    for (int u = 0; u < SU; ++u) {
+      const int idx = base + u * int(blockDim.x);
+      const int r = idx / KT;
+      const int64_t h = row0 + r;
+      hv[u] = make_double2(0.0, 0.0);
+      if (idx < nst && h < p.row_end) hv[u] = __ldg(hi + int64_t(hidx[idx - r * KT]) * p.hi_len + h);
     }
-    double* row = bsd + r * RS;
-    row[t] = br + bi;
-    row[KT + t] = br;
-    row[2 * KT + t] = bi;
+#pragma unroll
+    for (int u = 0; u < SU; ++u) {
+      const int idx = base + u * int(blockDim.x);
+      if (idx >= nst) break;
+      const int r = idx / KT;
+      const int t = idx - r * KT;
+      const double cr = coef[2 * t], ci = coef[2 * t + 1];
+      const double br = hv[u].x * cr - hv[u].y * ci;
+      const double bi = hv[u].x * ci + hv[u].y * cr;
+      double* row = bsd + r * RS;
+      row[t] = br + bi;
+      row[KT + t] = br;
+      row[2 * KT + t] = bi;
+    }
   }
   __syncthreads();
 

@@ -180,8 +180,10 @@ def local_table(seg: Segment, rank: int, nloc: int) -> GateTable:
 
 
 def simulate_distributed(circuit: Circuit, *, rank: int, world: int, group=None, dtype=np.complex128,
-                         run_local=None, exchange=None, init=None):
-    """This rank's shard of the uncut state (device tensor by default)."""
+                         run_local=None, exchange=None, init=None, comm=None):
+    """This rank's shard of the uncut state (device tensor by default). The
+    half-shard swaps go through `comm` (comm.NcclComm: libcutsim's grouped
+    ncclSend/ncclRecv) when given, else torch.distributed P2P on `group`."""
     import torch
 
     steps, nloc = plan(circuit, world)
@@ -203,6 +205,8 @@ def simulate_distributed(circuit: Circuit, *, rank: int, world: int, group=None,
             run_table(sh.view(1, -1), nloc, table, dtype=dtype)
     else:
         shard = init(nloc) if init is not None else None
+    if exchange is None and comm is not None:
+        exchange = comm.sendrecv
     if exchange is None:
         import torch.distributed as dist
 

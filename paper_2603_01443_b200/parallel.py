@@ -79,7 +79,9 @@ def gather_states(local: dict, counts: list[int], lengths: list[int], world: int
         real = _as_real(t).reshape(sl.v1 - sl.v0, n * 2)
         for i in range(sl.v1 - sl.v0):
             mine[(flat_index0 + i) * max_len * 2:(flat_index0 + i) * max_len * 2 + n * 2] = real[i]
-    parts = [make_buffer(per * max_len * 2) for _ in range(world)]
+    # the receive buffers are consecutive views of one allocation (what a
+    # single all-gather writes; dist.all_gather takes them as a list)
+    parts = list(make_buffer(world * per * max_len * 2).split(per * max_len * 2))
     all_gather(parts, mine)
     full = make_buffer(int(offs[-1]) * 2)
     g = 0
@@ -110,12 +112,15 @@ def _as_complex(t):
 
 
 def run_cut_sharded(circuit, n: int, *, rank: int, world: int, dtype=np.complex128, out=None,
-                    group=None, simulate_slice=None, merge_shard=None, all_gather=None, merge_events=None):
+                    group=None, simulate_slice=None, merge_shard=None, all_gather=None, merge_events=None,
+                    comm=None):
     """Cut pipeline on `world` ranks; returns (ShardedState-like tensor, (begin, end)).
 
     simulate_slice(family, v0, v1) -> tensor [v1-v0, 2^q_i] and
     merge_shard(chain, batches, (begin, end)) -> tensor default to the sm_100a
-    kernels; the CPU tests inject oracle-backed versions."""
+    kernels; the CPU tests inject oracle-backed versions. `comm` (a
+    comm.NcclComm) routes the all-gather through libcutsim's NCCL binding;
+    otherwise torch.distributed's collective on `group` is used."""
     import torch
     import torch.distributed as dist
 
@@ -144,6 +149,8 @@ def run_cut_sharded(circuit, n: int, *, rank: int, world: int, dtype=np.complex1
     def make_buffer(nf):
         return torch.zeros(nf, dtype=torch.float64, device=device)
 
+    if all_gather is None and comm is not None:
+        all_gather = comm.gather_parts
     if all_gather is None:
         def all_gather(parts, mine):
             dist.all_gather(parts, mine, group=group)

@@ -434,3 +434,30 @@ def test_one_call_pipeline_unequal_sizes_bonds_events(cb):
     with pytest.raises(ValidationError):
         cb.run_cut(circ, 4, workspace=torch.empty(16, dtype=torch.uint8, device="cuda"),
                    out=torch.empty(1 << 16, dtype=torch.complex128, device="cuda"))
+
+
+def test_native_nccl_comm_world1(cb):
+    """libcutsim's NCCL binding on one GPU: all-gather, self send/recv, and the
+    sharded pipeline routed through it."""
+    import torch
+
+    from paper_2603_01443_b200.comm import NcclComm
+    from paper_2603_01443_b200.parallel import run_cut_sharded
+
+    comm = NcclComm.create(0, 1)
+    try:
+        send = torch.arange(1000, dtype=torch.float64, device="cuda")
+        recv = torch.empty_like(send)
+        comm.all_gather(recv, send)
+        torch.cuda.synchronize()
+        assert torch.equal(recv, send)
+        back = torch.empty_like(send)
+        comm.sendrecv(send * 2, back, 0)
+        torch.cuda.synchronize()
+        assert torch.equal(back, send * 2)
+        circ = cb.build_brickwall(cb.BrickwallSpec(16, 5, 2, 2, 4))
+        res, (b, e) = run_cut_sharded(circ, 2, rank=0, world=1, comm=comm)
+        assert (b, e) == (0, 1 << 16)
+        assert np.array_equal(res.cpu().numpy(), cb.run_cut(circ, 2).amps)
+    finally:
+        comm.destroy()
