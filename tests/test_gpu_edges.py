@@ -1,0 +1,112 @@
+"""Edge cases of the cut path on the GPU against the oracle: empty circuits,
+no cuts (K = 1), one-qubit segments (n = q), the smallest q, thousands of
+merge terms (launch chunking), repeated cuts at one position, complex64 with
+n = 3, CX cuts with the target on either side, and the one-call pipeline on
+all of them."""
+import numpy as np
+import pytest
+
+from oracle import cutbench_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+TOL_C64 = 1e-5
+
+
+@pytest.fixture(scope="module")
+def cb():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2603_01443_b200 as pkg
+
+    return pkg
+
+
+def ref_state(c):
+    return orc.simulate(c.num_qubits, c.kinds, c.qa, c.qb, c.params)
+
+
+def both_paths(cb, circ, n, **kw):
+    """run_cut (one native call) and the step-by-step drop-in API."""
+    one = cb.run_cut(circ, n, **kw).amps
+    subs = cb.decompose(circ, cb.plan_cut(circ, n))
+    states = [[cb.simulate(c) for c in fam.circuits] for fam in subs.segments]
+    step = cb.merge(cb.merge_input_from(subs, states)).amps
+    return one, step
+
+
+def test_empty_circuit(cb):
+    from paper_2603_01443_b200.circuits import Circuit
+
+    circ = Circuit(6, [])
+    one, step = both_paths(cb, circ, 2)
+    want = np.zeros(64, complex)
+    want[0] = 1
+    assert np.array_equal(one, want) and np.array_equal(step, want)
+    assert np.array_equal(cb.simulate(circ).amps, want)
+
+
+def test_no_cuts(cb):
+    from paper_2603_01443_b200.circuits import Circuit, cz, h, t
+
+    circ = Circuit(8, [h(i) for i in range(8)] + [cz(0, 1), t(3), cz(5, 6), h(7)])
+    plan = cb.plan_cut(circ, 2)
+    assert plan.c_total == 0
+    one, step = both_paths(cb, circ, 2)
+    ref = ref_state(circ)
+    assert np.abs(one - ref).max() < TOL and np.abs(step - ref).max() < TOL
+
+
+@pytest.mark.parametrize("q", [2, 3, 6])
+def test_one_qubit_segments(cb, q):
+    circ = cb.build_staircase(cb.BenchmarkSpec(q=q, n=q, blocks=2))
+    one, step = both_paths(cb, circ, q)
+    ref = ref_state(circ)
+    assert np.abs(one - ref).max() < TOL and np.abs(step - ref).max() < TOL
+
+
+def test_thousands_of_terms(cb):
+    # c_total = 11 cuts on one boundary: K = 2048 terms (> one launch's table)
+    circ = cb.build_brickwall(cb.BrickwallSpec(12, 4, 2, 11, 5))
+    assert cb.plan_cut(circ, 2).c_total == 11
+    one, step = both_paths(cb, circ, 2)
+    ref = ref_state(circ)
+    assert np.abs(one - ref).max() < TOL and np.abs(step - ref).max() < TOL
+
+
+def test_repeated_cuts_same_layer(cb):
+    # c > d forces several cuts into one layer at the same position
+    circ = cb.build_brickwall(cb.BrickwallSpec(10, 2, 2, 5, 1))
+    pos = [bg.position for bg in cb.plan_cut(circ, 2).boundary_gates]
+    assert len(pos) == 5
+    one, _ = both_paths(cb, circ, 2)
+    assert np.abs(one - ref_state(circ)).max() < TOL
+
+
+def test_complex64_three_segments(cb):
+    circ = cb.build_brickwall(cb.BrickwallSpec(15, 6, 3, 4, 2))
+    got = cb.run_cut(circ, 3, dtype=np.complex64).amps
+    assert got.dtype == np.complex64
+    assert np.abs(got - ref_state(circ)).max() < TOL_C64
+
+
+def test_cx_cuts_both_orientations(cb):
+    from paper_2603_01443_b200.circuits import Circuit, cx, h, t
+
+    gates = [h(i) for i in range(8)] + [cx(3, 4), t(4), cx(4, 3), t(3), cx(3, 4), h(2), cx(4, 3)]
+    circ = Circuit(8, gates)
+    assert cb.plan_cut(circ, 2).c_total == 4
+    one, step = both_paths(cb, circ, 2)
+    ref = ref_state(circ)
+    assert np.abs(one - ref).max() < TOL and np.abs(step - ref).max() < TOL
+
+
+def test_unequal_sizes_one_call(cb):
+    circ = cb.build_staircase(cb.BenchmarkSpec(q=10, n=2, blocks=3))
+    ref = ref_state(circ)
+    for sizes in [(1, 9), (9, 1), (3, 7), (2, 3, 5), (1, 1, 1, 7)]:
+        got = cb.run_cut(circ, len(sizes), sizes=sizes).amps
+        assert np.abs(got - ref).max() < TOL, sizes
