@@ -50,7 +50,8 @@ int cs_device_count(int32_t* count);
 
 /* Options: "tile_bits" (multi-sweep tile, default 12 for c128),
  * "low_bits" (contiguous low qubits per tile, default 5), "fuse" (1q gate
- * fusion, default 1), "threads" (0 = auto), "merge_streaming" (evict-first
+ * fusion, default 1; 2 = U3 split into phase . Ry . phase with phases
+ * commuted through diagonal gates), "threads" (0 = auto), "merge_streaming" (evict-first
  * output stores, default 1), "merge_iters" (0 = auto), "merge_dmma" (FP64
  * tensor-core merge for K = 8..64: 0 off, 1 four real GEMMs per complex
  * product, 2 three (3M) for K <= 32; default 2), "engine" (1 register-tile

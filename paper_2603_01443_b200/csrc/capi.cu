@@ -212,7 +212,12 @@ std::shared_ptr<const Program> build_schedule(int nq, const uint8_t* kinds, cons
   const int vb = choose_vb(n_states);
   std::string key;
   key.reserve(size_t(n_gates) * 45 + 32);
-  const int32_t hdr[9] = {nq, T, L, int32_t(g_opt.fuse), slots ? 1 : 0, dtype, vb, g_sweep_minb,
+  // fuse 2 (split U3 + commuted phases) measured slower than fused complex
+  // 2x2s even with the specialised kernels (cfg4a uncut 286 vs 212 ms: a
+  // phase on a thread bit diverges, and the longer op list grows the
+  // straight-line code), so it stays opt-in
+  const int fuse = int(g_opt.fuse);
+  const int32_t hdr[9] = {nq, T, L, int32_t(fuse), slots ? 1 : 0, dtype, vb, g_sweep_minb,
                           int32_t(g_opt.engine)};
   key.append(reinterpret_cast<const char*>(hdr), sizeof(hdr));
   key.append(reinterpret_cast<const char*>(kinds), size_t(n_gates));
@@ -225,8 +230,9 @@ std::shared_ptr<const Program> build_schedule(int nq, const uint8_t* kinds, cons
     auto it = g_cache.find(key);
     if (it != g_cache.end()) return it->second;
   }
-  std::vector<LOp> ops = lower_gates(nq, kinds, qa, qb, params, slots, n_gates);
-  if (g_opt.fuse) ops = fuse_ops(ops);
+  std::vector<LOp> ops = lower_gates(nq, kinds, qa, qb, params, slots, n_gates, fuse == 2);
+  if (fuse == 2) ops = fuse_ops(commute_phases(ops), true);
+  else if (fuse == 1) ops = fuse_ops(ops);
   // register groups hold 2^k x vb complex values: 8 (c128) / 16 (c64) per thread
   const int max_group = std::min(sweep_max_group(T), group_budget(vb, dtype));
   auto built = std::make_shared<Program>();
@@ -684,7 +690,8 @@ int cs_set_option(const char* key, int64_t value) {
     if (value < 1 || value > 12) return fail(CS_ERR_INVALID, "low_bits must be in [1, 12]");
     g_opt.low_bits = value;
   } else if (k == "fuse") {
-    g_opt.fuse = value ? 1 : 0;
+    if (value < 0 || value > 2) return fail(CS_ERR_INVALID, "fuse must be 0, 1 or 2");
+    g_opt.fuse = value;
   } else if (k == "threads") {
     if (value != 0 && (value < 32 || value > 256 || (value & 31)))
       return fail(CS_ERR_INVALID, "threads must be 0 or a multiple of 32 in [32, 256]");

@@ -68,7 +68,7 @@ uint64_t qubit_mask(const LOp& o) {
 }  // namespace
 
 std::vector<LOp> lower_gates(int nq, const uint8_t* kinds, const int64_t* qa, const int64_t* qb,
-                             const double* params, const int32_t* slots, int64_t n_gates) {
+                             const double* params, const int32_t* slots, int64_t n_gates, bool split_u3) {
   std::vector<LOp> ops;
   ops.reserve(size_t(n_gates));
   for (int64_t g = 0; g < n_gates; ++g) {
@@ -138,6 +138,25 @@ std::vector<LOp> lower_gates(int nq, const uint8_t* kinds, const int64_t* qa, co
         if (!std::isfinite(th) || !std::isfinite(ph) || !std::isfinite(la))
           throw PlanError{CS_ERR_INVALID, "non-finite U3 parameter at position " + std::to_string(g)};
         const double c = std::cos(th / 2), s = std::sin(th / 2);
+        if (split_u3) {
+          LOp pl;  // diag(1, e^{i la}) first, then Ry(th), then diag(1, e^{i ph})
+          pl.type = OP_PHASE;
+          pl.mask = 1ull << a;
+          pl.m[0] = std::cos(la);
+          pl.m[1] = std::sin(la);
+          if (la != 0.0) ops.push_back(pl);
+          LOp ry;
+          ry.type = OP_DENSE;
+          ry.target = int(a);
+          set2(ry.m, c, 0, -s, 0, s, 0, c, 0);
+          ops.push_back(ry);
+          o.type = OP_PHASE;
+          o.mask = 1ull << a;
+          o.m[0] = std::cos(ph);
+          o.m[1] = std::sin(ph);
+          if (ph == 0.0) continue;
+          break;
+        }
         o.type = OP_DENSE;
         o.target = int(a);
         set2(o.m, c, 0, -std::cos(la) * s, -std::sin(la) * s, std::cos(ph) * s, std::sin(ph) * s,
@@ -152,7 +171,7 @@ std::vector<LOp> lower_gates(int nq, const uint8_t* kinds, const int64_t* qa, co
   return ops;
 }
 
-std::vector<LOp> fuse_ops(const std::vector<LOp>& ops) {
+std::vector<LOp> fuse_ops(const std::vector<LOp>& ops, bool same_type_only) {
   std::vector<LOp> out;
   out.reserve(ops.size());
   int last[64];
@@ -162,7 +181,8 @@ std::vector<LOp> fuse_ops(const std::vector<LOp>& ops) {
       const int q = single_qubit(op);
       if (last[q] >= 0) {
         LOp& prev = out[size_t(last[q])];
-        if (prev.slot < 0 || op.slot < 0 || prev.slot == op.slot) {
+        const bool types_ok = !same_type_only || prev.type == op.type;
+        if (types_ok && (prev.slot < 0 || op.slot < 0 || prev.slot == op.slot)) {
           LOp f;
           f.slot = std::max(prev.slot, op.slot);
           double A[8], B[8];
@@ -201,6 +221,71 @@ std::vector<LOp> fuse_ops(const std::vector<LOp>& ops) {
       }
     }
   }
+  return out;
+}
+
+std::vector<LOp> commute_phases(const std::vector<LOp>& ops) {
+  std::vector<LOp> out;
+  out.reserve(ops.size());
+  LOp pend[64];
+  bool has[64] = {false};
+  uint64_t pending = 0;
+  auto flush_all = [&]() {
+    uint64_t m = pending;
+    while (m) {
+      const int q = ctz64(m);
+      m &= m - 1;
+      out.push_back(pend[q]);
+      has[q] = false;
+    }
+    pending = 0;
+  };
+  for (const LOp& op : ops) {
+    if (op.type == OP_PHASE && popcount64(op.mask) == 1) {
+      const int q = ctz64(op.mask);
+      if (!has[q]) {
+        pend[q] = op;
+        has[q] = true;
+        pending |= 1ull << q;
+        continue;
+      }
+      LOp& prev = pend[q];
+      if (prev.slot < 0 || op.slot < 0 || prev.slot == op.slot) {
+        // diag(1, a) . diag(1, b) = diag(1, ab), per variant alternative
+        LOp f;
+        f.type = OP_PHASE;
+        f.mask = op.mask;
+        f.slot = std::max(prev.slot, op.slot);
+        const double* a0 = prev.m;
+        const double* a1 = prev.slot >= 0 ? prev.alt : prev.m;
+        const double* b0 = op.m;
+        const double* b1 = op.slot >= 0 ? op.alt : op.m;
+        f.m[0] = a0[0] * b0[0] - a0[1] * b0[1];
+        f.m[1] = a0[0] * b0[1] + a0[1] * b0[0];
+        if (f.slot >= 0) {
+          f.alt[0] = a1[0] * b1[0] - a1[1] * b1[1];
+          f.alt[1] = a1[0] * b1[1] + a1[1] * b1[0];
+        }
+        prev = f;
+        continue;
+      }
+      // two different cut slots on one qubit: emit the older one here
+      out.push_back(prev);
+      prev = op;
+      continue;
+    }
+    if (op.type == OP_PHASE) {  // multi-qubit diagonal: commutes with every pending phase
+      out.push_back(op);
+      continue;
+    }
+    if (pending & (1ull << op.target)) {  // the phase must precede this op
+      out.push_back(pend[op.target]);
+      has[op.target] = false;
+      pending &= ~(1ull << op.target);
+    }
+    out.push_back(op);
+  }
+  flush_all();
   return out;
 }
 

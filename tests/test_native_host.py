@@ -88,9 +88,19 @@ def execute_schedule(plan, nq, variant=0):
     return amps
 
 
+@pytest.fixture(params=[1, 2], ids=["fuse-complex", "fuse-split-u3"])
+def fuse_mode(request):
+    """Both lowerings: fused complex 2x2s (interpreter default) and split U3 =
+    phase . Ry . phase with commuted phases (the specialised-kernel default)."""
+    old = _native.get_option("fuse")
+    _native.set_option("fuse", request.param)
+    yield request.param
+    _native.set_option("fuse", old)
+
+
 @pytest.mark.parametrize("tile_bits", [4, 6, 12])
 @pytest.mark.parametrize("q,d,n,c,seed", [(9, 4, 3, 4, 1), (10, 5, 2, 3, 0), (14, 3, 2, 2, 2)])
-def test_schedule_reproduces_oracle_uncut(q, d, n, c, seed, tile_bits):
+def test_schedule_reproduces_oracle_uncut(q, d, n, c, seed, tile_bits, fuse_mode):
     circ = G.build_brickwall(G.BrickwallSpec(q, d, n, c, seed))
     plan = json.loads(_native.sweep_plan_json(q, circ.table, tile_bits=tile_bits))
     T = plan["sweeps"][0]["T"]
@@ -102,7 +112,7 @@ def test_schedule_reproduces_oracle_uncut(q, d, n, c, seed, tile_bits):
 
 @pytest.mark.parametrize("key", ["stair_q8_n4_b2", "stair_q6_n2_b3", "shadow_q9_d4_n3_c4_s3",
                                  "padded_q6_n2_b1_p1"])
-def test_schedule_of_variant_templates_matches_reference_states(golden, key):
+def test_schedule_of_variant_templates_matches_reference_states(golden, key, fuse_mode):
     q, n = int(golden[f"{key}/q"]), int(golden[f"{key}/n"])
     circ = C.Circuit.from_table(q, C.GateTable(golden[f"{key}/kinds"], golden[f"{key}/qa"],
                                                golden[f"{key}/qb"]))
@@ -125,6 +135,23 @@ def test_depth_padded_fusion_collapses_pad():
     got = execute_schedule(plan, 6)
     ref = orc.simulate(6, circ.kinds, circ.qa, circ.qb)
     assert np.abs(got - ref).max() < 1e-10
+
+
+def test_split_u3_lowering_counts():
+    """fuse=2 on cfg4a: one real rotation per U3 and one merged phase per
+    qubit per layer (plus the trailing ones); CZs untouched."""
+    circ = G.build_brickwall(G.BASELINE_CONFIGS["cfg4a"])
+    old = _native.get_option("fuse")
+    try:
+        _native.set_option("fuse", 2)
+        plan = json.loads(_native.sweep_plan_json(30, circ.table))
+    finally:
+        _native.set_option("fuse", old)
+    ents = [e for s in plan["sweeps"] for e in s["entries"]]
+    dense = [e for e in ents if e["type"] == 0]
+    assert len(dense) == 300 and all(e["m"][1::2] == [0, 0, 0, 0] for e in dense)  # real
+    n_cz = int((circ.kinds == C.KIND_CZ).sum())
+    assert len(ents) - len(dense) == n_cz + 300 + 30
 
 
 def test_uncut_q30_schedule_is_compact():
@@ -251,7 +278,7 @@ def _reg_plan(nq, table, slots=None, tile_bits=0):
 
 @pytest.mark.parametrize("tile_bits", [4, 6, 9, 12])
 @pytest.mark.parametrize("q,d,n,c,seed", [(9, 4, 3, 4, 1), (14, 3, 2, 2, 2), (16, 3, 4, 3, 5)])
-def test_register_programs_reproduce_oracle(q, d, n, c, seed, tile_bits):
+def test_register_programs_reproduce_oracle(q, d, n, c, seed, tile_bits, fuse_mode):
     circ = G.build_brickwall(G.BrickwallSpec(q, d, n, c, seed))
     plan = _reg_plan(q, circ.table, tile_bits=tile_bits)
     got = execute_reg_programs(plan, q)
@@ -261,7 +288,7 @@ def test_register_programs_reproduce_oracle(q, d, n, c, seed, tile_bits):
 
 @pytest.mark.parametrize("key", ["stair_q8_n4_b2", "stair_q6_n2_b3", "shadow_q9_d4_n3_c4_s3",
                                  "stair_q12_n3_b1"])
-def test_register_programs_of_variant_templates(golden, key):
+def test_register_programs_of_variant_templates(golden, key, fuse_mode):
     q, n = int(golden[f"{key}/q"]), int(golden[f"{key}/n"])
     circ = C.Circuit.from_table(q, C.GateTable(golden[f"{key}/kinds"], golden[f"{key}/qa"],
                                                golden[f"{key}/qb"]))
