@@ -37,6 +37,8 @@ CASES = [  # (K, S, H, W, rows)
     (8, 1, 256, 1024, None), (8, 2, 64, 256, (5, 60)), (16, 1, 128, 512, None), (16, 2, 40, 128, (3, 37)),
     (12, 1, 64, 256, None), (32, 1, 32, 128, None), (64, 1, 16, 256, None), (3, 1, 8, 2, None),
     (16, 1, 64, 2, None), (8, 1, 100, 4, None),
+    # wide enough for the pipelined 3M kernel (16 warps x 16 / 8 columns), ragged rows
+    (16, 2, 40, 256, (3, 37)), (32, 1, 20, 256, None), (8, 3, 24, 512, (1, 23)), (16, 1, 700, 512, None),
 ]
 
 
