@@ -39,6 +39,9 @@ UNIT = "amplitudes/s"
 WORKLOAD = "cfg4a"
 
 
+DFMA_PEAK_TF = 36.5  # measured on this B200 pool (tools/fp64_peak.cu)
+
+
 def load_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -324,6 +327,7 @@ def run_ours(args):
 
     # the uncut simulator on the same circuit (the cut-vs-uncut comparison point)
     uncut_ms = None
+    uncut = None
     if world == 1 and not args.no_uncut:
         cb.simulate(circ)  # builds (and JIT-compiles) the uncut program
         torch.cuda.synchronize()
@@ -336,6 +340,23 @@ def run_ours(args):
         uncut_ms = u0.elapsed_time(u1)
         del sv
         torch.cuda.empty_cache()
+        # per-sweep HBM rate and FP64 use of the uncut simulator
+        plan = json.loads(_native.sweep_plan_json(q, circ.table))
+        n_sweeps = len(plan["sweeps"])
+        n_dense = 0
+        for sw in plan["sweeps"]:
+            ents, i = sw["entries"], 0
+            while i < len(ents):  # a slotted op occupies two entries
+                n_dense += ents[i]["type"] == 0
+                i += 2 if ents[i]["slot"] >= 0 else 1
+        t = uncut_ms / 1e3
+        uncut = {"ms": uncut_ms, "sweeps": n_sweeps, "dense_ops": n_dense,
+                 "hbm_gbs": 32.0 * total * n_sweeps / t / 1e9,
+                 "hbm_frac": 32.0 * total * n_sweeps / t / 1e9 / peak,
+                 "fp64_tflops_alg": 16.0 * total * n_dense / t / 1e12,
+                 "fp64_frac_of_dfma_peak": 16.0 * total * n_dense / t / 1e12 / DFMA_PEAK_TF,
+                 "note": "32 B/amplitude per sweep (read+write); 8 FMA (16 flop) per amplitude per dense "
+                         "2x2 op; DFMA peak 36.5 TF/s measured with tools/fp64_peak.cu"}
 
     # roofline of the dominant kernel (merge) from the timed region
     roofline = None
@@ -414,6 +435,7 @@ def run_ours(args):
                        "l2": "no flush: each step writes the 16 GiB output (>> 126 MB L2)"},
             "stage_ms": stage,
             "uncut_ms": uncut_ms,
+            "uncut": uncut,
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
