@@ -30,7 +30,7 @@ int merge_cols_per_thread(int K);
 cudaError_t launch_merge_dmma(const MergeParams& p, int K, dim3 grid, int threads, size_t smem,
                               cudaStream_t stream);
 int merge_dmma_cols_per_warp(int K);
-cudaError_t launch_merge_dmma3(const MergeParams& p, int K, dim3 grid, int threads, size_t smem,
+cudaError_t launch_merge_dmma3(const MergeParams& p, int K, int warps, dim3 grid, size_t smem,
                                cudaStream_t stream);
 int merge_dmma3_cols_per_warp(int K);
 int merge_dmma3_row_blocks(int K);
@@ -60,6 +60,7 @@ struct Options {
   int64_t merge_streaming = 1;
   int64_t merge_iters = 0;
   int64_t vb = 0;  // states per CTA in a variant batch (0 = auto)
+  int64_t merge_dmma3_warps = 8;  // warps per CTA of the 3M kernel (8: 2 CTAs/SM, 4: 4 CTAs/SM)
   int64_t merge_smem_kb = 96;  // staged-row budget per CTA of the tensor-core merge
   int64_t merge_dmma = 2;  // FP64 tensor-core merge: 2 = three-GEMM (3M) for K <= 32, four-GEMM K = 64
   int64_t engine = 1;      // 1: register-tile kernel (rsweep), 0: shared-memory tile kernel (sweep)
@@ -272,13 +273,14 @@ int merge_launch_one(int S, int Kc, const int32_t* hidx, const int32_t* lidx, co
     // complex columns; a CTA spans >= 128 columns so row staging is amortised
     const int64_t cw = m3 ? merge_dmma3_cols_per_warp(Kc) : merge_dmma_cols_per_warp(Kc);
     const int64_t ncg = std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(8, 256 / cw), lo_len / cw));
+    const int warps3 = int(g_opt.merge_dmma3_warps);
+    const int64_t smem_budget = m3 ? g_opt.merge_smem_kb * 1024 * warps3 / 8 : g_opt.merge_smem_kb * 1024;
     const int64_t C = cw * ncg;
     const int64_t nrows = row_end - row_begin;
     const int RS = m3 ? 3 * Kc + 4 : 2 * Kc + 4;
     // row blocks processed together
     const int64_t rbg = m3 ? merge_dmma3_row_blocks(Kc) : 8 / (merge_dmma_cols_per_warp(Kc) / 4);
-    int64_t iters = std::max<int64_t>(1, std::min<int64_t>((g_opt.merge_smem_kb * 1024) / (8 * RS * 8),
-                                                           (nrows + 7) / 8));
+    int64_t iters = std::max<int64_t>(1, std::min<int64_t>(smem_budget / (8 * RS * 8), (nrows + 7) / 8));
     iters = std::min<int64_t>(iters, 64);
     // keep at least two CTAs per SM for small products
     const int64_t col_blocks = std::max<int64_t>(1, lo_len / C);
@@ -320,7 +322,7 @@ int merge_launch_one(int S, int Kc, const int32_t* hidx, const int32_t* lidx, co
         char* base_out = static_cast<char*>(out) + size_t(s0) * size_t(out_slot_stride) * eb0;
         pd.out = base_out + size_t(r0 - row_begin) * size_t(lo_len) * eb0;
         dim3 grid(unsigned(lo_len / C), unsigned((r1 - r0 + rows_cta - 1) / rows_cta), unsigned(sc));
-        cudaError_t e = m3 ? launch_merge_dmma3(pd, Kc, grid, threads, smem, stream)
+        cudaError_t e = m3 ? launch_merge_dmma3(pd, Kc, warps3, grid, smem, stream)
                            : launch_merge_dmma(pd, Kc, grid, threads, smem, stream);
         g_launches.fetch_add(1);
         if (e != cudaSuccess) return cuda_fail(e, "merge_dmma_kernel launch");
@@ -707,6 +709,9 @@ int cs_set_option(const char* key, int64_t value) {
   } else if (k == "merge_smem_kb") {
     if (value < 8 || value > 112) return fail(CS_ERR_INVALID, "merge_smem_kb must be in [8, 112]");
     g_opt.merge_smem_kb = value;
+  } else if (k == "merge_dmma3_warps") {
+    if (value != 4 && value != 8) return fail(CS_ERR_INVALID, "merge_dmma3_warps must be 4 or 8");
+    g_opt.merge_dmma3_warps = value;
   } else if (k == "merge_dmma") {
     if (value < 0 || value > 2) return fail(CS_ERR_INVALID, "merge_dmma must be 0, 1 or 2");
     g_opt.merge_dmma = value;
@@ -744,6 +749,7 @@ int64_t cs_get_option(const char* key) {
   if (k == "jit_max_cost") return g_opt.jit_max_cost;
   if (k == "merge_dmma") return g_opt.merge_dmma;
   if (k == "merge_smem_kb") return g_opt.merge_smem_kb;
+  if (k == "merge_dmma3_warps") return g_opt.merge_dmma3_warps;
   if (k == "plan_json") return g_opt.plan_json;
   if (k == "sweep_minb") return g_sweep_minb;
   return -1;

@@ -817,8 +817,8 @@ __global__ void __launch_bounds__(256, 2) merge_dmma_kernel(const __grid_constan
 // Rounding: |error| <= ~K eps (|br|+|bi|)(|ar|+|ai|) per output, far inside
 // the 1e-10 parity bound.
 // ---------------------------------------------------------------------------
-template <int KT, int NT, int RB>
-__global__ void __launch_bounds__(256, 2) merge_dmma3_kernel(const __grid_constant__ MergeParams p) {
+template <int KT, int NT, int RB, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) merge_dmma3_kernel(const __grid_constant__ MergeParams p) {
   constexpr int KS = KT / 4;       // mma k-steps per GEMM
   constexpr int RS = 3 * KT + 4;   // smem row stride (doubles)
   constexpr int COLS_W = 8 * NT;   // complex columns per warp
@@ -939,16 +939,16 @@ __global__ void __launch_bounds__(256, 2) merge_dmma3_kernel(const __grid_consta
   }
 }
 
-template <int KT, int NT, int RB>
-static cudaError_t launch_dmma3_kt(const MergeParams& p, dim3 grid, int threads, size_t smem, cudaStream_t stream) {
+template <int KT, int NT, int RB, int WARPS>
+static cudaError_t launch_dmma3_kt(const MergeParams& p, dim3 grid, size_t smem, cudaStream_t stream) {
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(merge_dmma3_kernel<KT, NT, RB>,
+    cudaError_t e = cudaFuncSetAttribute(merge_dmma3_kernel<KT, NT, RB, WARPS>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     configured = smem;
   }
-  merge_dmma3_kernel<KT, NT, RB><<<grid, threads, smem, stream>>>(p);
+  merge_dmma3_kernel<KT, NT, RB, WARPS><<<grid, WARPS * 32, smem, stream>>>(p);
   return cudaGetLastError();
 }
 
@@ -956,12 +956,22 @@ static cudaError_t launch_dmma3_kt(const MergeParams& p, dim3 grid, int threads,
 int merge_dmma3_cols_per_warp(int K) { return K <= 16 ? 16 : 8; }
 int merge_dmma3_row_blocks(int K) { return K <= 16 ? 2 : 4; }
 
-cudaError_t launch_merge_dmma3(const MergeParams& p, int K, dim3 grid, int threads, size_t smem,
+// warps = 8 (2 CTAs per SM) or 4 (4 CTAs per SM: staging of one CTA overlaps
+// three others' math)
+cudaError_t launch_merge_dmma3(const MergeParams& p, int K, int warps, dim3 grid, size_t smem,
                                cudaStream_t stream) {
+  if (warps == 4) {
+    switch (K) {
+      case 8: return launch_dmma3_kt<8, 2, 2, 4>(p, grid, smem, stream);
+      case 16: return launch_dmma3_kt<16, 2, 2, 4>(p, grid, smem, stream);
+      case 32: return launch_dmma3_kt<32, 1, 4, 4>(p, grid, smem, stream);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   switch (K) {
-    case 8: return launch_dmma3_kt<8, 2, 2>(p, grid, threads, smem, stream);
-    case 16: return launch_dmma3_kt<16, 2, 2>(p, grid, threads, smem, stream);
-    case 32: return launch_dmma3_kt<32, 1, 4>(p, grid, threads, smem, stream);
+    case 8: return launch_dmma3_kt<8, 2, 2, 8>(p, grid, smem, stream);
+    case 16: return launch_dmma3_kt<16, 2, 2, 8>(p, grid, smem, stream);
+    case 32: return launch_dmma3_kt<32, 1, 4, 8>(p, grid, smem, stream);
     default: return cudaErrorInvalidValue;
   }
 }
