@@ -1,0 +1,38 @@
+"""Module-level drop-in: make `import cutbench` (and its submodules) resolve to
+this package, so code written against the reference runs unchanged.
+
+    import paper_2603_01443_b200 as b200
+    b200.install_as_cutbench()
+    from cutbench.harness import measure, sweep_heatmap    # GPU-backed
+    from cutbench.costmodel import threshold_uniform
+
+Mapping (reference module -> this package, `/root/reference/pkg/src/cutbench/`):
+circuits, cutting, engine, merging, errors, cli -> same names; costmodel ->
+theory; svmfit -> boundary_fit; harness -> harness + sweeps (one namespace).
+"""
+from __future__ import annotations
+
+import sys
+import types
+
+
+def install_as_cutbench(name: str = "cutbench", *, replace: bool = False) -> types.ModuleType:
+    """Register this package under `name` in sys.modules (refuses to shadow an
+    already-imported module of that name unless replace=True)."""
+    import paper_2603_01443_b200 as pkg
+
+    from . import boundary_fit, circuits, cli, cutting, engine, errors, harness, merging, sweeps, theory
+
+    if name in sys.modules and sys.modules[name] is not pkg and not replace:
+        raise RuntimeError(f"module {name!r} is already imported; pass replace=True to shadow it")
+    combined = types.ModuleType(f"{name}.harness", harness.__doc__)
+    for mod in (harness, sweeps):
+        for attr, val in vars(mod).items():
+            if not attr.startswith("__"):
+                setattr(combined, attr, val)
+    subs = {"circuits": circuits, "cutting": cutting, "engine": engine, "merging": merging, "errors": errors,
+            "cli": cli, "costmodel": theory, "svmfit": boundary_fit, "harness": combined}
+    sys.modules[name] = pkg
+    for sub, mod in subs.items():
+        sys.modules[f"{name}.{sub}"] = mod
+    return pkg

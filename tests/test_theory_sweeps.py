@@ -145,3 +145,41 @@ def test_cli_ranges_and_grid_validation():
     with pytest.raises(ValidationError):
         sweeps.scan_feasible([0], 0.0)
     assert cli.main(["sweep", "--q", "6", "--c", "3", "--n", "3"]) == cli.EXIT_VALIDATION
+
+
+def test_install_as_cutbench_aliases_reference_modules():
+    import sys
+
+    import paper_2603_01443_b200 as pkg
+
+    name = "cutbench_alias_test"
+    pkg.install_as_cutbench(name)
+    try:
+        import importlib
+
+        cbm = importlib.import_module(name)
+        assert cbm is pkg
+        h = importlib.import_module(f"{name}.harness")
+        assert h.sweep_heatmap is sweeps.sweep_heatmap and h.measure is pkg.measure
+        assert importlib.import_module(f"{name}.costmodel").threshold_uniform is theory.threshold_uniform
+        assert importlib.import_module(f"{name}.svmfit").fit_weighted_line is boundary_fit.fit_weighted_line
+        assert importlib.import_module(f"{name}.cutting").plan_cut is pkg.plan_cut
+        # every name the reference package exports (cutbench/__init__.py:68-125)
+        for attr in ("BenchmarkSpec", "BoundaryFit", "BoundaryGate", "BudgetExceededError", "CapacityError",
+                     "Circuit", "CostParams", "Crossovers", "CutPlan", "CutbenchError", "DEFAULT_MAX_QUBITS",
+                     "DegenerateFitError", "FeasibilityScan", "Gate", "GateKind", "MergeInput", "RegimeRatios",
+                     "StateVec", "SubcircuitSet", "SweepResult", "ThresholdReport", "TimingBreakdown",
+                     "UnsupportedTopologyError", "ValidationError", "apply_gate", "breakdown_series",
+                     "build_benchmark", "build_depth_padded", "build_staircase", "compute_depth",
+                     "count_subcircuits", "decompose", "detect_crossovers", "dump_amplitudes", "fit_boundary",
+                     "fit_weighted_line", "measure", "merge", "merge_input_from", "merge_streaming",
+                     "n_sub_uniform", "plan_cut", "plan_cut_sizes", "predict_costs", "regime_ratios",
+                     "scan_feasible", "simulate", "split_sweep", "sweep_heatmap", "tensor", "threshold_line",
+                     "threshold_nonuniform", "threshold_uniform"):
+            assert hasattr(cbm, attr), attr
+        with pytest.raises(RuntimeError):
+            sys.modules["cutbench_alias_other"] = object()
+            pkg.install_as_cutbench("cutbench_alias_other")
+    finally:
+        for k in [k for k in sys.modules if k.startswith(name) or k.startswith("cutbench_alias_other")]:
+            del sys.modules[k]
