@@ -67,3 +67,35 @@ def test_cli_sweep_json(sw, tmp_path):
     with redirect_stdout(buf):
         assert cli.main(["breakdown", "--q", "4:6:2", "--c", "2", "--reps", "1", "--report", "-"]) == 0
     assert "q_pre_cross" in buf.getvalue()
+
+
+def test_reference_style_code_through_alias():
+    """Code written against the reference (`import cutbench ...`) runs on the
+    GPU path after install_as_cutbench(): the harness's cut pipeline
+    (harness.py:125-145) and measure()."""
+    import sys
+
+    import numpy as np
+
+    import paper_2603_01443_b200 as pkg
+    from oracle import cutbench_oracle as orc
+
+    pkg.install_as_cutbench("cutbench_gpu_alias")
+    try:
+        import importlib
+
+        cutbench = importlib.import_module("cutbench_gpu_alias")
+        harness = importlib.import_module("cutbench_gpu_alias.harness")
+        spec = cutbench.BenchmarkSpec(q=10, n=2, blocks=3)
+        circuit = cutbench.build_benchmark(spec)
+        plan = cutbench.plan_cut(circuit, spec.n)
+        subs = cutbench.decompose(circuit, plan)
+        states = [[cutbench.simulate(c) for c in fam.circuits] for fam in subs.segments]
+        merged = cutbench.merge(cutbench.merge_input_from(subs, states))
+        ref = orc.simulate(10, circuit.kinds, circuit.qa, circuit.qb)
+        assert np.abs(merged.amps - ref).max() < 1e-10
+        row = harness.measure(spec, 2)
+        assert row.status == "ok" and row.t_cut == pytest.approx(row.t_pre + row.t_sub + row.t_merge)
+    finally:
+        for k in [k for k in sys.modules if k.startswith("cutbench_gpu_alias")]:
+            del sys.modules[k]
