@@ -29,7 +29,7 @@ import numpy as np
 from . import _device, _native
 from .cutting import COEFF_TERM0, COEFF_TERM1, coefficients_of, merge_table_of
 from .engine import DEFAULT_MAX_QUBITS, StateVec, check_capacity
-from .errors import BudgetExceededError, CapacityError, ValidationError
+from .errors import BudgetExceededError, ValidationError
 
 
 @dataclass(frozen=True)
@@ -250,13 +250,7 @@ def merge(minput: MergeInput, *, max_qubits: int = DEFAULT_MAX_QUBITS, deadline:
     if not (0 <= begin <= end <= (1 << q)):
         raise ValidationError(f"output range [{begin}, {end}) outside [0, 2^{q})")
     if out is None:
-        nbytes = (end - begin) * np.dtype(dt).itemsize
-        t = _device.torch()
-        free, _ = t.cuda.mem_get_info()
-        slack = t.cuda.memory_reserved() - t.cuda.memory_allocated()
-        if nbytes > free + slack:
-            raise CapacityError(f"merged state needs {nbytes / 2**30:.2f} GiB; device has "
-                                f"{(free + slack) / 2**30:.2f} GiB free")
+        _device.check_free((end - begin) * np.dtype(dt).itemsize, "merged state")
     batches = [segment_batch(states, dt) for states in minput.segment_states]
     if minput.chain is not None:
         res = merge_chain_device(minput.chain, batches, dtype=dt, out=out, out_range=(begin, end))

@@ -117,7 +117,7 @@ def run_cut(circuit: Circuit, n: int, *, dtype=np.complex128, max_qubits: int = 
     torch.cuda.Event with timing) are recorded around the two device stages
     without synchronising. Reference: harness.py:125-145 (cut leg)."""
     from . import _native
-    from .errors import CapacityError, ValidationError
+    from .errors import ValidationError
 
     q = circuit.num_qubits
     check_capacity(q, max_qubits)
@@ -136,13 +136,7 @@ def run_cut(circuit: Circuit, n: int, *, dtype=np.complex128, max_qubits: int = 
     if not (0 <= begin <= end <= (1 << q)):
         raise ValidationError(f"output range [{begin}, {end}) outside [0, 2^{q})")
     if out is None:
-        nbytes = (end - begin) * np.dtype(dtype).itemsize
-        if nbytes >= (1 << 30):
-            free, _ = t.cuda.mem_get_info()
-            slack = t.cuda.memory_reserved() - t.cuda.memory_allocated()
-            if nbytes > free + slack:
-                raise CapacityError(f"state needs {nbytes / 2**30:.2f} GiB; device has "
-                                    f"{(free + slack) / 2**30:.2f} GiB free")
+        _device.check_free((end - begin) * np.dtype(dtype).itemsize, "state")
         out = _device.empty_shape((end - begin,), dtype)
     k, qa, qb, prm = _native._table_args(circuit.table)
     sz = _native.c_i32(sizes)
