@@ -53,14 +53,30 @@ def stream_ptr(stream=None) -> int:
     return int(s.cuda_stream)
 
 
+_TOTAL = {}
+
+
+def _total_memory() -> int:
+    t = torch()
+    dev = t.cuda.current_device()
+    if dev not in _TOTAL:
+        _TOTAL[dev] = int(t.cuda.get_device_properties(dev).total_memory)
+    return _TOTAL[dev]
+
+
 def check_free(nbytes: int, what: str) -> None:
     """CapacityError if an allocation of nbytes cannot fit on the device.
     cudaMemGetInfo costs 0.3-10 ms per call (measured on the B200 box), so it
-    is only consulted for allocations of 1 GiB or more; smaller ones rely on
-    torch's own out-of-memory error."""
+    is only consulted for allocations of 1 GiB or more that exceed half of
+    what this process leaves of the device; smaller ones rely on torch's own
+    out-of-memory error."""
     if nbytes < (1 << 30):
         return
     t = torch()
+    # cheap bound first: device capacity minus what this process holds
+    total = _total_memory()
+    if nbytes < 0.5 * (total - t.cuda.memory_allocated()):
+        return
     free, _total = t.cuda.mem_get_info()
     cached = t.cuda.memory_reserved() - t.cuda.memory_allocated()
     if nbytes > free + cached:
