@@ -709,6 +709,9 @@ int cs_set_option(const char* key, int64_t value) {
   } else if (k == "merge_smem_kb") {
     if (value < 8 || value > 112) return fail(CS_ERR_INVALID, "merge_smem_kb must be in [8, 112]");
     g_opt.merge_smem_kb = value;
+  } else if (k == "jit_minb") {
+    if (value < 1 || value > 4) return fail(CS_ERR_INVALID, "jit_minb must be in [1, 4]");
+    g_jit_minb = int(value);
   } else if (k == "merge_dmma3_warps") {
     if (value != 4 && value != 8) return fail(CS_ERR_INVALID, "merge_dmma3_warps must be 4 or 8");
     g_opt.merge_dmma3_warps = value;
@@ -750,6 +753,7 @@ int64_t cs_get_option(const char* key) {
   if (k == "merge_dmma") return g_opt.merge_dmma;
   if (k == "merge_smem_kb") return g_opt.merge_smem_kb;
   if (k == "merge_dmma3_warps") return g_opt.merge_dmma3_warps;
+  if (k == "jit_minb") return g_jit_minb;
   if (k == "plan_json") return g_opt.plan_json;
   if (k == "sweep_minb") return g_sweep_minb;
   return -1;

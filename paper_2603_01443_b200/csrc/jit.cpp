@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <sstream>
 #include <thread>
@@ -110,7 +111,7 @@ std::string jit_source(const Sweep& sw, const std::vector<RegOp>& prog, int RB, 
   const int NR = 1 << RB;
   const int BD = 1 << (T - RB);
   std::ostringstream o;
-  o << "extern \"C\" __global__ void __launch_bounds__(" << BD << ") " << name
+  o << "extern \"C\" __global__ void __launch_bounds__(" << BD << ", " << g_jit_minb << ") " << name
     << "(V* __restrict__ states, long long stride, unsigned long long vbase, int init) {\n";
   o << "  extern __shared__ __align__(16) unsigned char smraw[];\n";
   o << "  V* sm = reinterpret_cast<V*>(smraw); (void)sm;\n";
@@ -274,6 +275,24 @@ bool compile_source(const std::string& code, std::vector<char>* cubin, std::stri
 
 }  // namespace
 
+// CUTSIM_JIT_DUMP=<dir>: also write each generated source and CUBIN there
+// (SASS inspection with cuobjdump; no effect otherwise)
+static void dump_artifact(const std::string& name, const std::string& code, const std::vector<char>& cubin) {
+  const char* dir = std::getenv("CUTSIM_JIT_DUMP");
+  if (!dir || !*dir) return;
+  const std::string base = std::string(dir) + "/" + name;
+  if (FILE* f = std::fopen((base + ".cu").c_str(), "wb")) {
+    std::fwrite(code.data(), 1, code.size(), f);
+    std::fclose(f);
+  }
+  if (FILE* f = std::fopen((base + ".cubin").c_str(), "wb")) {
+    std::fwrite(cubin.data(), 1, cubin.size(), f);
+    std::fclose(f);
+  }
+}
+
+int g_jit_minb = 1;  // __launch_bounds__ min blocks per SM of the generated kernels
+
 bool jit_cubin(const std::vector<const Sweep*>& sweeps, const std::vector<const std::vector<RegOp>*>& progs,
                int dtype, std::vector<char>* cubin, std::vector<std::string>* names, std::string* err) {
   std::string code = header(dtype);
@@ -286,7 +305,9 @@ bool jit_cubin(const std::vector<const Sweep*>& sweeps, const std::vector<const 
     names->push_back("cs_jit_" + std::to_string(i));
     code += jit_source(*sweeps[i], *progs[i], reg_bits_for(sweeps[i]->tile_bits), dtype, names->back());
   }
-  return compile_source(code, cubin, err);
+  const bool ok = compile_source(code, cubin, err);
+  if (ok) dump_artifact("selftest", code, *cubin);
+  return ok;
 }
 
 // One NVRTC program per launch, compiled on parallel host threads (NVRTC is
@@ -308,6 +329,7 @@ std::shared_ptr<JitModule> jit_compile(const std::vector<const Sweep*>& sweeps,
       const std::string code = header(dtype) + jit_source(*sweeps[i], *progs[i], reg_bits_for(sweeps[i]->tile_bits),
                                                         dtype, "cs_jit_" + std::to_string(i));
       ok[i] = compile_source(code, &cubins[i], &errs[i]) ? 1 : 0;
+      if (ok[i]) dump_artifact("cs_jit_" + std::to_string(i), code, cubins[i]);
     }
   };
   const size_t nt = std::max<size_t>(1, std::min<size_t>(n, std::max(1u, std::thread::hardware_concurrency())));

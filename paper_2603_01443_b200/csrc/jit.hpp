@@ -42,6 +42,9 @@ std::shared_ptr<JitModule> jit_compile(const std::vector<const Sweep*>& sweeps,
 bool jit_cubin(const std::vector<const Sweep*>& sweeps, const std::vector<const std::vector<RegOp>*>& progs,
                int dtype, std::vector<char>* cubin, std::vector<std::string>* names, std::string* err);
 
+// min CTAs per SM requested from the generated kernels (option "jit_minb")
+extern int g_jit_minb;
+
 // FP64 instructions the specialised code would contain (size guard).
 int64_t jit_cost(const std::vector<RegOp>& prog, int reg_bits);
 
