@@ -169,6 +169,7 @@ struct Program {
   mutable std::shared_ptr<JitModule> jit;
   mutable bool jit_tried = false;
   mutable std::atomic<int> uses{0};
+  int64_t n_states = 1;  // states per launch the program was scheduled for
 };
 
 std::mutex g_cache_mu;
@@ -238,6 +239,7 @@ std::shared_ptr<const Program> build_schedule(int nq, const uint8_t* kinds, cons
   const int max_group = std::min(sweep_max_group(T), group_budget(vb, dtype));
   auto built = std::make_shared<Program>();
   built->engine = int(g_opt.engine);
+  built->n_states = n_states;
   built->sweeps = schedule_sweeps(ops, nq, T, L, max_group);
   build_launches(*built);
   std::shared_ptr<const Program> prog = built;
@@ -449,17 +451,22 @@ std::shared_ptr<JitModule> program_jit(const Program& prog, int dtype) {
   prog.jit_tried = true;
   std::vector<const Sweep*> sw;
   std::vector<const std::vector<RegOp>*> rp;
+  std::vector<int> minb;
   bool any = false;
   for (const Launch& ln : prog.launches) {
     const Sweep& s = prog.sweeps[size_t(ln.sweep)];
     sw.push_back(&s);
+    // two CTAs per SM only pays when the launch has CTAs to fill them (and
+    // whole-state tiles can spill under the 128-register cap)
+    const int64_t ctas = (int64_t(1) << s.oq.size()) * prog.n_states;
+    minb.push_back(ctas >= 2 * 148 ? g_jit_minb : 1);
     const bool ok = jit_cost(ln.reg, reg_bits_for(s.tile_bits)) <= g_opt.jit_max_cost;
     rp.push_back(ok ? &ln.reg : nullptr);
     any |= ok;
   }
   if (!any) return nullptr;
   std::string err;
-  prog.jit = jit_compile(sw, rp, dtype, &err);
+  prog.jit = jit_compile(sw, rp, dtype, &err, &minb);
   if (!prog.jit) g_err = "JIT unavailable, using the interpreter kernel: " + err;
   return prog.jit;
 }

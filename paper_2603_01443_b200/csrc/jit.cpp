@@ -105,13 +105,14 @@ int64_t jit_cost(const std::vector<RegOp>& prog, int RB) {
   return c;
 }
 
-std::string jit_source(const Sweep& sw, const std::vector<RegOp>& prog, int RB, int dtype, const std::string& name) {
+std::string jit_source(const Sweep& sw, const std::vector<RegOp>& prog, int RB, int dtype, const std::string& name,
+                       int minb) {
   const int T = sw.tile_bits;
   const int L = sw.low_bits;
   const int NR = 1 << RB;
   const int BD = 1 << (T - RB);
   std::ostringstream o;
-  o << "extern \"C\" __global__ void __launch_bounds__(" << BD << ", " << g_jit_minb << ") " << name
+  o << "extern \"C\" __global__ void __launch_bounds__(" << BD << ", " << minb << ") " << name
     << "(V* __restrict__ states, long long stride, unsigned long long vbase, int init) {\n";
   o << "  extern __shared__ __align__(16) unsigned char smraw[];\n";
   o << "  V* sm = reinterpret_cast<V*>(smraw); (void)sm;\n";
@@ -291,7 +292,7 @@ static void dump_artifact(const std::string& name, const std::string& code, cons
   }
 }
 
-int g_jit_minb = 1;  // __launch_bounds__ min blocks per SM of the generated kernels
+int g_jit_minb = 2;  // __launch_bounds__ min blocks per SM of the streaming (many-tile) kernels
 
 bool jit_cubin(const std::vector<const Sweep*>& sweeps, const std::vector<const std::vector<RegOp>*>& progs,
                int dtype, std::vector<char>* cubin, std::vector<std::string>* names, std::string* err) {
@@ -303,7 +304,8 @@ bool jit_cubin(const std::vector<const Sweep*>& sweeps, const std::vector<const 
       continue;
     }
     names->push_back("cs_jit_" + std::to_string(i));
-    code += jit_source(*sweeps[i], *progs[i], reg_bits_for(sweeps[i]->tile_bits), dtype, names->back());
+    code += jit_source(*sweeps[i], *progs[i], reg_bits_for(sweeps[i]->tile_bits), dtype, names->back(),
+                       g_jit_minb);
   }
   const bool ok = compile_source(code, cubin, err);
   if (ok) dump_artifact("selftest", code, *cubin);
@@ -314,7 +316,7 @@ bool jit_cubin(const std::vector<const Sweep*>& sweeps, const std::vector<const 
 // thread-safe), so a 12-sweep program costs about one sweep's compile time.
 std::shared_ptr<JitModule> jit_compile(const std::vector<const Sweep*>& sweeps,
                                        const std::vector<const std::vector<RegOp>*>& progs, int dtype,
-                                       std::string* err) {
+                                       std::string* err, const std::vector<int>* minb) {
   const size_t n = sweeps.size();
   std::vector<std::vector<char>> cubins(n);
   std::vector<std::string> errs(n);
@@ -327,7 +329,8 @@ std::shared_ptr<JitModule> jit_compile(const std::vector<const Sweep*>& sweeps,
         continue;
       }
       const std::string code = header(dtype) + jit_source(*sweeps[i], *progs[i], reg_bits_for(sweeps[i]->tile_bits),
-                                                        dtype, "cs_jit_" + std::to_string(i));
+                                                        dtype, "cs_jit_" + std::to_string(i),
+                                                        minb ? (*minb)[i] : 1);
       ok[i] = compile_source(code, &cubins[i], &errs[i]) ? 1 : 0;
       if (ok[i]) dump_artifact("cs_jit_" + std::to_string(i), code, cubins[i]);
     }

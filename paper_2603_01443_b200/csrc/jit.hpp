@@ -29,20 +29,23 @@ struct JitModule {
 // (dense/phase/remap) with the tile geometry, masks, matrices (hex-float
 // literals) and remap index maps baked in.
 std::string jit_source(const Sweep& sw, const std::vector<RegOp>& prog, int reg_bits, int dtype,
-                       const std::string& name);
+                       const std::string& name, int minb = 1);
 
 // Compile every launch of a program into one module (sm_100a CUBIN via
 // NVRTC, loaded with cudaLibraryLoadData). Returns null and sets *err on
 // failure (NVRTC missing, compile error).
+// minb[i]: __launch_bounds__ min CTAs per SM of launch i (null: 1)
 std::shared_ptr<JitModule> jit_compile(const std::vector<const Sweep*>& sweeps,
                                        const std::vector<const std::vector<RegOp>*>& progs, int dtype,
-                                       std::string* err);
+                                       std::string* err, const std::vector<int>* minb = nullptr);
 
 // NVRTC step only (no device needed): the CUBIN and kernel names.
 bool jit_cubin(const std::vector<const Sweep*>& sweeps, const std::vector<const std::vector<RegOp>*>& progs,
                int dtype, std::vector<char>* cubin, std::vector<std::string>* names, std::string* err);
 
-// min CTAs per SM requested from the generated kernels (option "jit_minb")
+// min CTAs per SM requested from the generated kernels that stream many
+// tiles (option "jit_minb", default 2: <= 128 registers, two 256-thread CTAs
+// per SM; measured uncut q=30 182 ms vs 261 ms at one CTA per SM)
 extern int g_jit_minb;
 
 // FP64 instructions the specialised code would contain (size guard).
