@@ -56,6 +56,7 @@ struct Options {
   int64_t tile_bits = 0;  // 0 = per-dtype default
   int64_t low_bits = 5;
   int64_t fuse = 1;
+  int64_t dense_norm = 2;  // normalised dense 2x2s: 0 off, 1 on, 2 when NVRTC kernels are enabled
   int64_t threads = 0;
   int64_t merge_streaming = 1;
   int64_t merge_iters = 0;
@@ -219,8 +220,11 @@ std::shared_ptr<const Program> build_schedule(int nq, const uint8_t* kinds, cons
   // phase on a thread bit diverges, and the longer op list grows the
   // straight-line code), so it stays opt-in
   const int fuse = int(g_opt.fuse);
-  const int32_t hdr[9] = {nq, T, L, int32_t(fuse), slots ? 1 : 0, dtype, vb, g_sweep_minb,
-                          int32_t(g_opt.engine)};
+  // normalised 2x2s only pay where the 1-coefficients become free (the
+  // NVRTC-specialised kernels); the interpreter keeps the plain matrices
+  const int norm = g_opt.dense_norm == 2 ? (g_opt.jit != 0 && g_opt.engine == 1 ? 1 : 0) : int(g_opt.dense_norm);
+  const int32_t hdr[10] = {nq, T, L, int32_t(fuse), slots ? 1 : 0, dtype, vb, g_sweep_minb,
+                           int32_t(g_opt.engine), norm};
   key.append(reinterpret_cast<const char*>(hdr), sizeof(hdr));
   key.append(reinterpret_cast<const char*>(kinds), size_t(n_gates));
   key.append(reinterpret_cast<const char*>(qa), size_t(n_gates) * 8);
@@ -235,6 +239,7 @@ std::shared_ptr<const Program> build_schedule(int nq, const uint8_t* kinds, cons
   std::vector<LOp> ops = lower_gates(nq, kinds, qa, qb, params, slots, n_gates, fuse == 2);
   if (fuse == 2) ops = fuse_ops(commute_phases(ops), true);
   else if (fuse == 1) ops = fuse_ops(ops);
+  if (norm) ops = normalize_dense(ops, nq);
   // register groups hold 2^k x vb complex values: 8 (c128) / 16 (c64) per thread
   const int max_group = std::min(sweep_max_group(T), group_budget(vb, dtype));
   auto built = std::make_shared<Program>();
@@ -716,6 +721,9 @@ int cs_set_option(const char* key, int64_t value) {
   } else if (k == "merge_smem_kb") {
     if (value < 8 || value > 112) return fail(CS_ERR_INVALID, "merge_smem_kb must be in [8, 112]");
     g_opt.merge_smem_kb = value;
+  } else if (k == "dense_norm") {
+    if (value < 0 || value > 2) return fail(CS_ERR_INVALID, "dense_norm must be 0, 1 or 2");
+    g_opt.dense_norm = value;
   } else if (k == "jit_minb") {
     if (value < 1 || value > 4) return fail(CS_ERR_INVALID, "jit_minb must be in [1, 4]");
     g_jit_minb = int(value);
@@ -761,6 +769,7 @@ int64_t cs_get_option(const char* key) {
   if (k == "merge_smem_kb") return g_opt.merge_smem_kb;
   if (k == "merge_dmma3_warps") return g_opt.merge_dmma3_warps;
   if (k == "jit_minb") return g_jit_minb;
+  if (k == "dense_norm") return g_opt.dense_norm;
   if (k == "plan_json") return g_opt.plan_json;
   if (k == "sweep_minb") return g_sweep_minb;
   return -1;

@@ -198,6 +198,12 @@ std::string jit_source(const Sweep& sw, const std::vector<RegOp>& prog, int RB, 
           std::string e;
           auto add = [&](double c, const std::string& cs, const char* v, bool neg) {
             if (c == 0.0) return;
+            if (c == 1.0 || c == -1.0) {  // unit coefficient (normalised matrices): no multiply
+              const bool minus = neg != (c < 0);
+              if (!e.empty() || minus) e += minus ? " - " : " + ";
+              e += v;
+              return;
+            }
             if (!e.empty() || neg) e += neg ? " - " : " + ";
             e += cs + " * " + v;
           };

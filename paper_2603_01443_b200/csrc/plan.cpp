@@ -224,6 +224,94 @@ std::vector<LOp> fuse_ops(const std::vector<LOp>& ops, bool same_type_only) {
   return out;
 }
 
+namespace {
+
+struct Cx {
+  double r = 1, i = 0;
+};
+inline Cx cmulx(Cx a, Cx b) { return {a.r * b.r - a.i * b.i, a.r * b.i + a.i * b.r}; }
+inline Cx cdivx(Cx a, Cx b) {
+  const double n = b.r * b.r + b.i * b.i;
+  return {(a.r * b.r + a.i * b.i) / n, (a.i * b.r - a.r * b.i) / n};
+}
+inline double cabs2(Cx a) { return a.r * a.r + a.i * a.i; }
+inline bool is_one(Cx a) { return a.r == 1.0 && a.i == 0.0; }
+
+LOp phase_op(int q, Cx v) {
+  LOp o;
+  o.type = OP_PHASE;
+  o.mask = 1ull << q;
+  o.m[0] = v.r;
+  o.m[1] = v.i;
+  return o;
+}
+
+}  // namespace
+
+std::vector<LOp> normalize_dense(const std::vector<LOp>& ops, int nq) {
+  std::vector<LOp> out;
+  out.reserve(ops.size() + size_t(nq) + 1);
+  std::vector<Cx> d0(static_cast<size_t>(nq)), d1(static_cast<size_t>(nq));
+  Cx scale;
+  auto flush = [&](int q) {
+    const size_t k = size_t(q);
+    if (is_one(d0[k]) && is_one(d1[k])) return;
+    scale = cmulx(scale, d0[k]);  // D = d0 . diag(1, d1/d0)
+    const Cx r = cdivx(d1[k], d0[k]);
+    if (!is_one(r)) out.push_back(phase_op(q, r));
+    d0[k] = Cx{};
+    d1[k] = Cx{};
+  };
+  long last_dense = -1;
+  for (const LOp& op : ops) {
+    if (op.type == OP_PHASE) {  // diagonal: commutes with every pending D
+      out.push_back(op);
+      continue;
+    }
+    const int q = op.target;
+    if (op.mask != 0 || op.slot >= 0) {  // controlled (or variant-switched) dense: apply D first
+      flush(q);
+      out.push_back(op);
+      continue;
+    }
+    // M . D_q, then rows normalised by their pivot
+    LOp n = op;
+    const size_t k = size_t(q);
+    Cx m[2][2];
+    for (int r = 0; r < 2; ++r)
+      for (int c = 0; c < 2; ++c) m[r][c] = Cx{op.m[2 * (2 * r + c)], op.m[2 * (2 * r + c) + 1]};
+    for (int r = 0; r < 2; ++r) {
+      m[r][0] = cmulx(m[r][0], d0[k]);
+      m[r][1] = cmulx(m[r][1], d1[k]);
+    }
+    Cx dn[2];
+    for (int r = 0; r < 2; ++r) {
+      const int piv = cabs2(m[r][0]) >= cabs2(m[r][1]) ? 0 : 1;
+      dn[r] = m[r][piv];
+      for (int c = 0; c < 2; ++c) {
+        const Cx v = c == piv ? Cx{} : cdivx(m[r][c], dn[r]);
+        n.m[2 * (2 * r + c)] = v.r;
+        n.m[2 * (2 * r + c) + 1] = v.i;
+      }
+    }
+    d0[k] = dn[0];
+    d1[k] = dn[1];
+    last_dense = long(out.size());
+    out.push_back(n);
+  }
+  for (int q = 0; q < nq; ++q) flush(q);
+  // the scalar only arises from diagonals some uncontrolled dense op created
+  if (!is_one(scale) && last_dense >= 0) {
+    LOp& l = out[size_t(last_dense)];
+    for (int e = 0; e < 4; ++e) {
+      const Cx v = cmulx(Cx{l.m[2 * e], l.m[2 * e + 1]}, scale);
+      l.m[2 * e] = v.r;
+      l.m[2 * e + 1] = v.i;
+    }
+  }
+  return out;
+}
+
 std::vector<LOp> commute_phases(const std::vector<LOp>& ops) {
   std::vector<LOp> out;
   out.reserve(ops.size());

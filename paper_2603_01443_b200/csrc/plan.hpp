@@ -40,6 +40,17 @@ std::vector<LOp> lower_gates(int nq, const uint8_t* kinds, const int64_t* qa, co
 // 4 FP64 instructions per amplitude against 7 for a complex 2x2).
 std::vector<LOp> fuse_ops(const std::vector<LOp>& ops, bool same_type_only = false);
 
+// Rewrite every uncontrolled dense 2x2 M as D . M' with M' having a 1 in
+// each row (pivot = the row's larger entry, so the other |entry| <= 1) and
+// push the diagonal D into the next dense op on that qubit (M_next . D):
+// a normalised complex 2x2 costs 4 FP64 instructions per amplitude in the
+// specialised kernels (the 1-coefficient term is the FMA accumulator)
+// instead of 7. Pending diagonals are emitted as phase ops (times a global
+// scalar) before an op that does not commute with them (a controlled dense
+// op on that target) and at the end; the global scalar is folded into the
+// last dense op, which stays un-normalised.
+std::vector<LOp> normalize_dense(const std::vector<LOp>& ops, int nq);
+
 // Defer single-qubit phases past everything they commute with (diagonal
 // ops, dense ops controlled by or not touching their qubit) and merge the
 // phases of one qubit; a qubit's pending phase is emitted right before the

@@ -88,14 +88,18 @@ def execute_schedule(plan, nq, variant=0):
     return amps
 
 
-@pytest.fixture(params=[1, 2], ids=["fuse-complex", "fuse-split-u3"])
+@pytest.fixture(params=[(1, 0), (2, 0), (1, 1), (2, 1)],
+                ids=["fuse-complex", "fuse-split-u3", "normalised", "split-normalised"])
 def fuse_mode(request):
-    """Both lowerings: fused complex 2x2s (interpreter default) and split U3 =
-    phase . Ry . phase with commuted phases (the specialised-kernel default)."""
-    old = _native.get_option("fuse")
-    _native.set_option("fuse", request.param)
+    """The lowerings: fused complex 2x2s (interpreter default), split U3 =
+    phase . Ry . phase with commuted phases, and normalised 2x2s with the
+    deferred diagonals (the specialised-kernel default)."""
+    old = _native.get_option("fuse"), _native.get_option("dense_norm")
+    _native.set_option("fuse", request.param[0])
+    _native.set_option("dense_norm", request.param[1])
     yield request.param
-    _native.set_option("fuse", old)
+    _native.set_option("fuse", old[0])
+    _native.set_option("dense_norm", old[1])
 
 
 @pytest.mark.parametrize("tile_bits", [4, 6, 12])
@@ -152,6 +156,28 @@ def test_split_u3_lowering_counts():
     assert len(dense) == 300 and all(e["m"][1::2] == [0, 0, 0, 0] for e in dense)  # real
     n_cz = int((circ.kinds == C.KIND_CZ).sum())
     assert len(ents) - len(dense) == n_cz + 300 + 30
+
+
+def test_normalised_dense_ops_have_unit_pivots():
+    circ = G.build_brickwall(G.BASELINE_CONFIGS["cfg4a"])
+    old = _native.get_option("dense_norm")
+    try:
+        _native.set_option("dense_norm", 1)
+        plan = json.loads(_native.sweep_plan_json(30, circ.table))
+    finally:
+        _native.set_option("dense_norm", old)
+    dense = [e for s in plan["sweeps"] for e in s["entries"] if e["type"] == 0]
+    unit = 0
+    for e in dense:
+        m = np.array(e["m"]).reshape(2, 2, 2)  # row, col, (re, im)
+        for r in range(2):
+            ones = [c for c in range(2) if tuple(m[r, c]) == (1.0, 0.0)]
+            if ones:
+                other = m[r, 1 - ones[0]]
+                assert np.hypot(*other) <= 1 + 1e-12
+                unit += 1
+    # every row of every dense op but the last (which carries the global scalar)
+    assert unit >= 2 * len(dense) - 2
 
 
 def test_uncut_q30_schedule_is_compact():
