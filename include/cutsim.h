@@ -57,7 +57,8 @@ int cs_device_count(int32_t* count);
  * product, 2 three (3M) for K <= 32; default 2), "engine" (1 register-tile
  * sweep kernel, 0 shared-memory tile kernel), "jit" (0 never, 1 from a
  * program's second use, 2 always: NVRTC-specialised sweep kernels),
- * "jit_max_cost", "vb", "sweep_minb", "merge_smem_kb", "merge_dmma3_warps", "plan_json" (tuning /
+ * "jit_max_cost", "vb", "sweep_minb", "merge_smem_kb", "merge_dmma3_warps", "jit_minb", "dense_norm" (normalised 2x2s:
+ * 0 off, 1 on, 2 = with the NVRTC kernels), "reg_bits", "plan_json" (tuning /
  * testing). */
 int cs_set_option(const char* key, int64_t value);
 int64_t cs_get_option(const char* key);

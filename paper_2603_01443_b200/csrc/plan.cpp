@@ -539,8 +539,12 @@ std::string sweeps_to_json(const std::vector<Sweep>& sweeps, int nq) {
 // ---------------------------------------------------------------------------
 // register-tile lowering
 // ---------------------------------------------------------------------------
+int g_reg_bits = 0;
+
 int reg_bits_for(int tile_bits) {
   if (tile_bits <= 2) return std::max(1, tile_bits);
+  // override (tuning): only where it keeps 32..512 threads per tile
+  if (g_reg_bits >= 2 && tile_bits - g_reg_bits >= 5 && tile_bits - g_reg_bits <= 9) return g_reg_bits;
   return std::max(2, std::min(4, tile_bits - 8));
 }
 

@@ -1,5 +1,5 @@
 """Uncut simulator (NVRTC kernels) with a given __launch_bounds__ min-blocks
-for the generated kernels:  python tools/uncut_minb.py MINB [cfg]"""
+for the generated kernels:  python tools/uncut_minb.py MINB [cfg] [REG_BITS]"""
 import sys
 
 import numpy as np
@@ -11,6 +11,8 @@ from paper_2603_01443_b200 import _native  # noqa: E402
 
 _native.set_option("jit", 2)
 _native.set_option("jit_minb", int(sys.argv[1]))
+if len(sys.argv) > 3:
+    _native.set_option("reg_bits", int(sys.argv[3]))
 name = sys.argv[2] if len(sys.argv) > 2 else "cfg4a"
 circ = cb.build_brickwall(cb.BASELINE_CONFIGS[name])
 sv = cb.simulate(circ, max_qubits=circ.num_qubits)
@@ -26,4 +28,4 @@ for _ in range(3):
     times.append(e0.elapsed_time(e1))
     assert torch.equal(sv.device_tensor()[:1 << 20], ref)
     del sv
-print(f"{name} jit_minb={sys.argv[1]}: {np.median(times):.1f} ms {[round(t, 1) for t in times]}", flush=True)
+print(f"{name} jit_minb={sys.argv[1]} reg_bits={_native.get_option('reg_bits')}: {np.median(times):.1f} ms {[round(t, 1) for t in times]}", flush=True)
