@@ -52,3 +52,30 @@ def test_jit_controlled_gates_and_complex64(jit_on):
     assert np.abs(cb.simulate(circ).amps - ref).max() < 1e-10
     got = cb.simulate(circ, dtype=np.complex64).amps
     assert np.abs(got - ref).max() < 1e-5
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("key", ["stair_q8_n4_b2", "stair_q6_n2_b3", "shadow_q9_d4_n3_c4_s3", "stair_q12_n3_b1",
+                                 "padded_q6_n2_b1_p1"])
+def test_jit_normalised_kernels_match_reference_golden(jit_on, golden, key):
+    """The default specialised lowering (normalised 2x2s with deferred
+    diagonals) on the reference's own golden uncut and merged states."""
+    import paper_2603_01443_b200 as cb
+
+    assert _native.get_option("dense_norm") == 2
+    q, n = int(golden[f"{key}/q"]), int(golden[f"{key}/n"])
+    circ = cb.Circuit.from_table(q, cb.GateTable(golden[f"{key}/kinds"], golden[f"{key}/qa"],
+                                                 golden[f"{key}/qb"]))
+    assert np.abs(cb.simulate(circ).amps - golden[f"{key}/uncut"]).max() < 1e-12
+    assert np.abs(cb.run_cut(circ, n).amps - golden[f"{key}/merged"]).max() < 1e-12
+
+
+@pytest.mark.gpu
+def test_jit_q22_multisweep_u3(jit_on):
+    import paper_2603_01443_b200 as cb
+
+    circ = cb.build_brickwall(cb.BrickwallSpec(22, 8, 2, 3, 7))
+    ref = orc.simulate(22, circ.kinds, circ.qa, circ.qb, circ.params)
+    got = cb.simulate(circ).amps
+    assert np.abs(got - ref).max() < 1e-10
+    assert abs(np.vdot(got, got).real - 1) < 1e-12
