@@ -195,16 +195,19 @@ std::string jit_source(const Sweep& sw, const std::vector<RegOp>& prog, int RB, 
         auto comp = [&](int re, int im, const char* ax, const char* ay, const char* bx, const char* by, bool imag) {
           // imag == false: real part  = m[re]*ax - m[im]*ay + m[re+2]*bx - m[im+2]*by
           // imag == true : imag part  = m[re]*ay + m[im]*ax + m[re+2]*by + m[im+2]*bx
-          std::string e;
+          // unit-coefficient terms (normalised matrices) go first, without a
+          // multiply: left-to-right evaluation then makes them the FMA
+          // accumulator (u + c1*x - c2*y = 2 DFMA; c1*x - c2*y + u = 3 ops)
+          std::string e, unit;
           auto add = [&](double c, const std::string& cs, const char* v, bool neg) {
             if (c == 0.0) return;
-            if (c == 1.0 || c == -1.0) {  // unit coefficient (normalised matrices): no multiply
+            if (c == 1.0 || c == -1.0) {
               const bool minus = neg != (c < 0);
-              if (!e.empty() || minus) e += minus ? " - " : " + ";
-              e += v;
+              if (!unit.empty() || minus) unit += minus ? " - " : " + ";
+              unit += v;
               return;
             }
-            if (!e.empty() || neg) e += neg ? " - " : " + ";
+            e += neg ? " - " : " + ";
             e += cs + " * " + v;
           };
           if (!imag) {
@@ -218,7 +221,9 @@ std::string jit_source(const Sweep& sw, const std::vector<RegOp>& prog, int RB, 
             add(op.m[re + 2], m[re + 2], by, false);
             add(op.m[im + 2], m[im + 2], bx, false);
           }
-          return e.empty() ? std::string("R(0)") : (e[0] == ' ' ? "R(0)" + e : e);
+          if (unit.empty() && e.empty()) return std::string("R(0)");
+          if (unit.empty()) return e.compare(0, 3, " + ") == 0 ? e.substr(3) : "R(0)" + e;
+          return (unit[0] == ' ' ? "R(0)" + unit : unit) + e;
         };
         o << " { const V a = v" << j << ", b = v" << jb << ";";
         o << " v" << j << ".x = " << comp(0, 1, "a.x", "a.y", "b.x", "b.y", false) << ";";
