@@ -259,6 +259,16 @@ bool dmma_eligible(int K, int dtype, int64_t lo_len) {
          lo_len >= merge_dmma_cols_per_warp(K);
 }
 
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n < 1) n = 148;
+  }
+  return n;
+}
+
 // merge_dmma = 2: the three-GEMM (3M) tensor-core kernel where it is
 // instantiated (K = 8, 16, 32); K = 64 keeps the four-GEMM kernel
 bool dmma3_eligible(int K, int dtype, int64_t lo_len) {
@@ -457,6 +467,7 @@ std::shared_ptr<JitModule> program_jit(const Program& prog, int dtype) {
   std::vector<const Sweep*> sw;
   std::vector<const std::vector<RegOp>*> rp;
   std::vector<int> minb;
+  std::vector<char> pers;
   bool any = false;
   for (const Launch& ln : prog.launches) {
     const Sweep& s = prog.sweeps[size_t(ln.sweep)];
@@ -464,14 +475,18 @@ std::shared_ptr<JitModule> program_jit(const Program& prog, int dtype) {
     // two CTAs per SM only pays when the launch has CTAs to fill them (and
     // whole-state tiles can spill under the 128-register cap)
     const int64_t ctas = (int64_t(1) << s.oq.size()) * prog.n_states;
-    minb.push_back(ctas >= 2 * 148 ? g_jit_minb : 1);
+    // many tiles of one state: the persistent prefetching form (one CTA per
+    // SM); else one CTA per tile, two per SM when there are enough
+    const bool p = g_jit_persistent && prog.n_states == 1 && (int64_t(1) << s.oq.size()) >= 4 * 148;
+    pers.push_back(p ? 1 : 0);
+    minb.push_back(p ? 1 : (ctas >= 2 * 148 ? g_jit_minb : 1));
     const bool ok = jit_cost(ln.reg, reg_bits_for(s.tile_bits)) <= g_opt.jit_max_cost;
     rp.push_back(ok ? &ln.reg : nullptr);
     any |= ok;
   }
   if (!any) return nullptr;
   std::string err;
-  prog.jit = jit_compile(sw, rp, dtype, &err, &minb);
+  prog.jit = jit_compile(sw, rp, dtype, &err, &minb, &pers);
   if (!prog.jit) g_err = "JIT unavailable, using the interpreter kernel: " + err;
   return prog.jit;
 }
@@ -503,7 +518,8 @@ int run_program(const Program& prog_ref, int nq, void* states, int64_t n_states,
         long long stride_arg = state_stride;
         unsigned long long vbase_arg = variant_base + uint64_t(v0);
         int init_arg = (first && init_zero) ? 1 : 0;
-        void* args[] = {&sp_arg, &stride_arg, &vbase_arg, &init_arg};
+        unsigned long long ntiles_arg = n_tiles;
+        void* args[] = {&sp_arg, &stride_arg, &vbase_arg, &init_arg, &ntiles_arg};
         e = cudaSuccess;
         if (jk->smem > 48 * 1024) {
           int dev = 0;
@@ -512,7 +528,9 @@ int run_program(const Program& prog_ref, int nq, void* states, int64_t n_states,
                                               int(jk->smem), dev);
         }
         if (e == cudaSuccess)
-          e = cudaLaunchKernel(reinterpret_cast<const void*>(jk->kernel), dim3(n_tiles, unsigned(vc), 1),
+          e = cudaLaunchKernel(reinterpret_cast<const void*>(jk->kernel),
+                               dim3(jk->persistent ? std::min<uint32_t>(n_tiles, uint32_t(sm_count())) : n_tiles,
+                                    unsigned(vc), 1),
                                dim3(unsigned(jk->threads), 1, 1), args, jk->smem, st);
       } else if (prog->engine == 1) {
         if (ln.reg.size() > size_t(kMaxRegOps)) return fail(CS_ERR_INTERNAL, "register program too long");
@@ -727,6 +745,8 @@ int cs_set_option(const char* key, int64_t value) {
   } else if (k == "dense_norm") {
     if (value < 0 || value > 2) return fail(CS_ERR_INVALID, "dense_norm must be 0, 1 or 2");
     g_opt.dense_norm = value;
+  } else if (k == "jit_persistent") {
+    g_jit_persistent = value ? 1 : 0;
   } else if (k == "jit_minb") {
     if (value < 1 || value > 4) return fail(CS_ERR_INVALID, "jit_minb must be in [1, 4]");
     g_jit_minb = int(value);
@@ -772,6 +792,7 @@ int64_t cs_get_option(const char* key) {
   if (k == "merge_smem_kb") return g_opt.merge_smem_kb;
   if (k == "merge_dmma3_warps") return g_opt.merge_dmma3_warps;
   if (k == "jit_minb") return g_jit_minb;
+  if (k == "jit_persistent") return g_jit_persistent;
   if (k == "dense_norm") return g_opt.dense_norm;
   if (k == "reg_bits") return g_reg_bits;
   if (k == "plan_json") return g_opt.plan_json;

@@ -79,6 +79,13 @@ DEV void ap(V& a, V& b, R m0r, R m0i, R m1r, R m1i, R m2r, R m2i, R m3r, R m3i) 
 }
 DEV void ph(V& a, R pr, R pi) { const R x = a.x * pr - a.y * pi; a.y = a.x * pi + a.y * pr; a.x = x; }
 DEV void ng(V& a) { a.x = -a.x; a.y = -a.y; }
+DEV void cpa(V* dst, const V* src) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  if (sizeof(V) == 16) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(sa), "l"(src) : "memory");
+  else asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(sa), "l"(src) : "memory");
+}
+DEV void cpc() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+DEV void cpw() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 )";
 
 }  // namespace
@@ -106,35 +113,68 @@ int64_t jit_cost(const std::vector<RegOp>& prog, int RB) {
 }
 
 std::string jit_source(const Sweep& sw, const std::vector<RegOp>& prog, int RB, int dtype, const std::string& name,
-                       int minb) {
+                       int minb, bool persistent) {
   const int T = sw.tile_bits;
   const int L = sw.low_bits;
   const int NR = 1 << RB;
   const int BD = 1 << (T - RB);
+  bool remap = false;
+  for (const RegOp& r : prog) remap |= r.kind == ROP_REMAP;
   std::ostringstream o;
   o << "extern \"C\" __global__ void __launch_bounds__(" << BD << ", " << minb << ") " << name
-    << "(V* __restrict__ states, long long stride, unsigned long long vbase, int init) {\n";
+    << "(V* __restrict__ states, long long stride, unsigned long long vbase, int init, unsigned long long n_tiles) {\n";
   o << "  extern __shared__ __align__(16) unsigned char smraw[];\n";
   o << "  V* sm = reinterpret_cast<V*>(smraw); (void)sm;\n";
   o << "  const unsigned tid = threadIdx.x;\n";
-  o << "  const unsigned long long tile = blockIdx.x;\n";
-  o << "  unsigned long long base = 0ull;\n";
-  for (size_t j = 0; j < sw.oq.size(); ++j)
-    o << "  base |= ((tile >> " << j << ") & 1ull) << " << sw.oq[j] << ";\n";
   o << "  const unsigned long long variant = vbase + blockIdx.y; (void)variant;\n";
   o << "  V* st = states + (long long)blockIdx.y * stride;\n";
-  auto gidx = [&](int j) {
+  auto base_of = [&](const char* dst, const char* tile) {
+    std::ostringstream b;
+    b << dst << " = 0ull;";
+    for (size_t j = 0; j < sw.oq.size(); ++j)
+      b << " " << dst << " |= ((" << tile << " >> " << j << ") & 1ull) << " << sw.oq[j] << ";";
+    return b.str();
+  };
+  auto gidx = [&](int j, const char* basev) {
     std::ostringstream g;
     g << "{ const unsigned e = tid + " << (j * BD) << "u; const unsigned c = e >> " << L
-      << "; unsigned long long g = base + (e & " << ((1u << L) - 1u) << "u);";
+      << "; unsigned long long g = " << basev << " + (e & " << ((1u << L) - 1u) << "u);";
     for (size_t i = 0; i < sw.hq.size(); ++i)
       g << " g |= (unsigned long long)((c >> " << i << ") & 1u) << " << sw.hq[i] << ";";
     return g.str();
   };
   for (int j = 0; j < NR; ++j) o << "  V v" << j << ";\n";
-  for (int j = 0; j < NR; ++j)
-    o << "  " << gidx(j) << " if (init) { v" << j << ".x = (base == 0ull && e == 0u) ? R(1) : R(0); v" << j
-      << ".y = R(0); } else v" << j << " = st[g]; }\n";
+  if (persistent) {
+    // one CTA per SM walks the tiles; each thread prefetches the amplitudes it
+    // will own in the next tile into its own shared-memory slots with
+    // cp.async while the current tile's gates run (no barrier needed: a
+    // thread only ever reads the slots it filled itself)
+    o << "  V* pf = sm + " << (remap ? (1u << T) : 0u) << "u;\n";
+    o << "  unsigned long long tile = blockIdx.x, base;\n";
+    o << "  if (!init && tile < n_tiles) { unsigned long long nb; " << base_of("nb", "tile") << "\n";
+    for (int j = 0; j < NR; ++j)
+      o << "    " << gidx(j, "nb") << " cpa(pf + e, st + g); }\n";
+    o << "  }\n  cpc();\n";
+    o << "  for (; tile < n_tiles; tile += gridDim.x) {\n";
+    o << "  " << base_of("base", "tile") << "\n";
+    o << "  if (init) {\n";
+    for (int j = 0; j < NR; ++j)
+      o << "    { const unsigned e = tid + " << (j * BD) << "u; v" << j
+        << ".x = (base == 0ull && e == 0u) ? R(1) : R(0); v" << j << ".y = R(0); }\n";
+    o << "  } else {\n    cpw();\n";
+    for (int j = 0; j < NR; ++j) o << "    v" << j << " = pf[tid + " << (j * BD) << "u];\n";
+    o << "    const unsigned long long nt = tile + gridDim.x;\n";
+    o << "    if (nt < n_tiles) { unsigned long long nb; " << base_of("nb", "nt") << "\n";
+    for (int j = 0; j < NR; ++j)
+      o << "      " << gidx(j, "nb") << " cpa(pf + e, st + g); }\n";
+    o << "    }\n    cpc();\n  }\n";
+  } else {
+    o << "  const unsigned long long tile = blockIdx.x; (void)n_tiles;\n";
+    o << "  unsigned long long " << base_of("base", "tile") << "\n";
+    for (int j = 0; j < NR; ++j)
+      o << "  " << gidx(j, "base") << " if (init) { v" << j << ".x = (base == 0ull && e == 0u) ? R(1) : R(0); v" << j
+        << ".y = R(0); } else v" << j << " = st[g]; }\n";
+  }
   o << "  unsigned tp = tid; (void)tp;\n";
   int rpos[4];
   for (int k = 0; k < RB; ++k) rpos[k] = T - RB + k;
@@ -242,7 +282,8 @@ std::string jit_source(const Sweep& sw, const std::vector<RegOp>& prog, int RB, 
     o << " } }\n";
     i += slotted ? 2 : 1;
   }
-  for (int j = 0; j < NR; ++j) o << "  " << gidx(j) << " st[g] = v" << j << "; }\n";
+  for (int j = 0; j < NR; ++j) o << "  " << gidx(j, "base") << " st[g] = v" << j << "; }\n";
+  if (persistent) o << "  }\n";
   o << "}\n";
   (void)dtype;
   return o.str();
@@ -303,6 +344,7 @@ static void dump_artifact(const std::string& name, const std::string& code, cons
   }
 }
 
+int g_jit_persistent = 0;  // prefetching persistent kernels for streaming sweeps (measured slower: opt-in)
 int g_jit_minb = 2;  // __launch_bounds__ min blocks per SM of the streaming (many-tile) kernels
 
 bool jit_cubin(const std::vector<const Sweep*>& sweeps, const std::vector<const std::vector<RegOp>*>& progs,
@@ -316,7 +358,7 @@ bool jit_cubin(const std::vector<const Sweep*>& sweeps, const std::vector<const 
     }
     names->push_back("cs_jit_" + std::to_string(i));
     code += jit_source(*sweeps[i], *progs[i], reg_bits_for(sweeps[i]->tile_bits), dtype, names->back(),
-                       g_jit_minb);
+                       g_jit_minb, g_jit_persistent != 0);
   }
   const bool ok = compile_source(code, cubin, err);
   if (ok) dump_artifact("selftest", code, *cubin);
@@ -327,7 +369,8 @@ bool jit_cubin(const std::vector<const Sweep*>& sweeps, const std::vector<const 
 // thread-safe), so a 12-sweep program costs about one sweep's compile time.
 std::shared_ptr<JitModule> jit_compile(const std::vector<const Sweep*>& sweeps,
                                        const std::vector<const std::vector<RegOp>*>& progs, int dtype,
-                                       std::string* err, const std::vector<int>* minb) {
+                                       std::string* err, const std::vector<int>* minb,
+                                       const std::vector<char>* persistent) {
   const size_t n = sweeps.size();
   std::vector<std::vector<char>> cubins(n);
   std::vector<std::string> errs(n);
@@ -341,7 +384,8 @@ std::shared_ptr<JitModule> jit_compile(const std::vector<const Sweep*>& sweeps,
       }
       const std::string code = header(dtype) + jit_source(*sweeps[i], *progs[i], reg_bits_for(sweeps[i]->tile_bits),
                                                         dtype, "cs_jit_" + std::to_string(i),
-                                                        minb ? (*minb)[i] : 1);
+                                                        minb ? (*minb)[i] : 1,
+                                                        persistent && (*persistent)[i]);
       ok[i] = compile_source(code, &cubins[i], &errs[i]) ? 1 : 0;
       if (ok[i]) dump_artifact("cs_jit_" + std::to_string(i), code, cubins[i]);
     }
@@ -379,7 +423,9 @@ std::shared_ptr<JitModule> jit_compile(const std::vector<const Sweep*>& sweeps,
     k.threads = 1 << (T - RB);
     bool remap = false;
     for (const RegOp& r : *progs[i]) remap |= r.kind == ROP_REMAP;
-    k.smem = remap ? (size_t(1) << T) * (dtype == 0 ? 16 : 8) : 0;
+    k.persistent = persistent && (*persistent)[i];
+    const size_t tile_bytes = (size_t(1) << T) * (dtype == 0 ? 16 : 8);
+    k.smem = (remap ? tile_bytes : 0) + (k.persistent ? tile_bytes : 0);
   }
   return mod;
 }

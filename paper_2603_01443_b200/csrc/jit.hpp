@@ -17,6 +17,7 @@ struct JitKernel {
   cudaKernel_t kernel = nullptr;
   size_t smem = 0;
   int threads = 0;
+  bool persistent = false;  // one CTA per SM walking the tiles, next tile prefetched
 };
 
 struct JitModule {
@@ -29,15 +30,17 @@ struct JitModule {
 // (dense/phase/remap) with the tile geometry, masks, matrices (hex-float
 // literals) and remap index maps baked in.
 std::string jit_source(const Sweep& sw, const std::vector<RegOp>& prog, int reg_bits, int dtype,
-                       const std::string& name, int minb = 1);
+                       const std::string& name, int minb = 1, bool persistent = false);
 
 // Compile every launch of a program into one module (sm_100a CUBIN via
 // NVRTC, loaded with cudaLibraryLoadData). Returns null and sets *err on
 // failure (NVRTC missing, compile error).
-// minb[i]: __launch_bounds__ min CTAs per SM of launch i (null: 1)
+// minb[i]: __launch_bounds__ min CTAs per SM of launch i (null: 1);
+// persistent[i]: the prefetching tile-walking form (null: none)
 std::shared_ptr<JitModule> jit_compile(const std::vector<const Sweep*>& sweeps,
                                        const std::vector<const std::vector<RegOp>*>& progs, int dtype,
-                                       std::string* err, const std::vector<int>* minb = nullptr);
+                                       std::string* err, const std::vector<int>* minb = nullptr,
+                                       const std::vector<char>* persistent = nullptr);
 
 // NVRTC step only (no device needed): the CUBIN and kernel names.
 bool jit_cubin(const std::vector<const Sweep*>& sweeps, const std::vector<const std::vector<RegOp>*>& progs,
@@ -47,6 +50,11 @@ bool jit_cubin(const std::vector<const Sweep*>& sweeps, const std::vector<const 
 // tiles (option "jit_minb", default 2: <= 128 registers, two 256-thread CTAs
 // per SM; measured uncut q=30 182 ms vs 261 ms at one CTA per SM)
 extern int g_jit_minb;
+// option "jit_persistent": streaming sweeps as persistent kernels that
+// prefetch the next tile with cp.async (1) or one CTA per tile (0, default:
+// the persistent form needs 128 KB of shared memory = one 8-warp CTA per SM
+// and measured 171 vs 146 ms on the q=30 uncut circuit)
+extern int g_jit_persistent;
 
 // FP64 instructions the specialised code would contain (size guard).
 int64_t jit_cost(const std::vector<RegOp>& prog, int reg_bits);
