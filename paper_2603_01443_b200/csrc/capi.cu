@@ -223,8 +223,8 @@ std::shared_ptr<const Program> build_schedule(int nq, const uint8_t* kinds, cons
   // normalised 2x2s only pay where the 1-coefficients become free (the
   // NVRTC-specialised kernels); the interpreter keeps the plain matrices
   const int norm = g_opt.dense_norm == 2 ? (g_opt.jit != 0 && g_opt.engine == 1 ? 1 : 0) : int(g_opt.dense_norm);
-  const int32_t hdr[11] = {nq, T, L, int32_t(fuse), slots ? 1 : 0, dtype, vb, g_sweep_minb,
-                           int32_t(g_opt.engine), norm, g_reg_bits};
+  const int32_t hdr[13] = {nq, T, L, int32_t(fuse), slots ? 1 : 0, dtype, vb, g_sweep_minb,
+                           int32_t(g_opt.engine), norm, g_reg_bits, g_jit_minb, g_jit_persistent};
   key.append(reinterpret_cast<const char*>(hdr), sizeof(hdr));
   key.append(reinterpret_cast<const char*>(kinds), size_t(n_gates));
   key.append(reinterpret_cast<const char*>(qa), size_t(n_gates) * 8);

@@ -79,3 +79,25 @@ def test_jit_q22_multisweep_u3(jit_on):
     got = cb.simulate(circ).amps
     assert np.abs(got - ref).max() < 1e-10
     assert abs(np.vdot(got, got).real - 1) < 1e-12
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("persistent,minb", [(1, 1), (0, 1), (0, 2)])
+def test_jit_streaming_kernel_forms(jit_on, persistent, minb):
+    """The opt-in persistent prefetching form and both launch-bound settings
+    of the many-tile (streaming) kernels against the oracle."""
+    import paper_2603_01443_b200 as cb
+
+    old = _native.get_option("jit_persistent"), _native.get_option("jit_minb")
+    _native.set_option("jit_persistent", persistent)
+    _native.set_option("jit_minb", minb)
+    try:
+        circ = cb.build_brickwall(cb.BrickwallSpec(23, 5, 2, 2, 3))
+        ref = orc.simulate(23, circ.kinds, circ.qa, circ.qb, circ.params)
+        assert np.abs(cb.simulate(circ).amps - ref).max() < 1e-10
+        stair = cb.build_staircase(cb.BenchmarkSpec(q=22, n=2, blocks=2))
+        ref = orc.simulate(22, stair.kinds, stair.qa, stair.qb)
+        assert np.abs(cb.simulate(stair).amps - ref).max() < 1e-10
+    finally:
+        _native.set_option("jit_persistent", old[0])
+        _native.set_option("jit_minb", old[1])
