@@ -92,10 +92,10 @@ def test_jit_streaming_kernel_forms(jit_on, persistent, minb):
     _native.set_option("jit_persistent", persistent)
     _native.set_option("jit_minb", minb)
     try:
-        circ = cb.build_brickwall(cb.BrickwallSpec(24, 5, 2, 2, 3))
-        ref = orc.simulate(24, circ.kinds, circ.qa, circ.qb, circ.params)
+        circ = cb.build_brickwall(cb.BrickwallSpec(22, 4, 2, 2, 3))
+        ref = orc.simulate(22, circ.kinds, circ.qa, circ.qb, circ.params)
         assert np.abs(cb.simulate(circ).amps - ref).max() < 1e-10
-        stair = cb.build_staircase(cb.BenchmarkSpec(q=22, n=2, blocks=2))
+        stair = cb.build_staircase(cb.BenchmarkSpec(q=22, n=2, blocks=1))
         ref = orc.simulate(22, stair.kinds, stair.qa, stair.qb)
         assert np.abs(cb.simulate(stair).amps - ref).max() < 1e-10
     finally:
