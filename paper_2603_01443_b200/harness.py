@@ -77,6 +77,21 @@ def build(spec) -> Circuit:
     raise ValidationError(f"unknown spec type {type(spec).__name__}")
 
 
+def _cut_once_native(circuit: Circuit, n: int, *, max_qubits: int, deadline: float | None):
+    """The same three stages through the one-call pipeline (cs_cut_run):
+    t_pre = its C++ plan/decompose, t_sub / t_merge = CUDA events around the
+    batched variant sweeps and the merge (the call synchronises)."""
+    from .pipeline import StageTimes, run_cut
+
+    if deadline is not None and time.monotonic() > deadline:
+        raise BudgetExceededError("cut pipeline exceeded its budget before starting")
+    times = StageTimes()
+    merged = run_cut(circuit, n, max_qubits=max_qubits, timers=times)
+    if deadline is not None and time.monotonic() > deadline:
+        raise BudgetExceededError("cut pipeline exceeded its budget")
+    return times.pre, times.sub, times.merge, merged
+
+
 def _cut_once(circuit: Circuit, n: int, *, max_qubits: int, deadline: float | None, batched: bool = True):
     """One timed pass of the cut pipeline: (t_pre, t_sub, t_merge, state)."""
     _sync()
@@ -126,9 +141,16 @@ def _mean_std(values: Sequence[float], skip: int):
 
 def measure(spec, repetitions: int = 10, *, budget: float | None = None,
             max_qubits: int = DEFAULT_MAX_QUBITS, discard_warmup: bool = False,
-            pipelines: tuple[str, ...] = ("cut", "orig")) -> TimingBreakdown:
+            pipelines: tuple[str, ...] = ("cut", "orig"), cut_path: str = "api") -> TimingBreakdown:
     """Measure one configuration: phase-timed cut pipeline plus uncut baseline
-    (same protocol as the reference `measure`, harness.py:154-244)."""
+    (same protocol as the reference `measure`, harness.py:154-244).
+    cut_path "api": the drop-in Python API stage by stage (plan_cut +
+    decompose, simulate per family, merge_input_from + merge), as the
+    reference times itself; "native": the same stages inside one
+    cs_cut_run call (C++ preprocess, event-timed device stages)."""
+    if cut_path not in ("api", "native"):
+        raise ValidationError(f"cut_path must be 'api' or 'native', got {cut_path!r}")
+    cut_once = _cut_once if cut_path == "api" else _cut_once_native
     if repetitions < 1:
         raise ValidationError(f"repetitions must be >= 1, got {repetitions}")
     unknown = set(pipelines) - {"cut", "orig"}
@@ -144,7 +166,7 @@ def measure(spec, repetitions: int = 10, *, budget: float | None = None,
     # (harness.py:95-111)
     if "cut" in pipelines:
         try:
-            _cut_once(circuit, spec.n, max_qubits=max_qubits, deadline=None)
+            cut_once(circuit, spec.n, max_qubits=max_qubits, deadline=None)
         except BudgetExceededError:
             pass
     if "orig" in pipelines and (budget is None or circuit.num_qubits <= 26):
@@ -153,7 +175,7 @@ def measure(spec, repetitions: int = 10, *, budget: float | None = None,
         if "cut" in pipelines and not cut_timeout:
             deadline = time.monotonic() + budget if budget is not None else None
             try:
-                t_pre, t_sub, t_merge, merged = _cut_once(circuit, spec.n, max_qubits=max_qubits,
+                t_pre, t_sub, t_merge, merged = cut_once(circuit, spec.n, max_qubits=max_qubits,
                                                           deadline=deadline)
                 samples["pre"].append(t_pre)
                 samples["sub"].append(t_sub)

@@ -113,7 +113,8 @@ def _mean_breakdown(rows: list[TimingBreakdown]) -> TimingBreakdown:
 def sweep_heatmap(q_values: Iterable[int] | None = None, c_values: Iterable[int] | None = None, n: int = 2,
                   repetitions: int = 10, *, pad_exponent: int | None = None, budget: float | None = None,
                   parallel_points: int = 1, max_qubits: int = DEFAULT_MAX_QUBITS, tag: str | None = None,
-                  family: str = "staircase", depth: int = 10, seeds: Sequence[int] = (0,)) -> SweepResult:
+                  family: str = "staircase", depth: int = 10, seeds: Sequence[int] = (0,),
+                  cut_path: str = "api") -> SweepResult:
     """Relative overhead delta = (t_cut - t_orig) / t_orig on a (q, c_total)
     grid, one `measure` per point (mean over seeds for the brick-wall family)."""
     if q_values is None or c_values is None:
@@ -129,7 +130,7 @@ def sweep_heatmap(q_values: Iterable[int] | None = None, c_values: Iterable[int]
     points = []
     for q, c in grid:
         rows = [measure(_spec(family, q, n, c, pad_exponent=pad_exponent, depth=depth, seed=s), repetitions,
-                        budget=budget, max_qubits=max_qubits)
+                        budget=budget, max_qubits=max_qubits, cut_path=cut_path)
                 for s in (seeds if family == "brickwall" else (0,))]
         points.append(_mean_breakdown(rows))
     if parallel_points > 1:
@@ -138,7 +139,7 @@ def sweep_heatmap(q_values: Iterable[int] | None = None, c_values: Iterable[int]
     meta = {"schema_version": SCHEMA_VERSION, "n": n, "repetitions": repetitions,
             "pad_exponent": pad_exponent, "budget_seconds": budget, "parallel_points": parallel_points,
             "machine_tag": machine_tag(tag), "timestamp": datetime.now(timezone.utc).isoformat(),
-            "family": family, "device": _device_name()}
+            "family": family, "device": _device_name(), "cut_path": cut_path}
     if family == "brickwall":
         meta.update(depth=depth, seeds=list(seeds))
     return SweepResult(points=points, metadata=meta)

@@ -99,3 +99,14 @@ def test_reference_style_code_through_alias():
     finally:
         for k in [k for k in sys.modules if k.startswith("cutbench_gpu_alias")]:
             del sys.modules[k]
+
+
+def test_measure_native_cut_path(sw):
+    from paper_2603_01443_b200 import harness
+    from paper_2603_01443_b200.generators import BrickwallSpec
+
+    row = harness.measure(BrickwallSpec(16, 5, 2, 3, 1), 2, cut_path="native")
+    assert row.status == "ok" and row.t_pre > 0 and row.t_sub > 0 and row.t_merge > 0
+    assert row.t_cut == pytest.approx(row.t_pre + row.t_sub + row.t_merge)
+    res = sw.sweep_heatmap([12], [1, 2], n=2, repetitions=1, family="brickwall", depth=4, cut_path="native")
+    assert res.metadata["cut_path"] == "native" and len(res.points) == 2
