@@ -140,9 +140,9 @@ int single_tile_max_vb(int dtype, int vb) {
 
 int choose_tile_bits(int nq, int64_t n_states, int tile_bits, int dtype) {
   const int vb = choose_vb(n_states);
-  if (nq <= single_tile_max_vb(dtype, vb)) return nq;
   if (tile_bits > 0) return std::min(tile_bits, nq);
   if (g_opt.tile_bits > 0) return std::min(int(g_opt.tile_bits), nq);
+  if (nq <= single_tile_max_vb(dtype, vb)) return nq;
   const int dflt = multi_tile_bits(dtype);
   if (n_states > 1) {
     // small batches of mid-size states (cut variants): shrink the tile until
