@@ -142,7 +142,14 @@ int choose_tile_bits(int nq, int64_t n_states, int tile_bits, int dtype) {
   const int vb = choose_vb(n_states);
   if (tile_bits > 0) return std::min(tile_bits, nq);
   if (g_opt.tile_bits > 0) return std::min(int(g_opt.tile_bits), nq);
-  if (nq <= single_tile_max_vb(dtype, vb)) return nq;
+  // one CTA per state runs the whole circuit in shared memory; for 12-13
+  // qubit states in small batches that leaves most SMs idle and runs long
+  // straight-line code once per CTA, so they take the chip-filling
+  // multi-tile path below (measured, NVRTC kernels, 4 variants per segment:
+  // 12 qubits 63 -> 46 us, 13 qubits 104 -> 49 us; at <= 11 qubits the
+  // single tile stays faster: 10 qubits 26 vs 37 us)
+  const bool small_batch = n_states > 1 && n_states < 148 && nq >= 12;
+  if (nq <= single_tile_max_vb(dtype, vb) && !small_batch) return nq;
   const int dflt = multi_tile_bits(dtype);
   if (n_states > 1) {
     // small batches of mid-size states (cut variants): shrink the tile until
