@@ -1,4 +1,4 @@
-import sys, time
+import sys
 sys.path.insert(0, ".")
 import paper_2603_01443_b200 as cb
 from paper_2603_01443_b200 import _native, harness
