@@ -192,3 +192,24 @@ def test_native_preprocess_full_size_u3(name):
         assert np.array_equal(np.array(seg["slots"]), fam.slots)
     with pytest.raises(UnsupportedTopologyError):
         _native.cut_describe(3, C.Circuit(3, [C.h(0), C.cx(0, 2)]).table, [1, 1, 1])
+
+
+def test_native_preprocess_validation_matches_python():
+    """cs_cut_run's planner rejects what plan_cut_sizes rejects
+    (reference cutting.py:70-136 error contract)."""
+    import os
+
+    from paper_2603_01443_b200 import _native
+
+    if not os.path.exists(_native.LIB_PATH):
+        pytest.skip("libcutsim.so not built")
+    circ = G.build_brickwall(G.BrickwallSpec(8, 3, 2, 2, 0))
+    for sizes in ([8], [4, 5], [4, 4, 0], [0, 8], [-1, 9]):
+        with pytest.raises(ValidationError):
+            K.plan_cut_sizes(circ, tuple(sizes))
+        with pytest.raises(ValidationError):
+            _native.cut_describe(8, circ.table, sizes)
+    d = _native.cut_describe(8, circ.table, [2, 2, 2, 2])
+    plan = K.plan_cut_sizes(circ, (2, 2, 2, 2))
+    assert [c[0] for c in d["cuts"]] == [bg.position for bg in plan.boundary_gates]
+    assert [c[1] for c in d["cuts"]] == [bg.boundary for bg in plan.boundary_gates]
