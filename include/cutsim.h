@@ -155,6 +155,19 @@ int cs_cut_run(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int64_
                int32_t force_bond, int64_t out_begin, int64_t out_end, void* out, void* workspace,
                int64_t workspace_bytes, int32_t dtype, void* stream, void* const* stage_events,
                double* stage_ms);
+/* Host-only: the C++ preprocess as flat tables — replaces plan_cut_sizes +
+ * decompose (cutting.py:70-136, 190-248). cuts[4j..4j+3] = position,
+ * boundary, control segment, target segment of cut j; seg_counts[2s],
+ * [2s+1] = template gates and adjacent cuts of segment s; the segments'
+ * template tables (local qubits; slots[g] = cut bit patching gate g, or -1)
+ * and adjacent-cut ids are concatenated in segment order. needed[0..1] =
+ * total template gates, c_total; when they exceed gate_cap / cut_cap only
+ * `needed` is written. */
+int cs_cut_tables(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int64_t* qb,
+                  const double* params, int64_t n_gates, int32_t n_seg, const int32_t* seg_sizes,
+                  int64_t* cuts, int32_t* seg_counts, uint8_t* out_kinds, int64_t* out_qa,
+                  int64_t* out_qb, double* out_params, int32_t* out_slots, int32_t* out_cut_ids,
+                  int64_t gate_cap, int64_t cut_cap, int64_t* needed);
 /* Host-only: the C++ preprocess result as JSON (cuts and per-segment
  * template tables with their cut slots) — checked against the Python
  * planner and the reference's golden tables in the CPU tests. */

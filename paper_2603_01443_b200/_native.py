@@ -63,6 +63,8 @@ SIGNATURES = {
     "cs_cut_run": (ctypes.c_int, [_i32, _vp, _vp, _vp, _vp, _i64, _i32, _vp, _i32, _i64, _i64, _vp, _vp,
                                   _i64, _i32, _vp, _vp, _vp]),
     "cs_cut_describe_json": (ctypes.c_int, [_i32, _vp, _vp, _vp, _vp, _i64, _i32, _vp, _vp, _i64, _vp]),
+    "cs_cut_tables": (ctypes.c_int, [_i32, _vp, _vp, _vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                     _vp, _vp, _i64, _i64, _vp]),
     "cs_maxabsdiff": (ctypes.c_int, [_vp, _vp, _i64, _i32, _vp, _vp]),
     "cs_maxabs": (ctypes.c_int, [_vp, _i64, _i32, _vp, _vp]),
     "cs_inner": (ctypes.c_int, [_vp, _vp, _i64, _i32, _vp, _vp]),
@@ -206,6 +208,31 @@ def cut_workspace(nq, table, sizes, force_bond=-1, dtype=CS_C128):
     check(load().cs_cut_workspace(nq, ptr(k), ptr(qa), ptr(qb), ptr(prm), len(k), len(sz), ptr(sz), force_bond,
                                   dtype, ptr(ws), ptr(ql), ptr(ct)), "cs_cut_workspace")
     return int(ws[0]), int(ql[0]), int(ct[0])
+
+
+def cut_tables(nq, table, sizes):
+    """Host-only C++ plan + decompose as flat numpy tables:
+    (cuts [c,4], seg_counts [n,2], kinds, qa, qb, params [G,3], slots, cut_ids)."""
+    k, qa, qb, prm = _table_args(table)
+    sz = c_i32(sizes)
+    n = len(sz)
+    n2 = int(np.count_nonzero((k == 5) | (k == 6)))
+    gcap = len(k) + 4 * n2 + 1
+    ccap = n2 + 1
+    cuts = np.empty((ccap, 4), np.int64)
+    counts = np.empty((n, 2), np.int32)
+    ok = np.empty(gcap, np.uint8)
+    oa = np.empty(gcap, np.int64)
+    ob = np.empty(gcap, np.int64)
+    op = np.empty((gcap, 3), np.float64)
+    osl = np.empty(gcap, np.int32)
+    oc = np.empty(2 * ccap, np.int32)
+    need = np.zeros(2, np.int64)
+    check(load().cs_cut_tables(nq, ptr(k), ptr(qa), ptr(qb), ptr(prm), len(k), n, ptr(sz), ptr(cuts), ptr(counts),
+                               ptr(ok), ptr(oa), ptr(ob), ptr(op), ptr(osl), ptr(oc), gcap, ccap, ptr(need)),
+          "cs_cut_tables")
+    g, c = int(need[0]), int(need[1])
+    return cuts[:c], counts, ok[:g], oa[:g], ob[:g], op[:g], osl[:g], oc[:int(counts[:, 1].sum())]
 
 
 def cut_describe(nq, table, sizes) -> dict:

@@ -958,6 +958,51 @@ int cs_cut_describe_json(int32_t nq, const uint8_t* kinds, const int64_t* qa, co
   return CS_OK;
 }
 
+int cs_cut_tables(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int64_t* qb, const double* params,
+                  int64_t n_gates, int32_t n_seg, const int32_t* seg_sizes, int64_t* cuts, int32_t* seg_counts,
+                  uint8_t* out_kinds, int64_t* out_qa, int64_t* out_qb, double* out_params, int32_t* out_slots,
+                  int32_t* out_cut_ids, int64_t gate_cap, int64_t cut_cap, int64_t* needed) {
+  if (nq < 2 || nq > 62 || !seg_sizes || !needed) return fail(CS_ERR_INVALID, "bad qubit count or segment sizes");
+  CutPrep pr;
+  try {
+    pr = cut_prepare(nq, kinds, qa, qb, params, n_gates, n_seg, seg_sizes);
+  } catch (const PlanError& pe) {
+    return fail(pe.code, pe.msg);
+  }
+  int64_t total = 0, adj = 0;
+  for (const SegmentPlan& sp : pr.segs) {
+    total += int64_t(sp.kinds.size());
+    adj += int64_t(sp.cut_ids.size());
+  }
+  needed[0] = total;
+  needed[1] = pr.c_total();
+  if (total > gate_cap || pr.c_total() > cut_cap || adj > 2 * cut_cap) return CS_OK;  // sizes only
+  if (!cuts || !seg_counts || !out_kinds || !out_qa || !out_qb || !out_params || !out_slots || !out_cut_ids)
+    return fail(CS_ERR_INVALID, "null output buffer");
+  for (int j = 0; j < pr.c_total(); ++j) {
+    cuts[4 * j] = pr.cut_pos[size_t(j)];
+    cuts[4 * j + 1] = pr.cut_boundary[size_t(j)];
+    cuts[4 * j + 2] = pr.cut_ctrl[size_t(j)];
+    cuts[4 * j + 3] = pr.cut_tgt[size_t(j)];
+  }
+  int64_t g = 0, c = 0;
+  for (size_t s = 0; s < pr.segs.size(); ++s) {
+    const SegmentPlan& sp = pr.segs[s];
+    const size_t m = sp.kinds.size();
+    seg_counts[2 * s] = int32_t(m);
+    seg_counts[2 * s + 1] = int32_t(sp.cut_ids.size());
+    std::memcpy(out_kinds + g, sp.kinds.data(), m);
+    std::memcpy(out_qa + g, sp.qa.data(), m * sizeof(int64_t));
+    std::memcpy(out_qb + g, sp.qb.data(), m * sizeof(int64_t));
+    std::memcpy(out_params + 3 * g, sp.params.data(), 3 * m * sizeof(double));
+    std::memcpy(out_slots + g, sp.slots.data(), m * sizeof(int32_t));
+    std::memcpy(out_cut_ids + c, sp.cut_ids.data(), sp.cut_ids.size() * sizeof(int32_t));
+    g += int64_t(m);
+    c += int64_t(sp.cut_ids.size());
+  }
+  return CS_OK;
+}
+
 int cs_cut_run(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int64_t* qb, const double* params,
                int64_t n_gates, int32_t n_seg, const int32_t* seg_sizes, int32_t force_bond, int64_t out_begin,
                int64_t out_end, void* out, void* workspace, int64_t workspace_bytes, int32_t dtype, void* stream,

@@ -96,6 +96,9 @@ def plan_cut_sizes(circuit: Circuit, sizes) -> CutPlan:
     if sum(sizes) != circuit.num_qubits:
         raise ValidationError(f"segment sizes {sizes} must sum to q={circuit.num_qubits}")
 
+    nt = _native_tables(circuit, sizes)
+    if nt is not None:
+        return _plan_from_tables(circuit, sizes, nt)
     seg_of = np.repeat(np.arange(n, dtype=np.int64), sizes)
     kinds = circuit.kinds
     two = np.flatnonzero((kinds == KIND_CX) | (kinds == KIND_CZ))
@@ -132,6 +135,61 @@ def plan_cut_sizes(circuit: Circuit, sizes) -> CutPlan:
         c_total=int(counts.sum()),
         c_max=int(c_i.max()),
     )
+
+
+def _native_tables(circuit: Circuit, sizes):
+    """plan + decompose by libcutsim's C++ planner (cs_cut_tables, ~10x the
+    numpy path's speed) or None when the library cannot be loaded (the numpy
+    path below is the same algorithm; tests check the two agree with each
+    other and with the reference's golden tables)."""
+    from . import _native
+
+    try:
+        _native.load()
+    except Exception:  # noqa: BLE001  (no library here: host-only numpy planning)
+        return None
+    return _native.cut_tables(circuit.num_qubits, circuit.table, sizes)
+
+
+def _plan_from_tables(circuit: Circuit, sizes: tuple[int, ...], nt) -> CutPlan:
+    n = len(sizes)
+    cuts = nt[0]
+    boundary_gates = tuple(BoundaryGate(int(p), int(b), int(x), int(y)) for p, b, x, y in cuts.tolist())
+    counts = np.bincount(cuts[:, 1], minlength=n - 1).astype(np.int64)
+    c_i = np.zeros(n, dtype=np.int64)
+    c_i[:-1] += counts
+    c_i[1:] += counts
+    plan = CutPlan(
+        n=n,
+        segment_sizes=sizes,
+        segment_of=tuple(int(v) for v in np.repeat(np.arange(n), sizes)),
+        boundary_gates=boundary_gates,
+        c_per_boundary=tuple(int(v) for v in counts),
+        c_i=tuple(int(v) for v in c_i),
+        c_total=int(counts.sum()),
+        c_max=int(c_i.max()),
+    )
+    # decompose() reuses the tables for the same circuit (identity of its columns)
+    object.__setattr__(plan, "_tables", (circuit.table.kinds, nt))
+    return plan
+
+
+def _families_from_tables(plan: CutPlan, nt) -> list[SegmentFamily]:
+    _cuts, counts, k, a, b, p, sl, cid = nt
+    fams = []
+    g0 = c0 = 0
+    firsts = plan.first_qubit
+    for seg in range(plan.n):
+        m, nc = int(counts[seg, 0]), int(counts[seg, 1])
+        slots = sl[g0:g0 + m]
+        idx = np.flatnonzero(slots >= 0)
+        patch = idx[np.argsort(slots[idx], kind="stable")].astype(np.int64)
+        fams.append(SegmentFamily(seg, firsts[seg], plan.segment_sizes[seg],
+                                  GateTable(k[g0:g0 + m], a[g0:g0 + m], b[g0:g0 + m], p[g0:g0 + m]),
+                                  slots, patch, tuple(int(v) for v in cid[c0:c0 + nc])))
+        g0 += m
+        c0 += nc
+    return fams
 
 
 def count_subcircuits(plan: CutPlan) -> int:
@@ -340,6 +398,15 @@ def decompose(circuit: Circuit, plan: CutPlan) -> SubcircuitSet:
     seg_of = np.asarray(plan.segment_of, dtype=np.int64)
     if seg_of.size != circuit.num_qubits:
         raise ValidationError("plan does not match the circuit's qubit count")
+    cached = getattr(plan, "_tables", None)
+    nt = cached[1] if cached is not None and cached[0] is circuit.table.kinds else None
+    if nt is None and cached is None:
+        nt = _native_tables(circuit, plan.segment_sizes)
+        if nt is not None and [int(v) for v in nt[0][:, 0]] != [bg.position for bg in plan.boundary_gates]:
+            nt = None  # a plan that is not this circuit's own: follow it literally
+    if nt is not None:
+        return SubcircuitSet(plan, _families_from_tables(plan, nt), merge_table_of(plan),
+                             coefficients_of(plan.c_total))
     cut_pos = np.array([bg.position for bg in plan.boundary_gates], dtype=np.int64)
     owner = seg_of[circuit.qa] if circuit.gate_count else np.zeros(0, np.int64)
     owner = owner.copy()

@@ -11,6 +11,22 @@ from paper_2603_01443_b200 import generators as G
 from paper_2603_01443_b200.errors import UnsupportedTopologyError, ValidationError
 
 
+@pytest.fixture(params=["native", "numpy"])
+def planner(request, monkeypatch):
+    """Both planners behind plan_cut/decompose: libcutsim's C++ tables and
+    the numpy restatement (used when the library cannot be loaded)."""
+    if request.param == "numpy":
+        monkeypatch.setattr(K, "_native_tables", lambda circuit, sizes: None)
+    else:
+        import os
+
+        from paper_2603_01443_b200 import _native
+
+        if not os.path.exists(_native.LIB_PATH):
+            pytest.skip("libcutsim.so not built")
+    return request.param
+
+
 def _circuit(golden, key):
     q = int(golden[f"{key}/q"]) if f"{key}/q" in golden else None
     tab = C.GateTable(golden[f"{key}/kinds"], golden[f"{key}/qa"], golden[f"{key}/qb"])
@@ -37,13 +53,13 @@ def _check_tables(golden, key, circ, n):
 
 
 @pytest.mark.parametrize("key", golden_cases())
-def test_plan_and_decompose_match_reference(golden, key):
+def test_plan_and_decompose_match_reference(golden, key, planner):
     circ = _circuit(golden, key)
     _check_tables(golden, key, circ, int(golden[f"{key}/n"]))
 
 
 @pytest.mark.parametrize("key", golden_tables())
-def test_full_size_tables_match_reference(golden, key):
+def test_full_size_tables_match_reference(golden, key, planner):
     q, d, n, c, seed = (int(v) for v in golden[f"{key}/spec"])
     circ = G.build_brickwall(G.BrickwallSpec(q, d, n, c, seed, one_qubit="clifford_t"))
     assert circ.gate_count == int(golden[f"{key}/G"])
@@ -67,7 +83,7 @@ def test_generator_matches_oracle_restatement(q, d, n, c, seed, shadow):
     assert np.array_equal(circ.params, p)
 
 
-def test_variant_tables_equal_oracle_variants():
+def test_variant_tables_equal_oracle_variants(planner):
     k, a, b, p = orc.brickwall(9, 4, 3, 4, 1)
     circ = C.Circuit.from_table(9, C.GateTable(k, a, b, p))
     plan = K.plan_cut(circ, 3)
@@ -91,7 +107,7 @@ def test_cut_distribution():
     assert G.cut_distribution(2, 6) == [6]
 
 
-def test_reference_error_contract():
+def test_reference_error_contract(planner):
     # tests/test_cutting.py:58-66, 75-83 of the reference
     circ = C.build_staircase(C.BenchmarkSpec(q=6, n=2, blocks=1))
     with pytest.raises(ValidationError):
@@ -114,7 +130,7 @@ def test_coefficients_exact():
         assert np.allclose(np.abs(K.coefficients_of(c)), 2.0 ** (-c / 2), rtol=1e-12)
 
 
-def test_json_shape_and_lazy_circuits():
+def test_json_shape_and_lazy_circuits(planner):
     circ = C.build_staircase(C.BenchmarkSpec(q=4, n=2, blocks=1))
     subs = K.decompose(circ, K.plan_cut(circ, 2))
     data = subs.to_json_dict()
@@ -150,10 +166,11 @@ def test_staircase_and_padded_generators_match_oracle():
 
 
 @pytest.mark.parametrize("key", golden_cases())
-def test_native_preprocess_matches_python_and_reference(golden, key):
-    """cs_cut_run's C++ preprocess == the Python planner (pinned to the reference)."""
+def test_native_preprocess_matches_python_and_reference(golden, key, monkeypatch):
+    """cs_cut_run's C++ preprocess == the numpy planner (pinned to the reference)."""
     import os
 
+    monkeypatch.setattr(K, "_native_tables", lambda circuit, sizes: None)
     from paper_2603_01443_b200 import _native
 
     if not os.path.exists(_native.LIB_PATH):
@@ -175,9 +192,10 @@ def test_native_preprocess_matches_python_and_reference(golden, key):
 
 
 @pytest.mark.parametrize("name", list(G.BASELINE_CONFIGS))
-def test_native_preprocess_full_size_u3(name):
+def test_native_preprocess_full_size_u3(name, monkeypatch):
     import os
 
+    monkeypatch.setattr(K, "_native_tables", lambda circuit, sizes: None)
     from paper_2603_01443_b200 import _native
 
     if not os.path.exists(_native.LIB_PATH):
@@ -194,11 +212,12 @@ def test_native_preprocess_full_size_u3(name):
         _native.cut_describe(3, C.Circuit(3, [C.h(0), C.cx(0, 2)]).table, [1, 1, 1])
 
 
-def test_native_preprocess_validation_matches_python():
+def test_native_preprocess_validation_matches_python(monkeypatch):
     """cs_cut_run's planner rejects what plan_cut_sizes rejects
     (reference cutting.py:70-136 error contract)."""
     import os
 
+    monkeypatch.setattr(K, "_native_tables", lambda circuit, sizes: None)
     from paper_2603_01443_b200 import _native
 
     if not os.path.exists(_native.LIB_PATH):
