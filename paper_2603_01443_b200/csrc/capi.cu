@@ -279,7 +279,7 @@ int sm_count() {
 // merge_dmma = 2: the three-GEMM (3M) tensor-core kernel where it is
 // instantiated (K = 8, 16, 32); K = 64 keeps the four-GEMM kernel
 bool dmma3_eligible(int K, int dtype, int64_t lo_len) {
-  return g_opt.merge_dmma == 2 && dtype == CS_C128 && (K == 8 || K == 16 || K == 32) &&
+  return g_opt.merge_dmma == 2 && dtype == CS_C128 && (K == 8 || K == 16 || K == 32 || K == 64) &&
          lo_len >= merge_dmma3_cols_per_warp(K);
 }
 
@@ -297,8 +297,10 @@ int merge_launch_one(int S, int Kc, const int32_t* hidx, const int32_t* lidx, co
     // complex columns; a CTA spans >= 128 columns so row staging is amortised
     const int64_t cw = m3 ? merge_dmma3_cols_per_warp(Kc) : merge_dmma_cols_per_warp(Kc);
     const int64_t ncg = std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(8, 256 / cw), lo_len / cw));
-    const int warps3 = int(g_opt.merge_dmma3_warps);
-    const int64_t smem_budget = m3 ? g_opt.merge_smem_kb * 1024 * warps3 / 8 : g_opt.merge_smem_kb * 1024;
+    const int warps3 = Kc == 64 ? 8 : int(g_opt.merge_dmma3_warps);
+    // K = 64 (3M) runs one CTA per SM: twice the staging budget
+    const int64_t smem_budget = m3 ? g_opt.merge_smem_kb * 1024 * warps3 / 8 * (Kc == 64 ? 2 : 1)
+                                   : g_opt.merge_smem_kb * 1024;
     const int64_t C = cw * ncg;
     const int64_t nrows = row_end - row_begin;
     const int RS = m3 ? 3 * Kc + 4 : 2 * Kc + 4;

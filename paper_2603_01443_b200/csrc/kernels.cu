@@ -817,8 +817,8 @@ __global__ void __launch_bounds__(256, 2) merge_dmma_kernel(const __grid_constan
 // Rounding: |error| <= ~K eps (|br|+|bi|)(|ar|+|ai|) per output, far inside
 // the 1e-10 parity bound.
 // ---------------------------------------------------------------------------
-template <int KT, int NT, int RB, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) merge_dmma3_kernel(const __grid_constant__ MergeParams p) {
+template <int KT, int NT, int RB, int WARPS, int MINB>
+__global__ void __launch_bounds__(WARPS * 32, MINB) merge_dmma3_kernel(const __grid_constant__ MergeParams p) {
   constexpr int KS = KT / 4;       // mma k-steps per GEMM
   constexpr int RS = 3 * KT + 4;   // smem row stride (doubles)
   constexpr int COLS_W = 8 * NT;   // complex columns per warp
@@ -939,22 +939,23 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) merge_dmma3_kernel(con
   }
 }
 
-template <int KT, int NT, int RB, int WARPS>
+template <int KT, int NT, int RB, int WARPS, int MINB = 16 / WARPS>
 static cudaError_t launch_dmma3_kt(const MergeParams& p, dim3 grid, size_t smem, cudaStream_t stream) {
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(merge_dmma3_kernel<KT, NT, RB, WARPS>,
+    cudaError_t e = cudaFuncSetAttribute(merge_dmma3_kernel<KT, NT, RB, WARPS, MINB>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     configured = smem;
   }
-  merge_dmma3_kernel<KT, NT, RB, WARPS><<<grid, WARPS * 32, smem, stream>>>(p);
+  merge_dmma3_kernel<KT, NT, RB, WARPS, MINB><<<grid, WARPS * 32, smem, stream>>>(p);
   return cudaGetLastError();
 }
 
 // 3M kernel geometry per K: complex columns per warp and row blocks per pass
+// (K = 64 keeps 48 B-operand doubles per thread in registers: one CTA per SM)
 int merge_dmma3_cols_per_warp(int K) { return K <= 16 ? 16 : 8; }
-int merge_dmma3_row_blocks(int K) { return K <= 16 ? 2 : 4; }
+int merge_dmma3_row_blocks(int K) { return K <= 16 ? 2 : (K == 32 ? 4 : 2); }
 
 // warps = 8 (2 CTAs per SM) or 4 (4 CTAs per SM: staging of one CTA overlaps
 // three others' math)
@@ -972,6 +973,7 @@ cudaError_t launch_merge_dmma3(const MergeParams& p, int K, int warps, dim3 grid
     case 8: return launch_dmma3_kt<8, 2, 2, 8>(p, grid, smem, stream);
     case 16: return launch_dmma3_kt<16, 2, 2, 8>(p, grid, smem, stream);
     case 32: return launch_dmma3_kt<32, 1, 4, 8>(p, grid, smem, stream);
+    case 64: return launch_dmma3_kt<64, 1, 2, 8, 1>(p, grid, smem, stream);
     default: return cudaErrorInvalidValue;
   }
 }
