@@ -54,7 +54,7 @@ int cs_device_count(int32_t* count);
  * commuted through diagonal gates), "threads" (0 = auto), "merge_streaming" (evict-first
  * output stores, default 1), "merge_iters" (0 = auto), "merge_dmma" (FP64
  * tensor-core merge for K = 8..64: 0 off, 1 four real GEMMs per complex
- * product, 2 three (3M) for K <= 32; default 2), "engine" (1 register-tile
+ * product, 2 three (3M); default 2), "engine" (1 register-tile
  * sweep kernel, 0 shared-memory tile kernel), "jit" (0 never, 1 from a
  * program's second use, 2 always: NVRTC-specialised sweep kernels),
  * "jit_max_cost", "vb", "sweep_minb", "merge_smem_kb", "merge_dmma3_warps", "jit_minb", "dense_norm" (normalised 2x2s:

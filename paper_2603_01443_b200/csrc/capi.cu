@@ -63,7 +63,7 @@ struct Options {
   int64_t vb = 0;  // states per CTA in a variant batch (0 = auto)
   int64_t merge_dmma3_warps = 8;  // warps per CTA of the 3M kernel (8: 2 CTAs/SM, 4: 4 CTAs/SM)
   int64_t merge_smem_kb = 96;  // staged-row budget per CTA of the tensor-core merge
-  int64_t merge_dmma = 2;  // FP64 tensor-core merge: 2 = three-GEMM (3M) for K <= 32, four-GEMM K = 64
+  int64_t merge_dmma = 2;  // FP64 tensor-core merge: 1 = four real GEMMs, 2 = three (3M)
   int64_t engine = 1;      // 1: register-tile kernel (rsweep), 0: shared-memory tile kernel (sweep)
   int64_t jit = 0;         // 0 never, 1 from a program's 2nd use, 2 always: NVRTC-specialised sweeps (opt-in: compile ~1-7 s)
   int64_t jit_max_cost = 40000;  // FP64 instructions per specialised launch (code-size guard)
