@@ -96,7 +96,10 @@ _WORKSPACE: dict = {}
 
 
 def cut_workspace_tensor(nbytes: int):
-    """The per-device workspace of cs_cut_run (grown on demand, reused)."""
+    """The per-device workspace of cs_cut_run (grown on demand, reused). It is
+    shared by every run_cut call on the device without an explicit
+    ``workspace=``, which is safe for calls ordered on one stream; callers
+    running cut pipelines concurrently on several streams pass their own."""
     t = _device.torch()
     dev = t.cuda.current_device()
     ws = _WORKSPACE.get(dev)
