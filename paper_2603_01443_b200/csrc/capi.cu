@@ -180,8 +180,17 @@ struct Program {
   int64_t n_states = 1;  // states per launch the program was scheduled for
 };
 
+// content-keyed program cache with least-recently-used eviction (a clear-all
+// policy recompiled the NVRTC kernels of a program between a sweep point's
+// warm-up and its timed repetitions once 256 programs had accumulated)
+struct CacheEntry {
+  std::shared_ptr<const Program> prog;
+  uint64_t last_use = 0;
+};
+constexpr size_t kProgramCacheCap = 512;
 std::mutex g_cache_mu;
-std::unordered_map<std::string, std::shared_ptr<const Program>> g_cache;
+std::unordered_map<std::string, CacheEntry> g_cache;
+uint64_t g_cache_clock = 0;
 
 // Split each sweep's entries into launches that fit the kernel parameter
 // block (never splitting a slotted pair); the register kernel's chunks are
@@ -241,7 +250,10 @@ std::shared_ptr<const Program> build_schedule(int nq, const uint8_t* kinds, cons
   {
     std::lock_guard<std::mutex> lk(g_cache_mu);
     auto it = g_cache.find(key);
-    if (it != g_cache.end()) return it->second;
+    if (it != g_cache.end()) {
+      it->second.last_use = ++g_cache_clock;
+      return it->second.prog;
+    }
   }
   std::vector<LOp> ops = lower_gates(nq, kinds, qa, qb, params, slots, n_gates, fuse == 2);
   if (fuse == 2) ops = fuse_ops(commute_phases(ops), true);
@@ -256,8 +268,13 @@ std::shared_ptr<const Program> build_schedule(int nq, const uint8_t* kinds, cons
   build_launches(*built);
   std::shared_ptr<const Program> prog = built;
   std::lock_guard<std::mutex> lk(g_cache_mu);
-  if (g_cache.size() >= 256) g_cache.clear();
-  g_cache.emplace(std::move(key), prog);
+  if (g_cache.size() >= kProgramCacheCap) {
+    auto lru = g_cache.begin();
+    for (auto it = g_cache.begin(); it != g_cache.end(); ++it)
+      if (it->second.last_use < lru->second.last_use) lru = it;
+    g_cache.erase(lru);
+  }
+  g_cache[std::move(key)] = CacheEntry{prog, ++g_cache_clock};
   return prog;
 }
 
