@@ -1,3 +1,5 @@
+"""Per-repetition merge/sub stage samples of harness.measure at small q
+(diagnostic of host-side noise):  python tools/diag_measure.py [JIT]"""
 import sys
 sys.path.insert(0, ".")
 import paper_2603_01443_b200 as cb
