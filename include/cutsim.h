@@ -155,6 +155,20 @@ int cs_cut_run(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int64_
                int32_t force_bond, int64_t out_begin, int64_t out_end, void* out, void* workspace,
                int64_t workspace_bytes, int32_t dtype, void* stream, void* const* stage_events,
                double* stage_ms);
+/* The same pipeline delivering the full 2^nq state into HOST memory
+ * (host_out: 2^nq amplitudes, ideally pinned) — the reference API's contract
+ * of a host-resident result. The merge runs in `chunks` row ranges into two
+ * device staging buffers (part of `workspace`, size from
+ * cs_cut_host_workspace) and each chunk's device-to-host copy overlaps the
+ * next chunk's merge; returns when host_out is complete. stage_ms
+ * (nullable): host preprocess, variant stage, merge + copies. */
+int cs_cut_host_workspace(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int64_t* qb,
+                          const double* params, int64_t n_gates, int32_t n_seg, const int32_t* seg_sizes,
+                          int32_t chunks, int32_t dtype, int64_t* workspace_bytes);
+int cs_cut_run_to_host(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int64_t* qb,
+                       const double* params, int64_t n_gates, int32_t n_seg, const int32_t* seg_sizes,
+                       int32_t chunks, void* host_out, void* workspace, int64_t workspace_bytes,
+                       int32_t dtype, void* stream, double* stage_ms);
 /* Host-only: the C++ preprocess as flat tables — replaces plan_cut_sizes +
  * decompose (cutting.py:70-136, 190-248). cuts[4j..4j+3] = position,
  * boundary, control segment, target segment of cut j; seg_counts[2s],

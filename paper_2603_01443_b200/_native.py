@@ -62,6 +62,9 @@ SIGNATURES = {
                                         _vp]),
     "cs_cut_run": (ctypes.c_int, [_i32, _vp, _vp, _vp, _vp, _i64, _i32, _vp, _i32, _i64, _i64, _vp, _vp,
                                   _i64, _i32, _vp, _vp, _vp]),
+    "cs_cut_host_workspace": (ctypes.c_int, [_i32, _vp, _vp, _vp, _vp, _i64, _i32, _vp, _i32, _i32, _vp]),
+    "cs_cut_run_to_host": (ctypes.c_int, [_i32, _vp, _vp, _vp, _vp, _i64, _i32, _vp, _i32, _vp, _vp, _i64, _i32,
+                                          _vp, _vp]),
     "cs_cut_describe_json": (ctypes.c_int, [_i32, _vp, _vp, _vp, _vp, _i64, _i32, _vp, _vp, _i64, _vp]),
     "cs_cut_tables": (ctypes.c_int, [_i32, _vp, _vp, _vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                      _vp, _vp, _i64, _i64, _vp]),

@@ -1022,6 +1022,167 @@ int cs_cut_tables(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int
   return CS_OK;
 }
 
+namespace {
+
+// Programs of every segment's variant family, NVRTC-compiled if enabled
+// (host side of the variant stage; compile before any timing).
+int cut_programs(const CutJob& job, int dtype, std::vector<std::shared_ptr<const Program>>* progs) {
+  try {
+    for (const SegmentPlan& sp : job.prep.segs)
+      progs->push_back(build_schedule(sp.nq, sp.kinds.data(), sp.qa.data(), sp.qb.data(), sp.params.data(),
+                                      sp.slots.data(), int64_t(sp.kinds.size()),
+                                      int64_t(1) << sp.cut_ids.size(), 0, dtype));
+  } catch (const PlanError& pe) {
+    return fail(pe.code, pe.msg);
+  }
+  for (const auto& pg : *progs) program_jit(*pg, dtype);
+  return CS_OK;
+}
+
+// Batched subcircuit simulation: every segment's variant family at once,
+// segments on side streams forked from / joined into `st`.
+int cut_segments(const CutJob& job, const std::vector<std::shared_ptr<const Program>>& progs, void* workspace,
+                 int dtype, cudaStream_t st, std::vector<const void*>* seg_states) {
+  const CutPrep& pr = job.prep;
+  cudaEvent_t fork = nullptr;
+  if (pr.n > 1) {
+    cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
+    cudaEventRecord(fork, st);
+  }
+  int rc = CS_OK;
+  for (size_t s = 0; s < pr.segs.size(); ++s) {
+    const SegmentPlan& sp = pr.segs[s];
+    void* states = static_cast<char*>(workspace) + job.seg_off[s];
+    seg_states->push_back(states);
+    const int64_t nv = int64_t(1) << sp.cut_ids.size();
+    cudaStream_t ss = pr.n > 1 ? side_stream(int(s % 4)) : st;
+    if (fork) cudaStreamWaitEvent(ss, fork, 0);
+    rc = run_program(*progs[s], sp.nq, states, nv, int64_t(1) << sp.nq, 0, 1, dtype, ss);
+    if (rc != CS_OK) break;
+    if (ss != st) {
+      cudaEvent_t done = nullptr;
+      cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
+      cudaEventRecord(done, ss);
+      cudaStreamWaitEvent(st, done, 0);
+      cudaEventDestroy(done);
+    }
+  }
+  if (fork) cudaEventDestroy(fork);
+  return rc;
+}
+
+int64_t host_chunk_amps(const CutJob& job, int nq, int chunks) {
+  const int64_t unit = int64_t(1) << job.plan.q_low;
+  const int64_t total = int64_t(1) << nq;
+  const int64_t c = std::max<int64_t>(1, chunks);
+  return std::max(unit, (total / c) / unit * unit);
+}
+
+cudaStream_t copy_stream() {
+  static std::mutex mu;
+  static std::vector<cudaStream_t> per_device;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (int(per_device.size()) <= dev) per_device.resize(size_t(dev) + 1, nullptr);
+  if (!per_device[size_t(dev)]) cudaStreamCreateWithFlags(&per_device[size_t(dev)], cudaStreamNonBlocking);
+  return per_device[size_t(dev)];
+}
+
+}  // namespace
+
+int cs_cut_host_workspace(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int64_t* qb,
+                          const double* params, int64_t n_gates, int32_t n_seg, const int32_t* seg_sizes,
+                          int32_t chunks, int32_t dtype, int64_t* workspace_bytes) {
+  if (!valid_dtype(dtype)) return fail(CS_ERR_INVALID, "dtype must be CS_C128 or CS_C64");
+  if (nq < 2 || nq > 62 || !seg_sizes || !workspace_bytes) return fail(CS_ERR_INVALID, "bad arguments");
+  CutJob job;
+  int rc = CS_OK;
+  if (!cut_job(nq, kinds, qa, qb, params, n_gates, n_seg, seg_sizes, -1, dtype, &job, &rc)) return rc;
+  const int64_t chunk_bytes = host_chunk_amps(job, nq, chunks) * int64_t(elem_bytes(dtype));
+  *workspace_bytes = job.total_bytes + 2 * ((chunk_bytes + 255) / 256 * 256);
+  return CS_OK;
+}
+
+int cs_cut_run_to_host(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int64_t* qb, const double* params,
+                       int64_t n_gates, int32_t n_seg, const int32_t* seg_sizes, int32_t chunks, void* host_out,
+                       void* workspace, int64_t workspace_bytes, int32_t dtype, void* stream, double* stage_ms) {
+  if (!valid_dtype(dtype)) return fail(CS_ERR_INVALID, "dtype must be CS_C128 or CS_C64");
+  if (nq < 2 || nq > 62 || !seg_sizes) return fail(CS_ERR_INVALID, "bad qubit count or segment sizes");
+  if (!host_out) return fail(CS_ERR_INVALID, "null host output pointer");
+  const auto t0 = std::chrono::steady_clock::now();
+  CutJob job;
+  int rc = CS_OK;
+  if (!cut_job(nq, kinds, qa, qb, params, n_gates, n_seg, seg_sizes, -1, dtype, &job, &rc)) return rc;
+  const size_t eb = elem_bytes(dtype);
+  const int64_t step = host_chunk_amps(job, nq, chunks);
+  const int64_t buf_bytes = (step * int64_t(eb) + 255) / 256 * 256;
+  if (!workspace || workspace_bytes < job.total_bytes + 2 * buf_bytes)
+    return fail(CS_ERR_INVALID, "workspace too small (query cs_cut_host_workspace)");
+  std::vector<std::shared_ptr<const Program>> progs;
+  rc = cut_programs(job, dtype, &progs);
+  if (rc != CS_OK) return rc;
+  const double t_pre = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  cudaStream_t st = as_stream(stream);
+  cudaStream_t cp = copy_stream();
+  cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
+  if (stage_ms) {
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventCreate(&e2);
+    cudaEventRecord(e0, st);
+  }
+  std::vector<const void*> seg_states;
+  rc = cut_segments(job, progs, workspace, dtype, st, &seg_states);
+  if (rc != CS_OK) return rc;
+  if (e1) cudaEventRecord(e1, st);
+  // chunked merge into two device buffers; each chunk's device-to-host copy
+  // runs on the copy stream while the next chunk is merged (PCIe-bound)
+  char* bufs[2] = {static_cast<char*>(workspace) + job.total_bytes,
+                   static_cast<char*>(workspace) + job.total_bytes + buf_bytes};
+  cudaEvent_t ready[2], copied[2] = {nullptr, nullptr};
+  for (auto& e : ready) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  const int64_t total = int64_t(1) << nq;
+  int i = 0;
+  for (int64_t b = 0; b < total && rc == CS_OK; b += step, ++i) {
+    const int64_t e = std::min(total, b + step);
+    const int k = i & 1;
+    if (copied[k]) cudaStreamWaitEvent(st, copied[k], 0);  // buffer k free again
+    rc = run_chain(job.plan, job.prep.n, seg_states.data(), b, e, bufs[k],
+                   static_cast<char*>(workspace) + job.chain_off, job.total_bytes - job.chain_off, dtype, st);
+    if (rc != CS_OK) break;
+    cudaEventRecord(ready[k], st);
+    cudaStreamWaitEvent(cp, ready[k], 0);
+    cudaError_t ce = cudaMemcpyAsync(static_cast<char*>(host_out) + size_t(b) * eb, bufs[k],
+                                     size_t(e - b) * eb, cudaMemcpyDeviceToHost, cp);
+    if (ce != cudaSuccess) rc = cuda_fail(ce, "cudaMemcpyAsync(device to host)");
+    if (!copied[k]) cudaEventCreateWithFlags(&copied[k], cudaEventDisableTiming);
+    cudaEventRecord(copied[k], cp);
+  }
+  // the host state is complete when this returns (the reference returns host memory)
+  cudaError_t se = cudaStreamSynchronize(cp);
+  if (e2) {
+    cudaEventRecord(e2, st);
+    cudaEventSynchronize(e2);
+    float a = 0, m = 0;
+    cudaEventElapsedTime(&a, e0, e1);
+    cudaEventElapsedTime(&m, e1, e2);
+    stage_ms[0] = t_pre;
+    stage_ms[1] = a;
+    stage_ms[2] = m;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaEventDestroy(e2);
+  }
+  for (auto& e : ready) cudaEventDestroy(e);
+  for (auto& e : copied)
+    if (e) cudaEventDestroy(e);
+  if (rc != CS_OK) return rc;
+  if (se != cudaSuccess) return cuda_fail(se, "device-to-host copy");
+  cudaError_t le = cudaGetLastError();
+  return le == cudaSuccess ? CS_OK : cuda_fail(le, "cut pipeline to host");
+}
+
 int cs_cut_run(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int64_t* qb, const double* params,
                int64_t n_gates, int32_t n_seg, const int32_t* seg_sizes, int32_t force_bond, int64_t out_begin,
                int64_t out_end, void* out, void* workspace, int64_t workspace_bytes, int32_t dtype, void* stream,
@@ -1037,15 +1198,8 @@ int cs_cut_run(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int64_
     return fail(CS_ERR_INVALID, "cut workspace too small (query cs_cut_workspace)");
   const CutPrep& pr = job.prep;
   std::vector<std::shared_ptr<const Program>> progs;
-  try {
-    for (const SegmentPlan& sp : pr.segs)
-      progs.push_back(build_schedule(sp.nq, sp.kinds.data(), sp.qa.data(), sp.qb.data(), sp.params.data(),
-                                     sp.slots.data(), int64_t(sp.kinds.size()),
-                                     int64_t(1) << sp.cut_ids.size(), 0, dtype));
-  } catch (const PlanError& pe) {
-    return fail(pe.code, pe.msg);
-  }
-  for (const auto& pg : progs) program_jit(*pg, dtype);  // compile before any timing
+  rc = cut_programs(job, dtype, &progs);  // compile before any timing
+  if (rc != CS_OK) return rc;
   const double t_pre = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   cudaStream_t st = as_stream(stream);
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
@@ -1055,35 +1209,9 @@ int cs_cut_run(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int64_
     for (auto& e : ev) cudaEventCreate(&e);
   }
   if (ev[0]) cudaEventRecord(ev[0], st);
-  // batched subcircuit simulation: every segment's variant family at once,
-  // segments on side streams forked from / joined into the caller's stream
   std::vector<const void*> seg_states;
-  cudaEvent_t fork = nullptr;
-  if (pr.n > 1) {
-    cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
-    cudaEventRecord(fork, st);
-  }
-  for (size_t s = 0; s < pr.segs.size(); ++s) {
-    const SegmentPlan& sp = pr.segs[s];
-    void* states = static_cast<char*>(workspace) + job.seg_off[s];
-    seg_states.push_back(states);
-    const int64_t nv = int64_t(1) << sp.cut_ids.size();
-    cudaStream_t ss = pr.n > 1 ? side_stream(int(s % 4)) : st;
-    if (fork) cudaStreamWaitEvent(ss, fork, 0);
-    rc = run_program(*progs[s], sp.nq, states, nv, int64_t(1) << sp.nq, 0, 1, dtype, ss);
-    if (rc != CS_OK) {
-      if (fork) cudaEventDestroy(fork);
-      return rc;
-    }
-    if (ss != st) {
-      cudaEvent_t done = nullptr;
-      cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
-      cudaEventRecord(done, ss);
-      cudaStreamWaitEvent(st, done, 0);
-      cudaEventDestroy(done);
-    }
-  }
-  if (fork) cudaEventDestroy(fork);
+  rc = cut_segments(job, progs, workspace, dtype, st, &seg_states);
+  if (rc != CS_OK) return rc;
   if (ev[1]) cudaEventRecord(ev[1], st);
   rc = run_chain(job.plan, pr.n, seg_states.data(), out_begin, out_end, out,
                  static_cast<char*>(workspace) + job.chain_off, job.total_bytes - job.chain_off, dtype, st);

@@ -12,7 +12,6 @@ kernel writing the state (or this GPU's shard of it) once.
 from __future__ import annotations
 
 import ctypes
-import time
 from dataclasses import dataclass
 
 import numpy as np
@@ -168,55 +167,67 @@ def cut_simulate(circuit: Circuit, n: int, **kw) -> StateVec:
 
 
 def run_cut_to_host(circuit: Circuit, n: int, host_out, *, dtype=np.complex128, chunks: int = 8,
-                    buffers=None, workspace=None, timers: StageTimes | None = None,
-                    max_qubits: int = DEFAULT_MAX_QUBITS):
-    """Cut-simulate and deliver the full state into ``host_out`` (a pinned
-    host tensor of 2^q amplitudes), the reference API's contract of returning
-    host memory. The merge is issued in row chunks into two device buffers
-    and each chunk's device->host copy runs on a second stream while the next
-    chunk is merged, so the copy (PCIe-bound) hides the merge."""
+                    workspace=None, timers: StageTimes | None = None, max_qubits: int = DEFAULT_MAX_QUBITS,
+                    sizes=None):
+    """Cut-simulate and deliver the full state into ``host_out`` (a host
+    tensor or array of 2^q amplitudes, ideally pinned): the reference API's
+    contract of returning host memory. One native call (cs_cut_run_to_host):
+    the merge runs in ``chunks`` row ranges into two device staging buffers
+    and each chunk's device->host copy overlaps the next chunk's merge
+    (PCIe-bound); returns when ``host_out`` is complete."""
+    from . import _native
+    from .errors import ValidationError
+
     q = circuit.num_qubits
     check_capacity(q, max_qubits)
     t = _device.require_cuda()
-    compute = t.cuda.current_stream()
-    copy = _copy_stream()
-    total = 1 << q
-    if host_out.numel() != total:
-        raise ValueError("host_out must hold 2^q amplitudes")
-    t0 = time.perf_counter()
-    prep = preprocess(circuit, n)
+    if sizes is None:
+        if n < 2 or q % n:
+            raise ValidationError(f"q must be divisible by n >= 2: q={q}, n={n}")
+        sizes = (q // n,) * n
+    if isinstance(host_out, np.ndarray):
+        if host_out.size != 1 << q or host_out.dtype != np.dtype(dtype) or not host_out.flags.c_contiguous:
+            raise ValidationError("host_out must be a contiguous array of 2^q amplitudes of the dtype")
+        host_ptr = host_out.ctypes.data
+    else:
+        if host_out.numel() != 1 << q or host_out.device.type != "cpu" or not host_out.is_contiguous():
+            raise ValidationError("host_out must be a contiguous host tensor of 2^q amplitudes")
+        host_ptr = host_out.data_ptr()
+    k, qa, qb, prm = _native._table_args(circuit.table)
+    sz = _native.c_i32(sizes)
+    code = _device.code_of(dtype)
+    need = np.zeros(1, np.int64)
+    _native.check(_native.load().cs_cut_host_workspace(q, _native.ptr(k), _native.ptr(qa), _native.ptr(qb),
+                                                       _native.ptr(prm), len(k), len(sz), _native.ptr(sz), chunks,
+                                                       code, _native.ptr(need)), "cs_cut_host_workspace")
+    if workspace is None or workspace.numel() < int(need[0]):
+        workspace = cut_workspace_tensor(int(need[0]))
+    stage = np.zeros(3) if timers is not None else None
+    _native.check(_native.load().cs_cut_run_to_host(q, _native.ptr(k), _native.ptr(qa), _native.ptr(qb),
+                                                    _native.ptr(prm), len(k), len(sz), _native.ptr(sz), chunks,
+                                                    host_ptr, workspace.data_ptr(), workspace.numel(), code,
+                                                    _device.stream_ptr(), _native.ptr(stage)),
+                  "cs_cut_run_to_host")
     if timers is not None:
-        timers.pre = time.perf_counter() - t0
-    batches = simulate_segments(prep, dtype=dtype, max_qubits=max_qubits)
-    _ws, _bond, qlow = prep.chain.plan(dtype)
-    unit = 1 << qlow
-    step = max(unit, (total // max(1, chunks)) // unit * unit)
-    if buffers is None:
-        buffers = [_device.empty_shape((step,), dtype) for _ in range(2)]
-    done = [None, None]
-    for i, begin in enumerate(range(0, total, step)):
-        end = min(total, begin + step)
-        b = i % 2
-        if done[b] is not None:
-            compute.wait_event(done[b])
-        buf = buffers[b][: end - begin]
-        merge_chain_device(prep.chain, batches, dtype=dtype, out=buf, out_range=(begin, end),
-                           workspace=workspace)
-        ready = t.cuda.Event()
-        ready.record(compute)
-        copy.wait_event(ready)
-        with t.cuda.stream(copy):
-            host_out[begin:end].copy_(buf, non_blocking=True)
-            ev = t.cuda.Event()
-            ev.record(copy)
-        done[b] = ev
-    for ev in done:
-        if ev is not None:
-            ev.synchronize()
+        timers.pre, timers.sub, timers.merge = (float(v) / 1e3 for v in stage)
+    del t
     return host_out
 
 
-_COPY_STREAMS = {}
+def host_workspace_bytes(circuit: Circuit, n: int, *, chunks: int = 8, dtype=np.complex128) -> int:
+    """Device workspace run_cut_to_host needs (variant states, merge
+    intermediates and two staging buffers of 2^q / chunks amplitudes)."""
+    from . import _native
+
+    q = circuit.num_qubits
+    k, qa, qb, prm = _native._table_args(circuit.table)
+    sz = _native.c_i32((q // n,) * n)
+    need = np.zeros(1, np.int64)
+    _native.check(_native.load().cs_cut_host_workspace(q, _native.ptr(k), _native.ptr(qa), _native.ptr(qb),
+                                                       _native.ptr(prm), len(k), len(sz), _native.ptr(sz), chunks,
+                                                       _device.code_of(dtype), _native.ptr(need)),
+                  "cs_cut_host_workspace")
+    return int(need[0])
 
 
 def _copy_stream():

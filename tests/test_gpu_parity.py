@@ -348,16 +348,32 @@ def test_distributed_uncut_emulated_on_one_gpu(cb, world, q, d):
 
 
 def test_run_cut_to_host_matches_device_state(cb):
-    """The e2e path of bench.py: chunked merge overlapped with D2H into pinned memory."""
+    """The e2e path of bench.py (cs_cut_run_to_host: chunked merge overlapped
+    with D2H into host memory) for pinned tensors, numpy arrays, ragged chunk
+    counts, n = 3 and complex64."""
     import torch
 
-    from paper_2603_01443_b200.pipeline import run_cut_to_host
+    from paper_2603_01443_b200.pipeline import StageTimes, run_cut_to_host
 
     circ = cb.build_brickwall(cb.BrickwallSpec(20, 6, 2, 2, 3))
-    host = torch.empty(1 << 20, dtype=torch.complex128, pin_memory=True)
-    run_cut_to_host(circ, 2, host, chunks=8)
     dev = cb.run_cut(circ, 2).amps
-    assert np.array_equal(host.numpy(), dev)
+    for chunks in (1, 3, 8, 64):
+        host = torch.empty(1 << 20, dtype=torch.complex128, pin_memory=True)
+        run_cut_to_host(circ, 2, host, chunks=chunks)
+        assert np.array_equal(host.numpy(), dev), chunks
+    arr = np.empty(1 << 20, np.complex128)
+    t = StageTimes()
+    run_cut_to_host(circ, 2, arr, timers=t)
+    assert np.array_equal(arr, dev) and t.sub > 0 and t.merge > 0
+    c3 = cb.build_brickwall(cb.BrickwallSpec(18, 5, 3, 4, 1))
+    arr3 = np.empty(1 << 18, np.complex128)
+    run_cut_to_host(c3, 3, arr3, chunks=5)
+    assert np.array_equal(arr3, cb.run_cut(c3, 3).amps)
+    a64 = np.empty(1 << 20, np.complex64)
+    run_cut_to_host(circ, 2, a64, dtype=np.complex64)
+    assert np.abs(a64 - dev).max() < 1e-5
+    with pytest.raises(cb.ValidationError):
+        run_cut_to_host(circ, 2, np.empty(10, np.complex128))
 
 
 def test_sharded_pipeline_over_nccl_world1(cb):
