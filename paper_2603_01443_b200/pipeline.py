@@ -180,7 +180,7 @@ def run_cut_to_host(circuit: Circuit, n: int, host_out, *, dtype=np.complex128, 
 
     q = circuit.num_qubits
     check_capacity(q, max_qubits)
-    t = _device.require_cuda()
+    _device.require_cuda()
     if sizes is None:
         if n < 2 or q % n:
             raise ValidationError(f"q must be divisible by n >= 2: q={q}, n={n}")
@@ -210,7 +210,6 @@ def run_cut_to_host(circuit: Circuit, n: int, host_out, *, dtype=np.complex128, 
                   "cs_cut_run_to_host")
     if timers is not None:
         timers.pre, timers.sub, timers.merge = (float(v) / 1e3 for v in stage)
-    del t
     return host_out
 
 
@@ -230,9 +229,3 @@ def host_workspace_bytes(circuit: Circuit, n: int, *, chunks: int = 8, dtype=np.
     return int(need[0])
 
 
-def _copy_stream():
-    t = _device.torch()
-    dev = t.cuda.current_device()
-    if dev not in _COPY_STREAMS:
-        _COPY_STREAMS[dev] = t.cuda.Stream()
-    return _COPY_STREAMS[dev]
