@@ -110,3 +110,34 @@ def test_unequal_sizes_one_call(cb):
     for sizes in [(1, 9), (9, 1), (3, 7), (2, 3, 5), (1, 1, 1, 7)]:
         got = cb.run_cut(circ, len(sizes), sizes=sizes).amps
         assert np.abs(got - ref).max() < TOL, sizes
+
+
+@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("jit", [0, 2])
+def test_random_circuits_cut_equals_oracle(cb, seed, jit):
+    """Random circuits over the full gate set (incl. U3, CX either way,
+    repeated and back-to-back cuts) with random segment sizes: the one-call
+    pipeline and the uncut simulator against the oracle, interpreter and
+    NVRTC kernels."""
+    from paper_2603_01443_b200 import _native
+    from paper_2603_01443_b200.errors import UnsupportedTopologyError
+    from test_host_cutting import _random_circuit
+
+    rng = np.random.default_rng(1000 + seed)
+    q = int(rng.integers(4, 11))
+    circ = _random_circuit(rng, q, int(rng.integers(10, 70)))
+    n = int(rng.integers(2, min(q, 4) + 1))
+    cuts = np.sort(rng.choice(np.arange(1, q), size=n - 1, replace=False))
+    sizes = tuple(int(v) for v in np.diff(np.concatenate([[0], cuts, [q]])))
+    old = _native.get_option("jit")
+    _native.set_option("jit", jit)
+    try:
+        ref = ref_state(circ)
+        assert np.abs(cb.simulate(circ).amps - ref).max() < TOL
+        try:
+            got = cb.run_cut(circ, n, sizes=sizes).amps
+        except UnsupportedTopologyError:
+            return
+        assert np.abs(got - ref).max() < TOL
+    finally:
+        _native.set_option("jit", old)

@@ -232,3 +232,60 @@ def test_native_preprocess_validation_matches_python(monkeypatch):
     plan = K.plan_cut_sizes(circ, (2, 2, 2, 2))
     assert [c[0] for c in d["cuts"]] == [bg.position for bg in plan.boundary_gates]
     assert [c[1] for c in d["cuts"]] == [bg.boundary for bg in plan.boundary_gates]
+
+
+def _random_circuit(rng, q, g):
+    """Random gate table over the reference gate set + U3; two-qubit gates
+    only between qubits at distance <= 2 (so small segments can be crossed
+    by non-adjacent spans, exercising the topology error too)."""
+    kinds, qa, qb, prm = [], [], [], []
+    for _ in range(g):
+        k = int(rng.integers(0, 8))
+        a = int(rng.integers(0, q))
+        b = -1
+        if k in (5, 6):
+            b = a + int(rng.choice([-2, -1, 1, 2]))
+            if not 0 <= b < q:
+                b = a - 1 if a > 0 else a + 1
+        kinds.append(k)
+        qa.append(a)
+        qb.append(b)
+        prm.append(rng.uniform(0, 6.3, 3) if k == 7 else np.zeros(3))
+    return C.Circuit.from_table(q, C.GateTable(np.array(kinds, np.uint8), np.array(qa), np.array(qb),
+                                               np.array(prm)))
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_native_and_numpy_planners_agree_on_random_circuits(seed, monkeypatch):
+    import os
+
+    from paper_2603_01443_b200 import _native
+
+    if not os.path.exists(_native.LIB_PATH):
+        pytest.skip("libcutsim.so not built")
+    rng = np.random.default_rng(seed)
+    q = int(rng.integers(2, 12))
+    circ = _random_circuit(rng, q, int(rng.integers(0, 60)))
+    n = int(rng.integers(2, q + 1))
+    cuts = np.sort(rng.choice(np.arange(1, q), size=n - 1, replace=False))
+    sizes = tuple(int(v) for v in np.diff(np.concatenate([[0], cuts, [q]])))
+    results = []
+    for native in (True, False):
+        if not native:
+            monkeypatch.setattr(K, "_native_tables", lambda circuit, sizes: None)
+        try:
+            plan = K.plan_cut_sizes(circ, sizes)
+            subs = K.decompose(circ, plan)
+            results.append(("ok", plan, subs))
+        except UnsupportedTopologyError:
+            results.append(("topology", None, None))
+    assert results[0][0] == results[1][0]
+    if results[0][0] == "ok":
+        (_, p1, s1), (_, p2, s2) = results
+        assert p1 == p2
+        assert np.array_equal(s1.merge_table, s2.merge_table) and np.array_equal(s1.coeffs, s2.coeffs)
+        for f1, f2 in zip(s1.segments, s2.segments):
+            for col in ("kinds", "qa", "qb", "params"):
+                assert np.array_equal(getattr(f1.template, col), getattr(f2.template, col)), col
+            assert np.array_equal(f1.slots, f2.slots) and np.array_equal(f1.patch_offsets, f2.patch_offsets)
+            assert f1.cut_ids == f2.cut_ids
