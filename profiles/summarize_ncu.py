@@ -1,5 +1,8 @@
 """Summarise ncu captures brought back in gpurun_out/ into profiles/ (run here,
-no GPU needed):  python profiles/summarize_ncu.py <round-tag> <rep> [<rep>...]"""
+no GPU needed):  python profiles/summarize_ncu.py <tag> <rep> [<rep>...]
+Writes profiles/<tag>_ncu_full.json; tags starting with "r" (the round's
+bench capture of the merge kernel) also refresh profiles/ncu_summary.json,
+which bench.py reads for the roofline's `traffic`."""
 import csv
 import io
 import json
@@ -8,6 +11,9 @@ import subprocess
 import sys
 
 KEYS = [
+    "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
+    "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum", "smsp__sass_thread_inst_executed_op_dmul_pred_on.sum",
+    "smsp__sass_thread_inst_executed_op_dadd_pred_on.sum",
     "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
     "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
     "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
@@ -55,8 +61,9 @@ def main():
         b = [x.get("dram__bytes_read.sum", 0) + x.get("dram__bytes_write.sum", 0) for x in lst]
         agg[name] = {"dram_bytes_per_launch": sum(b) / len(b), "launches_captured": len(lst),
                      "duration_s": sum(x.get("gpu__time_duration.sum", 0) for x in lst) / len(lst)}
-    with open(os.path.join(here, "ncu_summary.json"), "w") as fh:
-        json.dump({"round": tag, **agg}, fh, indent=1)
+    if tag.startswith("r") and "_" not in tag:
+        with open(os.path.join(here, "ncu_summary.json"), "w") as fh:
+            json.dump({"round": tag, **agg}, fh, indent=1)
     print(json.dumps(agg, indent=1))
 
 
