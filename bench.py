@@ -256,9 +256,6 @@ def run_ours(args):
     # warm-up steps, outside the timed region (as the reference's warm_up()
     # keeps numba JIT out of its timers, harness.py:95-111)
     _native.set_option("jit", 0 if args.no_jit else 2)
-    # back-to-back steps on one dedicated workspace: the next step's variant
-    # stage overlaps this step's merge (cs_cut_run's cut_pipelining mode)
-    _native.set_option("cut_pipelining", 0 if args.no_pipelining else 1)
     peak, peak_src = load_peaks()
 
     # shard geometry and preallocated output / workspace
@@ -447,7 +444,6 @@ def run_ours(args):
             "clocks": clocks.summary(),
             "gpu_launches": launches,
             "jit": _native.get_option("jit"),
-            "cut_pipelining": _native.get_option("cut_pipelining"),
         }
         print(json.dumps(line), flush=True)
     if dist:
@@ -469,8 +465,6 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-uncut", action="store_true")
     ap.add_argument("--no-jit", action="store_true", help="interpreter sweep kernels only")
-    ap.add_argument("--no-pipelining", action="store_true",
-                    help="serialise each step's variant stage behind the previous merge")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

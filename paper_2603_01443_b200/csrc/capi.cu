@@ -62,7 +62,6 @@ struct Options {
   int64_t merge_iters = 0;
   int64_t vb = 0;  // states per CTA in a variant batch (0 = auto)
   int64_t merge_dmma3_warps = 8;  // warps per CTA of the 3M kernel (8: 2 CTAs/SM, 4: 4 CTAs/SM)
-  int64_t cut_pipelining = 0;  // cs_cut_run: overlap the next call's variant stage with this merge
   int64_t merge_smem_kb = 96;  // staged-row budget per CTA of the tensor-core merge
   int64_t merge_dmma = 2;  // FP64 tensor-core merge: 1 = four real GEMMs, 2 = three (3M)
   int64_t engine = 1;      // 1: register-tile kernel (rsweep), 0: shared-memory tile kernel (sweep)
@@ -651,11 +650,8 @@ struct CutJob {
   CutPrep prep;
   ChainPlan plan;
   std::vector<int32_t> seg_nq, seg_ncuts, seg_cut_ids;
-  std::vector<int64_t> seg_off;  // byte offsets of the segment batches inside one states half
-  // workspace: [states half 0][states half 1][merge intermediates]; the two
-  // halves let the next call's variant stage run while this call's merge
-  // still reads its states (option "cut_pipelining")
-  int64_t states_bytes = 0, chain_off = 0, total_bytes = 0;
+  std::vector<int64_t> seg_off;  // workspace byte offsets of the segment batches
+  int64_t chain_off = 0, total_bytes = 0;
 };
 
 const double kTermCoef[4] = {0.5, -0.5, 0.5, 0.5};  // (1-i)/2, (1+i)/2 (reference cutting.py:34-35)
@@ -693,8 +689,6 @@ bool cut_job(int nq, const uint8_t* kinds, const int64_t* qa, const int64_t* qb,
     job->seg_off.push_back(off);
     off += ((int64_t(1) << (sp.cut_ids.size() + size_t(sp.nq))) * eb + 255) / 256 * 256;
   }
-  job->states_bytes = off;
-  off *= 2;
   job->chain_off = off;
   for (int64_t a : job->plan.buf_amps) off += (a * eb + 255) / 256 * 256;
   job->total_bytes = off;
@@ -782,8 +776,6 @@ int cs_set_option(const char* key, int64_t value) {
   } else if (k == "jit_minb") {
     if (value < 1 || value > 4) return fail(CS_ERR_INVALID, "jit_minb must be in [1, 4]");
     g_jit_minb = int(value);
-  } else if (k == "cut_pipelining") {
-    g_opt.cut_pipelining = value ? 1 : 0;
   } else if (k == "merge_dmma3_warps") {
     if (value != 4 && value != 8) return fail(CS_ERR_INVALID, "merge_dmma3_warps must be 4 or 8");
     g_opt.merge_dmma3_warps = value;
@@ -825,7 +817,6 @@ int64_t cs_get_option(const char* key) {
   if (k == "merge_dmma") return g_opt.merge_dmma;
   if (k == "merge_smem_kb") return g_opt.merge_smem_kb;
   if (k == "merge_dmma3_warps") return g_opt.merge_dmma3_warps;
-  if (k == "cut_pipelining") return g_opt.cut_pipelining;
   if (k == "jit_minb") return g_jit_minb;
   if (k == "jit_persistent") return g_jit_persistent;
   if (k == "dense_norm") return g_opt.dense_norm;
@@ -1050,28 +1041,22 @@ int cut_programs(const CutJob& job, int dtype, std::vector<std::shared_ptr<const
 
 // Batched subcircuit simulation: every segment's variant family at once,
 // segments on side streams forked from / joined into `st`.
-// start_after: the event the variant stage waits for instead of the caller's
-// stream (pipelined calls: the last merge that read this states half; it may
-// be null for the half's first use, then the caller's stream is waited for)
-int cut_segments(const CutJob& job, const std::vector<std::shared_ptr<const Program>>& progs, char* states_base,
-                 int dtype, cudaStream_t st, std::vector<const void*>* seg_states, bool pipelined = false,
-                 cudaEvent_t start_after = nullptr) {
+int cut_segments(const CutJob& job, const std::vector<std::shared_ptr<const Program>>& progs, void* workspace,
+                 int dtype, cudaStream_t st, std::vector<const void*>* seg_states) {
   const CutPrep& pr = job.prep;
   cudaEvent_t fork = nullptr;
-  const bool use_fork = pr.n > 1 || pipelined;
-  if (use_fork && !(pipelined && start_after)) {
+  if (pr.n > 1) {
     cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
     cudaEventRecord(fork, st);
   }
-  cudaEvent_t gate = fork ? fork : start_after;
   int rc = CS_OK;
   for (size_t s = 0; s < pr.segs.size(); ++s) {
     const SegmentPlan& sp = pr.segs[s];
-    void* states = states_base + job.seg_off[s];
+    void* states = static_cast<char*>(workspace) + job.seg_off[s];
     seg_states->push_back(states);
     const int64_t nv = int64_t(1) << sp.cut_ids.size();
-    cudaStream_t ss = (pr.n > 1 || pipelined) ? side_stream(int(s % 4)) : st;
-    if (gate) cudaStreamWaitEvent(ss, gate, 0);
+    cudaStream_t ss = pr.n > 1 ? side_stream(int(s % 4)) : st;
+    if (fork) cudaStreamWaitEvent(ss, fork, 0);
     rc = run_program(*progs[s], sp.nq, states, nv, int64_t(1) << sp.nq, 0, 1, dtype, ss);
     if (rc != CS_OK) break;
     if (ss != st) {
@@ -1085,13 +1070,6 @@ int cut_segments(const CutJob& job, const std::vector<std::shared_ptr<const Prog
   if (fork) cudaEventDestroy(fork);
   return rc;
 }
-
-struct PipeState {
-  int next = 0;
-  cudaEvent_t last_read[2] = {nullptr, nullptr};
-};
-std::mutex g_pipe_mu;
-std::unordered_map<void*, PipeState> g_pipe;  // per pipelined workspace
 
 int64_t host_chunk_amps(const CutJob& job, int nq, int chunks) {
   const int64_t unit = int64_t(1) << job.plan.q_low;
@@ -1155,7 +1133,7 @@ int cs_cut_run_to_host(int32_t nq, const uint8_t* kinds, const int64_t* qa, cons
     cudaEventRecord(e0, st);
   }
   std::vector<const void*> seg_states;
-  rc = cut_segments(job, progs, static_cast<char*>(workspace), dtype, st, &seg_states);
+  rc = cut_segments(job, progs, workspace, dtype, st, &seg_states);
   if (rc != CS_OK) return rc;
   if (e1) cudaEventRecord(e1, st);
   // chunked merge into two device buffers; each chunk's device-to-host copy
@@ -1231,33 +1209,13 @@ int cs_cut_run(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int64_
     for (auto& e : ev) cudaEventCreate(&e);
   }
   if (ev[0]) cudaEventRecord(ev[0], st);
-  // pipelined calls alternate the two states halves of a dedicated workspace
-  // and start the variant stage after the merge that last read that half,
-  // not after all earlier work on the caller's stream
-  const bool pipelined = g_opt.cut_pipelining != 0 && !stage_ms;
-  int half = 0;
-  cudaEvent_t after = nullptr;
-  if (pipelined) {
-    std::lock_guard<std::mutex> lk(g_pipe_mu);
-    PipeState& ps = g_pipe[workspace];
-    half = ps.next;
-    ps.next ^= 1;
-    after = ps.last_read[half];
-  }
-  char* states_base = static_cast<char*>(workspace) + int64_t(half) * job.states_bytes;
   std::vector<const void*> seg_states;
-  rc = cut_segments(job, progs, states_base, dtype, st, &seg_states, pipelined, after);
+  rc = cut_segments(job, progs, workspace, dtype, st, &seg_states);
   if (rc != CS_OK) return rc;
   if (ev[1]) cudaEventRecord(ev[1], st);
   rc = run_chain(job.plan, pr.n, seg_states.data(), out_begin, out_end, out,
                  static_cast<char*>(workspace) + job.chain_off, job.total_bytes - job.chain_off, dtype, st);
   if (rc != CS_OK) return rc;
-  if (pipelined) {
-    std::lock_guard<std::mutex> lk(g_pipe_mu);
-    PipeState& ps = g_pipe[workspace];
-    if (!ps.last_read[half]) cudaEventCreateWithFlags(&ps.last_read[half], cudaEventDisableTiming);
-    cudaEventRecord(ps.last_read[half], st);
-  }
   if (ev[2]) cudaEventRecord(ev[2], st);
   if (stage_ms) {
     cudaError_t e = cudaEventSynchronize(ev[2]);

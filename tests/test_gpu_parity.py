@@ -477,31 +477,3 @@ def test_native_nccl_comm_world1(cb):
         assert np.array_equal(res.cpu().numpy(), cb.run_cut(circ, 2).amps)
     finally:
         comm.destroy()
-
-
-def test_pipelined_cut_calls_match(cb):
-    """cut_pipelining: back-to-back cs_cut_run calls on one dedicated workspace
-    overlap the next call's variant stage with this call's merge (alternating
-    states halves). Every result must equal the unpipelined one."""
-    import torch
-
-    from paper_2603_01443_b200 import _native
-
-    circs = [cb.build_brickwall(cb.BrickwallSpec(20, 6, 2, 2, s)) for s in range(3)]
-    circs.append(cb.build_brickwall(cb.BrickwallSpec(21, 5, 3, 4, 1)))
-    want = [cb.run_cut(c, 2 if c.num_qubits == 20 else 3).amps for c in circs]
-    ws_bytes = max(_native.cut_workspace(c.num_qubits, c.table, [c.num_qubits // (2 if c.num_qubits == 20 else 3)]
-                                         * (2 if c.num_qubits == 20 else 3))[0] for c in circs)
-    ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
-    outs = [torch.empty(1 << c.num_qubits, dtype=torch.complex128, device="cuda") for c in circs]
-    old = _native.get_option("cut_pipelining")
-    _native.set_option("cut_pipelining", 1)
-    try:
-        for _ in range(3):
-            for c, o in zip(circs, outs):
-                cb.run_cut(c, 2 if c.num_qubits == 20 else 3, out=o, workspace=ws)
-        torch.cuda.synchronize()
-    finally:
-        _native.set_option("cut_pipelining", old)
-    for o, w in zip(outs, want):
-        assert np.array_equal(o.cpu().numpy(), w)
