@@ -91,6 +91,13 @@ DEV void cpw() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 }  // namespace
 
 JitModule::~JitModule() {
+  // a module dies when its program is evicted from the cache; launches of its
+  // kernels may still be queued on some stream, so drain the device first
+  // (eviction is rare: the cache holds 512 programs)
+  bool any = false;
+  for (cudaLibrary_t l : libs) any |= l != nullptr;
+  if (!any) return;
+  cudaDeviceSynchronize();
   for (cudaLibrary_t l : libs)
     if (l) cudaLibraryUnload(l);
 }
