@@ -63,6 +63,19 @@ def load_traffic():
         return None
 
 
+def load_dram_pct():
+    """ncu's dram throughput (% of its DRAM peak) for the committed capture of
+    the same merge launch, for reading `frac` (which is against the measured
+    read+write copy rate) next to the DRAM-peak view."""
+    path = os.path.join(ROOT, "profiles", "r01_ncu_full.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["merge_kernel"][0]["gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"])
+    except (OSError, ValueError, KeyError, IndexError, TypeError):
+        return None
+
+
 class ClockSampler:
     """SM clocks and throttle reasons sampled every few ms during the timed
     region (NVML through nvidia_ml_py; nvidia-smi as a fallback)."""
@@ -369,7 +382,7 @@ def run_ours(args):
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                     "frac": achieved / peak, "traffic": load_traffic(), "kernel": "merge_kernel",
                     "algorithmic_bytes_per_launch": alg, "avg_launch_ms": dur * 1e3,
-                    "peak_source": peak_src}
+                    "peak_source": peak_src, "ncu_dram_pct_of_peak": load_dram_pct()}
 
     # e2e through the public API into pinned host memory (N=1)
     e2e = None
