@@ -258,7 +258,8 @@ std::shared_ptr<const Program> build_schedule(int nq, const uint8_t* kinds, cons
   std::vector<LOp> ops = lower_gates(nq, kinds, qa, qb, params, slots, n_gates, fuse == 2);
   if (fuse == 2) ops = fuse_ops(commute_phases(ops), true);
   else if (fuse == 1) ops = fuse_ops(ops);
-  if (norm) ops = normalize_dense(ops, nq);
+  // growth budget: amplitudes stay below 2^200 (c128) / 2^20 (c64)
+  if (norm) ops = normalize_dense(ops, nq, dtype == CS_C128 ? 200.0 : 20.0);
   // register groups hold 2^k x vb complex values: 8 (c128) / 16 (c64) per thread
   const int max_group = std::min(sweep_max_group(T), group_budget(vb, dtype));
   auto built = std::make_shared<Program>();

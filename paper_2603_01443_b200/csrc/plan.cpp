@@ -248,19 +248,29 @@ LOp phase_op(int q, Cx v) {
 
 }  // namespace
 
-std::vector<LOp> normalize_dense(const std::vector<LOp>& ops, int nq) {
+std::vector<LOp> normalize_dense(const std::vector<LOp>& ops, int nq, double max_growth_bits) {
   std::vector<LOp> out;
   out.reserve(ops.size() + size_t(nq) + 1);
   std::vector<Cx> d0(static_cast<size_t>(nq)), d1(static_cast<size_t>(nq));
+  // amplification of the executed state over the true one: each qubit's
+  // pending D contributes -log2 min(|d0|, |d1|) bits, the deferred global
+  // scalar -log2 |scale|; kept under max_growth_bits (each normalised op adds
+  // up to 1/2 bit, so deep circuits would otherwise overflow / underflow)
+  std::vector<double> grow(static_cast<size_t>(nq), 0.0);
+  double grow_sum = 0.0, grow_scale = 0.0;
   Cx scale;
+  auto bits_of = [](Cx a, Cx b) { return -0.5 * std::log2(std::min(cabs2(a), cabs2(b))); };
   auto flush = [&](int q) {
     const size_t k = size_t(q);
     if (is_one(d0[k]) && is_one(d1[k])) return;
     scale = cmulx(scale, d0[k]);  // D = d0 . diag(1, d1/d0)
+    grow_scale = -0.5 * std::log2(cabs2(scale));
     const Cx r = cdivx(d1[k], d0[k]);
     if (!is_one(r)) out.push_back(phase_op(q, r));
     d0[k] = Cx{};
     d1[k] = Cx{};
+    grow_sum -= grow[k];
+    grow[k] = 0.0;
   };
   long last_dense = -1;
   for (const LOp& op : ops) {
@@ -285,17 +295,39 @@ std::vector<LOp> normalize_dense(const std::vector<LOp>& ops, int nq) {
       m[r][1] = cmulx(m[r][1], d1[k]);
     }
     Cx dn[2];
+    int piv[2];
     for (int r = 0; r < 2; ++r) {
-      const int piv = cabs2(m[r][0]) >= cabs2(m[r][1]) ? 0 : 1;
-      dn[r] = m[r][piv];
-      for (int c = 0; c < 2; ++c) {
-        const Cx v = c == piv ? Cx{} : cdivx(m[r][c], dn[r]);
-        n.m[2 * (2 * r + c)] = v.r;
-        n.m[2 * (2 * r + c) + 1] = v.i;
-      }
+      piv[r] = cabs2(m[r][0]) >= cabs2(m[r][1]) ? 0 : 1;
+      dn[r] = m[r][piv[r]];
     }
-    d0[k] = dn[0];
-    d1[k] = dn[1];
+    const double g = bits_of(dn[0], dn[1]);
+    if (grow_sum - grow[k] + g + grow_scale > max_growth_bits) {
+      // over budget: execute M . D_q (times the deferred scalar) as it is,
+      // which brings the executed state back to the true scale
+      for (int r = 0; r < 2; ++r)
+        for (int c = 0; c < 2; ++c) {
+          const Cx v = cmulx(m[r][c], scale);
+          n.m[2 * (2 * r + c)] = v.r;
+          n.m[2 * (2 * r + c) + 1] = v.i;
+        }
+      scale = Cx{};
+      grow_scale = 0.0;
+      d0[k] = Cx{};
+      d1[k] = Cx{};
+      grow_sum -= grow[k];
+      grow[k] = 0.0;
+    } else {
+      for (int r = 0; r < 2; ++r)
+        for (int c = 0; c < 2; ++c) {
+          const Cx v = c == piv[r] ? Cx{} : cdivx(m[r][c], dn[r]);
+          n.m[2 * (2 * r + c)] = v.r;
+          n.m[2 * (2 * r + c) + 1] = v.i;
+        }
+      d0[k] = dn[0];
+      d1[k] = dn[1];
+      grow_sum += g - grow[k];
+      grow[k] = g;
+    }
     last_dense = long(out.size());
     out.push_back(n);
   }

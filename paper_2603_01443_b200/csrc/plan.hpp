@@ -48,8 +48,11 @@ std::vector<LOp> fuse_ops(const std::vector<LOp>& ops, bool same_type_only = fal
 // instead of 7. Pending diagonals are emitted as phase ops (times a global
 // scalar) before an op that does not commute with them (a controlled dense
 // op on that target) and at the end; the global scalar is folded into the
-// last dense op, which stays un-normalised.
-std::vector<LOp> normalize_dense(const std::vector<LOp>& ops, int nq);
+// last dense op, which stays un-normalised. Normalising inflates the executed
+// state by up to 1/2 bit per op; whenever the total would exceed
+// max_growth_bits an op is emitted un-normalised (with the pending diagonal
+// and scalar applied), restoring the true scale.
+std::vector<LOp> normalize_dense(const std::vector<LOp>& ops, int nq, double max_growth_bits);
 
 // Defer single-qubit phases past everything they commute with (diagonal
 // ops, dense ops controlled by or not touching their qubit) and merge the

@@ -101,3 +101,16 @@ def test_jit_streaming_kernel_forms(jit_on, persistent, minb):
     finally:
         _native.set_option("jit_persistent", old[0])
         _native.set_option("jit_minb", old[1])
+
+
+@pytest.mark.gpu
+def test_jit_deep_circuit_complex64_stays_finite(jit_on):
+    """A 300-layer circuit through the normalised NVRTC kernels in complex64:
+    without the growth budget the executed amplitudes would pass 2^128."""
+    import paper_2603_01443_b200 as cb
+
+    circ = cb.build_brickwall(cb.BrickwallSpec(12, 300, 2, 2, 4))
+    ref = orc.simulate(12, circ.kinds, circ.qa, circ.qb, circ.params)
+    got = cb.simulate(circ, dtype=np.complex64).amps
+    assert np.isfinite(got).all() and np.abs(got - ref).max() < 1e-4
+    assert np.abs(cb.simulate(circ).amps - ref).max() < 1e-10

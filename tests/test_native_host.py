@@ -326,3 +326,44 @@ def test_register_programs_of_variant_templates(golden, key, fuse_mode):
             for v in range(fam.num_variants):
                 got = execute_reg_programs(plan, fam.num_qubits, v)
                 assert np.abs(got - ref[v]).max() < 1e-12
+
+
+@pytest.mark.parametrize("dtype,bound", [(_native.CS_C128, 200.5), (_native.CS_C64, 20.5)])
+def test_normalised_lowering_bounds_amplitude_growth(dtype, bound):
+    """Each normalised 2x2 inflates the executed state by up to 1/2 bit; the
+    planner re-applies the pending scale before the budget (2^200 for c128,
+    2^20 for c64) is exceeded, so deep circuits cannot overflow. Checked by
+    executing the exported schedule of a 600-layer circuit step by step."""
+    circ = G.build_brickwall(G.BrickwallSpec(8, 600, 2, 2, 0))
+    old = _native.get_option("dense_norm")
+    try:
+        _native.set_option("dense_norm", 1)
+        plan = json.loads(_native.sweep_plan_json(8, circ.table, dtype=dtype))
+    finally:
+        _native.set_option("dense_norm", old)
+    amps = orc.zero_state(8)
+    idx = np.arange(256)
+    peak = 0.0
+    for sw in plan["sweeps"]:
+        glob = list(range(sw["L"])) + list(sw["hq"])
+        for e in sw["entries"]:
+            mask = e["omask"]
+            for p in range(32):
+                if (e["lmask"] >> p) & 1:
+                    mask |= 1 << glob[p]
+            m = np.array(e["m"]).reshape(4, 2)
+            m = m[:, 0] + 1j * m[:, 1]
+            sel = (idx & mask) == mask
+            if e["type"] == 1:
+                amps[sel] *= m[0]
+            else:
+                t = glob[e["target"]]
+                i0 = idx[sel & (((idx >> t) & 1) == 0)]
+                i1 = i0 | (1 << t)
+                a, b = amps[i0].copy(), amps[i1].copy()
+                amps[i0] = m[0] * a + m[1] * b
+                amps[i1] = m[2] * a + m[3] * b
+            peak = max(peak, float(np.abs(amps).max()))
+    assert np.log2(peak) <= bound
+    ref = orc.simulate(8, circ.kinds, circ.qa, circ.qb, circ.params)
+    assert np.abs(amps - ref).max() < 1e-12
