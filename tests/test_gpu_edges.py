@@ -141,3 +141,31 @@ def test_random_circuits_cut_equals_oracle(cb, seed, jit):
         assert np.abs(got - ref).max() < TOL
     finally:
         _native.set_option("jit", old)
+
+
+@pytest.mark.parametrize("jit", [0, 2])
+def test_long_gate_tables_split_across_launches(cb, jit):
+    """6800 gates on 12 qubits: register programs split into many launches
+    (kMaxRegOps per launch, NVRTC cost guard) — interpreter and NVRTC."""
+    from paper_2603_01443_b200 import _native
+
+    circ = cb.build_brickwall(cb.BrickwallSpec(12, 400, 2, 3, 9))
+    assert circ.gate_count > 6000
+    old = _native.get_option("jit")
+    _native.set_option("jit", jit)
+    try:
+        ref = ref_state(circ)
+        assert np.abs(cb.simulate(circ).amps - ref).max() < TOL
+        assert np.abs(cb.run_cut(circ, 2).amps - ref).max() < TOL
+    finally:
+        _native.set_option("jit", old)
+
+
+def test_thousands_of_variants(cb):
+    """c_total = 12 at n = 2: 4096 variants per segment in one batched launch
+    sequence, a 4096-term merge."""
+    circ = cb.build_brickwall(cb.BrickwallSpec(16, 6, 2, 12, 2))
+    plan = cb.plan_cut(circ, 2)
+    assert plan.c_total == 12 and cb.count_subcircuits(plan) == 2 * 4096
+    got = cb.run_cut(circ, 2).amps
+    assert np.abs(got - ref_state(circ)).max() < TOL
