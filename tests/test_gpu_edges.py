@@ -169,3 +169,20 @@ def test_thousands_of_variants(cb):
     assert plan.c_total == 12 and cb.count_subcircuits(plan) == 2 * 4096
     got = cb.run_cut(circ, 2).amps
     assert np.abs(got - ref_state(circ)).max() < TOL
+
+
+@pytest.mark.parametrize("q,d,n,c,seed", [(15, 5, 3, 10, 1), (15, 4, 5, 8, 3), (16, 3, 8, 7, 5)])
+def test_many_segments_and_interior_cuts(cb, q, d, n, c, seed):
+    """Chain contraction with wide interior bonds (10 cuts over n=3) and long
+    chains (n = 5, 8 two-qubit segments), full state and a middle shard."""
+    circ = cb.build_brickwall(cb.BrickwallSpec(q, d, n, c, seed))
+    ref = ref_state(circ)
+    full = cb.run_cut(circ, n).amps
+    assert np.abs(full - ref).max() < TOL
+    from paper_2603_01443_b200 import _native
+
+    qlow = _native.cut_workspace(q, circ.table, [q // n] * n)[1]  # shard unit: the chosen bond's low side
+    unit = 1 << qlow
+    lo, hi = unit, min(1 << q, 3 * unit)
+    shard = cb.run_cut(circ, n, out_range=(lo, hi))
+    assert np.array_equal(shard.amps, full[lo:hi])
