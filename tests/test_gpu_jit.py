@@ -114,3 +114,25 @@ def test_jit_deep_circuit_complex64_stays_finite(jit_on):
     got = cb.simulate(circ, dtype=np.complex64).amps
     assert np.isfinite(got).all() and np.abs(got - ref).max() < 1e-4
     assert np.abs(cb.simulate(circ).amps - ref).max() < 1e-10
+
+
+@pytest.mark.gpu
+def test_jit_apply_circuit_on_arbitrary_state(jit_on):
+    """engine.apply_circuit (init = 0) on a random state through the normalised
+    NVRTC kernels: the deferred diagonals and global scalar must land on any
+    input state, not only |0...0>."""
+    import paper_2603_01443_b200 as cb
+    from paper_2603_01443_b200 import engine
+
+    rng = np.random.default_rng(17)
+    for q, d in ((10, 6), (16, 4)):
+        circ = cb.build_brickwall(cb.BrickwallSpec(q, d, 2, 2, 5))
+        amps = rng.normal(size=1 << q) + 1j * rng.normal(size=1 << q)
+        amps /= np.linalg.norm(amps)
+        sv = cb.StateVec(q, amps.copy())
+        for _ in range(2):  # second pass: compiled program reused on a new state
+            sv = cb.StateVec(q, amps.copy())
+            engine.apply_circuit(sv, circ)
+        ref = amps.copy()
+        orc.run_gates(ref, circ.kinds, circ.qa, circ.qb, circ.params)
+        assert np.abs(sv.amps - ref).max() < 1e-10
