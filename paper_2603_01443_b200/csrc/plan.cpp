@@ -624,6 +624,89 @@ void push_remap(std::vector<RegOp>& out, Mapping& map, const int* want) {
 
 }  // namespace
 
+int g_reg_reorder = 1;
+
+namespace {
+
+// Ops i < j of one sweep commute when reordering them cannot change the
+// result: two diagonal ops always; a dense op and a diagonal op when the
+// diagonal does not touch the dense target; two dense ops when neither
+// target is a qubit (target or control) of the other. Tile-local masks
+// only: outside-tile bits are constants within a tile.
+bool commutes(const SweepOp& a, const SweepOp& b) {
+  const bool da = a.type == OP_DENSE, db = b.type == OP_DENSE;
+  if (!da && !db) return true;
+  if (da && !db) return ((b.lmask >> a.target) & 1u) == 0;
+  if (!da && db) return ((a.lmask >> b.target) & 1u) == 0;
+  if (a.target == b.target) return false;
+  return ((b.lmask >> a.target) & 1u) == 0 && ((a.lmask >> b.target) & 1u) == 0;
+}
+
+// The sweep's ops (a slotted op = two consecutive entries) in an order that
+// needs fewer register remaps: list scheduling over the commutation DAG that
+// prefers any ready op whose dense target is already a register bit, and on
+// a miss loads the targets of the ready ops first, then the next ones in
+// program order. Returns entry-index starts of the units in the new order.
+std::vector<size_t> reorder_for_registers(const std::vector<SweepOp>& E, int RB, const int* rpos0, int T) {
+  std::vector<size_t> start;
+  for (size_t i = 0; i < E.size(); i += (E[i].slot >= 0 ? 2 : 1)) start.push_back(i);
+  const size_t n = start.size();
+  std::vector<std::vector<int>> succ(n);
+  std::vector<int> npred(n, 0);
+  for (size_t j = 0; j < n; ++j)
+    for (size_t i = 0; i < j; ++i)
+      if (!commutes(E[start[i]], E[start[j]])) {
+        succ[i].push_back(int(j));
+        ++npred[j];
+      }
+  std::vector<char> done(n, 0);
+  std::vector<size_t> order;
+  order.reserve(n);
+  bool inreg[32] = {false};
+  for (int k = 0; k < RB; ++k) inreg[rpos0[k]] = true;
+  auto take = [&](size_t u) {
+    done[u] = 1;
+    order.push_back(start[u]);
+    for (int v : succ[u]) --npred[v];
+  };
+  while (order.size() < n) {
+    bool progress = true;
+    while (progress) {  // everything runnable without a remap, in program order
+      progress = false;
+      for (size_t u = 0; u < n; ++u) {
+        if (done[u] || npred[u] > 0) continue;
+        const SweepOp& e = E[start[u]];
+        if (e.type != OP_DENSE || inreg[e.target]) {
+          take(u);
+          progress = true;
+        }
+      }
+    }
+    if (order.size() == n) break;
+    // miss: new register set = targets of ready dense ops (program order),
+    // then targets of the following dense ops, then current register bits
+    int want[4];
+    int m = 0;
+    auto add = [&](int t) {
+      for (int a = 0; a < m; ++a)
+        if (want[a] == t) return;
+      if (m < RB) want[m++] = t;
+    };
+    for (size_t u = 0; u < n && m < RB; ++u)
+      if (!done[u] && npred[u] == 0 && E[start[u]].type == OP_DENSE) add(E[start[u]].target);
+    for (size_t u = 0; u < n && m < RB; ++u)
+      if (!done[u] && E[start[u]].type == OP_DENSE) add(E[start[u]].target);
+    for (int b = 0; b < T && m < RB; ++b)
+      if (inreg[b]) add(b);
+    for (int b = 0; b < T && m < RB; ++b) add(b);
+    for (int b = 0; b < 32; ++b) inreg[b] = false;
+    for (int a = 0; a < m; ++a) inreg[want[a]] = true;
+  }
+  return order;
+}
+
+}  // namespace
+
 std::vector<RegOp> reg_program(const Sweep& sw, int RB) {
   RB = std::max(1, std::min(RB, 4));
   const int T = sw.tile_bits;
@@ -633,7 +716,16 @@ std::vector<RegOp> reg_program(const Sweep& sw, int RB) {
   for (int k = 0; k < RB; ++k) map.rpos[k] = T - RB + k;
   map.build();
   std::vector<RegOp> out;
-  const auto& E = sw.entries;
+  // optionally reorder the sweep's commuting ops so fewer remaps are needed
+  std::vector<SweepOp> reordered;
+  if (g_reg_reorder) {
+    const std::vector<size_t> order = reorder_for_registers(sw.entries, RB, map.rpos, T);
+    for (size_t st : order) {
+      reordered.push_back(sw.entries[st]);
+      if (sw.entries[st].slot >= 0) reordered.push_back(sw.entries[st + 1]);
+    }
+  }
+  const auto& E = g_reg_reorder ? reordered : sw.entries;
   for (size_t i = 0; i < E.size();) {
     const SweepOp& e = E[i];
     const size_t w = e.slot >= 0 ? 2 : 1;
