@@ -465,6 +465,8 @@ int sweep_max_group(int tile_bits) {
   return std::max(1, std::min(kMaxGroup, tile_bits - lg));
 }
 
+int g_sweep_windows = 1;
+
 std::vector<Sweep> schedule_sweeps(const std::vector<LOp>& ops, int nq, int tile_bits, int low_bits,
                                    int max_group) {
   std::vector<Sweep> sweeps;
@@ -484,12 +486,73 @@ std::vector<Sweep> schedule_sweeps(const std::vector<LOp>& ops, int nq, int tile
   const int L = std::max(1, std::min(low_bits, T - 1));
   std::vector<int> pending(ops.size());
   for (size_t i = 0; i < ops.size(); ++i) pending[i] = int(i);
+  // dense ops a fixed tile set would absorb from `pending` (same rules as the
+  // greedy pass below, without growing the set)
+  auto absorbed = [&](const bool* fixed) {
+    uint64_t bd = 0, bp = 0;
+    int count = 0;
+    for (int idx : pending) {
+      const LOp& op = ops[size_t(idx)];
+      const uint64_t qm = qubit_mask(op);
+      if (op.type == OP_PHASE) {
+        if (qm & bd) bp |= qm;
+        continue;
+      }
+      if ((qm & (bd | bp)) || !fixed[op.target]) bd |= qm;
+      else ++count;
+    }
+    return count;
+  };
   bool first = true;
   while (!pending.empty() || first) {
     first = false;
     bool inset[64] = {false};
     for (int q = 0; q < L; ++q) inset[q] = true;
     int room = T - L;
+    if (g_sweep_windows && nq - L > T - L) {
+      // candidate tile sets: the greedy first-need set (room filled below) vs
+      // every contiguous window of T - L high qubits; take the window when it
+      // absorbs more dense ops
+      int best = -1, best_a = -1;
+      for (int a = L; a + (T - L) <= nq; ++a) {
+        bool cand[64] = {false};
+        for (int q = 0; q < L; ++q) cand[q] = true;
+        for (int q = a; q < a + (T - L); ++q) cand[q] = true;
+        const int c = absorbed(cand);
+        if (c > best) {
+          best = c;
+          best_a = a;
+        }
+      }
+      // the greedy set, for comparison
+      bool g[64] = {false};
+      for (int q = 0; q < L; ++q) g[q] = true;
+      {
+        int r = T - L;
+        uint64_t bd = 0, bp = 0;
+        for (int idx : pending) {
+          const LOp& op = ops[size_t(idx)];
+          const uint64_t qm = qubit_mask(op);
+          if (op.type == OP_PHASE) {
+            if (qm & bd) bp |= qm;
+            continue;
+          }
+          if (qm & (bd | bp)) bd |= qm;
+          else if (!g[op.target]) {
+            if (r > 0) {
+              g[op.target] = true;
+              --r;
+            } else {
+              bd |= qm;
+            }
+          }
+        }
+      }
+      if (best > absorbed(g)) {
+        for (int q = best_a; q < best_a + (T - L); ++q) inset[q] = true;
+        room = 0;
+      }
+    }
     uint64_t blocked_dense = 0, blocked_phase = 0;
     std::vector<int> run, deferred;
     for (int idx : pending) {

@@ -85,7 +85,8 @@ std::string sweeps_to_json(const std::vector<Sweep>& sweeps, int nq);
 // REMAPs it needs (ends in the canonical mapping, register bits = top bits).
 int reg_bits_for(int tile_bits);
 extern int g_reg_bits;
-extern int g_reg_reorder;  // option "reg_reorder": list-schedule commuting ops to save remaps  // option "reg_bits": 0 = automatic, 2..4 = override where valid
+extern int g_reg_reorder;
+extern int g_sweep_windows;  // option "sweep_windows": also try contiguous qubit windows as tile sets  // option "reg_reorder": list-schedule commuting ops to save remaps  // option "reg_bits": 0 = automatic, 2..4 = override where valid
 std::vector<RegOp> reg_program(const Sweep& sw, int reg_bits);
 std::string reg_programs_to_json(const std::vector<Sweep>& sweeps, int nq);
 

@@ -17,6 +17,8 @@ if len(sys.argv) > 4:
     _native.set_option("jit_persistent", int(sys.argv[4]))
 if len(sys.argv) > 5:
     _native.set_option("reg_reorder", int(sys.argv[5]))
+if len(sys.argv) > 6:
+    _native.set_option("sweep_windows", int(sys.argv[6]))
 name = sys.argv[2] if len(sys.argv) > 2 else "cfg4a"
 circ = cb.build_brickwall(cb.BASELINE_CONFIGS[name])
 sv = cb.simulate(circ, max_qubits=circ.num_qubits)
@@ -33,4 +35,4 @@ for _ in range(3):
     assert torch.equal(sv.device_tensor()[:1 << 20], ref)
     del sv
 print(f"{name} jit_minb={sys.argv[1]} reg_bits={_native.get_option('reg_bits')} "
-      f"persistent={_native.get_option('jit_persistent')} reorder={_native.get_option('reg_reorder')}: {np.median(times):.1f} ms {[round(t, 1) for t in times]}", flush=True)
+      f"persistent={_native.get_option('jit_persistent')} reorder={_native.get_option('reg_reorder')} windows={_native.get_option('sweep_windows')}: {np.median(times):.1f} ms {[round(t, 1) for t in times]}", flush=True)
