@@ -240,7 +240,7 @@ std::shared_ptr<const Program> build_schedule(int nq, const uint8_t* kinds, cons
   // NVRTC-specialised kernels); the interpreter keeps the plain matrices
   const int norm = g_opt.dense_norm == 2 ? (g_opt.jit != 0 && g_opt.engine == 1 ? 1 : 0) : int(g_opt.dense_norm);
   const int32_t hdr[13] = {nq, T, L, int32_t(fuse), slots ? 1 : 0, dtype, vb, g_sweep_minb,
-                           int32_t(g_opt.engine), norm, g_reg_bits * 4 + g_reg_reorder * 2 + g_sweep_windows, g_jit_minb,
+                           int32_t(g_opt.engine), norm, g_reg_bits * 8 + g_reg_reorder * 4 + g_sweep_windows, g_jit_minb,
                            g_jit_persistent};
   key.append(reinterpret_cast<const char*>(hdr), sizeof(hdr));
   key.append(reinterpret_cast<const char*>(kinds), size_t(n_gates));
@@ -768,7 +768,8 @@ int cs_set_option(const char* key, int64_t value) {
     if (value < 8 || value > 112) return fail(CS_ERR_INVALID, "merge_smem_kb must be in [8, 112]");
     g_opt.merge_smem_kb = value;
   } else if (k == "sweep_windows") {
-    g_sweep_windows = value ? 1 : 0;
+    if (value < 0 || value > 2) return fail(CS_ERR_INVALID, "sweep_windows must be 0, 1 or 2");
+    g_sweep_windows = int(value);
   } else if (k == "reg_reorder") {
     g_reg_reorder = value ? 1 : 0;
   } else if (k == "reg_bits") {

@@ -488,20 +488,39 @@ std::vector<Sweep> schedule_sweeps(const std::vector<LOp>& ops, int nq, int tile
   for (size_t i = 0; i < ops.size(); ++i) pending[i] = int(i);
   // dense ops a fixed tile set would absorb from `pending` (same rules as the
   // greedy pass below, without growing the set)
-  auto absorbed = [&](const bool* fixed) {
+  auto absorbed_from = [&](const std::vector<int>& list, const bool* fixed, std::vector<int>* rest) {
     uint64_t bd = 0, bp = 0;
     int count = 0;
-    for (int idx : pending) {
+    for (int idx : list) {
       const LOp& op = ops[size_t(idx)];
       const uint64_t qm = qubit_mask(op);
       if (op.type == OP_PHASE) {
-        if (qm & bd) bp |= qm;
+        if (qm & bd) {
+          bp |= qm;
+          if (rest) rest->push_back(idx);
+        }
         continue;
       }
-      if ((qm & (bd | bp)) || !fixed[op.target]) bd |= qm;
-      else ++count;
+      if ((qm & (bd | bp)) || !fixed[op.target]) {
+        bd |= qm;
+        if (rest) rest->push_back(idx);
+      } else {
+        ++count;
+      }
     }
     return count;
+  };
+  auto absorbed = [&](const bool* fixed) { return absorbed_from(pending, fixed, nullptr); };
+  // best single-window count over a list (for the two-step look-ahead)
+  auto best_window = [&](const std::vector<int>& list) {
+    int best = 0;
+    for (int a = L; a + (T - L) <= nq; ++a) {
+      bool cand[64] = {false};
+      for (int q = 0; q < L; ++q) cand[q] = true;
+      for (int q = a; q < a + (T - L); ++q) cand[q] = true;
+      best = std::max(best, absorbed_from(list, cand, nullptr));
+    }
+    return best;
   };
   bool first = true;
   while (!pending.empty() || first) {
@@ -518,7 +537,14 @@ std::vector<Sweep> schedule_sweeps(const std::vector<LOp>& ops, int nq, int tile
         bool cand[64] = {false};
         for (int q = 0; q < L; ++q) cand[q] = true;
         for (int q = a; q < a + (T - L); ++q) cand[q] = true;
-        const int c = absorbed(cand);
+        int c;
+        if (g_sweep_windows >= 2) {  // score = this sweep + the best next window
+          std::vector<int> rest;
+          c = absorbed_from(pending, cand, &rest);
+          c += best_window(rest);
+        } else {
+          c = absorbed(cand);
+        }
         if (c > best) {
           best = c;
           best_a = a;
@@ -548,7 +574,15 @@ std::vector<Sweep> schedule_sweeps(const std::vector<LOp>& ops, int nq, int tile
           }
         }
       }
-      if (best > absorbed(g)) {
+      int greedy_score;
+      if (g_sweep_windows >= 2) {
+        std::vector<int> rest;
+        greedy_score = absorbed_from(pending, g, &rest);
+        greedy_score += best_window(rest);
+      } else {
+        greedy_score = absorbed(g);
+      }
+      if (best > greedy_score) {
         for (int q = best_a; q < best_a + (T - L); ++q) inset[q] = true;
         room = 0;
       }
