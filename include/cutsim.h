@@ -40,6 +40,7 @@ extern "C" {
 #define CS_ERR_INTERNAL 5
 #define CS_ERR_NODEVICE 6
 #define CS_ERR_TOPOLOGY 7
+#define CS_ERR_TIMEOUT 8   /* BudgetExceededError (cs_sim_batch_until) */
 
 #define CS_C128 0
 #define CS_C64 1
@@ -83,6 +84,15 @@ int cs_sim_batch(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int6
                  int64_t n_states, int64_t state_stride, uint64_t variant_base, int32_t init_zero,
                  int32_t dtype, void* stream);
 
+/* cs_sim_batch with a cooperative budget (the reference's `deadline`,
+ * engine.py:142-155): deadline_s is CLOCK_MONOTONIC seconds (Python's
+ * time.monotonic()); the stream is synchronised after every sweep launch and
+ * CS_ERR_TIMEOUT returned once the deadline has passed. The fused program is
+ * the same as cs_sim_batch's. */
+int cs_sim_batch_until(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int64_t* qb,
+                       const double* params, const int32_t* slots, int64_t n_gates, void* states,
+                       int64_t n_states, int64_t state_stride, uint64_t variant_base, int32_t init_zero,
+                       int32_t dtype, void* stream, double deadline_s);
 /* Host-only: the sweep schedule cs_sim_batch would run, as JSON. tile_bits
  * <= 0 uses the current option. Writes up to buflen bytes, *needed = full
  * length + 1. */

@@ -12,6 +12,7 @@ import threading
 import numpy as np
 
 from .errors import (
+    BudgetExceededError,
     CapacityError,
     CutbenchError,
     DeviceError,
@@ -33,6 +34,7 @@ _ERRORS = {
     5: CutbenchError,
     6: NativeUnavailableError,
     7: UnsupportedTopologyError,
+    8: BudgetExceededError,
 }
 
 _i32, _i64, _u64, _vp, _dp = (ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_void_p,
@@ -49,6 +51,8 @@ SIGNATURES = {
     "cs_init_basis": (ctypes.c_int, [_vp, _i32, _i64, _i64, _i32, _vp]),
     "cs_sim_batch": (ctypes.c_int, [_i32, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _i64, _i64, _u64, _i32,
                                     _i32, _vp]),
+    "cs_sim_batch_until": (ctypes.c_int, [_i32, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _i64, _i64, _u64, _i32,
+                                          _i32, _vp, ctypes.c_double]),
     "cs_sweep_plan_json": (ctypes.c_int, [_i32, _vp, _vp, _vp, _vp, _vp, _i64, _i32, _i32, _vp, _i64,
                                           _vp]),
     "cs_jit_selftest": (ctypes.c_int, [_i32, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i32, _vp]),

@@ -519,8 +519,11 @@ std::shared_ptr<JitModule> program_jit(const Program& prog, int dtype) {
   return prog.jit;
 }
 
+// deadline_s > 0: CLOCK_MONOTONIC seconds (Python's time.monotonic()); the
+// stream is synchronised after every launch and CS_ERR_TIMEOUT returned once
+// it has passed (the reference's cooperative budget, engine.py:142-155)
 int run_program(const Program& prog_ref, int nq, void* states, int64_t n_states, int64_t state_stride,
-                uint64_t variant_base, int init_zero, int dtype, cudaStream_t st) {
+                uint64_t variant_base, int init_zero, int dtype, cudaStream_t st, double deadline_s = 0.0) {
   const Program* prog = &prog_ref;
   std::shared_ptr<JitModule> jit = program_jit(*prog, dtype);
   static SweepParams p;
@@ -602,6 +605,14 @@ int run_program(const Program& prog_ref, int nq, void* states, int64_t n_states,
       if (e != cudaSuccess) return cuda_fail(e, "sweep kernel launch");
     }
     first = false;
+    if (deadline_s > 0.0 && li < prog->launches.size()) {
+      cudaError_t se = cudaStreamSynchronize(st);
+      if (se != cudaSuccess) return cuda_fail(se, "cudaStreamSynchronize");
+      const double now = std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+      if (now > deadline_s)
+        return fail(CS_ERR_TIMEOUT, "simulation exceeded its deadline after " + std::to_string(li) + "/" +
+                                        std::to_string(prog->launches.size()) + " sweep launches");
+    }
   }
   return CS_OK;
 }
@@ -867,6 +878,25 @@ int cs_sim_batch(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int6
     return fail(pe.code, pe.msg);
   }
   return run_program(*prog, nq, states, n_states, state_stride, variant_base, init_zero, dtype, st);
+}
+
+int cs_sim_batch_until(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int64_t* qb,
+                       const double* params, const int32_t* slots, int64_t n_gates, void* states, int64_t n_states,
+                       int64_t state_stride, uint64_t variant_base, int32_t init_zero, int32_t dtype, void* stream,
+                       double deadline_s) {
+  if (!valid_dtype(dtype)) return fail(CS_ERR_INVALID, "dtype must be CS_C128 or CS_C64");
+  if (nq < 1 || nq > 62) return fail(CS_ERR_INVALID, "qubit count out of range");
+  if (!states || n_states < 1) return fail(CS_ERR_INVALID, "empty state batch");
+  if (state_stride < (int64_t(1) << nq)) return fail(CS_ERR_INVALID, "state_stride smaller than 2^nq");
+  if (n_gates < 0 || (n_gates > 0 && (!kinds || !qa || !qb))) return fail(CS_ERR_INVALID, "bad gate table");
+  std::shared_ptr<const Program> prog;
+  try {
+    prog = build_schedule(nq, kinds, qa, qb, params, slots, n_gates, n_states, 0, dtype);
+  } catch (const PlanError& pe) {
+    return fail(pe.code, pe.msg);
+  }
+  return run_program(*prog, nq, states, n_states, state_stride, variant_base, init_zero, dtype, as_stream(stream),
+                     deadline_s);
 }
 
 int cs_sweep_plan_json(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int64_t* qb,

@@ -9,3 +9,4 @@
 #define CS_ERR_INTERNAL 5  /* -> CutbenchError */
 #define CS_ERR_NODEVICE 6  /* -> NativeUnavailableError */
 #define CS_ERR_TOPOLOGY 7  /* -> UnsupportedTopologyError */
+#define CS_ERR_TIMEOUT 8   /* -> BudgetExceededError */

@@ -139,8 +139,10 @@ def _expired(deadline) -> bool:
 
 
 def run_table(states, nq: int, table: GateTable, *, slots=None, variant_base: int = 0,
-              init_zero: bool = False, dtype=np.complex128, stream=None) -> None:
-    """Launch the sweep kernel on a device batch [n_states, 2^nq] (in place)."""
+              init_zero: bool = False, dtype=np.complex128, stream=None, deadline=None) -> None:
+    """Launch the sweep kernel on a device batch [n_states, 2^nq] (in place).
+    deadline (time.monotonic() seconds): checked after every sweep launch in
+    the library (cs_sim_batch_until), BudgetExceededError once passed."""
     lib = _native.load()
     k = np.ascontiguousarray(table.kinds, dtype=np.uint8)
     qa = _native.c_i64(table.qa)
@@ -149,6 +151,15 @@ def run_table(states, nq: int, table: GateTable, *, slots=None, variant_base: in
     sl = _native.c_i32(slots) if slots is not None else None
     n_states = states.shape[0] if states.dim() == 2 else 1
     stride = states.stride(0) if states.dim() == 2 else (1 << nq)
+    if deadline is not None and nq >= 1:
+        _native.check(
+            lib.cs_sim_batch_until(nq, _native.ptr(k), _native.ptr(qa), _native.ptr(qb), _native.ptr(prm),
+                                   _native.ptr(sl), len(k), states.data_ptr(), n_states, stride,
+                                   int(variant_base), 1 if init_zero else 0, _device.code_of(dtype),
+                                   _device.stream_ptr(stream), float(deadline)),
+            "cs_sim_batch_until",
+        )
+        return
     _native.check(
         lib.cs_sim_batch(nq, _native.ptr(k), _native.ptr(qa), _native.ptr(qb), _native.ptr(prm),
                          _native.ptr(sl), len(k), states.data_ptr(), n_states, stride,
@@ -158,38 +169,19 @@ def run_table(states, nq: int, table: GateTable, *, slots=None, variant_base: in
     )
 
 
-def _slice_table(table: GateTable, a: int, b: int) -> GateTable:
-    return GateTable(table.kinds[a:b], table.qa[a:b], table.qb[a:b], table.params[a:b])
-
-
 def simulate_table(nq: int, table: GateTable, *, n_states: int = 1, slots=None,
                    deadline=None, dtype=np.complex128, out=None, stream=None, variant_base: int = 0):
     """Simulate a (template) table for a batch of variant states; returns the
-    device tensor [n_states, 2^nq]. With a deadline, launches go in chunks
-    with a check (and a stream synchronise) between them."""
+    device tensor [n_states, 2^nq]. With a deadline the library synchronises
+    and checks it after every sweep launch (BudgetExceededError)."""
     _device.require_cuda()
     if _expired(deadline):
         raise BudgetExceededError(f"simulation exceeded its deadline after 0/{len(table)} gates")
     states = out if out is not None else _device.empty(n_states, nq, dtype)
-    if deadline is None:
-        run_table(states, nq, table, slots=slots, init_zero=True, dtype=dtype, stream=stream,
-                  variant_base=variant_base)
-        return states
-    chunk = max(1, min(len(table), (1 << 26) // max(1, (1 << nq) * n_states)))
-    g = len(table)
-    start = 0
-    first = True
-    while first or start < g:
-        stop = min(g, start + chunk)
-        run_table(states, nq, _slice_table(table, start, stop),
-                  slots=None if slots is None else slots[start:stop], init_zero=first,
-                  dtype=dtype, stream=stream, variant_base=variant_base)
-        first = False
-        start = stop
-        if start < g:
-            _device.torch().cuda.current_stream().synchronize()
-            if _expired(deadline):
-                raise BudgetExceededError(f"simulation exceeded its deadline after {start}/{g} gates")
+    # with a deadline the library checks it after every sweep launch (the
+    # fused program is unchanged; granularity = one sweep)
+    run_table(states, nq, table, slots=slots, init_zero=True, dtype=dtype, stream=stream,
+              variant_base=variant_base, deadline=deadline)
     return states
 
 

@@ -477,3 +477,18 @@ def test_native_nccl_comm_world1(cb):
         assert np.array_equal(res.cpu().numpy(), cb.run_cut(circ, 2).amps)
     finally:
         comm.destroy()
+
+
+def test_deadline_checked_per_sweep_without_splitting_the_program(cb):
+    """simulate(deadline=...) runs the same fused program as without one
+    (cs_sim_batch_until checks the budget after every sweep launch): results
+    identical, and a budget that expires mid-run raises BudgetExceededError
+    (the reference's cooperative timeout, engine.py:142-155)."""
+    circ = cb.build_brickwall(cb.BrickwallSpec(24, 10, 2, 2, 1))
+    free = cb.simulate(circ).amps
+    timed = cb.simulate(circ, deadline=time.monotonic() + 60).amps
+    assert np.array_equal(free, timed)
+    big = cb.build_brickwall(cb.BrickwallSpec(28, 10, 2, 2, 1))
+    cb.simulate(big, max_qubits=28)  # build (and compile) the program first
+    with pytest.raises(cb.BudgetExceededError):
+        cb.simulate(big, max_qubits=28, deadline=time.monotonic() + 1e-4)
