@@ -34,6 +34,9 @@ cudaError_t launch_merge_dmma3(const MergeParams& p, int K, int warps, dim3 grid
                                cudaStream_t stream);
 int merge_dmma3_cols_per_warp(int K);
 int merge_dmma3_row_blocks(int K);
+bool merge_ozaki_supported(int K, int64_t lo_len, int64_t nrows);
+cudaError_t launch_merge_ozaki(const MergeParams& mp, int64_t nrows, void* out, int accumulate, int sms,
+                               cudaStream_t stream);
 cudaError_t launch_init_basis(void* states, int64_t len, int64_t n_states, int64_t index, int dtype,
                               cudaStream_t stream);
 cudaError_t launch_reduce(const void* a, const void* b, int64_t n, int mode, int dtype, double2* scratch,
@@ -64,6 +67,8 @@ struct Options {
   int64_t merge_dmma3_warps = 8;  // warps per CTA of the 3M kernel (8: 2 CTAs/SM, 4: 4 CTAs/SM)
   int64_t merge_smem_kb = 96;  // staged-row budget per CTA of the tensor-core merge
   int64_t merge_dmma = 2;  // FP64 tensor-core merge: 1 = four real GEMMs, 2 = three (3M)
+  int64_t merge_ozaki = 1;        // int8 tcgen05 merge (exact FP64 splitting) for K >= merge_ozaki_min_k
+  int64_t merge_ozaki_min_k = 16;
   int64_t engine = 1;      // 1: register-tile kernel (rsweep), 0: shared-memory tile kernel (sweep)
   int64_t jit = 0;         // 0 never, 1 from a program's 2nd use, 2 always: NVRTC-specialised sweeps (opt-in: compile ~1-7 s)
   int64_t jit_max_cost = 40000;  // FP64 instructions per specialised launch (code-size guard)
@@ -302,6 +307,12 @@ bool dmma3_eligible(int K, int dtype, int64_t lo_len) {
          lo_len >= merge_dmma3_cols_per_warp(K);
 }
 
+// merge_ozaki: the int8 tcgen05 kernel (ozaki.cu) for K >= merge_ozaki_min_k
+bool ozaki_eligible(int K, int dtype, int64_t lo_len, int64_t nrows) {
+  return g_opt.merge_ozaki && dtype == CS_C128 && K >= g_opt.merge_ozaki_min_k &&
+         merge_ozaki_supported(K, lo_len, nrows);
+}
+
 // Launch one merge_terms problem whose K is one instantiated width.
 int merge_launch_one(int S, int Kc, const int32_t* hidx, const int32_t* lidx, const double* coef,
                      int64_t stride_terms, const void* hi, int64_t hi_len, const void* lo, int64_t lo_len,
@@ -310,6 +321,35 @@ int merge_launch_one(int S, int Kc, const int32_t* hidx, const int32_t* lidx, co
   // stride_terms: distance between consecutive slots' term lists in hidx/lidx
   const int threads = 256;
   const size_t eb0 = elem_bytes(dtype);
+  if (ozaki_eligible(Kc, dtype, lo_len, row_end - row_begin)) {
+    // int8 tensor-core merge (ozaki.cu): one problem per slot
+    static MergeParams po;
+    static std::mutex pom;
+    std::lock_guard<std::mutex> lk(pom);
+    for (int s = 0; s < S; ++s) {
+      std::memset(&po, 0, offsetof(MergeParams, hidx));
+      po.hi = hi;
+      po.lo = lo;
+      po.hi_len = hi_len;
+      po.lo_len = lo_len;
+      po.row_begin = row_begin;
+      po.row_end = row_end;
+      po.S = 1;
+      po.K = Kc;
+      for (int t = 0; t < Kc; ++t) {
+        const int64_t src = int64_t(s) * stride_terms + t;
+        po.hidx[t] = hidx[src];
+        po.lidx[t] = lidx[src];
+        po.coef[2 * t] = coef[2 * src];
+        po.coef[2 * t + 1] = coef[2 * src + 1];
+      }
+      void* o = static_cast<char*>(out) + size_t(s) * size_t(out_slot_stride) * elem_bytes(dtype);
+      cudaError_t e = launch_merge_ozaki(po, row_end - row_begin, o, accumulate, sm_count(), stream);
+      g_launches.fetch_add(3);
+      if (e != cudaSuccess) return cuda_fail(e, "merge_ozaki launch");
+    }
+    return CS_OK;
+  }
   const bool m3 = dmma3_eligible(Kc, dtype, lo_len);
   if (m3 || dmma_eligible(Kc, dtype, lo_len)) {
     // tensor-core path: 8 warps over ncg column groups of (16, 8 or 4)
@@ -473,8 +513,10 @@ int merge_terms_impl(int S, int K, const int32_t* hidx, const int32_t* lidx, con
   while (t0 < K) {
     int rem = K - t0;
     int kc = rem >= 16 ? 16 : rem >= 8 ? 8 : rem >= 4 ? 4 : rem >= 2 ? 2 : 1;
-    if (rem >= 64 && dmma_eligible(64, dtype, lo_len)) kc = 64;
-    else if (rem >= 32 && dmma_eligible(32, dtype, lo_len)) kc = 32;
+    if (rem >= 64 && (dmma_eligible(64, dtype, lo_len) || ozaki_eligible(64, dtype, lo_len, row_end - row_begin)))
+      kc = 64;
+    else if (rem >= 32 && (dmma_eligible(32, dtype, lo_len) || ozaki_eligible(32, dtype, lo_len, row_end - row_begin)))
+      kc = 32;
     int rc = merge_launch_one(S, kc, hidx + t0, lidx + t0, coef + 2 * t0, K, hi, hi_len, lo, lo_len, row_begin,
                               row_end, out, out_slot_stride, acc, dtype, stream);
     if (rc != CS_OK) return rc;
@@ -797,6 +839,12 @@ int cs_set_option(const char* key, int64_t value) {
   } else if (k == "merge_dmma3_warps") {
     if (value != 4 && value != 8) return fail(CS_ERR_INVALID, "merge_dmma3_warps must be 4 or 8");
     g_opt.merge_dmma3_warps = value;
+  } else if (k == "merge_ozaki") {
+    g_opt.merge_ozaki = value ? 1 : 0;
+  } else if (k == "merge_ozaki_min_k") {
+    if (value != 8 && value != 16 && value != 32 && value != 64)
+      return fail(CS_ERR_INVALID, "merge_ozaki_min_k must be 8, 16, 32 or 64");
+    g_opt.merge_ozaki_min_k = value;
   } else if (k == "merge_dmma") {
     if (value < 0 || value > 2) return fail(CS_ERR_INVALID, "merge_dmma must be 0, 1 or 2");
     g_opt.merge_dmma = value;
@@ -833,6 +881,8 @@ int64_t cs_get_option(const char* key) {
   if (k == "jit") return g_opt.jit;
   if (k == "jit_max_cost") return g_opt.jit_max_cost;
   if (k == "merge_dmma") return g_opt.merge_dmma;
+  if (k == "merge_ozaki") return g_opt.merge_ozaki;
+  if (k == "merge_ozaki_min_k") return g_opt.merge_ozaki_min_k;
   if (k == "merge_smem_kb") return g_opt.merge_smem_kb;
   if (k == "merge_dmma3_warps") return g_opt.merge_dmma3_warps;
   if (k == "jit_minb") return g_jit_minb;

@@ -1,0 +1,599 @@
+// Tensor-core merge for K >= 8 terms: the complex rank-K product of the n=2
+// merge (merging.py:86-94 `_axpy_outer`, summed over m as in merging.py:178-185)
+//   out[h][l] = sum_t (coef_t hi_t[h]) lo_t[l]
+// computed exactly on the int8 tensor cores (tcgen05.mma kind::i8, TMEM
+// accumulators) by error-free splitting of the FP64 operands (Ozaki scheme).
+//
+// Real GEMM form: D[l][(h,v)] = sum_k A[l][k] B[(h,v)][k], k = 2t+u,
+//   A[l] = (lr_0, li_0, lr_1, li_1, ...),
+//   B[(h,0)] = (Hr_0, -Hi_0, ...)  -> Re out,   B[(h,1)] = (Hi_0, Hr_0, ...) -> Im out.
+// Every row of A (per l) and every pair of rows of B (per h) is scaled by a
+// power of two 2^-e so its entries are < 1/2 in magnitude and split into
+// S = 8 balanced base-128 digits (int8, |d| <= 65) of its 56-bit fixed-point
+// rounding (exact for every entry's bits down to 2^-57 of the row maximum). Digit products of equal
+// weight i + j = p ("diagonal p") accumulate exactly in int32:
+//   D_p = sum_{i+j=p} A_i B_j^T,      out = 2^(e_l + e_h) sum_p 2^-7(p+2) D_p
+// keeping p <= S-1 (the dropped terms are < 2^-56 relative to the row/column
+// maxima: the rounding level of a K-term FP64 dot product).
+//
+// Diagonal stacking: the B digit slices of one h block are stacked along N
+// (slice j = rows 32j..32j+31), so ONE MMA per A slice i,
+//   D[:, 32i : 256] += A_i . [B_0; ...; B_{7-i}]^T      (N = 32 (8 - i)),
+// adds A_i B_{p-i} into every diagonal p >= i at once: 8 MMAs per k-step
+// instead of 36, each long enough (N = 32..256) to stay above the ~66-cycle
+// per-instruction issue cost measured for small N (tools/tc_i8_probe.cu).
+//
+// Roles per CTA (persistent, one per SM): warp 0 streams digit blocks with
+// cp.async.bulk (TMA bulk copies, mbarrier complete_tx), warp 1 issues the
+// MMAs (one elected lane) into one of two 256-column TMEM accumulators, warps
+// 2..9 drain TMEM (tcgen05.ld), combine the diagonals pairwise in int32,
+// convert to FP64, scale and write each output amplitude once
+// (st.global.cs, 512 contiguous bytes per warp store).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <map>
+#include <mutex>
+
+#include "ops.hpp"
+
+namespace cutsim {
+namespace {
+
+constexpr int kSlices = 8;
+constexpr int kHB = 16;                      // h rows per tile (32 real B rows per slice)
+constexpr int kLT = 128;                     // l rows per tile (MMA M)
+constexpr int kEpiWarps = 16;                // two groups of 8 (alternate tiles)
+constexpr int kThreads = 64 + 32 * kEpiWarps;
+constexpr int kABlock = kLT * 32;            // one (k-step, slice) block of A: 4 KiB
+constexpr int kBBlock = 2 * kHB * 32;        // one (k-step, slice) block of B: 1 KiB
+
+__device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(ptr));
+}
+
+// K-major, no-swizzle canonical layout: core matrix = 8 rows x 16 B (128 B
+// contiguous), 16-byte K chunks 128 B apart (LBO), 8-row groups 256 B apart (SBO)
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr) {
+  return uint64_t((saddr >> 4) & 0x3FFF) | (uint64_t(128 >> 4) << 16) | (uint64_t(256 >> 4) << 32) |
+         (uint64_t(1) << 46);
+}
+
+__host__ __device__ constexpr uint32_t idesc_i8(int n) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(n >> 3) << 17) | (uint32_t(kLT >> 4) << 24);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tWAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE;\n\tbra WAIT;\n\tDONE:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// whole-warp: one elected lane arms the barrier and issues the bulk copy
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%3], %2;\n\t"
+      "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n\t}" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// The tcgen05 issue helpers are executed by a whole warp; elect.sync inside
+// the asm picks the issuing lane. (Issued from a single-lane branch instead,
+// the compiler wraps each instruction in an ELECT loop and a chain of
+// dependent MMAs runs at ~240 cycles per instruction instead of the
+// 128 N / 256 floor: tools/tc_i8_probe.cu.)
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void tc_after_sync() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_before_sync() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(taddr));
+}
+
+// power-of-two exponent e with max|x| * 2^-e < 1/2, from the double's bits
+// (0 for an all-zero row)
+__device__ __forceinline__ int row_exponent(double mx) {
+  const int b = int((__double_as_longlong(mx) >> 52) & 0x7ff);
+  return b ? b - 1021 : 0;  // mx in [2^(b-1023), 2^(b-1022))
+}
+
+// 2^(56 - e): the fixed-point scale of a row (clamped for rows below ~1e-290,
+// whose digits then keep fewer bits)
+__device__ __forceinline__ double digit_scale(int e) {
+  const int b = min(max(56 - e + 1023, 1), 2046);
+  return __hiloint2double(b << 20, 0);
+}
+
+// 8 balanced base-128 digits of y = x 2^-e (|y| <= 1/2): Y = rint(y 2^56)
+// (|Y| <= 2^55: the 2^-57 rounding is the scheme's truncation level), then
+// d_7..d_1 = ((Y + 64) & 127) - 64 in [-64, 63] from the least significant
+// end and d_0 = what remains (|d_0| <= 65); y ~ sum_i d_i 128^-(i+1).
+__device__ __forceinline__ void digits8(double x, double scale, int (&d)[kSlices]) {
+  long long Y = __double2ll_rn(x * scale);
+#pragma unroll
+  for (int i = kSlices - 1; i > 0; --i) {
+    const int di = int((Y + 64) & 127) - 64;
+    d[i] = di;
+    Y = (Y - di) >> 7;
+  }
+  d[0] = int(Y);
+}
+
+__device__ __forceinline__ uint32_t cm_row_off(int r) { return uint32_t((r >> 3) * 256 + (r & 7) * 16); }
+
+__device__ __forceinline__ uint32_t pack2(int a, int b) {
+  return uint32_t(uint8_t(int8_t(a))) | (uint32_t(uint8_t(int8_t(b))) << 8);
+}
+
+// the digit-preparation kernels' inputs (one slot, K <= 64 terms; a small
+// parameter block keeps their launches cheap)
+struct OzPrep {
+  const double2* hi;
+  const double2* lo;
+  int64_t hi_len, lo_len, row_begin;
+  int32_t K;
+  int32_t hidx[64];
+  int32_t lidx[64];
+  double2 coef[64];
+};
+
+// ---------------------------------------------------------------------------
+// digit preparation: A (the lo side), one thread per (l, k-step)
+// adig layout: [l_tile][ks][slice][4096 B canonical block]; sa[l] = 2^(e_l - 35)
+// ---------------------------------------------------------------------------
+template <int KS>
+__global__ void ozaki_prep_lo(const __grid_constant__ OzPrep p, int8_t* adig, double* sa) {
+  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= p.lo_len * KS) return;
+  const int ks = int(idx / p.lo_len);
+  const int64_t l = idx - int64_t(ks) * p.lo_len;
+  const double2* lo = p.lo;
+  const int K = p.K;
+  double mx = 0.0;
+  for (int t = 0; t < K; ++t) {
+    const double2 v = __ldg(lo + int64_t(p.lidx[t]) * p.lo_len + l);
+    mx = fmax(mx, fmax(fabs(v.x), fabs(v.y)));
+  }
+  const int e = row_exponent(mx);
+  if (ks == 0) sa[l] = ldexp(1.0, e - 35);
+  const double sc = digit_scale(e);
+  uint32_t w[kSlices][8];
+#pragma unroll
+  for (int tt = 0; tt < 16; ++tt) {
+    const int t = 16 * ks + tt;
+    double2 v = make_double2(0.0, 0.0);
+    if (t < K) v = __ldg(lo + int64_t(p.lidx[t]) * p.lo_len + l);
+    int dr[kSlices], di[kSlices];
+    digits8(v.x, sc, dr);
+    digits8(v.y, sc, di);
+#pragma unroll
+    for (int i = 0; i < kSlices; ++i) {
+      // bytes 2tt, 2tt + 1 of the row's 32-byte k-step: (re, im)
+      const uint32_t pr = pack2(dr[i], di[i]) << (16 * (tt & 1));
+      if (tt & 1) w[i][tt >> 1] |= pr;
+      else w[i][tt >> 1] = pr;
+    }
+  }
+  int8_t* base = adig + (l >> 7) * int64_t(KS * kSlices * kABlock) + cm_row_off(int(l & 127));
+#pragma unroll
+  for (int i = 0; i < kSlices; ++i) {
+    int8_t* blk = base + (ks * kSlices + i) * kABlock;
+    *reinterpret_cast<uint4*>(blk) = make_uint4(w[i][0], w[i][1], w[i][2], w[i][3]);
+    *reinterpret_cast<uint4*>(blk + 128) = make_uint4(w[i][4], w[i][5], w[i][6], w[i][7]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// digit preparation: B (the hi side with the coefficients), one thread per
+// (h, k-step); bdig layout: [h_block][ks][slice][1024 B canonical block],
+// row r = 2 (h % 16) + v; sb[h] = 2^e_h
+// ---------------------------------------------------------------------------
+template <int KS>
+__global__ void ozaki_prep_hi(const __grid_constant__ OzPrep p, int64_t nrows, int8_t* bdig, double* sb) {
+  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= nrows * KS) return;
+  const int ks = int(idx / nrows);
+  const int64_t hr = idx - int64_t(ks) * nrows;
+  const int64_t h = p.row_begin + hr;
+  const double2* hi = p.hi;
+  const int K = p.K;
+  double mx = 0.0;
+  for (int t = 0; t < K; ++t) {
+    const double2 v = __ldg(hi + int64_t(p.hidx[t]) * p.hi_len + h);
+    const double cr = p.coef[t].x, ci = p.coef[t].y;
+    mx = fmax(mx, fmax(fabs(v.x * cr - v.y * ci), fabs(v.x * ci + v.y * cr)));
+  }
+  const int e = row_exponent(mx);
+  if (ks == 0) sb[hr] = ldexp(1.0, e);
+  const double sc = digit_scale(e);
+  uint32_t w0[kSlices][8], w1[kSlices][8];
+#pragma unroll
+  for (int tt = 0; tt < 16; ++tt) {
+    const int t = 16 * ks + tt;
+    double br = 0.0, bi = 0.0;
+    if (t < K) {
+      const double2 v = __ldg(hi + int64_t(p.hidx[t]) * p.hi_len + h);
+      const double cr = p.coef[t].x, ci = p.coef[t].y;
+      br = v.x * cr - v.y * ci;
+      bi = v.x * ci + v.y * cr;
+    }
+    int dr[kSlices], di[kSlices];
+    digits8(br, sc, dr);
+    digits8(bi, sc, di);
+#pragma unroll
+    for (int i = 0; i < kSlices; ++i) {
+      // row (h, 0): (Hr, -Hi) -> real part; row (h, 1): (Hi, Hr) -> imaginary part
+      const uint32_t p0 = pack2(dr[i], -di[i]) << (16 * (tt & 1));
+      const uint32_t p1 = pack2(di[i], dr[i]) << (16 * (tt & 1));
+      if (tt & 1) {
+        w0[i][tt >> 1] |= p0;
+        w1[i][tt >> 1] |= p1;
+      } else {
+        w0[i][tt >> 1] = p0;
+        w1[i][tt >> 1] = p1;
+      }
+    }
+  }
+  const int hl = int(hr & (kHB - 1));
+  int8_t* base = bdig + (hr / kHB) * int64_t(KS * kSlices * kBBlock);
+#pragma unroll
+  for (int i = 0; i < kSlices; ++i) {
+    int8_t* blk = base + (ks * kSlices + i) * kBBlock;
+    int8_t* r0 = blk + cm_row_off(2 * hl);
+    int8_t* r1 = blk + cm_row_off(2 * hl + 1);
+    *reinterpret_cast<uint4*>(r0) = make_uint4(w0[i][0], w0[i][1], w0[i][2], w0[i][3]);
+    *reinterpret_cast<uint4*>(r0 + 128) = make_uint4(w0[i][4], w0[i][5], w0[i][6], w0[i][7]);
+    *reinterpret_cast<uint4*>(r1) = make_uint4(w1[i][0], w1[i][1], w1[i][2], w1[i][3]);
+    *reinterpret_cast<uint4*>(r1 + 128) = make_uint4(w1[i][4], w1[i][5], w1[i][6], w1[i][7]);
+  }
+}
+
+struct OzParams {
+  const int8_t* adig;
+  const int8_t* bdig;
+  const double* sa;  // per l: 2^(e_l - 35)
+  const double* sb;  // per h: 2^e_h
+  double2* out;  // row 0 of the range
+  int64_t W;     // lo_len
+  int64_t n_hb;  // h blocks in the range
+  int64_t n_lt;   // l tiles (W / 128)
+  int64_t n_hc;   // h chunks: work unit u = (h chunk u / n_lt, l tile u % n_lt)
+  int64_t n_units;
+};
+
+// Work units = (h chunk, l tile), dealt round-robin to the persistent CTAs
+// with the l tile fastest: at any moment the CTAs write the same h rows at
+// consecutive l tiles (long contiguous row segments for the DRAM write
+// stream; h-chunk-major per CTA instead gave 2 KB row pieces scattered over
+// the state and ~5.5 TB/s). Inside a unit a CTA walks its h blocks with the
+// unit's A digits resident in shared memory.
+struct TileWalk {
+  const OzParams& p;
+  int64_t u, lt, hb, hb_end;
+  __device__ explicit TileWalk(const OzParams& pp) : p(pp), u(blockIdx.x) { begin(); }
+  __device__ void begin() {
+    if (u >= p.n_units) return;
+    const int64_t hc = u / p.n_lt;
+    lt = u - hc * p.n_lt;
+    hb = hc * p.n_hb / p.n_hc;
+    hb_end = (hc + 1) * p.n_hb / p.n_hc;
+  }
+  __device__ bool valid() const { return u < p.n_units; }
+  __device__ void next() {
+    if (++hb == hb_end) {
+      u += gridDim.x;
+      begin();
+    }
+  }
+};
+
+template <int KS, int NST, bool ACC>
+__global__ void __launch_bounds__(kThreads, 1) ozaki_merge_kernel(const __grid_constant__ OzParams p) {
+  constexpr uint32_t A_BYTES = KS * kSlices * kABlock;
+  constexpr uint32_t B_BYTES = KS * kSlices * kBBlock;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  int8_t* sA = reinterpret_cast<int8_t*>(smem);
+  int8_t* sB = reinterpret_cast<int8_t*>(smem + A_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + A_BYTES + NST * B_BYTES);
+  uint64_t* full = bars;             // [NST]
+  uint64_t* empty = bars + NST;      // [NST]
+  uint64_t* afull = bars + 2 * NST;
+  uint64_t* aempty = afull + 1;
+  uint64_t* tfull = aempty + 1;      // [2]
+  uint64_t* tempty = tfull + 2;      // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  // warp index through a shuffle so the compiler knows it is warp-uniform
+  // (TMEM addresses derived from it then stay in uniform registers)
+  const int warp = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0);
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    mbar_init(afull, 1);
+    mbar_init(aempty, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(tfull + b, 1);
+      mbar_init(tempty + b, kEpiWarps / 2);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_before_sync();
+  __syncthreads();
+  tc_after_sync();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    {
+      int64_t cur = -1;
+      uint32_t aph = 0;
+      int it = 0;
+      for (TileWalk w(p); w.valid(); w.next(), ++it) {
+        const int64_t lt = w.lt, hb = w.hb;
+        if (lt != cur) {
+          if (cur >= 0) {
+            mbar_wait(aempty, aph);
+            aph ^= 1;
+          }
+          bulk_load(sA, p.adig + lt * A_BYTES, A_BYTES, afull);
+          cur = lt;
+        }
+        const int st = it % NST;
+        const uint32_t ph = (it / NST) & 1;
+        mbar_wait(empty + st, ph ^ 1);
+        bulk_load(sB + st * B_BYTES, p.bdig + hb * B_BYTES, B_BYTES, full + st);
+      }
+    }
+  } else if (warp == 1) {
+    {
+      int64_t cur = -1;
+      uint32_t aph = 0;
+      int it = 0;
+      const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
+      for (TileWalk w(p); w.valid(); w.next(), ++it) {
+        const int64_t lt = w.lt;
+        if (lt != cur) {
+          if (cur >= 0) mma_commit(aempty);
+          mbar_wait(afull, aph);
+          aph ^= 1;
+          cur = lt;
+        }
+        const int st = it % NST;
+        mbar_wait(full + st, (it / NST) & 1);
+        const int b = it & 1;
+        mbar_wait(tempty + b, ((it >> 1) & 1) ^ 1);
+        tc_after_sync();
+        const uint32_t dbase = tmem + uint32_t(b * 256);
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          const uint64_t db = smem_desc(b0 + st * B_BYTES + ks * kSlices * kBBlock);
+#pragma unroll
+          for (int i = 0; i < kSlices; ++i) {
+            const uint64_t da = smem_desc(a0 + (ks * kSlices + i) * kABlock);
+            mma_i8(dbase + uint32_t(32 * i), da, db, idesc_i8(32 * (kSlices - i)), (ks | i) ? 1u : 0u);
+          }
+        }
+        mma_commit(empty + st);
+        mma_commit(tfull + b);
+      }
+    }
+  } else {
+    // two groups of 8 warps take alternate tiles (= alternate TMEM buffers), so
+    // one group's TMEM loads and barrier waits overlap the other's math and
+    // stores; in a group every lane quarter q has two warps, one per 8 h rows
+    const int g = (warp - 2) >> 3;
+    const int wg = (warp - 2) & 7;
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int hl_base = (wg >> 2) * 8;
+    const uint32_t tbase = tmem + (uint32_t(q * 32) << 16) + uint32_t(g * 256);
+    uint32_t n = 0;
+    int it = 0;
+    for (TileWalk w(p); w.valid(); w.next(), ++it) {
+      if ((it & 1) != g) continue;
+      const int64_t lt = w.lt, hb = w.hb;
+      const int64_t l = lt * kLT + q * 32 + lane;
+      const double sl = __ldg(p.sa + l);  // 2^(e_l - 35)
+      mbar_wait(tfull + g, n & 1);
+      ++n;
+      tc_after_sync();
+      uint32_t d[2][kSlices][8];
+#pragma unroll
+      for (int pd = 0; pd < kSlices; ++pd) tmem_ld8(tbase + uint32_t(pd * 32 + 2 * hl_base), d[0][pd]);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int pd = 0; pd < kSlices; ++pd) tmem_ld8(tbase + uint32_t(pd * 32 + 2 * (hl_base + 4)), d[1][pd]);
+#pragma unroll
+      for (int hc = 0; hc < 2; ++hc) {
+        if (hc == 1) {  // second chunk landed under the first one's math: hand the buffer back
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          tc_before_sync();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(tempty + g);
+        }
+        const int hl0 = hl_base + 4 * hc;
+        double2* dst = p.out + (hb * kHB + hl0) * p.W + l;
+        const double* sbp = p.sb + hb * kHB + hl0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j, dst += p.W) {
+          const double s = sl * __ldg(sbp + j);
+          double v2[2];
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            const int c = 2 * j + v;
+            // P_m = 128 D_2m + D_2m+1 (|D_p| < 2^23: exact in int32), then
+            // Q0 = 2^14 P_0 + P_1, Q1 = 2^14 P_2 + P_3 (|Q| < 2^45: exact in
+            // int64 and in a double), converted with the 1.5 * 2^52 bias:
+            //   sum_p 2^-7(p+2) D_p = 2^-35 (Q0 + 2^-28 Q1)
+            const int p0 = int(d[hc][0][c]) * 128 + int(d[hc][1][c]);
+            const int p1 = int(d[hc][2][c]) * 128 + int(d[hc][3][c]);
+            const int p2 = int(d[hc][4][c]) * 128 + int(d[hc][5][c]);
+            const int p3 = int(d[hc][6][c]) * 128 + int(d[hc][7][c]);
+            const long long q0 = (static_cast<long long>(p0) << 14) + p1;
+            const long long q1 = (static_cast<long long>(p2) << 14) + p3;
+            const double f0 = __longlong_as_double(q0 + 0x4338000000000000LL) - 0x1.8p52;
+            const double f1 = __longlong_as_double(q1 + 0x4338000000000000LL) - 0x1.8p52;
+            v2[v] = fma(f1, 0x1p-28, f0) * s;
+          }
+          double2 val = make_double2(v2[0], v2[1]);
+          if (ACC) {
+            const double2 prev = *dst;
+            val.x += prev.x;
+            val.y += prev.y;
+          }
+          __stcs(dst, val);  // evict-first: the state is written once
+        }
+      }
+    }
+  }
+  tc_before_sync();
+  __syncthreads();
+  tc_after_sync();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+template <int KS, int NST>
+constexpr size_t oz_smem() {
+  return size_t(KS) * kSlices * kABlock + size_t(NST) * KS * kSlices * kBBlock + 256;
+}
+
+// digit workspace per stream (grow-only; merges on different streams may overlap)
+struct Workspace {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+std::map<cudaStream_t, Workspace> g_oz_ws;
+std::mutex g_oz_mu;
+
+template <int KS, int NST>
+cudaError_t run_ozaki(const MergeParams& mp, int64_t nrows, void* out, int accumulate, int sms,
+                      cudaStream_t stream) {
+  const int64_t W = mp.lo_len;
+  const size_t a_bytes = size_t(W / kLT) * KS * kSlices * kABlock;
+  const size_t b_bytes = size_t(nrows / kHB) * KS * kSlices * kBBlock;
+  const size_t ea_bytes = size_t(W) * 8, eb_bytes = size_t(nrows) * 8;
+  const size_t need = a_bytes + b_bytes + ea_bytes + eb_bytes + 1024;
+  std::lock_guard<std::mutex> lk(g_oz_mu);
+  Workspace& ws = g_oz_ws[stream];
+  if (ws.bytes < need) {
+    if (ws.ptr) {
+      cudaError_t e = cudaStreamSynchronize(stream);
+      if (e != cudaSuccess) return e;
+      cudaFree(ws.ptr);
+      ws = Workspace{};
+    }
+    cudaError_t e = cudaMalloc(&ws.ptr, need);
+    if (e != cudaSuccess) return e;
+    ws.bytes = need;
+  }
+  int8_t* adig = static_cast<int8_t*>(ws.ptr);
+  int8_t* bdig = adig + a_bytes;
+  double* sa = reinterpret_cast<double*>(bdig + b_bytes);
+  double* sb = sa + W;
+  OzPrep pp;
+  pp.hi = static_cast<const double2*>(mp.hi);
+  pp.lo = static_cast<const double2*>(mp.lo);
+  pp.hi_len = mp.hi_len;
+  pp.lo_len = mp.lo_len;
+  pp.row_begin = mp.row_begin;
+  pp.K = mp.K;
+  for (int t = 0; t < mp.K; ++t) {
+    pp.hidx[t] = mp.hidx[t];
+    pp.lidx[t] = mp.lidx[t];
+    pp.coef[t] = make_double2(mp.coef[2 * t], mp.coef[2 * t + 1]);
+  }
+  ozaki_prep_lo<KS><<<unsigned((W * KS + 127) / 128), 128, 0, stream>>>(pp, adig, sa);
+  ozaki_prep_hi<KS><<<unsigned((nrows * KS + 127) / 128), 128, 0, stream>>>(pp, nrows, bdig, sb);
+  OzParams op;
+  op.adig = adig;
+  op.bdig = bdig;
+  op.sa = sa;
+  op.sb = sb;
+  op.out = static_cast<double2*>(out);
+  op.W = W;
+  op.n_hb = nrows / kHB;
+  op.n_lt = W / kLT;
+  {
+    // h chunks so that n_lt * n_hc is a multiple of the grid (equal work per CTA)
+    int64_t a = sms, b = op.n_lt;
+    while (b) {
+      const int64_t r = a % b;
+      a = b;
+      b = r;
+    }
+    op.n_hc = std::max<int64_t>(1, std::min<int64_t>(op.n_hb, sms / a));
+  }
+  op.n_units = op.n_lt * op.n_hc;
+
+  // at least ~116 KB of shared memory so that exactly one CTA (and one
+  // 512-column TMEM allocation) lives on each SM
+  const size_t smem = std::max<size_t>(oz_smem<KS, NST>(), 116 * 1024);
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(ozaki_merge_kernel<KS, NST, false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(ozaki_merge_kernel<KS, NST, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(smem));
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  const int64_t grid = std::min<int64_t>(sms, op.n_units);
+  if (accumulate) ozaki_merge_kernel<KS, NST, true><<<unsigned(grid), kThreads, smem, stream>>>(op);
+  else ozaki_merge_kernel<KS, NST, false><<<unsigned(grid), kThreads, smem, stream>>>(op);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+// K in {8, 16, 32, 64} terms (K = 8 pads the inner dimension to 32), complex128,
+// one slot; lo_len % 128 == 0 and (row_end - row_begin) % 16 == 0.
+bool merge_ozaki_supported(int K, int64_t lo_len, int64_t nrows) {
+  return (K == 8 || K == 16 || K == 32 || K == 64) && lo_len >= kLT && lo_len % kLT == 0 && nrows >= kHB &&
+         nrows % kHB == 0;
+}
+
+// mp: hi/lo/hidx/lidx/coef/K/row_begin/hi_len/lo_len as for the other merge
+// kernels (slot 0); out = row row_begin of the output.
+cudaError_t launch_merge_ozaki(const MergeParams& mp, int64_t nrows, void* out, int accumulate, int sms,
+                               cudaStream_t stream) {
+  switch (mp.K) {
+    case 8:
+    case 16: return run_ozaki<1, 6>(mp, nrows, out, accumulate, sms, stream);
+    case 32: return run_ozaki<2, 4>(mp, nrows, out, accumulate, sms, stream);
+    case 64: return run_ozaki<4, 2>(mp, nrows, out, accumulate, sms, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace cutsim

@@ -45,9 +45,13 @@ CASES = [  # (K, S, H, W, rows)
 @pytest.mark.parametrize("dmma", [2, 1, 0])
 @pytest.mark.parametrize("K,S,H,W,rows", CASES)
 def test_merge_terms_vs_numpy(dev, K, S, H, W, rows, dmma):
+    """The FP64 kernels (the int8 tensor-core path is switched off here and
+    tested in test_gpu_ozaki.py)."""
     torch, native = dev
     from paper_2603_01443_b200.merging import merge_terms_device
 
+    old_oz = native.get_option("merge_ozaki")
+    native.set_option("merge_ozaki", 0)
     rng = np.random.default_rng(K * 1000 + W)
     nh, nl = max(2, K), max(2, K)
     hi = rng.normal(size=(nh, H)) + 1j * rng.normal(size=(nh, H))
@@ -64,6 +68,7 @@ def test_merge_terms_vs_numpy(dev, K, S, H, W, rows, dmma):
                                  hidx, lidx, coef, S=S, rows=rows).cpu().numpy()
     finally:
         native.set_option("merge_dmma", old)
+        native.set_option("merge_ozaki", old_oz)
     scale = np.abs(want).max()
     assert np.abs(got - want).max() <= 1e-13 * max(1.0, scale) * K
 
@@ -99,7 +104,12 @@ def test_dmma_kernel_is_used(dev):
     hi = torch.ones(16, 32, dtype=torch.complex128, device="cuda")
     lo = torch.ones(16, 256, dtype=torch.complex128, device="cuda")
     idx = np.arange(16)
-    n0 = native.launch_count()
-    out = merge_terms_device(hi, lo, idx, idx, np.ones(16))
-    assert native.launch_count() == n0 + 1
+    old = native.get_option("merge_ozaki")
+    native.set_option("merge_ozaki", 0)
+    try:
+        n0 = native.launch_count()
+        out = merge_terms_device(hi, lo, idx, idx, np.ones(16))
+        assert native.launch_count() == n0 + 1
+    finally:
+        native.set_option("merge_ozaki", old)
     assert float(out.real.max().item()) == 16.0
