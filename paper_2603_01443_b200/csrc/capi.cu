@@ -67,6 +67,7 @@ struct Options {
   int64_t merge_dmma3_warps = 8;  // warps per CTA of the 3M kernel (8: 2 CTAs/SM, 4: 4 CTAs/SM)
   int64_t merge_smem_kb = 96;  // staged-row budget per CTA of the tensor-core merge
   int64_t merge_dmma = 2;  // FP64 tensor-core merge: 1 = four real GEMMs, 2 = three (3M)
+  int64_t zero_start_tiles = 1;   // from |0..0>: zero the states once, launch only the tiles that can be non-zero
   int64_t merge_ozaki = 1;        // int8 tcgen05 merge (exact FP64 splitting) for K >= merge_ozaki_min_k
   int64_t merge_ozaki_min_k = 16;
   int64_t engine = 1;      // 1: register-tile kernel (rsweep), 0: shared-memory tile kernel (sweep)
@@ -574,6 +575,23 @@ int run_program(const Program& prog_ref, int nq, void* states, int64_t n_states,
   std::lock_guard<std::mutex> lk(pm);
   bool first = true;
   size_t li = 0;
+  // Started from |0..0>, a sweep's tiles beyond 2^zero_tiles_log2 are still
+  // all zero (Sweep::zero_tiles_log2): zero the states once and launch only
+  // the others (cfg4a uncut: the first sweep is one tile instead of 2^18)
+  const bool sparse = init_zero && g_opt.zero_start_tiles &&
+                      std::any_of(prog->launches.begin(), prog->launches.end(), [&](const Launch& l) {
+                        const Sweep& s0 = prog->sweeps[size_t(l.sweep)];
+                        return s0.zero_tiles_log2 < nq - s0.tile_bits;
+                      });
+  if (sparse) {
+    // exactly the states (the caller may keep other data between strided states)
+    const size_t eb = elem_bytes(dtype);
+    cudaError_t e = state_stride == (int64_t(1) << nq)
+                        ? cudaMemsetAsync(states, 0, size_t(n_states) * (size_t(1) << nq) * eb, st)
+                        : cudaMemset2DAsync(states, size_t(state_stride) * eb, 0, (size_t(1) << nq) * eb,
+                                            size_t(n_states), st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
+  }
   for (const Launch& ln : prog->launches) {
     const JitKernel* jk = (jit && li < jit->kernels.size() && jit->kernels[li].kernel) ? &jit->kernels[li] : nullptr;
     ++li;
@@ -581,7 +599,7 @@ int run_program(const Program& prog_ref, int nq, void* states, int64_t n_states,
     const int T = sw.tile_bits;
     if (sw.hq.size() > size_t(kMaxTileBits) || sw.oq.size() > 64)
       return fail(CS_ERR_INTERNAL, "sweep geometry exceeds the kernel limits");
-    const uint32_t n_tiles = uint32_t(1) << (nq - T);
+    const uint32_t n_tiles = uint32_t(1) << (sparse ? std::min(sw.zero_tiles_log2, nq - T) : nq - T);
     for (int64_t v0 = 0; v0 < n_states; v0 += 65535) {
       const int64_t vc = std::min<int64_t>(65535, n_states - v0);
       void* sp = static_cast<char*>(states) + size_t(v0) * size_t(state_stride) * elem_bytes(dtype);
@@ -839,6 +857,8 @@ int cs_set_option(const char* key, int64_t value) {
   } else if (k == "merge_dmma3_warps") {
     if (value != 4 && value != 8) return fail(CS_ERR_INVALID, "merge_dmma3_warps must be 4 or 8");
     g_opt.merge_dmma3_warps = value;
+  } else if (k == "zero_start_tiles") {
+    g_opt.zero_start_tiles = value ? 1 : 0;
   } else if (k == "merge_ozaki") {
     g_opt.merge_ozaki = value ? 1 : 0;
   } else if (k == "merge_ozaki_min_k") {
@@ -882,6 +902,7 @@ int64_t cs_get_option(const char* key) {
   if (k == "jit_max_cost") return g_opt.jit_max_cost;
   if (k == "merge_dmma") return g_opt.merge_dmma;
   if (k == "merge_ozaki") return g_opt.merge_ozaki;
+  if (k == "zero_start_tiles") return g_opt.zero_start_tiles;
   if (k == "merge_ozaki_min_k") return g_opt.merge_ozaki_min_k;
   if (k == "merge_smem_kb") return g_opt.merge_smem_kb;
   if (k == "merge_dmma3_warps") return g_opt.merge_dmma3_warps;

@@ -467,8 +467,33 @@ int sweep_max_group(int tile_bits) {
 
 int g_sweep_windows = 1;
 
+// Order each sweep's tile-id qubits so that, for a start from |0..0>, the
+// tiles that can be non-zero are exactly t < 2^zero_tiles_log2: the qubits
+// already held by an earlier sweep's tile (the support) come first.
+static void order_tiles_for_zero_start(std::vector<Sweep>& sweeps) {
+  uint64_t support = 0;
+  for (Sweep& sw : sweeps) {
+    std::stable_partition(sw.oq.begin(), sw.oq.end(), [&](int q) { return (support >> q) & 1ull; });
+    int m = 0;
+    for (int q : sw.oq) m += int((support >> q) & 1ull);
+    sw.zero_tiles_log2 = m;
+    for (int q = 0; q < sw.low_bits; ++q) support |= 1ull << q;
+    for (int q : sw.hq) support |= 1ull << q;
+  }
+}
+
+static std::vector<Sweep> schedule_sweeps_impl(const std::vector<LOp>& ops, int nq, int tile_bits, int low_bits,
+                                               int max_group);
+
 std::vector<Sweep> schedule_sweeps(const std::vector<LOp>& ops, int nq, int tile_bits, int low_bits,
                                    int max_group) {
+  std::vector<Sweep> sweeps = schedule_sweeps_impl(ops, nq, tile_bits, low_bits, max_group);
+  order_tiles_for_zero_start(sweeps);
+  return sweeps;
+}
+
+static std::vector<Sweep> schedule_sweeps_impl(const std::vector<LOp>& ops, int nq, int tile_bits, int low_bits,
+                                               int max_group) {
   std::vector<Sweep> sweeps;
   if (nq <= tile_bits) {
     Sweep sw;
@@ -650,7 +675,7 @@ std::string sweeps_to_json(const std::vector<Sweep>& sweeps, int nq) {
     for (size_t i = 0; i < sw.hq.size(); ++i) os << (i ? "," : "") << sw.hq[i];
     os << "],\"oq\":[";
     for (size_t i = 0; i < sw.oq.size(); ++i) os << (i ? "," : "") << sw.oq[i];
-    os << "],\"entries\":[";
+    os << "],\"z\":" << sw.zero_tiles_log2 << ",\"entries\":[";
     for (size_t i = 0; i < sw.entries.size(); ++i) {
       const SweepOp& e = sw.entries[i];
       os << (i ? "," : "") << "{\"type\":" << e.type << ",\"target\":" << e.target

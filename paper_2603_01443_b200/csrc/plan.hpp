@@ -64,6 +64,11 @@ struct Sweep {
   int tile_bits = 0, low_bits = 0;
   std::vector<int> hq;           // qubits of local bits [L, T)
   std::vector<int> oq;           // qubits selected by the tile id
+  // started from |0..0>, only the tiles t < 2^zero_tiles_log2 can hold a
+  // non-zero amplitude when this sweep runs: oq lists the qubits some earlier
+  // sweep held in its tile first (a dense op never moves amplitude across
+  // tiles, so a qubit no earlier sweep held is still 0 everywhere)
+  int zero_tiles_log2 = 0;
   std::vector<SweepOp> entries;  // slotted ops take two consecutive entries
 };
 

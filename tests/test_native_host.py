@@ -52,10 +52,16 @@ def test_options_round_trip_and_errors():
 
 
 def execute_schedule(plan, nq, variant=0):
-    """Interpret the exported sweep schedule on a full numpy state."""
+    """Interpret the exported sweep schedule on a full numpy state. Before
+    every sweep, check the zero-start tile bound the kernels rely on: every
+    non-zero amplitude lies in a tile t < 2^z (tile-id bit j <-> qubit oq[j])."""
     amps = orc.zero_state(nq)
     idx = np.arange(1 << nq, dtype=np.int64)
     for sw in plan["sweeps"]:
+        high = 0
+        for q in sw["oq"][sw["z"]:]:
+            high |= 1 << q
+        assert not np.any((idx[np.abs(amps) > 0] & high) != 0), "amplitude outside the zero-start tiles"
         L, hq = sw["L"], sw["hq"]
         glob = list(range(L)) + list(hq)
         ents = sw["entries"]
