@@ -58,6 +58,11 @@ int cs_device_count(int32_t* count);
  * product, 2 three (3M); default 2), "engine" (1 register-tile
  * sweep kernel, 0 shared-memory tile kernel), "jit" (0 never, 1 from a
  * program's second use, 2 always: NVRTC-specialised sweep kernels),
+ * "merge_ozaki" (int8 tcgen05 tensor-core merge with exact FP64 splitting
+ * for one-slot products of K >= "merge_ozaki_min_k" terms, lo_len % 128 == 0,
+ * row ranges % 16 == 0; default 1, min K 16), "zero_start_tiles" (simulations
+ * from |0..0> zero the states once and launch only the tiles that can be
+ * non-zero; default 1),
  * "jit_max_cost", "vb", "sweep_minb", "merge_smem_kb", "merge_dmma3_warps", "jit_minb", "dense_norm" (normalised 2x2s:
  * 0 off, 1 on, 2 = with the NVRTC kernels), "reg_bits", "plan_json" (tuning /
  * testing). */
