@@ -578,7 +578,9 @@ int run_program(const Program& prog_ref, int nq, void* states, int64_t n_states,
   // Started from |0..0>, a sweep's tiles beyond 2^zero_tiles_log2 are still
   // all zero (Sweep::zero_tiles_log2): zero the states once and launch only
   // the others (cfg4a uncut: the first sweep is one tile instead of 2^18)
-  const bool sparse = init_zero && g_opt.zero_start_tiles &&
+  // (small batches — the variant stage's few-MiB L2-resident states — skip
+  // it: the extra zeroing launch costs more than the tiles it saves)
+  const bool sparse = init_zero && g_opt.zero_start_tiles && (int64_t(n_states) << nq) >= (int64_t(1) << 22) &&
                       std::any_of(prog->launches.begin(), prog->launches.end(), [&](const Launch& l) {
                         const Sweep& s0 = prog->sweeps[size_t(l.sweep)];
                         return s0.zero_tiles_log2 < nq - s0.tile_bits;

@@ -34,7 +34,7 @@ def both(native, fn):
 
 
 @pytest.mark.parametrize("jit", [0, 2])
-@pytest.mark.parametrize("q,d,tile_bits", [(18, 6, 10), (22, 8, 12), (16, 5, 6)])
+@pytest.mark.parametrize("q,d,tile_bits", [(22, 6, 10), (22, 8, 12), (24, 5, 6)])
 def test_uncut_bit_identical(env, q, d, tile_bits, jit):
     torch, cb, native, engine = env
     circ = cb.build_brickwall(cb.BrickwallSpec(q, d, 2, 2, 1))
@@ -49,16 +49,16 @@ def test_uncut_bit_identical(env, q, d, tile_bits, jit):
     assert torch.equal(a, b)
     from oracle import cutbench_oracle as orc
 
-    if q <= 18:
+    if q <= 22:
         ref = orc.simulate(q, circ.kinds, circ.qa, circ.qb, circ.params)
         assert np.abs(b.cpu().numpy() - ref).max() < 1e-10
 
 
 def test_variant_batch_and_strided_gaps(env):
     torch, cb, native, engine = env
-    circ = cb.build_brickwall(cb.BrickwallSpec(20, 6, 2, 3, 0))
+    circ = cb.build_brickwall(cb.BrickwallSpec(36, 4, 2, 6, 0))
     plan = cb.plan_cut(circ, 2)
-    fam = cb.decompose(circ, plan).segments[0]
+    fam = cb.decompose(circ, plan).segments[0]  # 18 qubits x 64 variants: above the zero-start size floor
     nq, nv = fam.num_qubits, fam.num_variants
     old = native.get_option("tile_bits")
     native.set_option("tile_bits", 6)  # several sweeps on the 10-qubit segment
