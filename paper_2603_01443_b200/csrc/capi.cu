@@ -231,7 +231,7 @@ void build_launches(Program& prog) {
 std::shared_ptr<const Program> build_schedule(int nq, const uint8_t* kinds, const int64_t* qa,
                                                          const int64_t* qb, const double* params,
                                                          const int32_t* slots, int64_t n_gates, int64_t n_states,
-                                                         int tile_bits, int dtype) {
+                                                         int tile_bits, int dtype, bool zero_start) {
   const int T = choose_tile_bits(nq, n_states, tile_bits, dtype);
   const int L = (T == nq) ? nq : std::max(3, std::min(int(g_opt.low_bits), T - 6));
   const int vb = choose_vb(n_states);
@@ -245,8 +245,11 @@ std::shared_ptr<const Program> build_schedule(int nq, const uint8_t* kinds, cons
   // normalised 2x2s only pay where the 1-coefficients become free (the
   // NVRTC-specialised kernels); the interpreter keeps the plain matrices
   const int norm = g_opt.dense_norm == 2 ? (g_opt.jit != 0 && g_opt.engine == 1 ? 1 : 0) : int(g_opt.dense_norm);
+  // the cost-aware tile-set policy (3) only pays for a start from |0..0>
+  // (zero-start tiles); other starts keep the most-absorbed-ops policy
+  const int windows = (g_sweep_windows == 3 && !zero_start) ? 1 : g_sweep_windows;
   const int32_t hdr[13] = {nq, T, L, int32_t(fuse), slots ? 1 : 0, dtype, vb, g_sweep_minb,
-                           int32_t(g_opt.engine), norm, g_reg_bits * 8 + g_reg_reorder * 4 + g_sweep_windows, g_jit_minb,
+                           int32_t(g_opt.engine), norm, g_reg_bits * 8 + g_reg_reorder * 4 + windows, g_jit_minb,
                            g_jit_persistent};
   key.append(reinterpret_cast<const char*>(hdr), sizeof(hdr));
   key.append(reinterpret_cast<const char*>(kinds), size_t(n_gates));
@@ -272,7 +275,7 @@ std::shared_ptr<const Program> build_schedule(int nq, const uint8_t* kinds, cons
   auto built = std::make_shared<Program>();
   built->engine = int(g_opt.engine);
   built->n_states = n_states;
-  built->sweeps = schedule_sweeps(ops, nq, T, L, max_group);
+  built->sweeps = schedule_sweeps(ops, nq, T, L, max_group, windows);
   build_launches(*built);
   std::shared_ptr<const Program> prog = built;
   std::lock_guard<std::mutex> lk(g_cache_mu);
@@ -841,7 +844,7 @@ int cs_set_option(const char* key, int64_t value) {
     if (value < 8 || value > 112) return fail(CS_ERR_INVALID, "merge_smem_kb must be in [8, 112]");
     g_opt.merge_smem_kb = value;
   } else if (k == "sweep_windows") {
-    if (value < 0 || value > 2) return fail(CS_ERR_INVALID, "sweep_windows must be 0, 1 or 2");
+    if (value < 0 || value > 3) return fail(CS_ERR_INVALID, "sweep_windows must be 0, 1, 2 or 3");
     g_sweep_windows = int(value);
   } else if (k == "reg_reorder") {
     g_reg_reorder = value ? 1 : 0;
@@ -946,7 +949,7 @@ int cs_sim_batch(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int6
   }
   std::shared_ptr<const Program> prog;
   try {
-    prog = build_schedule(nq, kinds, qa, qb, params, slots, n_gates, n_states, 0, dtype);
+    prog = build_schedule(nq, kinds, qa, qb, params, slots, n_gates, n_states, 0, dtype, init_zero != 0);
   } catch (const PlanError& pe) {
     return fail(pe.code, pe.msg);
   }
@@ -964,7 +967,7 @@ int cs_sim_batch_until(int32_t nq, const uint8_t* kinds, const int64_t* qa, cons
   if (n_gates < 0 || (n_gates > 0 && (!kinds || !qa || !qb))) return fail(CS_ERR_INVALID, "bad gate table");
   std::shared_ptr<const Program> prog;
   try {
-    prog = build_schedule(nq, kinds, qa, qb, params, slots, n_gates, n_states, 0, dtype);
+    prog = build_schedule(nq, kinds, qa, qb, params, slots, n_gates, n_states, 0, dtype, init_zero != 0);
   } catch (const PlanError& pe) {
     return fail(pe.code, pe.msg);
   }
@@ -979,7 +982,7 @@ int cs_sweep_plan_json(int32_t nq, const uint8_t* kinds, const int64_t* qa, cons
   if (nq < 1 || nq > 62) return fail(CS_ERR_INVALID, "qubit count out of range");
   std::string js;
   try {
-    auto prog = build_schedule(nq, kinds, qa, qb, params, slots, n_gates, 1, tile_bits, dtype);
+    auto prog = build_schedule(nq, kinds, qa, qb, params, slots, n_gates, 1, tile_bits, dtype, true);
     js = g_opt.plan_json ? reg_programs_to_json(prog->sweeps, nq) : sweeps_to_json(prog->sweeps, nq);
   } catch (const PlanError& pe) {
     return fail(pe.code, pe.msg);
@@ -999,7 +1002,7 @@ int cs_jit_selftest(int32_t nq, const uint8_t* kinds, const int64_t* qa, const i
   if (nq < 1 || nq > 62) return fail(CS_ERR_INVALID, "qubit count out of range");
   std::shared_ptr<const Program> prog;
   try {
-    prog = build_schedule(nq, kinds, qa, qb, params, slots, n_gates, n_states, 0, dtype);
+    prog = build_schedule(nq, kinds, qa, qb, params, slots, n_gates, n_states, 0, dtype, true);
   } catch (const PlanError& pe) {
     return fail(pe.code, pe.msg);
   }
@@ -1143,7 +1146,7 @@ int cut_programs(const CutJob& job, int dtype, std::vector<std::shared_ptr<const
     for (const SegmentPlan& sp : job.prep.segs)
       progs->push_back(build_schedule(sp.nq, sp.kinds.data(), sp.qa.data(), sp.qb.data(), sp.params.data(),
                                       sp.slots.data(), int64_t(sp.kinds.size()),
-                                      int64_t(1) << sp.cut_ids.size(), 0, dtype));
+                                      int64_t(1) << sp.cut_ids.size(), 0, dtype, true));
   } catch (const PlanError& pe) {
     return fail(pe.code, pe.msg);
   }

@@ -465,7 +465,7 @@ int sweep_max_group(int tile_bits) {
   return std::max(1, std::min(kMaxGroup, tile_bits - lg));
 }
 
-int g_sweep_windows = 1;
+int g_sweep_windows = 3;  // cost-aware tile sets (zero-start tiles); 1 = most absorbed ops per sweep
 
 // Order each sweep's tile-id qubits so that, for a start from |0..0>, the
 // tiles that can be non-zero are exactly t < 2^zero_tiles_log2: the qubits
@@ -483,17 +483,18 @@ static void order_tiles_for_zero_start(std::vector<Sweep>& sweeps) {
 }
 
 static std::vector<Sweep> schedule_sweeps_impl(const std::vector<LOp>& ops, int nq, int tile_bits, int low_bits,
-                                               int max_group);
+                                               int max_group, int windows);
 
 std::vector<Sweep> schedule_sweeps(const std::vector<LOp>& ops, int nq, int tile_bits, int low_bits,
-                                   int max_group) {
-  std::vector<Sweep> sweeps = schedule_sweeps_impl(ops, nq, tile_bits, low_bits, max_group);
+                                   int max_group, int windows) {
+  std::vector<Sweep> sweeps =
+      schedule_sweeps_impl(ops, nq, tile_bits, low_bits, max_group, windows < 0 ? g_sweep_windows : windows);
   order_tiles_for_zero_start(sweeps);
   return sweeps;
 }
 
 static std::vector<Sweep> schedule_sweeps_impl(const std::vector<LOp>& ops, int nq, int tile_bits, int low_bits,
-                                               int max_group) {
+                                               int max_group, int windows) {
   std::vector<Sweep> sweeps;
   if (nq <= tile_bits) {
     Sweep sw;
@@ -547,13 +548,74 @@ static std::vector<Sweep> schedule_sweeps_impl(const std::vector<LOp>& ops, int 
     }
     return best;
   };
+  // sweep_windows = 3: cost-aware choice for a start from |0..0> (zero-start
+  // tiles): a candidate tile set costs the fraction of tiles it launches,
+  // 2^(support qubits outside the set) / 2^(nq - T), times a dense-op term,
+  // plus a per-launch constant; the set with the most absorbed dense ops per
+  // unit cost wins. Once the support is complete every set costs the same
+  // and this is the plain most-absorbed choice.
+  uint64_t support = 0;
+  const uint64_t high_mask = (nq >= 64 ? ~0ull : ((1ull << nq) - 1)) & ~((1ull << L) - 1);
+  auto set_cost = [&](const bool* cand, int absorbed_ops) {
+    uint64_t m = 0;
+    for (int q = 0; q < nq; ++q)
+      if (cand[q]) m |= 1ull << q;
+    const int z = __builtin_popcountll(support & high_mask & ~m);
+    const double frac = std::ldexp(1.0, z - (nq - T));
+    return frac * (1.0 + 0.04 * absorbed_ops) + 0.002;
+  };
   bool first = true;
   while (!pending.empty() || first) {
     first = false;
     bool inset[64] = {false};
     for (int q = 0; q < L; ++q) inset[q] = true;
     int room = T - L;
-    if (g_sweep_windows && nq - L > T - L) {
+    if (windows == 3 && nq - L > T - L) {
+      double best_score = -1.0;
+      int best_a = -1;
+      for (int a = L; a + (T - L) <= nq; ++a) {
+        bool cand[64] = {false};
+        for (int q = 0; q < L; ++q) cand[q] = true;
+        for (int q = a; q < a + (T - L); ++q) cand[q] = true;
+        const int c = absorbed(cand);
+        if (c <= 0) continue;
+        const double sc = c / set_cost(cand, c);
+        if (sc > best_score) {
+          best_score = sc;
+          best_a = a;
+        }
+      }
+      // the greedy first-need set, for comparison (same rules as below)
+      bool g[64] = {false};
+      for (int q = 0; q < L; ++q) g[q] = true;
+      {
+        int r = T - L;
+        uint64_t bd = 0, bp = 0;
+        for (int idx : pending) {
+          const LOp& op = ops[size_t(idx)];
+          const uint64_t qm = qubit_mask(op);
+          if (op.type == OP_PHASE) {
+            if (qm & bd) bp |= qm;
+            continue;
+          }
+          if (qm & (bd | bp)) bd |= qm;
+          else if (!g[op.target]) {
+            if (r > 0) {
+              g[op.target] = true;
+              --r;
+            } else {
+              bd |= qm;
+            }
+          }
+        }
+      }
+      const int gc = absorbed(g);
+      const double gscore = gc > 0 ? gc / set_cost(g, gc) : -1.0;
+      if (best_a >= 0 && best_score > gscore) {
+        for (int q = best_a; q < best_a + (T - L); ++q) inset[q] = true;
+        room = 0;
+      }
+    } else if (windows && nq - L > T - L) {
       // candidate tile sets: the greedy first-need set (room filled below) vs
       // every contiguous window of T - L high qubits; take the window when it
       // absorbs more dense ops
@@ -563,7 +625,7 @@ static std::vector<Sweep> schedule_sweeps_impl(const std::vector<LOp>& ops, int 
         for (int q = 0; q < L; ++q) cand[q] = true;
         for (int q = a; q < a + (T - L); ++q) cand[q] = true;
         int c;
-        if (g_sweep_windows >= 2) {  // score = this sweep + the best next window
+        if (windows >= 2) {  // score = this sweep + the best next window
           std::vector<int> rest;
           c = absorbed_from(pending, cand, &rest);
           c += best_window(rest);
@@ -600,7 +662,7 @@ static std::vector<Sweep> schedule_sweeps_impl(const std::vector<LOp>& ops, int 
         }
       }
       int greedy_score;
-      if (g_sweep_windows >= 2) {
+      if (windows >= 2) {
         std::vector<int> rest;
         greedy_score = absorbed_from(pending, g, &rest);
         greedy_score += best_window(rest);
@@ -653,6 +715,8 @@ static std::vector<Sweep> schedule_sweeps_impl(const std::vector<LOp>& ops, int 
     std::sort(sw.hq.begin(), sw.hq.end());
     for (int q = L; q < nq; ++q)
       if (!inset[q]) sw.oq.push_back(q);
+    for (int q = 0; q < nq; ++q)
+      if (inset[q]) support |= 1ull << q;
     int local_pos[64];
     for (int q = 0; q < 64; ++q) local_pos[q] = -1;
     for (int q = 0; q < L; ++q) local_pos[q] = q;

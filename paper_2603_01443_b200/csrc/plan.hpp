@@ -75,8 +75,10 @@ struct Sweep {
 // Greedy tiling: every sweep holds the low qubits [0, L) plus up to T - L
 // more qubits chosen in order of first need; it absorbs every op whose
 // non-diagonal target is in the tile and that commutes with all deferred ops.
+// windows: tile-set policy (-1 = the sweep_windows option; 3 = cost-aware
+// for a start from |0..0>)
 std::vector<Sweep> schedule_sweeps(const std::vector<LOp>& ops, int nq, int tile_bits, int low_bits,
-                                  int max_group = kMaxGroup);
+                                  int max_group = kMaxGroup, int windows = -1);
 
 // Threads per CTA of the sweep kernel for a tile of 2^T amplitudes, and the
 // largest register group that still gives every thread a cell.
