@@ -227,6 +227,11 @@ void build_launches(Program& prog) {
   }
 }
 
+// Zero-start tiles pay from a few MiB of states up (below, the extra zeroing
+// launch costs more than the tiles it saves: the variant stage's small
+// L2-resident batches)
+bool zero_start_pays(int64_t n_states, int nq) { return (n_states << nq) >= (int64_t(1) << 22); }
+
 // Lowered, fused and scheduled program for a gate table; cached by content.
 std::shared_ptr<const Program> build_schedule(int nq, const uint8_t* kinds, const int64_t* qa,
                                                          const int64_t* qb, const double* params,
@@ -247,7 +252,10 @@ std::shared_ptr<const Program> build_schedule(int nq, const uint8_t* kinds, cons
   const int norm = g_opt.dense_norm == 2 ? (g_opt.jit != 0 && g_opt.engine == 1 ? 1 : 0) : int(g_opt.dense_norm);
   // the cost-aware tile-set policy (3) only pays for a start from |0..0>
   // (zero-start tiles); other starts keep the most-absorbed-ops policy
-  const int windows = (g_sweep_windows == 3 && !zero_start) ? 1 : g_sweep_windows;
+  const int windows = (g_sweep_windows == 3 && !(zero_start && g_opt.zero_start_tiles &&
+                                                 zero_start_pays(n_states, nq)))
+                          ? 1
+                          : g_sweep_windows;
   const int32_t hdr[13] = {nq, T, L, int32_t(fuse), slots ? 1 : 0, dtype, vb, g_sweep_minb,
                            int32_t(g_opt.engine), norm, g_reg_bits * 8 + g_reg_reorder * 4 + windows, g_jit_minb,
                            g_jit_persistent};
@@ -581,9 +589,7 @@ int run_program(const Program& prog_ref, int nq, void* states, int64_t n_states,
   // Started from |0..0>, a sweep's tiles beyond 2^zero_tiles_log2 are still
   // all zero (Sweep::zero_tiles_log2): zero the states once and launch only
   // the others (cfg4a uncut: the first sweep is one tile instead of 2^18)
-  // (small batches — the variant stage's few-MiB L2-resident states — skip
-  // it: the extra zeroing launch costs more than the tiles it saves)
-  const bool sparse = init_zero && g_opt.zero_start_tiles && (int64_t(n_states) << nq) >= (int64_t(1) << 22) &&
+  const bool sparse = init_zero && g_opt.zero_start_tiles && zero_start_pays(n_states, nq) &&
                       std::any_of(prog->launches.begin(), prog->launches.end(), [&](const Launch& l) {
                         const Sweep& s0 = prog->sweeps[size_t(l.sweep)];
                         return s0.zero_tiles_log2 < nq - s0.tile_bits;
