@@ -35,7 +35,7 @@ cudaError_t launch_merge_dmma3(const MergeParams& p, int K, int warps, dim3 grid
 int merge_dmma3_cols_per_warp(int K);
 int merge_dmma3_row_blocks(int K);
 bool merge_ozaki_supported(int K, int64_t lo_len, int64_t nrows);
-cudaError_t launch_merge_ozaki(const MergeParams& mp, int64_t nrows, void* out, int accumulate, int sms,
+cudaError_t launch_merge_ozaki(const MergeParams& mp, int64_t nrows, void* out, int accumulate, int sms, bool unit,
                                cudaStream_t stream);
 cudaError_t launch_init_basis(void* states, int64_t len, int64_t n_states, int64_t index, int dtype,
                               cudaStream_t stream);
@@ -356,7 +356,8 @@ int merge_launch_one(int S, int Kc, const int32_t* hidx, const int32_t* lidx, co
         po.coef[2 * t + 1] = coef[2 * src + 1];
       }
       void* o = static_cast<char*>(out) + size_t(s) * size_t(out_slot_stride) * elem_bytes(dtype);
-      cudaError_t e = launch_merge_ozaki(po, row_end - row_begin, o, accumulate, sm_count(), stream);
+      cudaError_t e = launch_merge_ozaki(po, row_end - row_begin, o, accumulate, sm_count(), g_opt.merge_ozaki == 2,
+                                         stream);
       g_launches.fetch_add(3);
       if (e != cudaSuccess) return cuda_fail(e, "merge_ozaki launch");
     }
@@ -871,7 +872,8 @@ int cs_set_option(const char* key, int64_t value) {
   } else if (k == "zero_start_tiles") {
     g_opt.zero_start_tiles = value ? 1 : 0;
   } else if (k == "merge_ozaki") {
-    g_opt.merge_ozaki = value ? 1 : 0;
+    if (value < 0 || value > 2) return fail(CS_ERR_INVALID, "merge_ozaki must be 0, 1 or 2");
+    g_opt.merge_ozaki = value;
   } else if (k == "merge_ozaki_min_k") {
     if (value != 8 && value != 16 && value != 32 && value != 64)
       return fail(CS_ERR_INVALID, "merge_ozaki_min_k must be 8, 16, 32 or 64");

@@ -55,8 +55,9 @@ CASES = [  # (K, S, H, W, rows)
 ]
 
 
+@pytest.mark.parametrize("mode", [1, 2], ids=["persistent", "unit-ctas"])
 @pytest.mark.parametrize("K,S,H,W,rows", CASES)
-def test_ozaki_vs_numpy_and_dfma(dev, K, S, H, W, rows):
+def test_ozaki_vs_numpy_and_dfma(dev, K, S, H, W, rows, mode):
     torch, native = dev
     rng = np.random.default_rng(K * 7 + W)
     nh = nl = max(2, K)
@@ -71,7 +72,7 @@ def test_ozaki_vs_numpy_and_dfma(dev, K, S, H, W, rows):
     rows = rows or (0, H)
     want = reference(hi, lo, hidx, lidx, coef, S, rows)
     n0 = native.launch_count()
-    got = run(torch, native, hi, lo, hidx, lidx, coef, S=S, rows=rows).cpu().numpy()
+    got = run(torch, native, hi, lo, hidx, lidx, coef, S=S, rows=rows, ozaki=mode).cpu().numpy()
     launches = native.launch_count() - n0
     dfma = run(torch, native, hi, lo, hidx, lidx, coef, S=S, rows=rows, ozaki=0).cpu().numpy()
     scale = np.abs(want).max()
@@ -87,7 +88,8 @@ def test_ozaki_vs_numpy_and_dfma(dev, K, S, H, W, rows):
     assert launches >= 3 * S * min(chunks, 2)
 
 
-def test_ozaki_accumulate(dev):
+@pytest.mark.parametrize("mode", [1, 2], ids=["persistent", "unit-ctas"])
+def test_ozaki_accumulate(dev, mode):
     torch, native = dev
     rng = np.random.default_rng(5)
     K, H, W = 32, 32, 256
@@ -97,7 +99,7 @@ def test_ozaki_accumulate(dev):
     coef = np.exp(1j * np.arange(K))
     base = rng.normal(size=(1, H * W)) + 1j * rng.normal(size=(1, H * W))
     out = torch.as_tensor(base.copy(), device="cuda")
-    run(torch, native, hi, lo, idx, idx, coef, out=out, accumulate=True)
+    run(torch, native, hi, lo, idx, idx, coef, out=out, accumulate=True, ozaki=mode)
     want = base + reference(hi, lo, idx, idx, coef, 1, (0, H))
     assert np.abs(out.cpu().numpy() - want).max() < 1e-12
 
@@ -121,7 +123,8 @@ def test_ineligible_shapes_fall_back(dev, H, W, rows):
     assert np.abs(got - want).max() <= 1e-13 * np.abs(want).max()
 
 
-def test_ozaki_large_product_vs_dfma(dev):
+@pytest.mark.parametrize("mode", [1, 2], ids=["persistent", "unit-ctas"])
+def test_ozaki_large_product_vs_dfma(dev, mode):
     """q = 28 (14 | 14), K = 16: 4 GiB state, every tile of a full-size grid."""
     torch, native = dev
     g = torch.Generator(device="cuda").manual_seed(0)
@@ -132,13 +135,14 @@ def test_ozaki_large_product_vs_dfma(dev):
     coef = np.exp(1j * np.arange(K)) / 4
     from paper_2603_01443_b200.merging import merge_terms_device
 
-    native.set_option("merge_ozaki", 1)
+    old = native.get_option("merge_ozaki")
+    native.set_option("merge_ozaki", mode)
     a = merge_terms_device(hi, lo, idx, idx, coef)
     native.set_option("merge_ozaki", 0)
     try:
         b = merge_terms_device(hi, lo, idx, idx, coef)
     finally:
-        native.set_option("merge_ozaki", 1)
+        native.set_option("merge_ozaki", old)
     torch.cuda.synchronize()
     diff = (a - b).abs().max().item()
     scale = b.abs().max().item()

@@ -19,7 +19,7 @@ template <int P>
 __global__ void __launch_bounds__(512, 1) stores(double2* out) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const double2 v = make_double2(1.0, 2.0);
-  if (P == 0 || P == 1 || P == 3) {
+  if (P == 0 || P == 1 || P == 3 || P == 11) {
     const int64_t n_lt = W / 128, n_hb = H / 16, tiles = n_lt * n_hb;
     const int64_t c0 = blockIdx.x * tiles / gridDim.x, c1 = (blockIdx.x + 1) * tiles / gridDim.x;
     for (int64_t k = 0;; ++k) {
@@ -28,13 +28,17 @@ __global__ void __launch_bounds__(512, 1) stores(double2* out) {
         t = c0 + k;
         if (t >= c1) break;
         lt = t / n_hb; hb = t % n_hb;
+      } else if (P == 11) {  // contiguous tile range per CTA, l fastest
+        t = c0 + k;
+        if (t >= c1) break;
+        hb = t / n_lt; lt = t % n_lt;
       } else {       // round robin, l tile fastest
         t = blockIdx.x + k * gridDim.x;
         if (t >= tiles) break;
         hb = t / n_lt; lt = t % n_lt;
       }
       double2* base = out + hb * 16 * W + lt * 128;
-      if (P == 0 || P == 3) {
+      if (P == 0 || P == 3 || P == 11) {
         const int q = warp & 3, r0 = (warp >> 2) * 4;  // 16 warps: 4 quarters x 4 row groups of 4
         for (int j = 0; j < 4; ++j) __stcs(base + (r0 + j) * W + q * 32 + lane, v);
       } else {
@@ -205,6 +209,85 @@ static int run_sync(double2* out, int every) {
   return 0;
 }
 
+// P12: non-persistent, NT consecutive tiles (l fastest) per CTA, one CTA per
+// SM resident at a time (150 KB of dynamic shared memory)
+template <int NT>
+__global__ void __launch_bounds__(512, 1) stores_chunk(double2* out) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double2 v = make_double2(1.0, 2.0);
+  const int64_t n_lt = W / 128;
+  for (int k = 0; k < NT; ++k) {
+    const int64_t t = int64_t(blockIdx.x) * NT + k;
+    const int64_t hb = t / n_lt, lt = t % n_lt;
+    double2* base = out + hb * 16 * W + lt * 128;
+    const int q = warp & 3, r0 = (warp >> 2) * 4;
+    for (int j = 0; j < 4; ++j) __stcs(base + (r0 + j) * W + q * 32 + lane, v);
+  }
+}
+
+template <int NT>
+static int run_chunk(double2* out, int smem) {
+  cudaEvent_t a, b;
+  cudaEventCreate(&a); cudaEventCreate(&b);
+  CK(cudaFuncSetAttribute(stores_chunk<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  const int grid = int((W / 128) * (H / 16) / NT);
+  stores_chunk<NT><<<grid, 512, smem>>>(out);
+  CK(cudaDeviceSynchronize());
+  cudaEventRecord(a);
+  for (int i = 0; i < 5; ++i) stores_chunk<NT><<<grid, 512, smem>>>(out);
+  cudaEventRecord(b);
+  CK(cudaEventSynchronize(b));
+  float ms; cudaEventElapsedTime(&ms, a, b);
+  ms /= 5;
+  printf("P12 non-persistent, %d tiles per CTA, smem %d: %.3f ms  %.0f GB/s\n", NT, smem, ms, 16.0 * W * H / ms / 1e6);
+  return 0;
+}
+
+// P13: persistent round-robin (as P3) with different store cache policies
+template <int POL>
+__global__ void __launch_bounds__(512, 1) stores_pol(double2* out) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t n_lt = W / 128, n_hb = H / 16, tiles = n_lt * n_hb;
+  for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    const int64_t hb = t / n_lt, lt = t % n_lt;
+    double2* base = out + hb * 16 * W + lt * 128;
+    const int q = warp & 3, r0 = (warp >> 2) * 4;
+    if (POL == 4) {  // 256-bit stores, L2::evict_first: a warp writes 1 KB of one row
+      for (int j = threadIdx.x; j < 1024; j += 512) {
+        const int r = j >> 6, c = (j & 63) * 2;
+        double* d = reinterpret_cast<double*>(base + r * W + c);
+        asm volatile("st.global.L1::no_allocate.L2::evict_first.v4.f64 [%0], {%1, %2, %3, %4};"
+                     :: "l"(d), "d"(1.0), "d"(2.0), "d"(1.0), "d"(2.0) : "memory");
+      }
+      continue;
+    }
+    for (int j = 0; j < 4; ++j) {
+      double2* d = base + (r0 + j) * W + q * 32 + lane;
+      if (POL == 0) __stcs(d, make_double2(1.0, 2.0));
+      else if (POL == 1) *d = make_double2(1.0, 2.0);
+      else if (POL == 2) __stwt(d, make_double2(1.0, 2.0));
+      else if (POL == 3) asm volatile("st.global.L1::no_allocate.v2.f64 [%0], {%1, %2};" :: "l"(d), "d"(1.0), "d"(2.0) : "memory");
+      else if (POL == 5) __stcg(d, make_double2(1.0, 2.0));
+    }
+  }
+}
+
+template <int POL>
+static int run_pol(double2* out, const char* name) {
+  cudaEvent_t a, b;
+  cudaEventCreate(&a); cudaEventCreate(&b);
+  stores_pol<POL><<<148, 512>>>(out);
+  CK(cudaDeviceSynchronize());
+  cudaEventRecord(a);
+  for (int i = 0; i < 5; ++i) stores_pol<POL><<<148, 512>>>(out);
+  cudaEventRecord(b);
+  CK(cudaEventSynchronize(b));
+  float ms; cudaEventElapsedTime(&ms, a, b);
+  ms /= 5;
+  printf("P13 persistent, %s: %.3f ms  %.0f GB/s\n", name, ms, 16.0 * W * H / ms / 1e6);
+  return 0;
+}
+
 static int run_dyn(double2* out) {
   unsigned long long* ctr;
   CK(cudaMalloc(&ctr, 8));
@@ -262,23 +345,9 @@ static int run(double2* out, const char* name) {
 int main() {
   double2* out;
   CK(cudaMalloc(&out, sizeof(double2) * W * H));
-  run<0>(out, "P0 128l x 16h, per-CTA range h-fastest, warp = 4 rows x 512 B");
-  run<1>(out, "P1 128l x 16h, round-robin l-fastest, warp = 1 row x 2 KB");
-  run<2>(out, "P2 1024l x 2h tiles, warp = 1 row x 2 KB");
-  run<3>(out, "P3 128l x 16h, round-robin l-fastest, warp = 4 rows x 512 B");
+  run_pol<0>(out, "st.global.cs"); run_pol<1>(out, "st.global"); run_pol<2>(out, "st.global.wt");
+  run_pol<3>(out, "L1::no_allocate"); run_pol<4>(out, "256-bit L1::no_allocate.L2::evict_first"); run_pol<5>(out, "st.global.cg");
   run2<4, 512, 1>(out, "P4 non-persistent, one tile per CTA");
-  run2<5, 256, 2>(out, "P5 persistent 2 CTA/SM x 256 thr");
-  run2<5, 512, 1>(out, "P5' persistent 1 CTA/SM x 512 thr");
-  run2<5, 1024, 1>(out, "P5'' persistent 1 CTA/SM x 1024 thr");
-  run2<6, 512, 1>(out, "P6 persistent 512 thr, 2 tiles/iter");
-  run2<7, 512, 1>(out, "P7 persistent 512 thr, 256-bit stores");
-  run2<5, 128, 4>(out, "P5 persistent 4 CTA/SM x 128 thr");
-  run_dyn(out);
-  run2<4, 512, 1>(out, "P4 non-persistent, one tile per CTA");
-  run2<5, 1024, 2>(out, "P5 persistent 2 CTA/SM x 1024 thr");
-  run_sync(out, 4); run_sync(out, 16); run_sync(out, 64); run_sync(out, 1000000);
-  run_tma<true>(out, "P9 TMA bulk stores, no fill");
-  run_tma<false>(out, "P9 TMA bulk stores, st.shared fill");
   cudaFree(out);
   return 0;
 }
