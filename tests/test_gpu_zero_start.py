@@ -21,15 +21,20 @@ def env():
     return torch, cb, _native, engine
 
 
-def both(native, fn):
-    old = native.get_option("zero_start_tiles")
+def both(native, fn, windows=1):
+    """fn() with zero-start tiles off and on, the tile-set policy pinned (the
+    default cost-aware policy 3 applies only with zero-start tiles, so with
+    `windows` = 1 both runs execute the same schedule)."""
+    old = native.get_option("zero_start_tiles"), native.get_option("sweep_windows")
     try:
+        native.set_option("sweep_windows", windows)
         native.set_option("zero_start_tiles", 0)
         a = fn()
         native.set_option("zero_start_tiles", 1)
         b = fn()
     finally:
-        native.set_option("zero_start_tiles", old)
+        native.set_option("zero_start_tiles", old[0])
+        native.set_option("sweep_windows", old[1])
     return a, b
 
 
@@ -47,6 +52,9 @@ def test_uncut_bit_identical(env, q, d, tile_bits, jit):
         native.set_option("tile_bits", old[0])
         native.set_option("jit", old[1])
     assert torch.equal(a, b)
+    # the default schedule (cost-aware tile sets) agrees to rounding
+    c = engine.simulate(circ).device_tensor()
+    assert (c - a).abs().max().item() < 1e-12
     from oracle import cutbench_oracle as orc
 
     if q <= 22:
