@@ -386,6 +386,44 @@ def run_ours(args):
                          "8 FMA (16 flop) per amplitude per dense 2x2 op; DFMA peak 36.5 TF/s measured "
                          "with tools/fp64_peak.cu"}
 
+    # the same merge with more cut terms (cfg5 c=4 / threshold region): the
+    # int8 tcgen05 kernel (exact FP64 splitting) vs the FP64 tensor-core 3M
+    # kernel, on the preallocated output (informational, not the headline)
+    int8_merge = None
+    if world == 1 and not args.no_uncut:
+        from paper_2603_01443_b200.merging import merge_terms_device
+
+        g = torch.Generator(device="cuda").manual_seed(0)
+        int8_merge = {}
+        for K in (16, 64):
+            hi = torch.randn(K, 1 << (q - q // 2), dtype=torch.complex128, device="cuda", generator=g) / 4
+            lo = torch.randn(K, 1 << (q // 2), dtype=torch.complex128, device="cuda", generator=g) / 4
+            idx = np.arange(K)
+            coef = np.exp(1j * np.arange(K)) / np.sqrt(K)
+            res = {}
+            for name, oz in (("int8_tcgen05", 1), ("fp64_dmma_3m", 0)):
+                _native.set_option("merge_ozaki", oz)
+                merge_terms_device(hi, lo, idx, idx, coef, out=out.view(1, -1))
+                torch.cuda.synchronize()
+                m0 = torch.cuda.Event(enable_timing=True)
+                m1 = torch.cuda.Event(enable_timing=True)
+                m0.record(stream)
+                for _ in range(3):
+                    merge_terms_device(hi, lo, idx, idx, coef, out=out.view(1, -1))
+                m1.record(stream)
+                m1.synchronize()
+                res[name] = m0.elapsed_time(m1) / 3
+            _native.set_option("merge_ozaki", 1)
+            t = res["int8_tcgen05"] / 1e3
+            int8_merge[f"K{K}"] = {"ms": res["int8_tcgen05"], "fp64_dmma_3m_ms": res["fp64_dmma_3m"],
+                                   "out_gbs": 16.0 * total / t / 1e9,
+                                   "fp64_tflops_alg": 8.0 * K * total / t / 1e12}
+            del hi, lo
+        int8_merge["note"] = ("q=30 rank-K product out[h][l] = sum_t c_t hi_t[h] lo_t[l] (n=2 merge with K cut "
+                              "terms) into the 16 GiB output: int8 tcgen05.mma with 8 base-128 digits per FP64 "
+                              "operand (max|d| vs DFMA ~1e-16) vs the FP64 tensor-core 3M kernel; 8K flop per "
+                              "output algorithmic")
+
     # roofline of the dominant kernel (merge) from the timed region
     roofline = None
     if merge_ms:
@@ -466,6 +504,7 @@ def run_ours(args):
             "stage_ms": stage,
             "uncut_ms": uncut_ms,
             "uncut": uncut,
+            "int8_merge": int8_merge,
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
