@@ -296,6 +296,41 @@ def test_q30_cfg4a_cut_vs_gpu_uncut_and_sampled_oracle(cb):
     del cut, uncut
 
 
+@pytest.mark.parametrize("c_total", [4, 6])
+def test_q30_int8_tensor_core_merge_cut_vs_uncut(cb, c_total):
+    """q=30 (15|15) with K = 2^c_total = 16 / 64 cut terms: the merge runs on
+    the int8 tcgen05 kernel (ozaki.cu); the full 16 GiB state against the
+    GPU uncut simulator and sampled amplitudes against the CPU oracle's
+    subcircuit states."""
+    from paper_2603_01443_b200 import _native, engine
+
+    assert _native.get_option("merge_ozaki") == 1
+    spec = cb.BrickwallSpec(30, 10, 2, c_total, 0)
+    circ = cb.build_brickwall(spec)
+    n0 = _native.launch_count()
+    cut = cb.run_cut(circ, 2)
+    assert _native.launch_count() - n0 >= 3  # prep_lo, prep_hi, the tcgen05 kernel
+    uncut = cb.simulate(circ)
+    assert engine.max_abs_diff(cut, uncut) < TOL
+    re, im = engine.inner(uncut, cut)
+    n1 = engine.inner(cut, cut)[0]
+    n2 = engine.inner(uncut, uncut)[0]
+    assert 1 - (re * re + im * im) / (n1 * n2) < FID_TOL
+    k, qa, qb, p = circ.kinds, circ.qa, circ.qb, circ.params
+    sizes = [15, 15]
+    bgs, counts, _ = orc.plan(k, qa, qb, sizes)
+    states = []
+    for seg in range(2):
+        vs = orc.segment_variants(k, qa, qb, p, sizes, bgs, seg)
+        states.append([orc.simulate(15, *v) for v in vs])
+    tab = orc.merge_table(2, bgs, sum(counts))
+    co = orc.coefficients(sum(counts))
+    idx = np.random.default_rng(7).integers(0, 1 << 30, size=2048)
+    want = orc.sample_amplitudes(states, tab, co, sizes, idx)
+    assert np.abs(engine.gather(cut, idx) - want).max() < TOL
+    del cut, uncut
+
+
 def test_q30_cfg4b_three_way(cb):
     from paper_2603_01443_b200 import engine
 
