@@ -476,6 +476,47 @@ def run_ours(args):
                          "frac": total * 16 / t_e2e / 1e9 / d2h_gbs}}
         del host, chunk
 
+    # e2e at N > 1 (or --sharded-e2e at N = 1): every rank runs the sharded
+    # pipeline (parallel.run_cut_sharded: its variant slice, the NCCL
+    # all-gather, its output rows) and copies its shard into pinned host memory
+    # over its own PCIe link; time = max over ranks, value = whole job
+    if (world > 1 or args.sharded_e2e) and not args.no_e2e:
+        if comm is None:  # --sharded-e2e at one rank: a world-1 NCCL communicator
+            from paper_2603_01443_b200.comm import NcclComm
+
+            comm = NcclComm.create(rank, world)
+        if "out" not in locals() or out is None:
+            out = torch.empty(end - begin, dtype=torch.complex128, device="cuda")
+        host = torch.empty(end - begin, dtype=torch.complex128, pin_memory=True)
+        g_bytes = int(sum(a.nbytes for a in (circ.kinds, circ.qa, circ.qb, circ.params)))
+
+        def e2e_step():
+            res, _ = run_cut_sharded(circ, spec.n, rank=rank, world=world, out=out, comm=comm)
+            host.copy_(res, non_blocking=True)
+            torch.cuda.synchronize()
+            del res
+
+        for _ in range(max(1, min(args.warmup, 2))):
+            e2e_step()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e_steps = max(1, min(args.steps, args.e2e_steps))
+        t0 = time.perf_counter()
+        for _ in range(e_steps):
+            e2e_step()
+        t_rank = (time.perf_counter() - t0) / e_steps
+        if dist:
+            tt = torch.tensor([t_rank], device="cuda", dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t_rank = float(tt.item())
+        e2e = {"value": total / t_rank, "unit": UNIT, "h2d_bytes_per_step": g_bytes * world,
+               "d2h_bytes_per_step": total * 16, "ms_per_step": t_rank * 1e3, "steps": e_steps,
+               "path": (f"parallel.run_cut_sharded on {world} rank(s) (variant slices, NCCL all-gather, "
+                        f"output rows [{begin}, {end}) per rank) + device->host copy of each shard into "
+                        "pinned host memory over the rank's own PCIe link; max over ranks")}
+        del host
+
     # CPU baseline (the oracle port, 1 thread = the reference's protocol), rank 0, N=1
     cpu = None
     if world == 1 and not args.no_cpu:
@@ -529,6 +570,8 @@ def main():
                     help="merge rows sampled by the CPU legs")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sharded-e2e", action="store_true",
+                    help="N=1: measure e2e through the sharded (multi-GPU) path instead (its test at one rank)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-uncut", action="store_true")
     ap.add_argument("--no-jit", action="store_true", help="interpreter sweep kernels only")
