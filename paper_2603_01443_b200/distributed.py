@@ -195,16 +195,26 @@ def simulate_distributed(circuit: Circuit, *, rank: int, world: int, group=None,
         from . import _native
 
         shard = _device.empty(1, nloc, dtype)[0]
-        if rank == 0:
-            _native.check(_native.load().cs_init_basis(shard.data_ptr(), nloc, 1, 0, _device.code_of(dtype),
-                                                       _device.stream_ptr()), "cs_init_basis")
-        else:
+        pending_init = [rank == 0]  # rank 0's |0..0> not written yet
+        if rank != 0:
             shard.zero_()
 
         def run_local(table, sh):
-            run_table(sh.view(1, -1), nloc, table, dtype=dtype)
+            # rank 0's first local segment starts from |0..0> inside the
+            # library (zero-start tiles); afterwards the shard holds the state
+            run_table(sh.view(1, -1), nloc, table, dtype=dtype, init_zero=pending_init[0])
+            pending_init[0] = False
+
+        def ensure_init():
+            if pending_init[0]:
+                _native.check(_native.load().cs_init_basis(shard.data_ptr(), nloc, 1, 0, _device.code_of(dtype),
+                                                           _device.stream_ptr()), "cs_init_basis")
+                pending_init[0] = False
     else:
         shard = init(nloc) if init is not None else None
+
+        def ensure_init():
+            pass
     if exchange is None and comm is not None:
         exchange = comm.sendrecv
     if exchange is None:
@@ -215,20 +225,32 @@ def simulate_distributed(circuit: Circuit, *, rank: int, world: int, group=None,
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
     buf = None
+    # ranks whose shard can be non-zero: from |0..0> only rank 0, and a swap
+    # on global bit j spreads it to the partner. Every rank tracks the same
+    # set; an all-zero shard stays zero under its local gates (skipped) and
+    # two all-zero partners skip their exchange.
+    nonzero = {0}
     for st in steps:
         if isinstance(st, Segment):
             table = local_table(st, rank, nloc)
-            if len(table):
+            if len(table) and rank in nonzero:
                 run_local(table, shard)
         else:
             b = (rank >> (st.global_bit - nloc)) & 1
             partner = rank ^ (1 << (st.global_bit - nloc))
+            bit = 1 << (st.global_bit - nloc)
+            was = set(nonzero)
+            nonzero |= {r ^ bit for r in was}
+            if rank not in was and partner not in was:
+                continue
             # keep local bit == b, exchange the half with local bit != b
             part = shard[half:] if b == 0 else shard[:half]
             if buf is None:
                 buf = torch.empty_like(part)
+            ensure_init()
             exchange(torch.view_as_real(part.contiguous()), torch.view_as_real(buf), partner)
             part.copy_(buf)
+    ensure_init()
     return shard
 
 
@@ -246,14 +268,16 @@ def simulate_emulated(circuit: Circuit, world: int, *, dtype=np.complex128):
     full.zero_()
     _native.check(_native.load().cs_init_basis(full.data_ptr(), nloc, 1, 0, _device.code_of(dtype),
                                                _device.stream_ptr()), "cs_init_basis")
+    nonzero = {0}  # as in simulate_distributed
     for st in steps:
         if isinstance(st, Segment):
             for r in range(world):
                 table = local_table(st, r, nloc)
-                if len(table):
+                if len(table) and r in nonzero:
                     run_table(full[r].view(1, -1), nloc, table, dtype=dtype)
         else:
             j = st.global_bit - nloc
+            nonzero |= {r ^ (1 << j) for r in set(nonzero)}
             for r in range(world):
                 if (r >> j) & 1:
                     continue

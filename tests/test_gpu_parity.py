@@ -382,6 +382,17 @@ def test_distributed_uncut_emulated_on_one_gpu(cb, world, q, d):
     assert np.abs(got - ref).max() < TOL
 
 
+def test_distributed_uncut_world1_default_path(cb):
+    """simulate_distributed's own device path at one rank (rank 0 starts from
+    |0..0> inside the library: zero-start tiles) equals simulate()."""
+    from paper_2603_01443_b200.distributed import simulate_distributed
+
+    circ = cb.build_brickwall(cb.BrickwallSpec(22, 6, 2, 2, 3))
+    got = simulate_distributed(circ, rank=0, world=1).cpu().numpy()
+    ref = cb.simulate(circ).amps
+    assert np.abs(got - ref).max() < 1e-12
+
+
 def test_run_cut_to_host_matches_device_state(cb):
     """The e2e path of bench.py (cs_cut_run_to_host: chunked merge overlapped
     with D2H into host memory) for pinned tensors, numpy arrays, ragged chunk
