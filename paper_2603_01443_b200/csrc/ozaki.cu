@@ -1,4 +1,4 @@
-// Tensor-core merge for K >= 8 terms: the complex rank-K product of the n=2
+// Tensor-core merge for K = 8..64 terms (used from K = 16 by default): the complex rank-K product of the n=2
 // merge (merging.py:86-94 `_axpy_outer`, summed over m as in merging.py:178-185)
 //   out[h][l] = sum_t (coef_t hi_t[h]) lo_t[l]
 // computed exactly on the int8 tensor cores (tcgen05.mma kind::i8, TMEM
@@ -8,9 +8,9 @@
 //   A[l] = (lr_0, li_0, lr_1, li_1, ...),
 //   B[(h,0)] = (Hr_0, -Hi_0, ...)  -> Re out,   B[(h,1)] = (Hi_0, Hr_0, ...) -> Im out.
 // Every row of A (per l) and every pair of rows of B (per h) is scaled by a
-// power of two 2^-e so its entries are < 1/2 in magnitude and split into
-// S = 8 balanced base-128 digits (int8, |d| <= 65) of its 56-bit fixed-point
-// rounding (exact for every entry's bits down to 2^-57 of the row maximum). Digit products of equal
+// power of two 2^-e so its entries are <= 1/2 in magnitude, rounded to
+// 56-bit fixed point (2^-57 of the row maximum) and split into S = 8
+// balanced base-128 digits (int8, |d| <= 65). Digit products of equal
 // weight i + j = p ("diagonal p") accumulate exactly in int32:
 //   D_p = sum_{i+j=p} A_i B_j^T,      out = 2^(e_l + e_h) sum_p 2^-7(p+2) D_p
 // keeping p <= S-1 (the dropped terms are < 2^-56 relative to the row/column
@@ -20,15 +20,16 @@
 // (slice j = rows 32j..32j+31), so ONE MMA per A slice i,
 //   D[:, 32i : 256] += A_i . [B_0; ...; B_{7-i}]^T      (N = 32 (8 - i)),
 // adds A_i B_{p-i} into every diagonal p >= i at once: 8 MMAs per k-step
-// instead of 36, each long enough (N = 32..256) to stay above the ~66-cycle
-// per-instruction issue cost measured for small N (tools/tc_i8_probe.cu).
+// instead of 36 (tools/tc_i8_probe.cu: 616 cycles per 8-MMA group against a
+// 576-cycle tensor floor).
 //
 // Roles per CTA (persistent, one per SM): warp 0 streams digit blocks with
 // cp.async.bulk (TMA bulk copies, mbarrier complete_tx), warp 1 issues the
-// MMAs (one elected lane) into one of two 256-column TMEM accumulators, warps
-// 2..9 drain TMEM (tcgen05.ld), combine the diagonals pairwise in int32,
-// convert to FP64, scale and write each output amplitude once
-// (st.global.cs, 512 contiguous bytes per warp store).
+// MMAs (one elected lane) into one of two 256-column TMEM accumulators, two
+// groups of 8 epilogue warps (warps 2..17, alternate tiles) drain TMEM
+// (tcgen05.ld), combine the diagonals pairwise in int32, convert to FP64,
+// scale and write each output amplitude once (st.global.cs, 512 contiguous
+// bytes per warp store). DESIGN.md §3 has the measurements.
 #include <cuda_runtime.h>
 
 #include <algorithm>
