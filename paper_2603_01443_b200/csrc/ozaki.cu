@@ -555,8 +555,9 @@ cudaError_t run_ozaki(const MergeParams& mp, int64_t nrows, void* out, int accum
   op.n_hb = nrows / kHB;
   op.n_lt = W / kLT;
   if (UNIT) {
-    // one unit (l tile x 16 h blocks) per CTA
-    op.n_hc = std::max<int64_t>(1, op.n_hb / 16);
+    // one unit (l tile x 64 h blocks) per CTA (8 / 16 / 32 / 128 measured
+    // slower or equal)
+    op.n_hc = std::max<int64_t>(1, op.n_hb / 64);
   } else {
     // h chunks so that n_lt * n_hc is a multiple of the grid (equal work per CTA)
     int64_t a = sms, b = op.n_lt;
