@@ -331,6 +331,30 @@ def test_q30_int8_tensor_core_merge_cut_vs_uncut(cb, c_total):
     del cut, uncut
 
 
+def test_q32_cfg5_c4_int8_merge_cut_vs_uncut(cb):
+    """BASELINE cfg5 at full size on one GPU: q=32 (16|16), c_total=4 (K=16,
+    int8 tcgen05 merge) — the 64 GiB cut state against the 64 GiB uncut
+    state from the GPU simulator (needs ~130 GB of free device memory)."""
+    import torch
+
+    from paper_2603_01443_b200 import engine
+
+    torch.cuda.empty_cache()
+    free, _total = torch.cuda.mem_get_info()
+    if free < 140 * 2**30:
+        pytest.skip(f"needs ~140 GB free device memory, {free / 2**30:.0f} GiB free")
+    circ = cb.build_brickwall(cb.BASELINE_CONFIGS["cfg5_q32_n2_c4"])
+    cut = cb.run_cut(circ, 2, max_qubits=32)
+    uncut = cb.simulate(circ, max_qubits=32)
+    assert engine.max_abs_diff(cut, uncut) < TOL
+    re, im = engine.inner(uncut, cut)
+    n1 = engine.inner(cut, cut)[0]
+    n2 = engine.inner(uncut, uncut)[0]
+    assert 1 - (re * re + im * im) / (n1 * n2) < FID_TOL
+    del cut, uncut
+    torch.cuda.empty_cache()
+
+
 def test_q30_cfg4b_three_way(cb):
     from paper_2603_01443_b200 import engine
 
