@@ -202,7 +202,13 @@ def run_reference(args):
     from paper_2603_01443_b200.generators import BASELINE_CONFIGS
 
     spec = BASELINE_CONFIGS[WORKLOAD]
-    threads = oracle_c.max_threads() if args.threads <= 0 else args.threads
+    # all host threads this process may use (torchrun sets OMP_NUM_THREADS=1
+    # for its workers; the C port passes num_threads explicitly)
+    try:
+        host_threads = len(os.sched_getaffinity(0))
+    except AttributeError:
+        host_threads = os.cpu_count() or oracle_c.max_threads()
+    threads = host_threads if args.threads <= 0 else args.threads
     frac = args.row_fraction
     for _ in range(args.warmup):
         cpu_sample(spec, threads, frac / 8)
