@@ -3,7 +3,7 @@ seeded U3 brick-walls with random (q, n, c_total, d); the one-call cut
 pipeline and the drop-in API path against the GPU uncut simulator (every
 config) and the CPU oracle (q <= 16). Exercises the int8 merge (K >= 16 on
 eligible shapes), chain merges, zero-start tiles and cost-aware schedules.
-    python tools/fuzz_parity.py [n_configs] [seed]"""
+    python tools/fuzz_parity.py [n_configs] [seed] [max_q]"""
 import sys
 import time
 
@@ -16,12 +16,13 @@ from paper_2603_01443_b200 import _native, engine  # noqa: E402
 
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 60
 rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 2026)
+QMAX = int(sys.argv[3]) if len(sys.argv) > 3 else 24
 _native.set_option("jit", 2)
 worst = 0.0
 t0 = time.time()
 for i in range(N):
     n = int(rng.choice([2, 2, 3, 4]))
-    q = int(rng.integers(max(4, 2 * n), 25))
+    q = int(rng.integers(max(4, 2 * n), QMAX + 1))
     q -= q % n
     d = int(rng.integers(1, 13))
     c = int(rng.integers(0, 9 if n == 2 else 11))
