@@ -435,6 +435,15 @@ __global__ void __launch_bounds__(oz_threads<UNIT>(), UNIT ? 2 : 1) ozaki_merge_
       const int64_t lt = w.lt, hb = w.hb;
       const int64_t l = lt * kLT + q * 32 + lane;
       const double sl = __ldg(p.sa + l);  // 2^(e_l - 35)
+      // accumulate (K > 64 in 64-term chunks): fetch the 8 outputs being
+      // added to before waiting for the accumulator, so the reads overlap
+      // the MMA chain instead of the epilogue
+      double2 prev[8];
+      if (ACC) {
+        const double2* src = p.out + (hb * kHB + hl_base) * p.W + l;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) prev[j] = __ldcs(src + j * p.W);
+      }
       mbar_wait(tfull + g, n & 1);
       ++n;
       tc_after_sync();
@@ -478,9 +487,8 @@ __global__ void __launch_bounds__(oz_threads<UNIT>(), UNIT ? 2 : 1) ozaki_merge_
           }
           double2 val = make_double2(v2[0], v2[1]);
           if (ACC) {
-            const double2 prev = *dst;
-            val.x += prev.x;
-            val.y += prev.y;
+            val.x += prev[4 * hc + j].x;
+            val.y += prev[4 * hc + j].y;
           }
           __stcs(dst, val);  // evict-first: the state is written once
         }
