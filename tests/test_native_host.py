@@ -120,6 +120,29 @@ def test_schedule_reproduces_oracle_uncut(q, d, n, c, seed, tile_bits, fuse_mode
     assert np.abs(got - ref).max() < 1e-12
 
 
+def test_cost_aware_zero_start_schedule_reproduces_oracle():
+    """From 2^22 amplitudes up the planner prices tile sets by the tiles they
+    launch (sweep_windows 3, zero-start tiles): the schedule of a q=22
+    brick-wall — many sweeps, most of them over a few tiles — executed here
+    (with the zero-start bound asserted before every sweep) equals the oracle;
+    its early sweeps launch a fraction of the tiles."""
+    q = 22
+    circ = G.build_brickwall(G.BrickwallSpec(q, 4, 2, 2, 5))
+    plan3 = json.loads(_native.sweep_plan_json(q, circ.table))
+    old = _native.get_option("sweep_windows")
+    _native.set_option("sweep_windows", 1)
+    try:
+        plan1 = json.loads(_native.sweep_plan_json(q, circ.table))
+    finally:
+        _native.set_option("sweep_windows", old)
+
+    assert plan3["sweeps"][0]["z"] == 0 and any(sw["z"] < q - sw["T"] for sw in plan3["sweeps"][1:])
+    assert plan3 != plan1
+    got = execute_schedule(plan3, q)
+    ref = orc.simulate(q, circ.kinds, circ.qa, circ.qb, circ.params)
+    assert np.abs(got - ref).max() < 1e-12
+
+
 @pytest.mark.parametrize("key", ["stair_q8_n4_b2", "stair_q6_n2_b3", "shadow_q9_d4_n3_c4_s3",
                                  "padded_q6_n2_b1_p1"])
 def test_schedule_of_variant_templates_matches_reference_states(golden, key, fuse_mode):
@@ -314,6 +337,29 @@ def test_register_programs_reproduce_oracle(q, d, n, c, seed, tile_bits, fuse_mo
     circ = G.build_brickwall(G.BrickwallSpec(q, d, n, c, seed))
     plan = _reg_plan(q, circ.table, tile_bits=tile_bits)
     got = execute_reg_programs(plan, q)
+    ref = orc.simulate(q, circ.kinds, circ.qa, circ.qb, circ.params)
+    assert np.abs(got - ref).max() < 1e-12
+
+
+def test_cost_aware_zero_start_schedule_reproduces_oracle():
+    """From 2^22 amplitudes up the planner prices tile sets by the tiles they
+    launch (sweep_windows 3, zero-start tiles): the schedule of a q=22
+    brick-wall — many sweeps, most of them over a few tiles — executed here
+    (with the zero-start bound asserted before every sweep) equals the oracle;
+    its early sweeps launch a fraction of the tiles."""
+    q = 22
+    circ = G.build_brickwall(G.BrickwallSpec(q, 4, 2, 2, 5))
+    plan3 = json.loads(_native.sweep_plan_json(q, circ.table))
+    old = _native.get_option("sweep_windows")
+    _native.set_option("sweep_windows", 1)
+    try:
+        plan1 = json.loads(_native.sweep_plan_json(q, circ.table))
+    finally:
+        _native.set_option("sweep_windows", old)
+
+    assert plan3["sweeps"][0]["z"] == 0 and any(sw["z"] < q - sw["T"] for sw in plan3["sweeps"][1:])
+    assert plan3 != plan1
+    got = execute_schedule(plan3, q)
     ref = orc.simulate(q, circ.kinds, circ.qa, circ.qb, circ.params)
     assert np.abs(got - ref).max() < 1e-12
 
