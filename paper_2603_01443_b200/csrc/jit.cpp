@@ -178,6 +178,13 @@ std::string jit_source(const Sweep& sw, const std::vector<RegOp>& prog, int RB, 
   } else {
     o << "  const unsigned long long tile = blockIdx.x; (void)n_tiles;\n";
     o << "  unsigned long long " << base_of("base", "tile") << "\n";
+    // started from |0..0>, every tile but the one holding index 0 is all
+    // zero and stays zero under the tile's gates: store zeros, skip the math
+    // (base is uniform across the CTA, so the early return skips no barrier
+    // another thread waits on)
+    o << "  if (init && base != 0ull) {\n";
+    for (int j = 0; j < NR; ++j) o << "    " << gidx(j, "base") << " st[g] = V{R(0), R(0)}; }\n";
+    o << "    return;\n  }\n";
     for (int j = 0; j < NR; ++j)
       o << "  " << gidx(j, "base") << " if (init) { v" << j << ".x = (base == 0ull && e == 0u) ? R(1) : R(0); v" << j
         << ".y = R(0); } else v" << j << " = st[g]; }\n";
