@@ -84,6 +84,25 @@ def check_free(nbytes: int, what: str) -> None:
                             f"{(free + cached) / 2**30:.2f} GiB free on the device")
 
 
+def check_out(out, n_amps: int, dtype, what: str = "out", *, device: str = "cuda"):
+    """Validate a caller-provided result buffer BEFORE its pointer reaches
+    native code: a torch tensor on ``device`` of exactly ``n_amps`` elements
+    of ``dtype``, contiguous. The kernels write n_amps * itemsize bytes, so a
+    smaller or differently typed buffer would be written past its end."""
+    t = torch()
+    if not isinstance(out, t.Tensor):
+        raise ValidationError(f"{what} must be a torch tensor, got {type(out).__name__}")
+    if out.device.type != device:
+        raise ValidationError(f"{what} must live on {device}, got {out.device}")
+    if out.dtype != torch_dtype(dtype):
+        raise ValidationError(f"{what} has dtype {out.dtype}, expected {torch_dtype(dtype)}")
+    if out.numel() != n_amps:
+        raise ValidationError(f"{what} has {out.numel()} elements, expected {n_amps}")
+    if not out.is_contiguous():
+        raise ValidationError(f"{what} must be contiguous")
+    return out
+
+
 def empty(n_states: int, nq: int, dtype=np.complex128, check_memory=True):
     """Uninitialised device batch [n_states, 2^nq]."""
     t = require_cuda()

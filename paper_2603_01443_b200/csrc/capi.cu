@@ -302,12 +302,16 @@ bool dmma_eligible(int K, int dtype, int64_t lo_len) {
          lo_len >= merge_dmma_cols_per_warp(K);
 }
 
+// SMs of the current device (cached per device: a process may drive several)
 int sm_count() {
-  static int n = 0;
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::atomic<int>& slot = cache[dev & 63];
+  int n = slot.load();
   if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
     if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n < 1) n = 148;
+    slot.store(n);
   }
   return n;
 }

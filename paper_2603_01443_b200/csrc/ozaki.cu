@@ -33,6 +33,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <utility>
 #include <cstdint>
 #include <map>
 #include <mutex>
@@ -174,12 +176,16 @@ __global__ void ozaki_prep_lo(const __grid_constant__ OzPrep p, int8_t* adig, do
   const double2* lo = p.lo;
   const int K = p.K;
   double mx = 0.0;
+  bool finite = true;
   for (int t = 0; t < K; ++t) {
     const double2 v = __ldg(lo + int64_t(p.lidx[t]) * p.lo_len + l);
+    finite &= isfinite(v.x) && isfinite(v.y);
     mx = fmax(mx, fmax(fabs(v.x), fabs(v.y)));
   }
-  const int e = row_exponent(mx);
-  if (ks == 0) sa[l] = ldexp(1.0, e - 35);
+  const int e = row_exponent(finite ? mx : 0.0);
+  // a NaN/Inf operand makes the whole output column NaN (as the FP64 kernels
+  // propagate it) instead of saturated digits turning it into a finite value
+  if (ks == 0) sa[l] = finite ? ldexp(1.0, e - 35) : __longlong_as_double(0x7ff8000000000000ll);
   const double sc = digit_scale(e);
   uint32_t w[kSlices][8];
 #pragma unroll
@@ -222,13 +228,16 @@ __global__ void ozaki_prep_hi(const __grid_constant__ OzPrep p, int64_t nrows, i
   const double2* hi = p.hi;
   const int K = p.K;
   double mx = 0.0;
+  bool finite = true;
   for (int t = 0; t < K; ++t) {
     const double2 v = __ldg(hi + int64_t(p.hidx[t]) * p.hi_len + h);
     const double cr = p.coef[t].x, ci = p.coef[t].y;
-    mx = fmax(mx, fmax(fabs(v.x * cr - v.y * ci), fabs(v.x * ci + v.y * cr)));
+    const double br = v.x * cr - v.y * ci, bi = v.x * ci + v.y * cr;
+    finite &= isfinite(br) && isfinite(bi);
+    mx = fmax(mx, fmax(fabs(br), fabs(bi)));
   }
-  const int e = row_exponent(mx);
-  if (ks == 0) sb[hr] = ldexp(1.0, e);
+  const int e = row_exponent(finite ? mx : 0.0);
+  if (ks == 0) sb[hr] = finite ? ldexp(1.0, e) : __longlong_as_double(0x7ff8000000000000ll);
   const double sc = digit_scale(e);
   uint32_t w0[kSlices][8], w1[kSlices][8];
 #pragma unroll
@@ -511,8 +520,13 @@ struct Workspace {
   void* ptr = nullptr;
   size_t bytes = 0;
 };
-std::map<cudaStream_t, Workspace> g_oz_ws;
+// keyed by (device, stream): the legacy default stream (0) is shared by all
+// devices, and a workspace allocated on one device must not serve another
+std::map<std::pair<int, cudaStream_t>, Workspace> g_oz_ws;
 std::mutex g_oz_mu;
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is per device: one bit
+// per (device, instantiation)
+std::atomic<uint64_t> g_oz_configured[8];
 
 template <int KS, int NST, bool UNIT>
 cudaError_t run_ozaki(const MergeParams& mp, int64_t nrows, void* out, int accumulate, int sms,
@@ -522,8 +536,13 @@ cudaError_t run_ozaki(const MergeParams& mp, int64_t nrows, void* out, int accum
   const size_t b_bytes = size_t(nrows / kHB) * KS * kSlices * kBBlock;
   const size_t ea_bytes = size_t(W) * 8, eb_bytes = size_t(nrows) * 8;
   const size_t need = a_bytes + b_bytes + ea_bytes + eb_bytes + 1024;
+  int dev = 0;
+  {
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+  }
   std::lock_guard<std::mutex> lk(g_oz_mu);
-  Workspace& ws = g_oz_ws[stream];
+  Workspace& ws = g_oz_ws[{dev, stream}];
   if (ws.bytes < need) {
     if (ws.ptr) {
       cudaError_t e = cudaStreamSynchronize(stream);
@@ -582,15 +601,16 @@ cudaError_t run_ozaki(const MergeParams& mp, int64_t nrows, void* out, int accum
   // (and one 512-column TMEM allocation) lives on each SM; unit CTAs: two
   // per SM (256 TMEM columns each)
   const size_t smem = UNIT ? oz_smem<KS, NST>() : std::max<size_t>(oz_smem<KS, NST>(), 116 * 1024);
-  static bool configured = false;
-  if (!configured) {
+  constexpr int inst = (KS == 1 ? 0 : KS == 2 ? 1 : 2) * 2 + (UNIT ? 1 : 0);
+  const uint64_t bit = uint64_t(1) << (dev & 63);
+  if (!(g_oz_configured[inst].load() & bit)) {
     cudaError_t e = cudaFuncSetAttribute(ozaki_merge_kernel<KS, NST, false, UNIT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(ozaki_merge_kernel<KS, NST, true, UNIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                int(smem));
     if (e != cudaSuccess) return e;
-    configured = true;
+    g_oz_configured[inst].fetch_or(bit);
   }
   const int64_t grid = UNIT ? op.n_units : std::min<int64_t>(sms, op.n_units);
   if (grid > 0x7fffffff) return cudaErrorInvalidValue;

@@ -106,12 +106,23 @@ class StateVec:
             self._owner = "device"
         return self._dev
 
+    def _sync_handed_out(self) -> None:
+        """The reference's apply_gate mutates ``amps`` in place
+        (engine.py:171-181): if a host array exists (the state was built from
+        one, or ``amps`` was read), copy the device result back INTO that same
+        array so references a caller holds see the new amplitudes. Both copies
+        are then current ("both")."""
+        if self._host is not None and self._host.dtype == self.dtype and self._host.flags.writeable \
+                and self._host.flags.c_contiguous:
+            _device.to_host(self._dev, out=self._host)
+            self._owner = "both"
+
     @property
     def on_device(self) -> bool:
-        return self._owner == "device"
+        return self._owner in ("device", "both")
 
     def norm(self) -> float:
-        if self._owner == "device":
+        if self._owner in ("device", "both"):
             re, _ = inner(self, self)
             return float(np.sqrt(max(re, 0.0)))
         return float(np.linalg.norm(self._host))
@@ -212,6 +223,7 @@ def apply_gate(state: StateVec, gate: Gate) -> StateVec:
     tiny = Circuit(state.num_qubits, (gate,))
     dev = state.device_tensor(for_write=True)
     run_table(dev.view(1, -1), state.num_qubits, tiny.table, init_zero=False, dtype=state.dtype)
+    state._sync_handed_out()
     return state
 
 
@@ -222,6 +234,7 @@ def apply_circuit(state: StateVec, circuit: Circuit) -> StateVec:
     _device.require_cuda()
     dev = state.device_tensor(for_write=True)
     run_table(dev.view(1, -1), state.num_qubits, circuit.table, init_zero=False, dtype=state.dtype)
+    state._sync_handed_out()
     return state
 
 

@@ -160,8 +160,16 @@ def merge_terms_device(hi, lo, hidx, lidx, coef, *, S=1, rows=None, out=None, dt
     lo_len = lo.shape[-1]
     r0, r1 = (0, hi_len) if rows is None else rows
     K = len(hidx) // S
+    tdt = _device.torch_dtype(dtype)
+    for name, x in (("hi", hi), ("lo", lo)):
+        if x.dtype != tdt or not x.is_contiguous() or x.device.type != "cuda":
+            raise ValidationError(f"{name} must be a contiguous CUDA tensor of {tdt}, got {x.dtype} on {x.device}")
+    if not (0 <= r0 <= r1 <= hi_len):
+        raise ValidationError(f"row range [{r0}, {r1}) outside [0, {hi_len})")
     if out is None:
         out = _device.empty_shape((S, (r1 - r0) * lo_len), dtype)
+    else:
+        _device.check_out(out, S * (r1 - r0) * lo_len, dtype)
     h = _native.c_i32(hidx)
     lidx_a = _native.c_i32(lidx)
     c = np.ascontiguousarray(np.asarray(coef, dtype=np.complex128).view(np.float64))
@@ -185,11 +193,18 @@ def merge_chain_device(chain: ChainSpec, seg_batches, *, dtype=np.complex128, ou
     ws_bytes, _bond, _qlow = chain.plan(dtype, force_bond)
     if workspace is None or workspace.numel() < ws_bytes:
         workspace = t.empty(max(ws_bytes, 1), dtype=t.uint8, device="cuda")
+    if not (0 <= begin <= end <= (1 << q)):
+        raise ValidationError(f"output range [{begin}, {end}) outside [0, 2^{q})")
     if out is None:
         out = _device.empty_shape((end - begin,), dtype)
+    else:
+        _device.check_out(out, end - begin, dtype)
+    tdt = _device.torch_dtype(dtype)
     for j, b in enumerate(seg_batches):
         if b.shape != (1 << chain.seg_ncuts[j], 1 << chain.seg_nq[j]) or not b.is_contiguous():
             raise ValidationError(f"segment {j} batch has shape {tuple(b.shape)}")
+        if b.dtype != tdt or b.device.type != "cuda":
+            raise ValidationError(f"segment {j} batch must be a CUDA tensor of {tdt}, got {b.dtype} on {b.device}")
     ptrs = np.array([b.data_ptr() for b in seg_batches], dtype=np.uint64)
     nq = _native.c_i32(chain.seg_nq)
     nc = _native.c_i32(chain.seg_ncuts)

@@ -140,6 +140,11 @@ def run_cut(circuit: Circuit, n: int, *, dtype=np.complex128, max_qubits: int = 
     if out is None:
         _device.check_free((end - begin) * np.dtype(dtype).itemsize, "state")
         out = _device.empty_shape((end - begin,), dtype)
+    else:
+        _device.check_out(out, end - begin, dtype)
+    if workspace is not None and (workspace.device.type != "cuda" or not workspace.is_contiguous()
+                                  or workspace.numel() * workspace.element_size() < ws_bytes):
+        raise ValidationError(f"workspace must be a contiguous CUDA buffer of >= {ws_bytes} bytes")
     k, qa, qb, prm = _native._table_args(circuit.table)
     sz = _native.c_i32(sizes)
     stage = np.zeros(3) if timers is not None else None
@@ -151,7 +156,7 @@ def run_cut(circuit: Circuit, n: int, *, dtype=np.complex128, max_qubits: int = 
     _native.check(
         _native.load().cs_cut_run(q, _native.ptr(k), _native.ptr(qa), _native.ptr(qb), _native.ptr(prm), len(k),
                                   len(sz), _native.ptr(sz), force_bond, begin, end, out.data_ptr(),
-                                  workspace.data_ptr(), workspace.numel(), code, _device.stream_ptr(),
+                                  workspace.data_ptr(), workspace.numel() * workspace.element_size(), code, _device.stream_ptr(),
                                   evp, _native.ptr(stage)),
         "cs_cut_run",
     )
@@ -190,8 +195,7 @@ def run_cut_to_host(circuit: Circuit, n: int, host_out, *, dtype=np.complex128, 
             raise ValidationError("host_out must be a contiguous array of 2^q amplitudes of the dtype")
         host_ptr = host_out.ctypes.data
     else:
-        if host_out.numel() != 1 << q or host_out.device.type != "cpu" or not host_out.is_contiguous():
-            raise ValidationError("host_out must be a contiguous host tensor of 2^q amplitudes")
+        _device.check_out(host_out, 1 << q, dtype, "host_out", device="cpu")
         host_ptr = host_out.data_ptr()
     k, qa, qb, prm = _native._table_args(circuit.table)
     sz = _native.c_i32(sizes)
@@ -200,12 +204,12 @@ def run_cut_to_host(circuit: Circuit, n: int, host_out, *, dtype=np.complex128, 
     _native.check(_native.load().cs_cut_host_workspace(q, _native.ptr(k), _native.ptr(qa), _native.ptr(qb),
                                                        _native.ptr(prm), len(k), len(sz), _native.ptr(sz), chunks,
                                                        code, _native.ptr(need)), "cs_cut_host_workspace")
-    if workspace is None or workspace.numel() < int(need[0]):
+    if workspace is None or workspace.numel() * workspace.element_size() < int(need[0]):
         workspace = cut_workspace_tensor(int(need[0]))
     stage = np.zeros(3) if timers is not None else None
     _native.check(_native.load().cs_cut_run_to_host(q, _native.ptr(k), _native.ptr(qa), _native.ptr(qb),
                                                     _native.ptr(prm), len(k), len(sz), _native.ptr(sz), chunks,
-                                                    host_ptr, workspace.data_ptr(), workspace.numel(), code,
+                                                    host_ptr, workspace.data_ptr(), workspace.numel() * workspace.element_size(), code,
                                                     _device.stream_ptr(), _native.ptr(stage)),
                   "cs_cut_run_to_host")
     if timers is not None:

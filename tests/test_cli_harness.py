@@ -12,12 +12,17 @@ from paper_2603_01443_b200.generators import BrickwallSpec
 
 
 def test_preprocess_json(tmp_path, capsys):
+    """Reference cli.py:136-143: the SubcircuitSet JSON goes to --out (or
+    stdout); --summary adds a plan line on stderr."""
     path = tmp_path / "subs.json"
-    rc = cli.main(["preprocess", "--q", "6", "--n", "3", "--blocks", "2", "--json", str(path)])
+    rc = cli.main(["preprocess", "--q", "6", "--n", "3", "--blocks", "2", "--out", str(path), "--summary"])
     assert rc == cli.EXIT_OK
     data = json.loads(path.read_text())
     assert data["c_total"] == 4 and len(data["segments"]) == 3
-    assert "N_sub=24" in capsys.readouterr().out
+    assert "N_sub=24" in capsys.readouterr().err
+    rc = cli.main(["preprocess", "--q", "6", "--n", "3", "--blocks", "2", "--machine-tag", "x", "--reps", "1"])
+    assert rc == cli.EXIT_OK
+    assert json.loads(capsys.readouterr().out) == data
 
 
 def test_validation_exit_code(capsys):
@@ -27,7 +32,7 @@ def test_validation_exit_code(capsys):
 def test_brickwall_preprocess(capsys):
     rc = cli.main(["preprocess", "--family", "brickwall", "--q", "12", "--n", "2", "--d", "4", "--c", "1"])
     assert rc == 0
-    assert "c_total=1" in capsys.readouterr().out
+    assert json.loads(capsys.readouterr().out)["c_total"] == 1
 
 
 def test_capacity_exit_code_before_any_device_work():
@@ -42,6 +47,16 @@ def test_cutrun_verify(capsys):
     out = capsys.readouterr().out
     err = float(out.split("reconstruction_linf_error=")[1].split()[0])
     assert err < 1e-10
+
+
+@pytest.mark.gpu
+def test_cutrun_streaming_verify(capsys):
+    """Reference cli.py:97-108: --streaming merges through merge_streaming."""
+    rc = cli.main(["cutrun", "--q", "8", "--n", "2", "--blocks", "2", "--streaming", "--verify",
+                   "--machine-tag", "t"])
+    assert rc == 0
+    out = capsys.readouterr().out
+    assert float(out.split("reconstruction_linf_error=")[1].split()[0]) < 1e-10
 
 
 @pytest.mark.gpu

@@ -147,3 +147,75 @@ def test_ozaki_large_product_vs_dfma(dev, mode):
     diff = (a - b).abs().max().item()
     scale = b.abs().max().item()
     assert diff <= 1e-15 * scale * K, (diff, scale)
+
+
+@pytest.mark.parametrize("mode", [1, 2], ids=["persistent", "unit-ctas"])
+def test_ozaki_propagates_non_finite(dev, mode):
+    """A NaN or Inf operand gives NaN outputs in its row/column (as the FP64
+    kernels do), never a finite value made of saturated digits."""
+    torch, native = dev
+    rng = np.random.default_rng(3)
+    K, H, W = 16, 32, 256
+    hi = rng.normal(size=(K, H)) + 1j * rng.normal(size=(K, H))
+    lo = rng.normal(size=(K, W)) + 1j * rng.normal(size=(K, W))
+    lo[2, 5] = np.nan
+    hi[4, 9] = np.inf
+    idx = np.arange(K)
+    coef = np.ones(K)
+    got = run(torch, native, hi, lo, idx, idx, coef, ozaki=mode).cpu().numpy().reshape(H, W)
+    assert np.isnan(got[:, 5]).all() and np.isnan(got[9, :]).all()
+    mask = np.ones((H, W), bool)
+    mask[:, 5] = False
+    mask[9, :] = False
+    assert np.isfinite(got[mask]).all()
+    want = reference(hi, lo, idx, idx, coef, 1, (0, H)).reshape(H, W)
+    assert np.abs(got[mask] - want[mask]).max() <= 1e-13 * np.abs(want[mask]).max()
+
+
+def test_out_buffers_are_validated_before_native_calls(dev):
+    """a wrong dtype / length / non-contiguous ``out`` raises
+    ValidationError instead of letting a kernel write past the buffer."""
+    torch, native = dev
+    from paper_2603_01443_b200 import BrickwallSpec, build_brickwall, run_cut
+    from paper_2603_01443_b200.errors import ValidationError
+    from paper_2603_01443_b200.merging import merge_terms_device
+
+    hi = torch.zeros(2, 16, dtype=torch.complex128, device="cuda")
+    lo = torch.zeros(2, 128, dtype=torch.complex128, device="cuda")
+    idx = np.arange(2)
+    for bad in (torch.zeros(16 * 128, dtype=torch.complex64, device="cuda"),
+                torch.zeros(16 * 128 - 1, dtype=torch.complex128, device="cuda"),
+                torch.zeros(2 * 16 * 128, dtype=torch.complex128, device="cuda")[::2],
+                torch.zeros(16 * 128, dtype=torch.complex128)):
+        with pytest.raises(ValidationError):
+            merge_terms_device(hi, lo, idx, idx, np.ones(2), out=bad)
+    with pytest.raises(ValidationError):
+        merge_terms_device(hi.to(torch.complex64), lo, idx, idx, np.ones(2))
+    circ = build_brickwall(BrickwallSpec(8, 2, 2, 1, 0))
+    for bad in (torch.zeros(256, dtype=torch.float64, device="cuda"),
+                torch.zeros(128, dtype=torch.complex128, device="cuda")):
+        with pytest.raises(ValidationError):
+            run_cut(circ, 2, out=bad)
+    from paper_2603_01443_b200.pipeline import run_cut_to_host
+
+    with pytest.raises(ValidationError):
+        run_cut_to_host(circ, 2, torch.zeros(256, dtype=torch.float64).view(torch.complex64))
+
+
+def test_apply_gate_updates_a_held_host_array(dev):
+    """Reference engine.py:171-181: apply_gate mutates the state in place, so
+    an ``amps`` array obtained earlier sees the new amplitudes."""
+    import paper_2603_01443_b200 as cb
+    from paper_2603_01443_b200.circuits import h, x
+
+    sv = cb.StateVec.zero_state(3)
+    a = sv.amps
+    cb.apply_gate(sv, h(0))
+    r = 0.7071067811865475
+    assert np.allclose(a, [r, r, 0, 0, 0, 0, 0, 0])
+    b = sv.amps
+    assert b is a
+    from paper_2603_01443_b200.engine import apply_circuit
+
+    apply_circuit(sv, cb.Circuit(3, (h(0), x(2))))
+    assert np.allclose(a, [0, 0, 0, 0, 1, 0, 0, 0])

@@ -341,29 +341,6 @@ def test_register_programs_reproduce_oracle(q, d, n, c, seed, tile_bits, fuse_mo
     assert np.abs(got - ref).max() < 1e-12
 
 
-def test_cost_aware_zero_start_schedule_reproduces_oracle():
-    """From 2^22 amplitudes up the planner prices tile sets by the tiles they
-    launch (sweep_windows 3, zero-start tiles): the schedule of a q=22
-    brick-wall — many sweeps, most of them over a few tiles — executed here
-    (with the zero-start bound asserted before every sweep) equals the oracle;
-    its early sweeps launch a fraction of the tiles."""
-    q = 22
-    circ = G.build_brickwall(G.BrickwallSpec(q, 4, 2, 2, 5))
-    plan3 = json.loads(_native.sweep_plan_json(q, circ.table))
-    old = _native.get_option("sweep_windows")
-    _native.set_option("sweep_windows", 1)
-    try:
-        plan1 = json.loads(_native.sweep_plan_json(q, circ.table))
-    finally:
-        _native.set_option("sweep_windows", old)
-
-    assert plan3["sweeps"][0]["z"] == 0 and any(sw["z"] < q - sw["T"] for sw in plan3["sweeps"][1:])
-    assert plan3 != plan1
-    got = execute_schedule(plan3, q)
-    ref = orc.simulate(q, circ.kinds, circ.qa, circ.qb, circ.params)
-    assert np.abs(got - ref).max() < 1e-12
-
-
 @pytest.mark.parametrize("key", ["stair_q8_n4_b2", "stair_q6_n2_b3", "shadow_q9_d4_n3_c4_s3",
                                  "stair_q12_n3_b1"])
 def test_register_programs_of_variant_templates(golden, key, fuse_mode):
