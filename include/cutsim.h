@@ -184,6 +184,33 @@ int cs_cut_run_to_host(int32_t nq, const uint8_t* kinds, const int64_t* qa, cons
                        const double* params, int64_t n_gates, int32_t n_seg, const int32_t* seg_sizes,
                        int32_t chunks, void* host_out, void* workspace, int64_t workspace_bytes,
                        int32_t dtype, void* stream, double* stage_ms);
+/* ---- the sharded (multi-GPU) cut pipeline, one call per rank -----------------
+ * the output is sharded on its high amplitude bits and the
+ * subcircuit variants are split across ranks. All segments must have equal
+ * qubit counts: the segments' variant batches, concatenated segment-major,
+ * form one array of `total` states split into `world` chunks of `per` states;
+ * rank r simulates chunk r IN PLACE in its workspace and one in-place NCCL
+ * all-gather (the pipeline's only exchange) completes the array on every rank
+ * — it is exactly the segment batches the chain merge reads. Each rank then
+ * writes output amplitudes [out_begin, out_end) (its rows of the reference
+ * merge's result, merging.py:156-186) into `out`. comm = NULL: no exchange,
+ * the rank simulates every variant itself (one GPU computing any rank's
+ * share). The reference is single-process; this has no reference
+ * counterpart beyond computing rows of merge().
+ * cs_cut_shard_plan (host only) fills info[8] = {workspace bytes, q_low,
+ * default out_begin, default out_end (rank's rows), first and end flat
+ * variant index of the rank's chunk, per, total}.
+ * stage_events (nullable): 4 cudaEvent_t recorded before the variant stage,
+ * after it, after the all-gather and after the merge; stage_ms (nullable,
+ * 4 doubles): host preprocess, variant stage, exchange, merge (synchronises). */
+int cs_cut_shard_plan(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int64_t* qb,
+                      const double* params, int64_t n_gates, int32_t n_seg, const int32_t* seg_sizes, int32_t world,
+                      int32_t rank, int32_t dtype, int64_t* info);
+int cs_cut_run_sharded(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int64_t* qb, const double* params,
+                       int64_t n_gates, int32_t n_seg, const int32_t* seg_sizes, void* comm, int32_t world,
+                       int32_t rank, int64_t out_begin, int64_t out_end, void* out, void* workspace,
+                       int64_t workspace_bytes, int32_t dtype, void* stream, void* const* stage_events,
+                       double* stage_ms);
 /* Host-only: the C++ preprocess as flat tables — replaces plan_cut_sizes +
  * decompose (cutting.py:70-136, 190-248). cuts[4j..4j+3] = position,
  * boundary, control segment, target segment of cut j; seg_counts[2s],

@@ -51,21 +51,34 @@ def simulate(q, kinds, qa, qb, params=None, threads=1):
 
 def merge_rows(seg_states, table, coeffs, rows, threads=1):
     """Reference merge (merging.py:156-186) restricted to output rows [r0, r1)
-    of the final (hi x seg0) fold, n = 2 only. Returns (acc, seconds)."""
+    of the final (segments n-1..1) x segment-0 fold, with the reference's
+    structure: zero-filled accumulator (merging.py:117), then per term m one
+    read-modify-write axpy pass acc += alpha_m * hi_m (x) psi_0 (merging.py:
+    86-94); for n >= 3 hi_m is the Kronecker product of segments n-1..1
+    (the reference's _outer_into fold, merging.py:140-150), built per term.
+    Returns (acc, seconds)."""
     lib = load()
-    if len(seg_states) != 2:
-        raise ValueError("bounded C merge sample supports n = 2")
-    lo_states, hi_states = seg_states
+    n = len(seg_states)
+    lo_states = seg_states[0]
     width = len(lo_states[0])
     r0, r1 = rows
     t0 = time.perf_counter()
     acc = np.empty((r1 - r0) * width, dtype=np.complex128)
     lib.or_zero(acc.ctypes.data, acc.size, threads)
     for m in range(table.shape[1]):
-        hi = np.ascontiguousarray(hi_states[table[1, m]])
+        if n == 2:
+            hi = np.ascontiguousarray(seg_states[1][table[1, m]])
+            h0, h1 = r0, r1
+        else:
+            cur = seg_states[n - 1][table[n - 1, m]]
+            for i in range(n - 2, 0, -1):
+                cur = np.multiply.outer(cur, seg_states[i][table[i, m]]).ravel()
+            hi = np.ascontiguousarray(cur[r0:r1])
+            h0, h1 = 0, r1 - r0
         lo = np.ascontiguousarray(lo_states[table[0, m]])
         c = complex(coeffs[m])
-        lib.or_axpy_outer(acc.ctypes.data, r0, r1, hi.ctypes.data, lo.ctypes.data, width, c.real, c.imag,
+        # or_axpy_outer writes acc rows [h0, h1) relative to row h0 of hi
+        lib.or_axpy_outer(acc.ctypes.data, h0, h1, hi.ctypes.data, lo.ctypes.data, width, c.real, c.imag,
                           threads)
     return acc, time.perf_counter() - t0
 

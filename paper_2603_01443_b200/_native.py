@@ -66,6 +66,9 @@ SIGNATURES = {
                                         _vp]),
     "cs_cut_run": (ctypes.c_int, [_i32, _vp, _vp, _vp, _vp, _i64, _i32, _vp, _i32, _i64, _i64, _vp, _vp,
                                   _i64, _i32, _vp, _vp, _vp]),
+    "cs_cut_shard_plan": (ctypes.c_int, [_i32, _vp, _vp, _vp, _vp, _i64, _i32, _vp, _i32, _i32, _i32, _vp]),
+    "cs_cut_run_sharded": (ctypes.c_int, [_i32, _vp, _vp, _vp, _vp, _i64, _i32, _vp, _vp, _i32, _i32, _i64, _i64,
+                                          _vp, _vp, _i64, _i32, _vp, _vp, _vp]),
     "cs_cut_host_workspace": (ctypes.c_int, [_i32, _vp, _vp, _vp, _vp, _i64, _i32, _vp, _i32, _i32, _vp]),
     "cs_cut_run_to_host": (ctypes.c_int, [_i32, _vp, _vp, _vp, _vp, _i64, _i32, _vp, _i32, _vp, _vp, _i64, _i32,
                                           _vp, _vp]),
@@ -215,6 +218,19 @@ def cut_workspace(nq, table, sizes, force_bond=-1, dtype=CS_C128):
     check(load().cs_cut_workspace(nq, ptr(k), ptr(qa), ptr(qb), ptr(prm), len(k), len(sz), ptr(sz), force_bond,
                                   dtype, ptr(ws), ptr(ql), ptr(ct)), "cs_cut_workspace")
     return int(ws[0]), int(ql[0]), int(ct[0])
+
+
+def cut_shard_plan(nq, table, sizes, world, rank, dtype=CS_C128) -> dict:
+    """Host-only: the sharded pipeline's layout for `rank` of `world`
+    (cs_cut_shard_plan): workspace bytes, q_low, the rank's default output
+    range and its chunk [var_begin, var_end) of the flattened variant list."""
+    k, qa, qb, prm = _table_args(table)
+    sz = c_i32(sizes)
+    info = np.zeros(8, np.int64)
+    check(load().cs_cut_shard_plan(nq, ptr(k), ptr(qa), ptr(qb), ptr(prm), len(k), len(sz), ptr(sz), world, rank,
+                                   dtype, ptr(info)), "cs_cut_shard_plan")
+    keys = ("workspace_bytes", "q_low", "out_begin", "out_end", "var_begin", "var_end", "per", "total")
+    return {k_: int(v) for k_, v in zip(keys, info)}
 
 
 def cut_tables(nq, table, sizes):

@@ -1151,14 +1151,26 @@ int cs_cut_tables(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int
 
 namespace {
 
-// Programs of every segment's variant family, NVRTC-compiled if enabled
-// (host side of the variant stage; compile before any timing).
-int cut_programs(const CutJob& job, int dtype, std::vector<std::shared_ptr<const Program>>* progs) {
+// One batch of consecutive variants [v0, v1) of segment `seg`, simulated
+// into `dst` (state v0 first). The single-GPU pipeline runs one piece per
+// segment (its whole family); a rank of the sharded pipeline runs the pieces
+// of its slice of the flattened variant list.
+struct Piece {
+  int seg = 0;
+  int64_t v0 = 0, v1 = 0;
+  void* dst = nullptr;
+};
+
+// Programs of the pieces' variant batches, NVRTC-compiled if enabled (host
+// side of the variant stage; compile before any timing).
+int piece_programs(const CutJob& job, const std::vector<Piece>& pieces, int dtype,
+                   std::vector<std::shared_ptr<const Program>>* progs) {
   try {
-    for (const SegmentPlan& sp : job.prep.segs)
+    for (const Piece& pc : pieces) {
+      const SegmentPlan& sp = job.prep.segs[size_t(pc.seg)];
       progs->push_back(build_schedule(sp.nq, sp.kinds.data(), sp.qa.data(), sp.qb.data(), sp.params.data(),
-                                      sp.slots.data(), int64_t(sp.kinds.size()),
-                                      int64_t(1) << sp.cut_ids.size(), 0, dtype, true));
+                                      sp.slots.data(), int64_t(sp.kinds.size()), pc.v1 - pc.v0, 0, dtype, true));
+    }
   } catch (const PlanError& pe) {
     return fail(pe.code, pe.msg);
   }
@@ -1166,25 +1178,22 @@ int cut_programs(const CutJob& job, int dtype, std::vector<std::shared_ptr<const
   return CS_OK;
 }
 
-// Batched subcircuit simulation: every segment's variant family at once,
-// segments on side streams forked from / joined into `st`.
-int cut_segments(const CutJob& job, const std::vector<std::shared_ptr<const Program>>& progs, void* workspace,
-                 int dtype, cudaStream_t st, std::vector<const void*>* seg_states) {
-  const CutPrep& pr = job.prep;
+// Batched subcircuit simulation of every piece, pieces on side streams
+// forked from / joined into `st` (segments are independent).
+int run_pieces(const CutJob& job, const std::vector<Piece>& pieces,
+               const std::vector<std::shared_ptr<const Program>>& progs, int dtype, cudaStream_t st) {
   cudaEvent_t fork = nullptr;
-  if (pr.n > 1) {
+  if (pieces.size() > 1) {
     cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
     cudaEventRecord(fork, st);
   }
   int rc = CS_OK;
-  for (size_t s = 0; s < pr.segs.size(); ++s) {
-    const SegmentPlan& sp = pr.segs[s];
-    void* states = static_cast<char*>(workspace) + job.seg_off[s];
-    seg_states->push_back(states);
-    const int64_t nv = int64_t(1) << sp.cut_ids.size();
-    cudaStream_t ss = pr.n > 1 ? side_stream(int(s % 4)) : st;
+  for (size_t i = 0; i < pieces.size(); ++i) {
+    const Piece& pc = pieces[i];
+    const SegmentPlan& sp = job.prep.segs[size_t(pc.seg)];
+    cudaStream_t ss = fork ? side_stream(int(i % 4)) : st;
     if (fork) cudaStreamWaitEvent(ss, fork, 0);
-    rc = run_program(*progs[s], sp.nq, states, nv, int64_t(1) << sp.nq, 0, 1, dtype, ss);
+    rc = run_program(*progs[i], sp.nq, pc.dst, pc.v1 - pc.v0, int64_t(1) << sp.nq, uint64_t(pc.v0), 1, dtype, ss);
     if (rc != CS_OK) break;
     if (ss != st) {
       cudaEvent_t done = nullptr;
@@ -1196,6 +1205,101 @@ int cut_segments(const CutJob& job, const std::vector<std::shared_ptr<const Prog
   }
   if (fork) cudaEventDestroy(fork);
   return rc;
+}
+
+// The single-GPU pieces: every segment's whole family at its workspace slot.
+std::vector<Piece> family_pieces(const CutJob& job, void* workspace, std::vector<const void*>* seg_states) {
+  std::vector<Piece> pieces;
+  for (size_t s = 0; s < job.prep.segs.size(); ++s) {
+    Piece pc;
+    pc.seg = int(s);
+    pc.v1 = int64_t(1) << job.prep.segs[s].cut_ids.size();
+    pc.dst = static_cast<char*>(workspace) + job.seg_off[s];
+    seg_states->push_back(pc.dst);
+    pieces.push_back(pc);
+  }
+  return pieces;
+}
+
+int cut_programs(const CutJob& job, int dtype, std::vector<std::shared_ptr<const Program>>* progs) {
+  std::vector<const void*> dummy;
+  return piece_programs(job, family_pieces(job, nullptr, &dummy), dtype, progs);
+}
+
+int cut_segments(const CutJob& job, const std::vector<std::shared_ptr<const Program>>& progs, void* workspace,
+                 int dtype, cudaStream_t st, std::vector<const void*>* seg_states) {
+  return run_pieces(job, family_pieces(job, workspace, seg_states), progs, dtype, st);
+}
+
+// ---- the sharded (multi-GPU) pipeline ----------------------------------------
+// Every segment has the same qubit count, so the segments' variant batches,
+// concatenated segment-major, are one array of `total` equal states. It is
+// split into `world` chunks of `per` states (the last padded); rank r
+// simulates chunk r in place and one in-place all-gather fills every chunk on
+// every rank — the gathered array IS the segment batches the merge reads, no
+// reassembly copies. Then each rank merges its own rows of the output.
+struct ShardLayout {
+  int64_t L = 0;                  // amplitudes per state
+  int64_t total = 0, per = 0;     // states overall / per rank
+  std::vector<int64_t> seg_first; // flat index of each segment's first variant
+  int64_t gather_bytes = 0;       // world * per states (256-byte aligned)
+  int64_t chain_off = 0, total_bytes = 0;
+  int64_t row_amps = 0, rows = 0; // the final product's row length and count
+};
+
+bool shard_layout(const CutJob& job, int nq, int world, int dtype, ShardLayout* lay, int* rc) {
+  const CutPrep& pr = job.prep;
+  for (const SegmentPlan& sp : pr.segs)
+    if (sp.nq != pr.segs[0].nq) {
+      *rc = fail(CS_ERR_INVALID, "the sharded pipeline needs equal segment sizes");
+      return false;
+    }
+  if (world < 1) {
+    *rc = fail(CS_ERR_INVALID, "world must be >= 1");
+    return false;
+  }
+  const int64_t eb = int64_t(elem_bytes(dtype));
+  lay->L = int64_t(1) << pr.segs[0].nq;
+  lay->total = 0;
+  for (const SegmentPlan& sp : pr.segs) {
+    lay->seg_first.push_back(lay->total);
+    lay->total += int64_t(1) << sp.cut_ids.size();
+  }
+  lay->per = (lay->total + world - 1) / world;
+  lay->gather_bytes = (int64_t(world) * lay->per * lay->L * eb + 255) / 256 * 256;
+  lay->chain_off = lay->gather_bytes;
+  int64_t off = lay->chain_off;
+  for (int64_t a : job.plan.buf_amps) off += (a * eb + 255) / 256 * 256;
+  lay->total_bytes = off;
+  lay->row_amps = int64_t(1) << job.plan.q_low;
+  lay->rows = (int64_t(1) << nq) >> job.plan.q_low;
+  return true;
+}
+
+// rank's rows [r0, r1) of the final product (parallel.shard_range)
+void shard_rows(const ShardLayout& lay, int world, int rank, int64_t* r0, int64_t* r1) {
+  *r0 = lay.rows * rank / world;
+  *r1 = lay.rows * (rank + 1) / world;
+}
+
+// rank's slice [g0, g1) of the flattened variant list, as per-segment pieces
+std::vector<Piece> shard_pieces(const CutJob& job, const ShardLayout& lay, int64_t g0, int64_t g1, void* ws,
+                                int dtype) {
+  std::vector<Piece> pieces;
+  const int64_t eb = int64_t(elem_bytes(dtype));
+  for (size_t s = 0; s < job.prep.segs.size(); ++s) {
+    const int64_t base = lay.seg_first[s];
+    const int64_t cnt = int64_t(1) << job.prep.segs[s].cut_ids.size();
+    const int64_t a = std::max(g0, base), b = std::min(g1, base + cnt);
+    if (a >= b) continue;
+    Piece pc;
+    pc.seg = int(s);
+    pc.v0 = a - base;
+    pc.v1 = b - base;
+    pc.dst = static_cast<char*>(ws) + a * lay.L * eb;
+    pieces.push_back(pc);
+  }
+  return pieces;
 }
 
 int64_t host_chunk_amps(const CutJob& job, int nq, int chunks) {
@@ -1358,6 +1462,103 @@ int cs_cut_run(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int64_
   }
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? CS_OK : cuda_fail(e, "cut pipeline");
+}
+
+int cs_cut_shard_plan(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int64_t* qb,
+                      const double* params, int64_t n_gates, int32_t n_seg, const int32_t* seg_sizes, int32_t world,
+                      int32_t rank, int32_t dtype, int64_t* info) {
+  if (!valid_dtype(dtype)) return fail(CS_ERR_INVALID, "dtype must be CS_C128 or CS_C64");
+  if (nq < 2 || nq > 62 || !seg_sizes || !info) return fail(CS_ERR_INVALID, "bad arguments");
+  if (world < 1 || rank < 0 || rank >= world) return fail(CS_ERR_INVALID, "bad rank / world");
+  CutJob job;
+  int rc = CS_OK;
+  if (!cut_job(nq, kinds, qa, qb, params, n_gates, n_seg, seg_sizes, -1, dtype, &job, &rc)) return rc;
+  ShardLayout lay;
+  if (!shard_layout(job, nq, world, dtype, &lay, &rc)) return rc;
+  if (world > lay.rows) return fail(CS_ERR_INVALID, "more ranks than output rows");
+  int64_t r0, r1;
+  shard_rows(lay, world, rank, &r0, &r1);
+  info[0] = lay.total_bytes;
+  info[1] = job.plan.q_low;
+  info[2] = r0 * lay.row_amps;
+  info[3] = r1 * lay.row_amps;
+  info[4] = std::min(lay.total, int64_t(rank) * lay.per);
+  info[5] = std::min(lay.total, int64_t(rank + 1) * lay.per);
+  info[6] = lay.per;
+  info[7] = lay.total;
+  return CS_OK;
+}
+
+int cs_cut_run_sharded(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int64_t* qb, const double* params,
+                       int64_t n_gates, int32_t n_seg, const int32_t* seg_sizes, void* comm, int32_t world,
+                       int32_t rank, int64_t out_begin, int64_t out_end, void* out, void* workspace,
+                       int64_t workspace_bytes, int32_t dtype, void* stream, void* const* stage_events,
+                       double* stage_ms) {
+  if (!valid_dtype(dtype)) return fail(CS_ERR_INVALID, "dtype must be CS_C128 or CS_C64");
+  if (nq < 2 || nq > 62 || !seg_sizes) return fail(CS_ERR_INVALID, "bad qubit count or segment sizes");
+  if (world < 1 || rank < 0 || rank >= world) return fail(CS_ERR_INVALID, "bad rank / world");
+  if (!out && out_end > out_begin) return fail(CS_ERR_INVALID, "null output pointer");
+  const auto t0 = std::chrono::steady_clock::now();
+  CutJob job;
+  int rc = CS_OK;
+  if (!cut_job(nq, kinds, qa, qb, params, n_gates, n_seg, seg_sizes, -1, dtype, &job, &rc)) return rc;
+  ShardLayout lay;
+  if (!shard_layout(job, nq, world, dtype, &lay, &rc)) return rc;
+  if (!workspace || workspace_bytes < lay.total_bytes)
+    return fail(CS_ERR_INVALID, "sharded cut workspace too small (query cs_cut_shard_plan)");
+  // with a communicator: this rank's chunk, then the all-gather; without one
+  // (comm == NULL): every variant here and no exchange (one GPU computing any
+  // rank's rows, e.g. a share of the q=34 job)
+  const bool exchange = comm != nullptr && world > 1;
+  const int64_t g0 = exchange ? std::min(lay.total, int64_t(rank) * lay.per) : 0;
+  const int64_t g1 = exchange ? std::min(lay.total, int64_t(rank + 1) * lay.per) : lay.total;
+  std::vector<Piece> pieces = shard_pieces(job, lay, g0, g1, workspace, dtype);
+  std::vector<std::shared_ptr<const Program>> progs;
+  rc = piece_programs(job, pieces, dtype, &progs);
+  if (rc != CS_OK) return rc;
+  const double t_pre = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  cudaStream_t st = as_stream(stream);
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  if (stage_events) {
+    for (int i = 0; i < 4; ++i) ev[i] = static_cast<cudaEvent_t>(stage_events[i]);
+  } else if (stage_ms) {
+    for (auto& e : ev) cudaEventCreate(&e);
+  }
+  if (ev[0]) cudaEventRecord(ev[0], st);
+  rc = run_pieces(job, pieces, progs, dtype, st);
+  if (rc != CS_OK) return rc;
+  if (ev[1]) cudaEventRecord(ev[1], st);
+  if (exchange) {
+    const int64_t chunk = lay.per * lay.L * int64_t(elem_bytes(dtype));
+    rc = cs_allgather_states(comm, static_cast<char*>(workspace) + int64_t(rank) * chunk, chunk, workspace, st);
+    if (rc != CS_OK) return rc;
+  }
+  if (ev[2]) cudaEventRecord(ev[2], st);
+  std::vector<const void*> seg_states;
+  for (size_t s = 0; s < job.prep.segs.size(); ++s)
+    seg_states.push_back(static_cast<char*>(workspace) + lay.seg_first[s] * lay.L * int64_t(elem_bytes(dtype)));
+  if (out_end > out_begin) {
+    rc = run_chain(job.plan, job.prep.n, seg_states.data(), out_begin, out_end, out,
+                   static_cast<char*>(workspace) + lay.chain_off, lay.total_bytes - lay.chain_off, dtype, st);
+    if (rc != CS_OK) return rc;
+  }
+  if (ev[3]) cudaEventRecord(ev[3], st);
+  if (stage_ms) {
+    cudaError_t e = cudaEventSynchronize(ev[3]);
+    float a = 0, b = 0, c = 0;
+    cudaEventElapsedTime(&a, ev[0], ev[1]);
+    cudaEventElapsedTime(&b, ev[1], ev[2]);
+    cudaEventElapsedTime(&c, ev[2], ev[3]);
+    if (!stage_events)
+      for (auto& x : ev) cudaEventDestroy(x);
+    if (e != cudaSuccess) return cuda_fail(e, "sharded cut pipeline");
+    stage_ms[0] = t_pre;
+    stage_ms[1] = a;
+    stage_ms[2] = b;
+    stage_ms[3] = c;
+  }
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? CS_OK : cuda_fail(e, "sharded cut pipeline");
 }
 
 static int reduce_common(const void* a, const void* b, int64_t n, int mode, int32_t dtype, double* result,

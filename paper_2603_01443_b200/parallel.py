@@ -116,18 +116,41 @@ def run_cut_sharded(circuit, n: int, *, rank: int, world: int, dtype=np.complex1
                     comm=None):
     """Cut pipeline on `world` ranks; returns (ShardedState-like tensor, (begin, end)).
 
+    With no injected functions and a `comm` (a comm.NcclComm; or world 1)
+    the whole rank step is ONE native call (pipeline.run_cut_sharded_native
+    -> cs_cut_run_sharded). Otherwise the host-orchestrated form runs:
     simulate_slice(family, v0, v1) -> tensor [v1-v0, 2^q_i] and
     merge_shard(chain, batches, (begin, end)) -> tensor default to the sm_100a
-    kernels; the CPU tests inject oracle-backed versions. `comm` (a
-    comm.NcclComm) routes the all-gather through libcutsim's NCCL binding;
-    otherwise torch.distributed's collective on `group` is used."""
+    kernels; the CPU tests inject oracle-backed versions, and the all-gather
+    is torch.distributed's collective on `group`."""
     import torch
     import torch.distributed as dist
 
-    from .pipeline import preprocess
+    from .pipeline import preprocess, run_cut_sharded_native
 
     if np.dtype(dtype) != np.complex128:
         raise ValidationError("the sharded path exchanges complex128 states")
+    q = circuit.num_qubits
+    native = (simulate_slice is None and merge_shard is None and all_gather is None
+              and (comm is not None or world == 1) and q % n == 0)
+    if native:
+        # the device path: ONE native call per rank (cs_cut_run_sharded) — C++
+        # preprocess, this rank's variant chunk simulated in place, the
+        # in-place NCCL all-gather, the chain merge of this rank's rows
+        timers = {} if merge_events is not None else None
+        evs = None
+        if merge_events is not None:
+            evs = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        res = run_cut_sharded_native(circuit, n, rank=rank, world=world, comm=comm, dtype=dtype, out=out,
+                                     events=evs)
+        if merge_events is not None:
+            merge_events["start"], merge_events["end"] = evs[2], evs[3]
+            merge_events["events"] = evs
+        from .merging import ShardedState
+
+        if isinstance(res, ShardedState):
+            return res.device, (res.begin, res.end)
+        return res.device_tensor(), (0, 1 << q)
     prep = preprocess(circuit, n)
     fams = prep.subs.segments
     counts = [f.num_variants for f in fams]

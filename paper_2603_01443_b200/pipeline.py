@@ -167,6 +167,74 @@ def run_cut(circuit: Circuit, n: int, *, dtype=np.complex128, max_qubits: int = 
     return StateVec(q, device=out)
 
 
+def run_cut_sharded_native(circuit: Circuit, n: int, *, rank: int = 0, world: int = 1, comm=None,
+                           dtype=np.complex128, out=None, out_range=None, workspace=None,
+                           timers: dict | None = None, events=None, max_qubits: int = 34):
+    """One rank's share of the multi-GPU cut pipeline in ONE native call
+    (cs_cut_run_sharded): C++ preprocess, this rank's chunk of the variant
+    list simulated in place, one in-place NCCL all-gather (``comm``, a
+    comm.NcclComm; None = simulate every variant here, no exchange), then the
+    chain merge of this rank's output rows (default: parallel.shard_range).
+    Returns a ShardedState (or a StateVec when the range is the whole state).
+    ``timers`` (a dict) receives pre/sub/exchange/merge seconds (synchronises);
+    ``events`` = four timing torch.cuda.Events recorded around the stages.
+    Each rank computes rows [begin, end) of reference merging.py:156-186."""
+    from . import _native
+    from .errors import ValidationError
+
+    q = circuit.num_qubits
+    check_capacity(q, max_qubits)
+    if n < 2 or q % n:
+        raise ValidationError(f"q must be divisible by n >= 2: q={q}, n={n}")
+    t = _device.require_cuda()
+    code = _device.code_of(dtype)
+    sizes = (q // n,) * n
+    lay = _native.cut_shard_plan(q, circuit.table, sizes, world, rank, code)
+    begin, end = (lay["out_begin"], lay["out_end"]) if out_range is None else tuple(out_range)
+    if not (0 <= begin <= end <= (1 << q)):
+        raise ValidationError(f"output range [{begin}, {end}) outside [0, 2^{q})")
+    if out is None:
+        _device.check_free((end - begin) * np.dtype(dtype).itemsize, "state shard")
+        out = _device.empty_shape((end - begin,), dtype)
+    else:
+        _device.check_out(out, end - begin, dtype)
+    if workspace is None:
+        workspace = t.empty(max(lay["workspace_bytes"], 1), dtype=t.uint8, device="cuda")
+    elif workspace.numel() * workspace.element_size() < lay["workspace_bytes"] or not workspace.is_contiguous():
+        raise ValidationError(f"workspace must be a contiguous CUDA buffer of >= {lay['workspace_bytes']} bytes")
+    k, qa, qb, prm = _native._table_args(circuit.table)
+    sz = _native.c_i32(sizes)
+    stage = np.zeros(4) if timers is not None else None
+    evp = None
+    if events is not None:
+        for ev in events:
+            ev.record()
+        evp = (ctypes.c_void_p * 4)(*(ev.cuda_event for ev in events))
+    handle = comm.handle if comm is not None else None
+    _native.check(
+        _native.load().cs_cut_run_sharded(q, _native.ptr(k), _native.ptr(qa), _native.ptr(qb), _native.ptr(prm),
+                                          len(k), len(sz), _native.ptr(sz), handle, world, rank, begin, end,
+                                          out.data_ptr(), workspace.data_ptr(),
+                                          workspace.numel() * workspace.element_size(), code,
+                                          _device.stream_ptr(), evp, _native.ptr(stage)),
+        "cs_cut_run_sharded",
+    )
+    if timers is not None:
+        for key, v in zip(("pre", "sub", "exchange", "merge"), stage):
+            timers[key] = float(v) / 1e3
+    if (begin, end) != (0, 1 << q):
+        return ShardedState(q, begin, end, out)
+    return StateVec(q, device=out)
+
+
+def shard_workspace_bytes(circuit: Circuit, n: int, world: int, dtype=np.complex128) -> int:
+    from . import _native
+
+    q = circuit.num_qubits
+    return _native.cut_shard_plan(q, circuit.table, (q // n,) * n, world, 0, _device.code_of(dtype))[
+        "workspace_bytes"]
+
+
 def cut_simulate(circuit: Circuit, n: int, **kw) -> StateVec:
     return run_cut(circuit, n, **kw)
 

@@ -106,3 +106,18 @@ def test_sample_amplitudes_matches_merge():
     idx = np.array([0, 1, 77, 300, 511])
     got = orc.sample_amplitudes(states, tab, co, [3, 3, 3], idx)
     assert np.abs(got - merged[idx]).max() < 1e-14
+
+
+@pytest.mark.parametrize("q,d,n,c,seed,rows", [(10, 4, 2, 2, 0, (3, 20)), (12, 5, 3, 4, 1, (0, 16)),
+                                               (12, 4, 4, 4, 2, (5, 64))])
+def test_c_port_matches_numpy_oracle(q, d, n, c, seed, rows):
+    """The C restatement (the CPU baseline bench.py times) equals the numpy
+    oracle: simulate on every variant, merge_rows on a row range (n = 2..4)."""
+    from oracle import oracle_c
+
+    k, a, b, p = orc.brickwall(q, d, n, c, seed)
+    merged, states, tab, co = orc.cut_pipeline(q, k, a, b, p, n)
+    assert np.abs(oracle_c.simulate(q, k, a, b, p, threads=2) - orc.simulate(q, k, a, b, p)).max() < 1e-13
+    acc, _ = oracle_c.merge_rows(states, tab, co, rows, threads=2)
+    w = len(states[0][0])
+    assert np.abs(acc - merged[rows[0] * w:rows[1] * w]).max() < 1e-13
