@@ -374,10 +374,12 @@ def run_ours(args):
                               f"output: run it on >= {(16 << q) // (150 * 2**30) + 1} GPUs"}), flush=True)
         return 0
     stream = torch.cuda.current_stream()
-    # NVRTC-specialise the sweep programs on first use: compiled during the
-    # warm-up steps, outside the timed region (as the reference's warm_up()
-    # keeps numba JIT out of its timers, harness.py:95-111)
-    _native.set_option("jit", 0 if args.no_jit else 2)
+    # tiered kernels (jit = 3): a new program runs the interpreter kernel at
+    # once while its NVRTC module compiles on a background thread; the warm-up
+    # ends with cs_jit_wait, so the timed steps run the compiled modules (as
+    # the reference's warm_up() keeps numba JIT out of its timers,
+    # harness.py:95-111) and the cold leg shows what an unseen circuit costs
+    _native.set_option("jit", 0 if args.no_jit else 3)
     peak, peak_src = load_peaks()
 
     prep0 = preprocess(circ, n)
@@ -411,6 +413,9 @@ def run_ours(args):
 
     for _ in range(args.warmup):
         step()
+    torch.cuda.synchronize()
+    _native.jit_wait(600)
+    step()  # first run of the compiled modules
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
@@ -634,7 +639,11 @@ def measure_cold(cb, spec, out, workspace, steps):
 
     from paper_2603_01443_b200.generators import BrickwallSpec
 
+    from paper_2603_01443_b200 import _native
+
     ts = []
+    c0 = _native.get_option("jit_units_compiled")
+    r0 = _native.get_option("jit_units_reused")
     for i in range(steps):
         c = cb.build_brickwall(BrickwallSpec(spec.q, spec.d, spec.n, spec.c_total, 1000 + i))
         torch.cuda.synchronize()
@@ -643,10 +652,15 @@ def measure_cold(cb, spec, out, workspace, steps):
         torch.cuda.synchronize()
         ts.append(time.perf_counter() - t0)
     t = float(np.median(ts))
+    _native.jit_wait(600)
     return {"ms_per_step": 1e3 * t, "value": (1 << spec.q) / t, "unit": UNIT, "steps": steps,
-            "max_ms": 1e3 * max(ts),
+            "max_ms": 1e3 * max(ts), "jit": _native.get_option("jit"),
+            "kernel_units_compiled": _native.get_option("jit_units_compiled") - c0,
+            "kernel_units_reused": _native.get_option("jit_units_reused") - r0,
             "note": "seeds 1000.. (same family, new angles and cut layers): every step a circuit the library "
-                    "has not seen; preprocess, schedules and kernel modules inside the timed region"}
+                    "has not seen, timed on the host wall clock around a synchronised run_cut: C++ "
+                    "preprocess, sweep schedules, and the variant stage on the interpreter kernel while the "
+                    "circuit's NVRTC modules compile in the background (jit = 3)"}
 
 
 def measure_uncut(cb, circ, q, stream, peak):
@@ -656,7 +670,9 @@ def measure_uncut(cb, circ, q, stream, peak):
 
     from paper_2603_01443_b200 import _native
 
-    cb.simulate(circ, max_qubits=q)  # builds (and JIT-compiles) the uncut program
+    cb.simulate(circ, max_qubits=q)  # builds the uncut program (its module compiles in the background)
+    _native.jit_wait(600)
+    cb.simulate(circ, max_qubits=q)
     torch.cuda.synchronize()
     u0 = torch.cuda.Event(enable_timing=True)
     u1 = torch.cuda.Event(enable_timing=True)

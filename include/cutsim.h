@@ -57,10 +57,19 @@ int cs_device_count(int32_t* count);
  * tensor-core merge for K = 8..64: 0 off, 1 four real GEMMs per complex
  * product, 2 three (3M); default 2), "engine" (1 register-tile
  * sweep kernel, 0 shared-memory tile kernel), "jit" (0 never, 1 from a
- * program's second use, 2 always: NVRTC-specialised sweep kernels),
+ * program's second use, 2 always: NVRTC-specialised sweep kernels compiled
+ * on first use, 3 tiered: interpreter until a background compile is done —
+ * see cs_jit_wait), "jit_struct" (structure-keyed modules with the
+ * coefficients passed as kernel parameters, so circuits differing only in
+ * angles share compiled code: 0 never, 1 small programs such as variant
+ * batches (default; their 2x2s are not normalised), 2 always),
+ * "jit_units_compiled" / "jit_units_reused" (read-only counters),
  * "merge_ozaki" (int8 tcgen05 tensor-core merge with exact FP64 splitting
  * for one-slot products of K >= "merge_ozaki_min_k" terms, lo_len % 128 == 0,
- * row ranges % 16 == 0; default 1, min K 16), "zero_start_tiles" (simulations
+ * row ranges % 16 == 0; default 1, min K 16), "merge_ozaki_digits" (8: 7
+ * balanced base-256 digits per operand, 7 int32 diagonals per output —
+ * default, truncation ~2e-15 of max|a| max|b|; 7: 8 base-128 digits, 8
+ * diagonals, ~6e-16), "zero_start_tiles" (simulations
  * from |0..0> zero the states once and launch only the tiles that can be
  * non-zero; default 1),
  * "jit_max_cost", "vb", "sweep_minb", "merge_smem_kb", "merge_dmma3_warps", "jit_minb", "dense_norm" (normalised 2x2s:
@@ -71,6 +80,11 @@ int64_t cs_get_option(const char* key);
 
 /* Kernels launched by this library since load (bench `gpu_launches`). */
 int64_t cs_launch_count(void);
+
+/* jit = 3 (tiered): programs run on the interpreter kernel while their
+ * NVRTC modules compile on a background thread. Block until that queue is
+ * drained (timeout_s < 0: no limit); CS_ERR_TIMEOUT if it is still busy. */
+int cs_jit_wait(double timeout_s);
 
 /* Set every state of a batch to the basis state |index>.
  * Replaces StateVec.zero_state (engine.py:47-51). */

@@ -48,6 +48,7 @@ SIGNATURES = {
     "cs_set_option": (ctypes.c_int, [ctypes.c_char_p, _i64]),
     "cs_get_option": (_i64, [ctypes.c_char_p]),
     "cs_launch_count": (_i64, []),
+    "cs_jit_wait": (ctypes.c_int, [ctypes.c_double]),
     "cs_init_basis": (ctypes.c_int, [_vp, _i32, _i64, _i64, _i32, _vp]),
     "cs_sim_batch": (ctypes.c_int, [_i32, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _i64, _i64, _u64, _i32,
                                     _i32, _vp]),
@@ -158,6 +159,11 @@ def get_option(key: str) -> int:
 
 def launch_count() -> int:
     return int(load().cs_launch_count())
+
+
+def jit_wait(timeout_s: float = -1.0) -> None:
+    """Block until the background kernel compiler (jit = 3) is idle."""
+    check(load().cs_jit_wait(float(timeout_s)), "cs_jit_wait")
 
 
 def sweep_plan_json(nq, table, slots=None, tile_bits=0, dtype=CS_C128) -> str:

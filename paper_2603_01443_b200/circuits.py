@@ -20,7 +20,7 @@ from __future__ import annotations
 import json
 import math
 from dataclasses import dataclass
-from enum import Enum
+from enum import Enum, EnumMeta
 
 import numpy as np
 
@@ -38,7 +38,19 @@ KIND_U3 = 7
 NUM_KINDS = 8
 
 
-class GateKind(Enum):
+class _KindMeta(EnumMeta):
+    """Iterating GateKind yields the reference's seven kinds (circuits.py:
+    25-33: code written against the reference enumerates exactly those);
+    the U3 extension stays reachable as GateKind.U3 / GateKind("U3")."""
+
+    def __iter__(cls):
+        return (m for m in super().__iter__() if m.name != "U3")
+
+    def __len__(cls):
+        return sum(1 for _ in cls.__iter__())
+
+
+class GateKind(Enum, metaclass=_KindMeta):
     """Gate kinds; the value is the JSON wire string."""
 
     H = "H"
@@ -247,7 +259,7 @@ class Circuit:
     tuple that is trusted to describe ``gates``.
     """
 
-    __slots__ = ("num_qubits", "_gates", "_table", "_depth")
+    __slots__ = ("num_qubits", "_gates", "_table", "_depth", "_origin")
 
     def __init__(self, num_qubits: int, gates=(), *, _table=None):
         if num_qubits < 0:
@@ -255,6 +267,7 @@ class Circuit:
         self.num_qubits = int(num_qubits)
         self._gates = tuple(gates)
         self._depth = None
+        self._origin = None  # (SegmentFamily, variant) for decompose()'s lazy variant circuits
         if _table is not None:
             self._table = _table if isinstance(_table, GateTable) else GateTable(*_table)
             if self._gates and len(self._gates) != len(self._table):
@@ -278,6 +291,7 @@ class Circuit:
         obj._table = table
         obj._gates = None
         obj._depth = None
+        obj._origin = None
         return obj
 
     # -- packed table ---------------------------------------------------

@@ -23,7 +23,8 @@ def install_as_cutbench(name: str = "cutbench", *, replace: bool = False) -> typ
 
     from . import boundary_fit, circuits, cli, cutting, engine, errors, harness, merging, sweeps, theory
 
-    if name in sys.modules and sys.modules[name] is not pkg and not replace:
+    cur = sys.modules.get(name)
+    if cur is not None and getattr(cur, "__dropin_of__", None) is not pkg and not replace:
         raise RuntimeError(f"module {name!r} is already imported; pass replace=True to shadow it")
     combined = types.ModuleType(f"{name}.harness", harness.__doc__)
     for mod in (harness, sweeps):
@@ -32,7 +33,19 @@ def install_as_cutbench(name: str = "cutbench", *, replace: bool = False) -> typ
                 setattr(combined, attr, val)
     subs = {"circuits": circuits, "cutting": cutting, "engine": engine, "merging": merging, "errors": errors,
             "cli": cli, "costmodel": theory, "svmfit": boundary_fit, "harness": combined}
-    sys.modules[name] = pkg
+    # a proxy package: the package's public names, with the submodule
+    # attributes pointing at the reference-named modules (so both
+    # `import cutbench.harness` and `from cutbench import harness` see the
+    # combined harness namespace)
+    proxy = types.ModuleType(name, pkg.__doc__)
+    for attr, val in vars(pkg).items():
+        if not attr.startswith("__"):
+            setattr(proxy, attr, val)
+    for sub, mod in subs.items():
+        setattr(proxy, sub, mod)
+    proxy.__path__ = []  # a package: submodules resolve through sys.modules
+    proxy.__dropin_of__ = pkg
+    sys.modules[name] = proxy
     for sub, mod in subs.items():
         sys.modules[f"{name}.{sub}"] = mod
-    return pkg
+    return proxy

@@ -4,6 +4,9 @@
 
 #include <algorithm>
 #include <atomic>
+#include <condition_variable>
+#include <deque>
+#include <thread>
 #include <chrono>
 #include <cstring>
 #include <memory>
@@ -36,7 +39,7 @@ int merge_dmma3_cols_per_warp(int K);
 int merge_dmma3_row_blocks(int K);
 bool merge_ozaki_supported(int K, int64_t lo_len, int64_t nrows);
 cudaError_t launch_merge_ozaki(const MergeParams& mp, int64_t nrows, void* out, int accumulate, int sms, bool unit,
-                               cudaStream_t stream);
+                               cudaStream_t stream, int digit_bits);
 cudaError_t launch_init_basis(void* states, int64_t len, int64_t n_states, int64_t index, int dtype,
                               cudaStream_t stream);
 cudaError_t launch_reduce(const void* a, const void* b, int64_t n, int mode, int dtype, double2* scratch,
@@ -70,8 +73,12 @@ struct Options {
   int64_t zero_start_tiles = 1;   // from |0..0>: zero the states once, launch only the tiles that can be non-zero
   int64_t merge_ozaki = 1;        // int8 tcgen05 merge (exact FP64 splitting) for K >= merge_ozaki_min_k
   int64_t merge_ozaki_min_k = 16;
+  int64_t merge_ozaki_digits = 8;  // digit bits of the int8 merge: 8 (7 slices, faster) or 7 (8 slices)
   int64_t engine = 1;      // 1: register-tile kernel (rsweep), 0: shared-memory tile kernel (sweep)
-  int64_t jit = 0;         // 0 never, 1 from a program's 2nd use, 2 always: NVRTC-specialised sweeps (opt-in: compile ~1-7 s)
+  int64_t jit = 0;         // 0 never, 1 from a program's 2nd use, 2 always (compile on first use, blocking),
+                           // 3 tiered: the interpreter runs while the module compiles on a background thread
+  int64_t jit_struct = 1;  // param-mode (structure-keyed) modules: 0 never, 1 for small programs (< 2^22
+                           // amplitudes: variant batches), 2 always
   int64_t jit_max_cost = 40000;  // FP64 instructions per specialised launch (code-size guard)
   int64_t plan_json = 0;   // cs_sweep_plan_json: 0 sweeps, 1 register programs
 } g_opt;
@@ -184,6 +191,7 @@ struct Program {
   mutable bool jit_tried = false;
   mutable std::atomic<int> uses{0};
   int64_t n_states = 1;  // states per launch the program was scheduled for
+  bool param_mode = false;  // structure-keyed kernels with the coefficients as kernel parameters
 };
 
 // content-keyed program cache with least-recently-used eviction (a clear-all
@@ -249,16 +257,23 @@ std::shared_ptr<const Program> build_schedule(int nq, const uint8_t* kinds, cons
   const int fuse = int(g_opt.fuse);
   // normalised 2x2s only pay where the 1-coefficients become free (the
   // NVRTC-specialised kernels); the interpreter keeps the plain matrices
-  const int norm = g_opt.dense_norm == 2 ? (g_opt.jit != 0 && g_opt.engine == 1 ? 1 : 0) : int(g_opt.dense_norm);
+  // param mode: small (latency-bound) programs get structure-keyed kernels;
+  // their normalisation is off (its pivot choice depends on the angles and
+  // would make the structure value-dependent)
+  const bool param_mode = g_opt.jit != 0 && g_opt.engine == 1 &&
+                          (g_opt.jit_struct == 2 || (g_opt.jit_struct == 1 && !zero_start_pays(n_states, nq)));
+  const int norm = param_mode ? 0
+                   : g_opt.dense_norm == 2 ? (g_opt.jit != 0 && g_opt.engine == 1 ? 1 : 0)
+                                           : int(g_opt.dense_norm);
   // the cost-aware tile-set policy (3) only pays for a start from |0..0>
   // (zero-start tiles); other starts keep the most-absorbed-ops policy
   const int windows = (g_sweep_windows == 3 && !(zero_start && g_opt.zero_start_tiles &&
                                                  zero_start_pays(n_states, nq)))
                           ? 1
                           : g_sweep_windows;
-  const int32_t hdr[13] = {nq, T, L, int32_t(fuse), slots ? 1 : 0, dtype, vb, g_sweep_minb,
+  const int32_t hdr[14] = {nq, T, L, int32_t(fuse), slots ? 1 : 0, dtype, vb, g_sweep_minb,
                            int32_t(g_opt.engine), norm, g_reg_bits * 8 + g_reg_reorder * 4 + windows, g_jit_minb,
-                           g_jit_persistent};
+                           g_jit_persistent, param_mode ? 1 : 0};
   key.append(reinterpret_cast<const char*>(hdr), sizeof(hdr));
   key.append(reinterpret_cast<const char*>(kinds), size_t(n_gates));
   key.append(reinterpret_cast<const char*>(qa), size_t(n_gates) * 8);
@@ -283,6 +298,7 @@ std::shared_ptr<const Program> build_schedule(int nq, const uint8_t* kinds, cons
   auto built = std::make_shared<Program>();
   built->engine = int(g_opt.engine);
   built->n_states = n_states;
+  built->param_mode = param_mode;
   built->sweeps = schedule_sweeps(ops, nq, T, L, max_group, windows);
   build_launches(*built);
   std::shared_ptr<const Program> prog = built;
@@ -361,7 +377,7 @@ int merge_launch_one(int S, int Kc, const int32_t* hidx, const int32_t* lidx, co
       }
       void* o = static_cast<char*>(out) + size_t(s) * size_t(out_slot_stride) * elem_bytes(dtype);
       cudaError_t e = launch_merge_ozaki(po, row_end - row_begin, o, accumulate, sm_count(), g_opt.merge_ozaki == 2,
-                                         stream);
+                                         stream, int(g_opt.merge_ozaki_digits));
       g_launches.fetch_add(3);
       if (e != cudaSuccess) return cuda_fail(e, "merge_ozaki launch");
     }
@@ -543,14 +559,8 @@ int merge_terms_impl(int S, int K, const int32_t* hidx, const int32_t* lidx, con
   return CS_OK;
 }
 
-// The program's specialised kernels, compiling them on first demand (engine 1).
-std::shared_ptr<JitModule> program_jit(const Program& prog, int dtype) {
-  if (prog.engine != 1 || g_opt.jit == 0) return nullptr;
-  const int uses = ++prog.uses;
-  if (g_opt.jit == 1 && uses < 2) return nullptr;
-  std::lock_guard<std::mutex> lk(prog.jit_mu);
-  if (prog.jit_tried) return prog.jit;
-  prog.jit_tried = true;
+// Compile a program's specialised kernels (sets prog.jit; caller holds jit_mu).
+void compile_program_jit(const Program& prog, int dtype) {
   std::vector<const Sweep*> sw;
   std::vector<const std::vector<RegOp>*> rp;
   std::vector<int> minb;
@@ -571,20 +581,91 @@ std::shared_ptr<JitModule> program_jit(const Program& prog, int dtype) {
     rp.push_back(ok ? &ln.reg : nullptr);
     any |= ok;
   }
-  if (!any) return nullptr;
+  if (!any) return;
   std::string err;
-  prog.jit = jit_compile(sw, rp, dtype, &err, &minb, &pers);
-  if (!prog.jit) g_err = "JIT unavailable, using the interpreter kernel: " + err;
+  auto mod = jit_compile(sw, rp, dtype, &err, &minb, &pers, prog.param_mode);
+  if (!mod) g_err = "JIT unavailable, using the interpreter kernel: " + err;
+  prog.jit = mod;
+}
+
+// Tiered compilation (jit = 3): one background thread compiles queued
+// programs while their calls run on the interpreter kernel.
+struct JitQueue {
+  std::mutex mu;
+  std::condition_variable cv, idle_cv;
+  std::deque<std::pair<std::shared_ptr<const Program>, int>> q;
+  int busy = 0;
+  bool started = false;
+};
+// never destroyed: the detached worker waits on cv for the life of the
+// process, and destroying a condition variable with a waiter blocks exit
+JitQueue& g_jitq = *new JitQueue;
+
+void jit_worker(int device) {
+  cudaSetDevice(device);
+  for (;;) {
+    std::pair<std::shared_ptr<const Program>, int> job;
+    {
+      std::unique_lock<std::mutex> lk(g_jitq.mu);
+      g_jitq.cv.wait(lk, [] { return !g_jitq.q.empty(); });
+      job = std::move(g_jitq.q.front());
+      g_jitq.q.pop_front();
+      ++g_jitq.busy;
+    }
+    {
+      std::lock_guard<std::mutex> lk(job.first->jit_mu);
+      compile_program_jit(*job.first, job.second);
+    }
+    std::lock_guard<std::mutex> lk(g_jitq.mu);
+    --g_jitq.busy;
+    g_jitq.idle_cv.notify_all();
+  }
+}
+
+void enqueue_jit(std::shared_ptr<const Program> prog, int dtype) {
+  std::lock_guard<std::mutex> lk(g_jitq.mu);
+  if (!g_jitq.started) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::thread(jit_worker, dev).detach();
+    g_jitq.started = true;
+  }
+  g_jitq.q.emplace_back(std::move(prog), dtype);
+  g_jitq.cv.notify_one();
+}
+
+// The program's specialised kernels, compiling them on first demand (engine
+// 1). jit = 3: never blocks — a program whose kernels are not compiled yet is
+// queued for the background compiler and runs on the interpreter meanwhile.
+std::shared_ptr<JitModule> program_jit(const std::shared_ptr<const Program>& pp, int dtype) {
+  const Program& prog = *pp;
+  if (prog.engine != 1 || g_opt.jit == 0) return nullptr;
+  const int uses = ++prog.uses;
+  if (g_opt.jit == 1 && uses < 2) return nullptr;
+  if (g_opt.jit == 3) {
+    std::unique_lock<std::mutex> lk(prog.jit_mu, std::try_to_lock);
+    if (!lk.owns_lock()) return nullptr;  // the background compiler holds it
+    if (prog.jit_tried) return prog.jit;
+    prog.jit_tried = true;
+    lk.unlock();
+    enqueue_jit(pp, dtype);
+    return nullptr;
+  }
+  std::lock_guard<std::mutex> lk(prog.jit_mu);
+  if (prog.jit_tried) return prog.jit;
+  prog.jit_tried = true;
+  compile_program_jit(prog, dtype);
   return prog.jit;
 }
 
 // deadline_s > 0: CLOCK_MONOTONIC seconds (Python's time.monotonic()); the
 // stream is synchronised after every launch and CS_ERR_TIMEOUT returned once
 // it has passed (the reference's cooperative budget, engine.py:142-155)
-int run_program(const Program& prog_ref, int nq, void* states, int64_t n_states, int64_t state_stride,
-                uint64_t variant_base, int init_zero, int dtype, cudaStream_t st, double deadline_s = 0.0) {
-  const Program* prog = &prog_ref;
-  std::shared_ptr<JitModule> jit = program_jit(*prog, dtype);
+int run_program(const std::shared_ptr<const Program>& prog_ptr, int nq, void* states, int64_t n_states,
+                int64_t state_stride, uint64_t variant_base, int init_zero, int dtype, cudaStream_t st,
+                double deadline_s = 0.0) {
+  const Program* prog = prog_ptr.get();
+  std::shared_ptr<JitModule> jit = program_jit(prog_ptr, dtype);
   static SweepParams p;
   static RegParams rp;
   static std::mutex pm;
@@ -609,7 +690,8 @@ int run_program(const Program& prog_ref, int nq, void* states, int64_t n_states,
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
   }
   for (const Launch& ln : prog->launches) {
-    const JitKernel* jk = (jit && li < jit->kernels.size() && jit->kernels[li].kernel) ? &jit->kernels[li] : nullptr;
+    const JitUnit* jk = (jit && li < jit->units.size() && jit->units[li]) ? jit->units[li].get() : nullptr;
+    const std::vector<unsigned char>* blob = jk ? &jit->blobs[li] : nullptr;
     ++li;
     const Sweep& sw = prog->sweeps[size_t(ln.sweep)];
     const int T = sw.tile_bits;
@@ -626,7 +708,9 @@ int run_program(const Program& prog_ref, int nq, void* states, int64_t n_states,
         unsigned long long vbase_arg = variant_base + uint64_t(v0);
         int init_arg = (first && init_zero) ? 1 : 0;
         unsigned long long ntiles_arg = n_tiles;
-        void* args[] = {&sp_arg, &stride_arg, &vbase_arg, &init_arg, &ntiles_arg};
+        // param mode: the launch's coefficients travel as the 6th argument
+        void* args[] = {&sp_arg, &stride_arg, &vbase_arg, &init_arg, &ntiles_arg,
+                        blob && !blob->empty() ? const_cast<unsigned char*>(blob->data()) : nullptr};
         e = cudaSuccess;
         if (jk->smem > 48 * 1024) {
           int dev = 0;
@@ -886,8 +970,14 @@ int cs_set_option(const char* key, int64_t value) {
     if (value < 0 || value > 2) return fail(CS_ERR_INVALID, "merge_dmma must be 0, 1 or 2");
     g_opt.merge_dmma = value;
   } else if (k == "jit") {
-    if (value < 0 || value > 2) return fail(CS_ERR_INVALID, "jit must be 0, 1 or 2");
+    if (value < 0 || value > 3) return fail(CS_ERR_INVALID, "jit must be 0, 1, 2 or 3");
     g_opt.jit = value;
+  } else if (k == "merge_ozaki_digits") {
+    if (value != 7 && value != 8) return fail(CS_ERR_INVALID, "merge_ozaki_digits must be 7 or 8");
+    g_opt.merge_ozaki_digits = value;
+  } else if (k == "jit_struct") {
+    if (value < 0 || value > 2) return fail(CS_ERR_INVALID, "jit_struct must be 0, 1 or 2");
+    g_opt.jit_struct = value;
   } else if (k == "jit_max_cost") {
     if (value < 0) return fail(CS_ERR_INVALID, "jit_max_cost must be >= 0");
     g_opt.jit_max_cost = value;
@@ -916,6 +1006,10 @@ int64_t cs_get_option(const char* key) {
   if (k == "vb") return g_opt.vb;
   if (k == "engine") return g_opt.engine;
   if (k == "jit") return g_opt.jit;
+  if (k == "jit_struct") return g_opt.jit_struct;
+  if (k == "merge_ozaki_digits") return g_opt.merge_ozaki_digits;
+  if (k == "jit_units_compiled") return jit_units_compiled();
+  if (k == "jit_units_reused") return jit_units_reused();
   if (k == "jit_max_cost") return g_opt.jit_max_cost;
   if (k == "merge_dmma") return g_opt.merge_dmma;
   if (k == "merge_ozaki") return g_opt.merge_ozaki;
@@ -935,6 +1029,18 @@ int64_t cs_get_option(const char* key) {
 }
 
 int64_t cs_launch_count(void) { return g_launches.load(); }
+
+int cs_jit_wait(double timeout_s) {
+  std::unique_lock<std::mutex> lk(g_jitq.mu);
+  auto done = [] { return g_jitq.q.empty() && g_jitq.busy == 0; };
+  if (timeout_s < 0) {
+    g_jitq.idle_cv.wait(lk, done);
+    return CS_OK;
+  }
+  if (!g_jitq.idle_cv.wait_for(lk, std::chrono::duration<double>(timeout_s), done))
+    return fail(CS_ERR_TIMEOUT, "background kernel compilation still running");
+  return CS_OK;
+}
 
 int cs_init_basis(void* states, int32_t nq, int64_t n_states, int64_t index, int32_t dtype, void* stream) {
   if (!valid_dtype(dtype)) return fail(CS_ERR_INVALID, "dtype must be CS_C128 or CS_C64");
@@ -965,7 +1071,7 @@ int cs_sim_batch(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int6
   } catch (const PlanError& pe) {
     return fail(pe.code, pe.msg);
   }
-  return run_program(*prog, nq, states, n_states, state_stride, variant_base, init_zero, dtype, st);
+  return run_program(prog, nq, states, n_states, state_stride, variant_base, init_zero, dtype, st);
 }
 
 int cs_sim_batch_until(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int64_t* qb,
@@ -983,7 +1089,7 @@ int cs_sim_batch_until(int32_t nq, const uint8_t* kinds, const int64_t* qa, cons
   } catch (const PlanError& pe) {
     return fail(pe.code, pe.msg);
   }
-  return run_program(*prog, nq, states, n_states, state_stride, variant_base, init_zero, dtype, as_stream(stream),
+  return run_program(prog, nq, states, n_states, state_stride, variant_base, init_zero, dtype, as_stream(stream),
                      deadline_s);
 }
 
@@ -1028,7 +1134,7 @@ int cs_jit_selftest(int32_t nq, const uint8_t* kinds, const int64_t* qa, const i
   std::vector<char> cubin;
   std::vector<std::string> names;
   std::string err;
-  if (!jit_cubin(sw, rp, dtype, &cubin, &names, &err)) return fail(CS_ERR_INTERNAL, err);
+  if (!jit_cubin(sw, rp, dtype, &cubin, &names, &err, prog->param_mode)) return fail(CS_ERR_INTERNAL, err);
   if (cubin_bytes) *cubin_bytes = int64_t(cubin.size());
   return CS_OK;
 }
@@ -1174,7 +1280,7 @@ int piece_programs(const CutJob& job, const std::vector<Piece>& pieces, int dtyp
   } catch (const PlanError& pe) {
     return fail(pe.code, pe.msg);
   }
-  for (const auto& pg : *progs) program_jit(*pg, dtype);
+  for (const auto& pg : *progs) program_jit(pg, dtype);
   return CS_OK;
 }
 
@@ -1193,7 +1299,7 @@ int run_pieces(const CutJob& job, const std::vector<Piece>& pieces,
     const SegmentPlan& sp = job.prep.segs[size_t(pc.seg)];
     cudaStream_t ss = fork ? side_stream(int(i % 4)) : st;
     if (fork) cudaStreamWaitEvent(ss, fork, 0);
-    rc = run_program(*progs[i], sp.nq, pc.dst, pc.v1 - pc.v0, int64_t(1) << sp.nq, uint64_t(pc.v0), 1, dtype, ss);
+    rc = run_program(progs[i], sp.nq, pc.dst, pc.v1 - pc.v0, int64_t(1) << sp.nq, uint64_t(pc.v0), 1, dtype, ss);
     if (rc != CS_OK) break;
     if (ss != st) {
       cudaEvent_t done = nullptr;

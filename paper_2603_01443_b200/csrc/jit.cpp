@@ -20,6 +20,8 @@
 #include <mutex>
 #include <sstream>
 #include <thread>
+#include <unordered_map>
+#include <cstring>
 
 namespace cutsim {
 
@@ -90,18 +92,6 @@ DEV void cpw() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 }  // namespace
 
-JitModule::~JitModule() {
-  // a module dies when its program is evicted from the cache; launches of its
-  // kernels may still be queued on some stream, so drain the device first
-  // (eviction is rare: the cache holds 512 programs)
-  bool any = false;
-  for (cudaLibrary_t l : libs) any |= l != nullptr;
-  if (!any) return;
-  cudaDeviceSynchronize();
-  for (cudaLibrary_t l : libs)
-    if (l) cudaLibraryUnload(l);
-}
-
 int64_t jit_cost(const std::vector<RegOp>& prog, int RB) {
   const int NR = 1 << RB;
   int64_t c = 0;
@@ -120,16 +110,25 @@ int64_t jit_cost(const std::vector<RegOp>& prog, int RB) {
 }
 
 std::string jit_source(const Sweep& sw, const std::vector<RegOp>& prog, int RB, int dtype, const std::string& name,
-                       int minb, bool persistent) {
+                       int minb, bool persistent, std::vector<double>* pvals) {
   const int T = sw.tile_bits;
   const int L = sw.low_bits;
   const int NR = 1 << RB;
   const int BD = 1 << (T - RB);
   bool remap = false;
   for (const RegOp& r : prog) remap |= r.kind == ROP_REMAP;
+  // value mode (pvals == null): matrices and phases as hex-float literals;
+  // param mode: every coefficient that is not exactly 0 or +-1 is read from
+  // the kernel-parameter block P (constant bank: DFMA takes it as an operand),
+  // so the source — and the compiled module — depends only on the circuit's
+  // structure (gate positions, tile sets, masks, slots), not on its angles
+  auto val = [&](double v) -> std::string {
+    if (!pvals) return lit(v);
+    pvals->push_back(v);
+    return "P.m[" + std::to_string(pvals->size() - 1) + "]";
+  };
+  auto trivial = [](double v) { return v == 0.0 || v == 1.0 || v == -1.0; };
   std::ostringstream o;
-  o << "extern \"C\" __global__ void __launch_bounds__(" << BD << ", " << minb << ") " << name
-    << "(V* __restrict__ states, long long stride, unsigned long long vbase, int init, unsigned long long n_tiles) {\n";
   o << "  extern __shared__ __align__(16) unsigned char smraw[];\n";
   o << "  V* sm = reinterpret_cast<V*>(smraw); (void)sm;\n";
   o << "  const unsigned tid = threadIdx.x;\n";
@@ -225,14 +224,17 @@ std::string jit_source(const Sweep& sw, const std::vector<RegOp>& prog, int RB, 
     if (!cond.empty()) o << " if (" << cond << ")";
     o << " {";
     std::string m[8];
+    const int nval = op.kind == ROP_DENSE ? 8 : 2;
     if (slotted) {
       o << " const bool sb = ((variant >> " << op.slot << ") & 1ull) != 0ull;";
-      for (int q = 0; q < 8; ++q) {
-        o << " const R m" << q << " = sb ? " << lit(alt->m[q]) << " : " << lit(op.m[q]) << ";";
+      for (int q = 0; q < nval; ++q) {
+        const std::string a = val(alt->m[q]);
+        const std::string b = val(op.m[q]);
+        o << " const R m" << q << " = sb ? " << a << " : " << b << ";";
         m[q] = "m" + std::to_string(q);
       }
     } else {
-      for (int q = 0; q < 8; ++q) m[q] = lit(op.m[q]);
+      for (int q = 0; q < nval; ++q) m[q] = trivial(op.m[q]) ? lit(op.m[q]) : val(op.m[q]);
     }
     if (op.kind == ROP_DENSE) {
       for (int j = 0; j < NR; ++j) {
@@ -300,7 +302,14 @@ std::string jit_source(const Sweep& sw, const std::vector<RegOp>& prog, int RB, 
   if (persistent) o << "  }\n";
   o << "}\n";
   (void)dtype;
-  return o.str();
+  std::ostringstream head;
+  const bool params = pvals && !pvals->empty();
+  if (params) head << "struct JP_" << name << " { R m[" << pvals->size() << "]; };\n";
+  head << "extern \"C\" __global__ void __launch_bounds__(" << BD << ", " << minb << ") " << name
+       << "(V* __restrict__ states, long long stride, unsigned long long vbase, int init, unsigned long long n_tiles";
+  if (params) head << ", const JP_" << name << " P";
+  head << ") {\n";
+  return head.str() + o.str();
 }
 
 namespace {
@@ -362,7 +371,8 @@ int g_jit_persistent = 0;  // prefetching persistent kernels for streaming sweep
 int g_jit_minb = 2;  // __launch_bounds__ min blocks per SM of the streaming (many-tile) kernels
 
 bool jit_cubin(const std::vector<const Sweep*>& sweeps, const std::vector<const std::vector<RegOp>*>& progs,
-               int dtype, std::vector<char>* cubin, std::vector<std::string>* names, std::string* err) {
+               int dtype, std::vector<char>* cubin, std::vector<std::string>* names, std::string* err,
+               bool param_mode) {
   std::string code = header(dtype);
   names->clear();
   for (size_t i = 0; i < sweeps.size(); ++i) {
@@ -371,75 +381,141 @@ bool jit_cubin(const std::vector<const Sweep*>& sweeps, const std::vector<const 
       continue;
     }
     names->push_back("cs_jit_" + std::to_string(i));
+    std::vector<double> vals;
     code += jit_source(*sweeps[i], *progs[i], reg_bits_for(sweeps[i]->tile_bits), dtype, names->back(),
-                       g_jit_minb, g_jit_persistent != 0);
+                       g_jit_minb, g_jit_persistent != 0, param_mode ? &vals : nullptr);
   }
   const bool ok = compile_source(code, cubin, err);
   if (ok) dump_artifact("selftest", code, *cubin);
   return ok;
 }
 
-// One NVRTC program per launch, compiled on parallel host threads (NVRTC is
-// thread-safe), so a 12-sweep program costs about one sweep's compile time.
+// Compiled units (one NVRTC program = one kernel) keyed by their full source:
+// two launches with the same source share the module (in param mode the
+// source is the launch's structure, so circuits that differ only in their
+// angles reuse every kernel). Units stay loaded; the cache is bounded by
+// evicting the least recently used unit no program references.
+namespace {
+std::mutex g_units_mu;
+struct UnitEntry {
+  std::shared_ptr<JitUnit> unit;
+  uint64_t last_use = 0;
+};
+std::unordered_map<std::string, UnitEntry> g_units;
+uint64_t g_units_clock = 0;
+constexpr size_t kUnitCacheCap = 4096;
+std::atomic<int64_t> g_units_compiled{0}, g_units_reused{0};
+}  // namespace
+
+JitUnit::~JitUnit() {
+  if (lib) {
+    cudaDeviceSynchronize();  // queued launches of this kernel must finish first
+    cudaLibraryUnload(lib);
+  }
+}
+
+int64_t jit_units_compiled() { return g_units_compiled.load(); }
+int64_t jit_units_reused() { return g_units_reused.load(); }
+
+// One NVRTC program per distinct launch source, compiled on parallel host
+// threads (NVRTC is thread-safe), so a 12-sweep program costs about one
+// sweep's compile time; sources already in the unit cache are not compiled.
 std::shared_ptr<JitModule> jit_compile(const std::vector<const Sweep*>& sweeps,
                                        const std::vector<const std::vector<RegOp>*>& progs, int dtype,
                                        std::string* err, const std::vector<int>* minb,
-                                       const std::vector<char>* persistent) {
+                                       const std::vector<char>* persistent, bool param_mode) {
   const size_t n = sweeps.size();
-  std::vector<std::vector<char>> cubins(n);
-  std::vector<std::string> errs(n);
-  std::vector<char> ok(n, 0);
+  auto mod = std::make_shared<JitModule>();
+  mod->units.assign(n, nullptr);
+  mod->blobs.assign(n, {});
+  std::vector<std::string> codes(n);
+  std::vector<size_t> todo;
+  {
+    std::lock_guard<std::mutex> lk(g_units_mu);
+    for (size_t i = 0; i < n; ++i) {
+      if (!progs[i]) continue;
+      std::vector<double> vals;
+      codes[i] = header(dtype) + jit_source(*sweeps[i], *progs[i], reg_bits_for(sweeps[i]->tile_bits), dtype,
+                                            "cs_jit_k", minb ? (*minb)[i] : 1, persistent && (*persistent)[i],
+                                            param_mode ? &vals : nullptr);
+      if (!vals.empty()) {
+        std::vector<unsigned char>& b = mod->blobs[i];
+        if (dtype == 0) {
+          b.resize(vals.size() * sizeof(double));
+          std::memcpy(b.data(), vals.data(), b.size());
+        } else {
+          std::vector<float> f(vals.begin(), vals.end());
+          b.resize(f.size() * sizeof(float));
+          std::memcpy(b.data(), f.data(), b.size());
+        }
+      }
+      auto it = g_units.find(codes[i]);
+      if (it != g_units.end()) {
+        it->second.last_use = ++g_units_clock;
+        mod->units[i] = it->second.unit;
+        ++g_units_reused;
+      } else {
+        bool dup = false;  // the same source twice in one program: compile once
+        for (size_t j : todo) dup |= codes[j] == codes[i];
+        if (!dup) todo.push_back(i);
+      }
+    }
+  }
+  std::vector<std::vector<char>> cubins(todo.size());
+  std::vector<std::string> errs(todo.size());
+  std::vector<char> ok(todo.size(), 0);
   std::atomic<size_t> next{0};
   auto work = [&] {
-    for (size_t i = next++; i < n; i = next++) {
-      if (!progs[i]) {
-        ok[i] = 1;
-        continue;
-      }
-      const std::string code = header(dtype) + jit_source(*sweeps[i], *progs[i], reg_bits_for(sweeps[i]->tile_bits),
-                                                        dtype, "cs_jit_" + std::to_string(i),
-                                                        minb ? (*minb)[i] : 1,
-                                                        persistent && (*persistent)[i]);
-      ok[i] = compile_source(code, &cubins[i], &errs[i]) ? 1 : 0;
-      if (ok[i]) dump_artifact("cs_jit_" + std::to_string(i), code, cubins[i]);
+    for (size_t t = next++; t < todo.size(); t = next++) {
+      const size_t i = todo[t];
+      ok[t] = compile_source(codes[i], &cubins[t], &errs[t]) ? 1 : 0;
+      if (ok[t]) dump_artifact("cs_jit_" + std::to_string(i), codes[i], cubins[t]);
     }
   };
-  const size_t nt = std::max<size_t>(1, std::min<size_t>(n, std::max(1u, std::thread::hardware_concurrency())));
+  const size_t nt =
+      std::max<size_t>(1, std::min<size_t>(todo.size(), std::max(1u, std::thread::hardware_concurrency())));
   std::vector<std::thread> pool;
   for (size_t t = 1; t < nt; ++t) pool.emplace_back(work);
   work();
   for (auto& th : pool) th.join();
-  for (size_t i = 0; i < n; ++i)
-    if (!ok[i]) {
-      *err = errs[i];
+  for (size_t t = 0; t < todo.size(); ++t) {
+    if (!ok[t]) {
+      *err = errs[t];
       return nullptr;
     }
-  auto mod = std::make_shared<JitModule>();
-  mod->libs.assign(n, nullptr);
-  mod->kernels.resize(n);
-  for (size_t i = 0; i < n; ++i) {
-    if (!progs[i]) continue;
-    cudaError_t e = cudaLibraryLoadData(&mod->libs[i], cubins[i].data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
+    const size_t i = todo[t];
+    auto u = std::make_shared<JitUnit>();
+    cudaError_t e = cudaLibraryLoadData(&u->lib, cubins[t].data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
     if (e != cudaSuccess) {
-      mod->libs[i] = nullptr;
+      u->lib = nullptr;
       *err = std::string("cudaLibraryLoadData: ") + cudaGetErrorString(e);
       return nullptr;
     }
-    JitKernel& k = mod->kernels[i];
-    const std::string name = "cs_jit_" + std::to_string(i);
-    e = cudaLibraryGetKernel(&k.kernel, mod->libs[i], name.c_str());
+    e = cudaLibraryGetKernel(&u->kernel, u->lib, "cs_jit_k");
     if (e != cudaSuccess) {
       *err = std::string("cudaLibraryGetKernel: ") + cudaGetErrorString(e);
       return nullptr;
     }
     const int T = sweeps[i]->tile_bits;
     const int RB = reg_bits_for(T);
-    k.threads = 1 << (T - RB);
+    u->threads = 1 << (T - RB);
     bool remap = false;
     for (const RegOp& r : *progs[i]) remap |= r.kind == ROP_REMAP;
-    k.persistent = persistent && (*persistent)[i];
+    u->persistent = persistent && (*persistent)[i];
     const size_t tile_bytes = (size_t(1) << T) * (dtype == 0 ? 16 : 8);
-    k.smem = (remap ? tile_bytes : 0) + (k.persistent ? tile_bytes : 0);
+    u->smem = (remap ? tile_bytes : 0) + (u->persistent ? tile_bytes : 0);
+    ++g_units_compiled;
+    std::lock_guard<std::mutex> lk(g_units_mu);
+    if (g_units.size() >= kUnitCacheCap) {
+      auto lru = g_units.end();
+      for (auto it = g_units.begin(); it != g_units.end(); ++it)
+        if (it->second.unit.use_count() == 1 && (lru == g_units.end() || it->second.last_use < lru->second.last_use))
+          lru = it;
+      if (lru != g_units.end()) g_units.erase(lru);
+    }
+    g_units[codes[i]] = UnitEntry{u, ++g_units_clock};
+    for (size_t j = 0; j < n; ++j)
+      if (progs[j] && !mod->units[j] && codes[j] == codes[i]) mod->units[j] = u;
   }
   return mod;
 }

@@ -12,25 +12,32 @@
 
 namespace cutsim {
 
-// One compiled launch: the kernel handle and its dynamic shared memory.
-struct JitKernel {
+// One compiled launch kernel (one NVRTC program): shared by every launch
+// whose generated source is identical (jit.cpp's unit cache).
+struct JitUnit {
+  cudaLibrary_t lib = nullptr;
   cudaKernel_t kernel = nullptr;
   size_t smem = 0;
   int threads = 0;
   bool persistent = false;  // one CTA per SM walking the tiles, next tile prefetched
+  ~JitUnit();
 };
 
+// A program's specialised launches: unit i (null = interpreter) and, in param
+// mode, the kernel-parameter block of launch i (its matrices and phases).
 struct JitModule {
-  std::vector<cudaLibrary_t> libs;  // one library per compiled launch
-  std::vector<JitKernel> kernels;  // one per launch, same order as the program's launches
-  ~JitModule();
+  std::vector<std::shared_ptr<JitUnit>> units;
+  std::vector<std::vector<unsigned char>> blobs;
 };
 
 // CUDA C++ source of one launch: straight-line code for the register program
 // (dense/phase/remap) with the tile geometry, masks, matrices (hex-float
 // literals) and remap index maps baked in.
+// pvals != null: param mode (coefficients other than 0 / +-1 go to the
+// kernel-parameter block, appended to *pvals in order)
 std::string jit_source(const Sweep& sw, const std::vector<RegOp>& prog, int reg_bits, int dtype,
-                       const std::string& name, int minb = 1, bool persistent = false);
+                       const std::string& name, int minb = 1, bool persistent = false,
+                       std::vector<double>* pvals = nullptr);
 
 // Compile every launch of a program into one module (sm_100a CUBIN via
 // NVRTC, loaded with cudaLibraryLoadData). Returns null and sets *err on
@@ -40,11 +47,17 @@ std::string jit_source(const Sweep& sw, const std::vector<RegOp>& prog, int reg_
 std::shared_ptr<JitModule> jit_compile(const std::vector<const Sweep*>& sweeps,
                                        const std::vector<const std::vector<RegOp>*>& progs, int dtype,
                                        std::string* err, const std::vector<int>* minb = nullptr,
-                                       const std::vector<char>* persistent = nullptr);
+                                       const std::vector<char>* persistent = nullptr, bool param_mode = false);
+
+// units compiled / served from the unit cache since load (cs_get_option
+// "jit_units_compiled" / "jit_units_reused")
+int64_t jit_units_compiled();
+int64_t jit_units_reused();
 
 // NVRTC step only (no device needed): the CUBIN and kernel names.
 bool jit_cubin(const std::vector<const Sweep*>& sweeps, const std::vector<const std::vector<RegOp>*>& progs,
-               int dtype, std::vector<char>* cubin, std::vector<std::string>* names, std::string* err);
+               int dtype, std::vector<char>* cubin, std::vector<std::string>* names, std::string* err,
+               bool param_mode = false);
 
 // min CTAs per SM requested from the generated kernels that stream many
 // tiles (option "jit_minb", default 2: <= 128 registers, two 256-thread CTAs

@@ -44,7 +44,32 @@
 namespace cutsim {
 namespace {
 
-constexpr int kSlices = 8;
+// Digit base 2^kDigitBits: 8 -> 7 balanced base-256 digits (|d| <= 128,
+// top digit <= 65), 7 int32 diagonals per output; 7 -> 8 base-128 digits, 8
+// diagonals. The epilogue reads every diagonal of every output from TMEM
+// (64 B/cycle per SM, the K <= 32 bound: DESIGN.md §3), so 7 diagonals cut
+// both that read stream and the digit-pair MMAs (28 instead of 36) by 1/8
+// and 2/9 at the same 2^-55 truncation level.
+// Option "merge_ozaki_digits" selects DB (8 default). Truncation measured in
+// a host emulation: max |error| / (max|a| max|b|) = 2.2e-15 (DB = 8) and
+// 5.6e-16 (DB = 7) over K = 16 terms.
+template <int DB>
+struct Digits {
+  static constexpr int S = DB == 8 ? 7 : 8;  // slices
+  // fixed-point bits of a row (|Y| < 2^Fix), chosen so the top digit fits int8
+  static constexpr int Fix = DB == 8 ? 54 : 55;
+  // sa[l] = 2^(e_l + SaShift): the epilogue's combined diagonals Q0 + 2^-Q1Shift
+  // Q1 times sa * sb is the product (base 256: Q0 = D_0..D_3 with D_3 at
+  // weight 1 = 2^72 of the 2^-110 fixed point -> 2^-38; base 128: 2^-35)
+  static constexpr int SaShift = DB == 8 ? -38 : -35;
+  static constexpr int Q1Shift = DB == 8 ? 24 : 28;
+};
+#define OZ_DIGIT_CONSTS                          \
+  constexpr int kDigitBits = DB;                 \
+  constexpr int kSlices = Digits<DB>::S;         \
+  constexpr int kFix = Digits<DB>::Fix;          \
+  constexpr int kSaShift = Digits<DB>::SaShift;  \
+  (void)kDigitBits; (void)kSlices; (void)kFix; (void)kSaShift;
 constexpr int kHB = 16;                      // h rows per tile (32 real B rows per slice)
 constexpr int kLT = 128;                     // l rows per tile (MMA M)
 constexpr int kEpiWarps = 16;                // two groups of 8 (alternate tiles)
@@ -123,24 +148,29 @@ __device__ __forceinline__ int row_exponent(double mx) {
   return b ? b - 1021 : 0;  // mx in [2^(b-1023), 2^(b-1022))
 }
 
-// 2^(56 - e): the fixed-point scale of a row (clamped for rows below ~1e-290,
-// whose digits then keep fewer bits)
+// 2^(kFix + 1 - e): the fixed-point scale of a row (|y| < 1/2 -> |Y| <
+// 2^kFix; clamped for rows below ~1e-290, whose digits then keep fewer bits)
+template <int DB>
 __device__ __forceinline__ double digit_scale(int e) {
-  const int b = min(max(56 - e + 1023, 1), 2046);
+  OZ_DIGIT_CONSTS
+  const int b = min(max(kFix + 1 - e + 1023, 1), 2046);
   return __hiloint2double(b << 20, 0);
 }
 
-// 8 balanced base-128 digits of y = x 2^-e (|y| <= 1/2): Y = rint(y 2^56)
-// (|Y| <= 2^55: the 2^-57 rounding is the scheme's truncation level), then
-// d_7..d_1 = ((Y + 64) & 127) - 64 in [-64, 63] from the least significant
-// end and d_0 = what remains (|d_0| <= 65); y ~ sum_i d_i 128^-(i+1).
-__device__ __forceinline__ void digits8(double x, double scale, int (&d)[kSlices]) {
+// kSlices balanced base-2^kDigitBits digits of y = x 2^-e (|y| < 1/2):
+// Y = rint(y 2^(kFix+1)) (the rounding is the scheme's truncation level),
+// then d_{S-1}..d_1 = ((Y + B/2) & (B-1)) - B/2 from the least significant
+// end and d_0 = what remains (|d_0| <= 65); y ~ sum_i d_i B^-(i+1) 2^(...).
+template <int DB>
+__device__ __forceinline__ void digits_split(double x, double scale, int (&d)[Digits<DB>::S]) {
+  OZ_DIGIT_CONSTS
+  constexpr long long B = 1ll << kDigitBits;
   long long Y = __double2ll_rn(x * scale);
 #pragma unroll
   for (int i = kSlices - 1; i > 0; --i) {
-    const int di = int((Y + 64) & 127) - 64;
+    const int di = int((Y + B / 2) & (B - 1)) - int(B / 2);
     d[i] = di;
-    Y = (Y - di) >> 7;
+    Y = (Y - di) >> kDigitBits;
   }
   d[0] = int(Y);
 }
@@ -165,10 +195,11 @@ struct OzPrep {
 
 // ---------------------------------------------------------------------------
 // digit preparation: A (the lo side), one thread per (l, k-step)
-// adig layout: [l_tile][ks][slice][4096 B canonical block]; sa[l] = 2^(e_l - 35)
+// adig layout: [l_tile][ks][slice][4096 B canonical block]; sa[l] = 2^(e_l + kSaShift)
 // ---------------------------------------------------------------------------
-template <int KS>
+template <int KS, int DB>
 __global__ void ozaki_prep_lo(const __grid_constant__ OzPrep p, int8_t* adig, double* sa) {
+  OZ_DIGIT_CONSTS
   const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (idx >= p.lo_len * KS) return;
   const int ks = int(idx / p.lo_len);
@@ -185,8 +216,8 @@ __global__ void ozaki_prep_lo(const __grid_constant__ OzPrep p, int8_t* adig, do
   const int e = row_exponent(finite ? mx : 0.0);
   // a NaN/Inf operand makes the whole output column NaN (as the FP64 kernels
   // propagate it) instead of saturated digits turning it into a finite value
-  if (ks == 0) sa[l] = finite ? ldexp(1.0, e - 35) : __longlong_as_double(0x7ff8000000000000ll);
-  const double sc = digit_scale(e);
+  if (ks == 0) sa[l] = finite ? ldexp(1.0, e + kSaShift) : __longlong_as_double(0x7ff8000000000000ll);
+  const double sc = digit_scale<DB>(e);
   uint32_t w[kSlices][8];
 #pragma unroll
   for (int tt = 0; tt < 16; ++tt) {
@@ -194,8 +225,8 @@ __global__ void ozaki_prep_lo(const __grid_constant__ OzPrep p, int8_t* adig, do
     double2 v = make_double2(0.0, 0.0);
     if (t < K) v = __ldg(lo + int64_t(p.lidx[t]) * p.lo_len + l);
     int dr[kSlices], di[kSlices];
-    digits8(v.x, sc, dr);
-    digits8(v.y, sc, di);
+    digits_split<DB>(v.x, sc, dr);
+    digits_split<DB>(v.y, sc, di);
 #pragma unroll
     for (int i = 0; i < kSlices; ++i) {
       // bytes 2tt, 2tt + 1 of the row's 32-byte k-step: (re, im)
@@ -218,8 +249,9 @@ __global__ void ozaki_prep_lo(const __grid_constant__ OzPrep p, int8_t* adig, do
 // (h, k-step); bdig layout: [h_block][ks][slice][1024 B canonical block],
 // row r = 2 (h % 16) + v; sb[h] = 2^e_h
 // ---------------------------------------------------------------------------
-template <int KS>
+template <int KS, int DB>
 __global__ void ozaki_prep_hi(const __grid_constant__ OzPrep p, int64_t nrows, int8_t* bdig, double* sb) {
+  OZ_DIGIT_CONSTS
   const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (idx >= nrows * KS) return;
   const int ks = int(idx / nrows);
@@ -238,7 +270,7 @@ __global__ void ozaki_prep_hi(const __grid_constant__ OzPrep p, int64_t nrows, i
   }
   const int e = row_exponent(finite ? mx : 0.0);
   if (ks == 0) sb[hr] = finite ? ldexp(1.0, e) : __longlong_as_double(0x7ff8000000000000ll);
-  const double sc = digit_scale(e);
+  const double sc = digit_scale<DB>(e);
   uint32_t w0[kSlices][8], w1[kSlices][8];
 #pragma unroll
   for (int tt = 0; tt < 16; ++tt) {
@@ -251,8 +283,8 @@ __global__ void ozaki_prep_hi(const __grid_constant__ OzPrep p, int64_t nrows, i
       bi = v.x * ci + v.y * cr;
     }
     int dr[kSlices], di[kSlices];
-    digits8(br, sc, dr);
-    digits8(bi, sc, di);
+    digits_split<DB>(br, sc, dr);
+    digits_split<DB>(bi, sc, di);
 #pragma unroll
     for (int i = 0; i < kSlices; ++i) {
       // row (h, 0): (Hr, -Hi) -> real part; row (h, 1): (Hi, Hr) -> imaginary part
@@ -284,7 +316,7 @@ __global__ void ozaki_prep_hi(const __grid_constant__ OzPrep p, int64_t nrows, i
 struct OzParams {
   const int8_t* adig;
   const int8_t* bdig;
-  const double* sa;  // per l: 2^(e_l - 35)
+  const double* sa;  // per l: 2^(e_l + kSaShift)
   const double* sb;  // per h: 2^e_h
   double2* out;  // row 0 of the range
   int64_t W;     // lo_len
@@ -328,8 +360,9 @@ struct TileWalk {
 template <bool UNIT>
 constexpr int oz_threads() { return 64 + 32 * (UNIT ? kEpiWarps / 2 : kEpiWarps); }
 
-template <int KS, int NST, bool ACC, bool UNIT>
+template <int KS, int NST, bool ACC, bool UNIT, int DB>
 __global__ void __launch_bounds__(oz_threads<UNIT>(), UNIT ? 2 : 1) ozaki_merge_kernel(const __grid_constant__ OzParams p) {
+  OZ_DIGIT_CONSTS
   constexpr int NBUF = UNIT ? 1 : 2;  // TMEM accumulators (= epilogue groups)
   constexpr uint32_t TCOLS = 256 * NBUF;
   constexpr uint32_t A_BYTES = KS * kSlices * kABlock;
@@ -443,15 +476,14 @@ __global__ void __launch_bounds__(oz_threads<UNIT>(), UNIT ? 2 : 1) ozaki_merge_
       if ((it % NBUF) != g) continue;
       const int64_t lt = w.lt, hb = w.hb;
       const int64_t l = lt * kLT + q * 32 + lane;
-      const double sl = __ldg(p.sa + l);  // 2^(e_l - 35)
-      // accumulate (K > 64 in 64-term chunks): fetch the 8 outputs being
-      // added to before waiting for the accumulator, so the reads overlap
-      // the MMA chain instead of the epilogue
-      double2 prev[8];
+      const double sl = __ldg(p.sa + l);  // 2^(e_l + kSaShift)
+      // accumulate (K > 64 in 64-term chunks): prefetch the 8 outputs being
+      // added to into L2 before waiting for the accumulator, so their DRAM
+      // reads overlap the MMA chain (held in registers instead, they spilled)
       if (ACC) {
         const double2* src = p.out + (hb * kHB + hl_base) * p.W + l;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) prev[j] = __ldcs(src + j * p.W);
+        for (int j = 0; j < 8; ++j) asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(src + j * p.W));
       }
       mbar_wait(tfull + g, n & 1);
       ++n;
@@ -480,24 +512,38 @@ __global__ void __launch_bounds__(oz_threads<UNIT>(), UNIT ? 2 : 1) ozaki_merge_
 #pragma unroll
           for (int v = 0; v < 2; ++v) {
             const int c = 2 * j + v;
-            // P_m = 128 D_2m + D_2m+1 (|D_p| < 2^23: exact in int32), then
-            // Q0 = 2^14 P_0 + P_1, Q1 = 2^14 P_2 + P_3 (|Q| < 2^45: exact in
-            // int64 and in a double), converted with the 1.5 * 2^52 bias:
-            //   sum_p 2^-7(p+2) D_p = 2^-35 (Q0 + 2^-28 Q1)
-            const int p0 = int(d[hc][0][c]) * 128 + int(d[hc][1][c]);
-            const int p1 = int(d[hc][2][c]) * 128 + int(d[hc][3][c]);
-            const int p2 = int(d[hc][4][c]) * 128 + int(d[hc][5][c]);
-            const int p3 = int(d[hc][6][c]) * 128 + int(d[hc][7][c]);
-            const long long q0 = (static_cast<long long>(p0) << 14) + p1;
-            const long long q1 = (static_cast<long long>(p2) << 14) + p3;
+            long long q0, q1;
+            if constexpr (kDigitBits == 8) {
+              // base 256, 7 diagonals (|D_p| < 2^24): Q0 = D_0 2^24 + D_1 2^16
+              // + D_2 2^8 + D_3, Q1 = D_4 2^16 + D_5 2^8 + D_6 (|Q0| < 2^49,
+              // |Q1| < 2^41: exact in int64 and in a double); product =
+              // 2^-38 (Q0 + 2^-24 Q1) sa sb
+              const long long a0 = (static_cast<long long>(int(d[hc][0][c])) << 8) + int(d[hc][1][c]);
+              const long long a1 = (static_cast<long long>(int(d[hc][2][c])) << 8) + int(d[hc][3][c]);
+              const long long a2 = (static_cast<long long>(int(d[hc][4][c])) << 8) + int(d[hc][5][c]);
+              q0 = (a0 << 16) + a1;
+              q1 = (a2 << 8) + int(d[hc][6][c]);
+            } else {
+              // base 128, 8 diagonals: P_m = 128 D_2m + D_2m+1 (|D_p| < 2^23:
+              // exact in int32), Q0 = 2^14 P_0 + P_1, Q1 = 2^14 P_2 + P_3;
+              // sum_p 2^-7(p+2) D_p = 2^-35 (Q0 + 2^-28 Q1)
+              const int p0 = int(d[hc][0][c]) * 128 + int(d[hc][1][c]);
+              const int p1 = int(d[hc][2][c]) * 128 + int(d[hc][3][c]);
+              const int p2 = int(d[hc][4][c]) * 128 + int(d[hc][5][c]);
+              const int p3 = int(d[hc][kSlices - 2][c]) * 128 + int(d[hc][kSlices - 1][c]);
+              q0 = (static_cast<long long>(p0) << 14) + p1;
+              q1 = (static_cast<long long>(p2) << 14) + p3;
+            }
+            // int64 -> double with the 1.5 * 2^52 bias (|q| < 2^51)
             const double f0 = __longlong_as_double(q0 + 0x4338000000000000LL) - 0x1.8p52;
             const double f1 = __longlong_as_double(q1 + 0x4338000000000000LL) - 0x1.8p52;
-            v2[v] = fma(f1, 0x1p-28, f0) * s;
+            v2[v] = fma(f1, kDigitBits == 8 ? 0x1p-24 : 0x1p-28, f0) * s;
           }
           double2 val = make_double2(v2[0], v2[1]);
           if (ACC) {
-            val.x += prev[4 * hc + j].x;
-            val.y += prev[4 * hc + j].y;
+            const double2 prev = __ldcs(dst);
+            val.x += prev.x;
+            val.y += prev.y;
           }
           __stcs(dst, val);  // evict-first: the state is written once
         }
@@ -510,8 +556,9 @@ __global__ void __launch_bounds__(oz_threads<UNIT>(), UNIT ? 2 : 1) ozaki_merge_
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TCOLS));
 }
 
-template <int KS, int NST>
+template <int KS, int NST, int DB>
 constexpr size_t oz_smem() {
+  constexpr int kSlices = Digits<DB>::S;
   return size_t(KS) * kSlices * kABlock + size_t(NST) * KS * kSlices * kBBlock + 256;
 }
 
@@ -526,11 +573,12 @@ std::map<std::pair<int, cudaStream_t>, Workspace> g_oz_ws;
 std::mutex g_oz_mu;
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is per device: one bit
 // per (device, instantiation)
-std::atomic<uint64_t> g_oz_configured[8];
+std::atomic<uint64_t> g_oz_configured[16];
 
-template <int KS, int NST, bool UNIT>
+template <int KS, int NST, bool UNIT, int DB>
 cudaError_t run_ozaki(const MergeParams& mp, int64_t nrows, void* out, int accumulate, int sms,
                       cudaStream_t stream) {
+  constexpr int kSlices = Digits<DB>::S;
   const int64_t W = mp.lo_len;
   const size_t a_bytes = size_t(W / kLT) * KS * kSlices * kABlock;
   const size_t b_bytes = size_t(nrows / kHB) * KS * kSlices * kBBlock;
@@ -570,8 +618,8 @@ cudaError_t run_ozaki(const MergeParams& mp, int64_t nrows, void* out, int accum
     pp.lidx[t] = mp.lidx[t];
     pp.coef[t] = make_double2(mp.coef[2 * t], mp.coef[2 * t + 1]);
   }
-  ozaki_prep_lo<KS><<<unsigned((W * KS + 127) / 128), 128, 0, stream>>>(pp, adig, sa);
-  ozaki_prep_hi<KS><<<unsigned((nrows * KS + 127) / 128), 128, 0, stream>>>(pp, nrows, bdig, sb);
+  ozaki_prep_lo<KS, DB><<<unsigned((W * KS + 127) / 128), 128, 0, stream>>>(pp, adig, sa);
+  ozaki_prep_hi<KS, DB><<<unsigned((nrows * KS + 127) / 128), 128, 0, stream>>>(pp, nrows, bdig, sb);
   OzParams op;
   op.adig = adig;
   op.bdig = bdig;
@@ -600,14 +648,14 @@ cudaError_t run_ozaki(const MergeParams& mp, int64_t nrows, void* out, int accum
   // persistent: at least ~116 KB of shared memory so that exactly one CTA
   // (and one 512-column TMEM allocation) lives on each SM; unit CTAs: two
   // per SM (256 TMEM columns each)
-  const size_t smem = UNIT ? oz_smem<KS, NST>() : std::max<size_t>(oz_smem<KS, NST>(), 116 * 1024);
-  constexpr int inst = (KS == 1 ? 0 : KS == 2 ? 1 : 2) * 2 + (UNIT ? 1 : 0);
+  const size_t smem = UNIT ? oz_smem<KS, NST, DB>() : std::max<size_t>(oz_smem<KS, NST, DB>(), 116 * 1024);
+  constexpr int inst = ((KS == 1 ? 0 : KS == 2 ? 1 : 2) * 2 + (UNIT ? 1 : 0)) * 2 + (DB == 8 ? 1 : 0);
   const uint64_t bit = uint64_t(1) << (dev & 63);
   if (!(g_oz_configured[inst].load() & bit)) {
-    cudaError_t e = cudaFuncSetAttribute(ozaki_merge_kernel<KS, NST, false, UNIT>,
+    cudaError_t e = cudaFuncSetAttribute(ozaki_merge_kernel<KS, NST, false, UNIT, DB>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(ozaki_merge_kernel<KS, NST, true, UNIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      e = cudaFuncSetAttribute(ozaki_merge_kernel<KS, NST, true, UNIT, DB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                int(smem));
     if (e != cudaSuccess) return e;
     g_oz_configured[inst].fetch_or(bit);
@@ -615,8 +663,8 @@ cudaError_t run_ozaki(const MergeParams& mp, int64_t nrows, void* out, int accum
   const int64_t grid = UNIT ? op.n_units : std::min<int64_t>(sms, op.n_units);
   if (grid > 0x7fffffff) return cudaErrorInvalidValue;
   constexpr int threads = oz_threads<UNIT>();
-  if (accumulate) ozaki_merge_kernel<KS, NST, true, UNIT><<<unsigned(grid), threads, smem, stream>>>(op);
-  else ozaki_merge_kernel<KS, NST, false, UNIT><<<unsigned(grid), threads, smem, stream>>>(op);
+  if (accumulate) ozaki_merge_kernel<KS, NST, true, UNIT, DB><<<unsigned(grid), threads, smem, stream>>>(op);
+  else ozaki_merge_kernel<KS, NST, false, UNIT, DB><<<unsigned(grid), threads, smem, stream>>>(op);
   return cudaGetLastError();
 }
 
@@ -634,16 +682,30 @@ bool merge_ozaki_supported(int K, int64_t lo_len, int64_t nrows) {
 // unit: short-lived CTAs (two per SM) for K <= 32; K = 64 (128 KB of A
 // digits per CTA) always runs persistent
 cudaError_t launch_merge_ozaki(const MergeParams& mp, int64_t nrows, void* out, int accumulate, int sms, bool unit,
-                               cudaStream_t stream) {
+                               cudaStream_t stream, int digit_bits) {
+  if (digit_bits == 7) {
+    switch (mp.K) {
+      case 8:
+      case 16:
+        return unit ? run_ozaki<1, 4, true, 7>(mp, nrows, out, accumulate, sms, stream)
+                    : run_ozaki<1, 6, false, 7>(mp, nrows, out, accumulate, sms, stream);
+      case 32:
+        return unit ? run_ozaki<2, 2, true, 7>(mp, nrows, out, accumulate, sms, stream)
+                    : run_ozaki<2, 4, false, 7>(mp, nrows, out, accumulate, sms, stream);
+      case 64: return run_ozaki<4, 2, false, 7>(mp, nrows, out, accumulate, sms, stream);
+      default: return cudaErrorInvalidValue;
+    }
+  }
+  // base 256 (7 slices: 7/8 of the A/B digit bytes): K = 64 fits a third B stage
   switch (mp.K) {
     case 8:
     case 16:
-      return unit ? run_ozaki<1, 4, true>(mp, nrows, out, accumulate, sms, stream)
-                  : run_ozaki<1, 6, false>(mp, nrows, out, accumulate, sms, stream);
+      return unit ? run_ozaki<1, 4, true, 8>(mp, nrows, out, accumulate, sms, stream)
+                  : run_ozaki<1, 6, false, 8>(mp, nrows, out, accumulate, sms, stream);
     case 32:
-      return unit ? run_ozaki<2, 2, true>(mp, nrows, out, accumulate, sms, stream)
-                  : run_ozaki<2, 4, false>(mp, nrows, out, accumulate, sms, stream);
-    case 64: return run_ozaki<4, 2, false>(mp, nrows, out, accumulate, sms, stream);
+      return unit ? run_ozaki<2, 2, true, 8>(mp, nrows, out, accumulate, sms, stream)
+                  : run_ozaki<2, 4, false, 8>(mp, nrows, out, accumulate, sms, stream);
+    case 64: return run_ozaki<4, 3, false, 8>(mp, nrows, out, accumulate, sms, stream);
     default: return cudaErrorInvalidValue;
   }
 }

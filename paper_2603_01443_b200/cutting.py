@@ -215,9 +215,9 @@ class _VariantCircuits:
         if not 0 <= b < len(self):
             raise IndexError(b)
         if b not in self._cache:
-            self._cache[b] = Circuit.from_table(
-                self._fam.num_qubits, self._fam.variant_table(b), validate=False
-            )
+            c = Circuit.from_table(self._fam.num_qubits, self._fam.variant_table(b), validate=False)
+            c._origin = (self._fam, b)  # engine.simulate batches the family's variants
+            self._cache[b] = c
         return self._cache[b]
 
     def __iter__(self):
@@ -244,6 +244,29 @@ class SegmentFamily:
 
     def __post_init__(self):
         self.circuits = _VariantCircuits(self)
+        self._pending = {}  # dtype -> (device batch, variants not yet handed out)
+
+    def claim_state(self, b: int, dtype, simulate_batch):
+        """Variant b's state from one batched simulation of the whole family.
+
+        The reference's call sequence simulates the variant circuits one by
+        one (harness.py:136-139, `[[simulate(c) for c in fam.circuits] ...]`).
+        The first request of a pass runs every variant in ONE batched launch
+        sequence (`simulate_batch`) and each variant's state is handed out
+        once, as a row of that batch (so merge() reads the batch in place);
+        asking for a variant again starts a new pass — every call returns a
+        fresh state, as the reference's simulate() does."""
+        key = np.dtype(dtype).str
+        batch, left = self._pending.get(key, (None, None))
+        if batch is None or b not in left:
+            batch = simulate_batch()
+            left = set(range(self.num_variants))
+        left.discard(b)
+        if left:
+            self._pending[key] = (batch, left)
+        else:
+            self._pending.pop(key, None)
+        return batch[b]
 
     @property
     def num_cuts(self) -> int:

@@ -198,8 +198,18 @@ def simulate_table(nq: int, table: GateTable, *, n_states: int = 1, slots=None,
 
 def simulate(circuit: Circuit, *, max_qubits: int = DEFAULT_MAX_QUBITS, deadline: float | None = None,
              dtype=np.complex128) -> StateVec:
-    """Apply every gate in order to |0...0> on the GPU and return the state."""
+    """Apply every gate in order to |0...0> on the GPU and return the state.
+
+    A variant circuit of decompose() (reference cutting.py:237-247) is served
+    from one batched simulation of its whole segment family
+    (SegmentFamily.claim_state): the reference's per-variant loop costs one
+    launch sequence per family instead of one per variant."""
     check_capacity(circuit.num_qubits, max_qubits)
+    origin = getattr(circuit, "_origin", None)
+    if origin is not None and deadline is None:
+        fam, b = origin
+        row = fam.claim_state(b, dtype, lambda: simulate_family(fam, dtype=dtype, max_qubits=max_qubits))
+        return StateVec(circuit.num_qubits, device=row)
     states = simulate_table(circuit.num_qubits, circuit.table, deadline=deadline, dtype=dtype)
     return StateVec(circuit.num_qubits, device=states[0])
 

@@ -186,3 +186,32 @@ def test_many_segments_and_interior_cuts(cb, q, d, n, c, seed):
     lo, hi = unit, min(1 << q, 3 * unit)
     shard = cb.run_cut(circ, n, out_range=(lo, hi))
     assert np.array_equal(shard.amps, full[lo:hi])
+
+
+def test_reference_variant_loop_runs_one_batch_per_family(cb):
+    """The reference's loop `[[simulate(c) for c in fam.circuits] ...]`
+    (harness.py:136-139) costs one batched launch sequence per segment
+    family; each call still returns a fresh, independent state equal to the
+    variant circuit simulated on its own, and merge() reads the batch in
+    place."""
+    from paper_2603_01443_b200 import _native
+    from paper_2603_01443_b200.circuits import h
+
+    circ = cb.build_brickwall(cb.BrickwallSpec(14, 5, 2, 4, 3))
+    subs = cb.decompose(circ, cb.plan_cut(circ, 2))
+    fam = subs.segments[0]
+    n0 = _native.launch_count()
+    first = cb.simulate(fam.circuits[0])
+    per_batch = _native.launch_count() - n0
+    states = [[first] + [cb.simulate(c) for c in fam.circuits[1:]]]
+    assert _native.launch_count() - n0 == per_batch  # the other variants came from the same batch
+    states.append([cb.simulate(c) for c in subs.segments[1].circuits])
+    for f, sts in zip(subs.segments, states):
+        for b, sv in enumerate(sts):
+            alone = cb.simulate(cb.Circuit.from_table(f.num_qubits, f.variant_table(b)))
+            assert np.array_equal(sv.amps, alone.amps)
+    merged = cb.merge(cb.merge_input_from(subs, states)).amps
+    assert np.abs(merged - ref_state(circ)).max() < TOL
+    again = cb.simulate(fam.circuits[1])  # a second request: a new pass, a fresh state
+    cb.apply_gate(again, h(0))
+    assert np.array_equal(states[0][1].amps, cb.simulate(fam.circuits[1]).amps)

@@ -20,6 +20,24 @@ def test_nvrtc_compiles_generated_kernels_on_cpu():
     assert _native.jit_selftest(14, stair.table, n_states=1) > 1000
 
 
+@pytest.mark.parametrize("dtype", [_native.CS_C128, _native.CS_C64])
+def test_nvrtc_compiles_param_mode_kernels_on_cpu(dtype):
+    """Param mode (jit_struct): the coefficients become kernel parameters;
+    the generated sources still compile to sm_100a CUBINs."""
+    old = (_native.get_option("jit"), _native.get_option("jit_struct"))
+    _native.set_option("jit", 2)
+    _native.set_option("jit_struct", 2)
+    try:
+        circ = G.build_brickwall(G.BrickwallSpec(14, 3, 2, 2, 0))
+        fam = preprocess(circ, 2).subs.segments[1]
+        assert _native.jit_selftest(fam.num_qubits, fam.template, fam.slots, n_states=fam.num_variants,
+                                    dtype=dtype) > 1000
+        assert _native.jit_selftest(14, circ.table, n_states=1, dtype=dtype) > 1000
+    finally:
+        _native.set_option("jit", old[0])
+        _native.set_option("jit_struct", old[1])
+
+
 @pytest.fixture
 def jit_on():
     import torch
@@ -136,3 +154,82 @@ def test_jit_apply_circuit_on_arbitrary_state(jit_on):
         ref = amps.copy()
         orc.run_gates(ref, circ.kinds, circ.qa, circ.qb, circ.params)
         assert np.abs(sv.amps - ref).max() < 1e-10
+
+
+def _angles_perturbed(circ, seed):
+    """The same gate structure with new U3 angles."""
+    rng = np.random.default_rng(seed)
+    p = circ.params.copy()
+    u3 = circ.kinds == C.KIND_U3
+    p[u3] = rng.uniform(0, np.pi, size=(int(u3.sum()), 3))
+    return C.Circuit.from_table(circ.num_qubits, C.GateTable(circ.kinds, circ.qa, circ.qb, p))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype,tol", [(np.complex128, 1e-10), (np.complex64, 1e-5)])
+def test_param_mode_kernels_match_oracle(jit_on, dtype, tol):
+    """jit_struct = 2: every program (uncut multi-sweep and variant batches)
+    on structure-keyed kernels with the coefficients as kernel parameters."""
+    import paper_2603_01443_b200 as cb
+
+    old = _native.get_option("jit_struct")
+    _native.set_option("jit_struct", 2)
+    try:
+        for spec in (cb.BrickwallSpec(16, 5, 2, 3, 4), cb.BrickwallSpec(12, 4, 3, 4, 5)):
+            circ = cb.build_brickwall(spec)
+            ref = orc.simulate(spec.q, circ.kinds, circ.qa, circ.qb, circ.params)
+            assert np.abs(cb.simulate(circ, dtype=dtype).amps - ref).max() < tol
+            assert np.abs(cb.run_cut(circ, spec.n, dtype=dtype).amps - ref).max() < tol
+        stair = cb.build_staircase(cb.BenchmarkSpec(q=12, n=2, blocks=2))
+        ref = orc.simulate(12, stair.kinds, stair.qa, stair.qb)
+        assert np.abs(cb.simulate(stair, dtype=dtype).amps - ref).max() < tol
+    finally:
+        _native.set_option("jit_struct", old)
+
+
+@pytest.mark.gpu
+def test_structure_keyed_modules_are_reused_across_angles(jit_on):
+    """A circuit with the same structure but new angles compiles no new
+    kernel for its variant batches (param mode) and is still exact."""
+    import paper_2603_01443_b200 as cb
+
+    base = cb.build_brickwall(cb.BrickwallSpec(20, 6, 2, 2, 9))
+    cb.run_cut(base, 2)
+    for seed in (1, 2):
+        circ = _angles_perturbed(base, seed)
+        n0 = _native.get_option("jit_units_compiled")
+        r0 = _native.get_option("jit_units_reused")
+        got = cb.run_cut(circ, 2).amps
+        assert _native.get_option("jit_units_compiled") == n0
+        assert _native.get_option("jit_units_reused") > r0
+        ref = orc.simulate(20, circ.kinds, circ.qa, circ.qb, circ.params)
+        assert np.abs(got - ref).max() < 1e-10
+
+
+@pytest.mark.gpu
+def test_tiered_jit_runs_interpreter_then_compiled_kernels():
+    """jit = 3: the first call of a new program runs the interpreter kernel
+    while the module compiles in the background; after cs_jit_wait the same
+    call runs the compiled kernels; all results exact."""
+    import torch
+
+    import paper_2603_01443_b200 as cb
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    old = _native.get_option("jit")
+    _native.set_option("jit", 3)
+    try:
+        circ = cb.build_brickwall(cb.BrickwallSpec(18, 7, 2, 2, 31))
+        ref = orc.simulate(18, circ.kinds, circ.qa, circ.qb, circ.params)
+        n0 = _native.get_option("jit_units_compiled")
+        first = cb.run_cut(circ, 2).amps
+        _native.jit_wait(120)
+        assert _native.get_option("jit_units_compiled") > n0
+        second = cb.run_cut(circ, 2).amps
+        assert np.abs(first - ref).max() < 1e-10 and np.abs(second - ref).max() < 1e-10
+        u_first = cb.simulate(circ).amps
+        _native.jit_wait(120)
+        assert np.abs(cb.simulate(circ).amps - u_first).max() < 1e-12
+    finally:
+        _native.set_option("jit", old)

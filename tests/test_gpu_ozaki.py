@@ -35,18 +35,20 @@ def reference(hi, lo, hidx, lidx, coef, S, rows):
     return np.stack(out)
 
 
-def run(torch, native, hi, lo, hidx, lidx, coef, S=1, rows=None, ozaki=1, out=None, accumulate=False):
+def run(torch, native, hi, lo, hidx, lidx, coef, S=1, rows=None, ozaki=1, out=None, accumulate=False, digits=8):
     from paper_2603_01443_b200.merging import merge_terms_device
 
-    old = native.get_option("merge_ozaki")
+    old = native.get_option("merge_ozaki"), native.get_option("merge_ozaki_digits")
     native.set_option("merge_ozaki", ozaki)
+    native.set_option("merge_ozaki_digits", digits)
     try:
         res = merge_terms_device(torch.as_tensor(hi, device="cuda"), torch.as_tensor(lo, device="cuda"),
                                  hidx, lidx, coef, S=S, rows=rows, out=out, accumulate=accumulate)
         torch.cuda.synchronize()
         return res
     finally:
-        native.set_option("merge_ozaki", old)
+        native.set_option("merge_ozaki", old[0])
+        native.set_option("merge_ozaki_digits", old[1])
 
 
 CASES = [  # (K, S, H, W, rows)
@@ -55,9 +57,10 @@ CASES = [  # (K, S, H, W, rows)
 ]
 
 
+@pytest.mark.parametrize("digits", [8, 7], ids=["base256", "base128"])
 @pytest.mark.parametrize("mode", [1, 2], ids=["persistent", "unit-ctas"])
 @pytest.mark.parametrize("K,S,H,W,rows", CASES)
-def test_ozaki_vs_numpy_and_dfma(dev, K, S, H, W, rows, mode):
+def test_ozaki_vs_numpy_and_dfma(dev, K, S, H, W, rows, mode, digits):
     torch, native = dev
     rng = np.random.default_rng(K * 7 + W)
     nh = nl = max(2, K)
@@ -72,13 +75,17 @@ def test_ozaki_vs_numpy_and_dfma(dev, K, S, H, W, rows, mode):
     rows = rows or (0, H)
     want = reference(hi, lo, hidx, lidx, coef, S, rows)
     n0 = native.launch_count()
-    got = run(torch, native, hi, lo, hidx, lidx, coef, S=S, rows=rows, ozaki=mode).cpu().numpy()
+    got = run(torch, native, hi, lo, hidx, lidx, coef, S=S, rows=rows, ozaki=mode, digits=digits).cpu().numpy()
     launches = native.launch_count() - n0
     dfma = run(torch, native, hi, lo, hidx, lidx, coef, S=S, rows=rows, ozaki=0).cpu().numpy()
     scale = np.abs(want).max()
     tol = 1e-13 * scale * max(1, K / 16)
     assert np.abs(got - want).max() <= tol
     assert np.abs(got - dfma).max() <= tol
+    # the truncation level of the digit scheme: 2^-55 of max|a| max|b| per
+    # kept diagonal (base 128) / 2^-49 (base 256), measured here against numpy
+    term = np.abs(lo).max() * np.abs(hi).max() * np.abs(coef).max()
+    assert np.abs(got - want).max() <= (4e-14 if digits == 8 else 1e-14) * term * max(1, K / 16)
     # the tiny row keeps its own relative accuracy (per-row power-of-two scaling)
     w2 = want.reshape(S, rows[1] - rows[0], W)
     g2 = got.reshape(S, rows[1] - rows[0], W)

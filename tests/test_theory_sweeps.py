@@ -158,7 +158,7 @@ def test_install_as_cutbench_aliases_reference_modules():
         import importlib
 
         cbm = importlib.import_module(name)
-        assert cbm is pkg
+        assert cbm.__dropin_of__ is pkg and cbm.simulate is pkg.simulate
         h = importlib.import_module(f"{name}.harness")
         assert h.sweep_heatmap is sweeps.sweep_heatmap and h.measure is pkg.measure
         assert importlib.import_module(f"{name}.costmodel").threshold_uniform is theory.threshold_uniform
