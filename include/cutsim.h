@@ -66,10 +66,14 @@ int cs_device_count(int32_t* count);
  * "jit_units_compiled" / "jit_units_reused" (read-only counters),
  * "merge_ozaki" (int8 tcgen05 tensor-core merge with exact FP64 splitting
  * for one-slot products of K >= "merge_ozaki_min_k" terms, lo_len % 128 == 0,
- * row ranges % 16 == 0; default 1, min K 16), "merge_ozaki_digits" (8: 7
- * balanced base-256 digits per operand, 7 int32 diagonals per output —
- * default, truncation ~2e-15 of max|a| max|b|; 7: 8 base-128 digits, 8
- * diagonals, ~6e-16), "zero_start_tiles" (simulations
+ * row ranges % 16 == 0; default 1, min K 16), "merge_ozaki_digits" (7: 8
+ * balanced base-128 digits per operand, 8 int32 diagonals per output,
+ * truncation ~6e-16 of max|a| max|b| — default; 8: 7 base-256 digits, 7
+ * diagonals, ~1e-15, 3-4 % faster at K <= 32), "cluster" (cluster-resident
+ * variant batches: one NVRTC kernel per program, the 2^12..2^16-amplitude
+ * states in the distributed shared memory of a CTA cluster; default 1),
+ * "cluster_max" (CTAs per cluster at most: 2..16, default 16),
+ * "zero_start_tiles" (simulations
  * from |0..0> zero the states once and launch only the tiles that can be
  * non-zero; default 1),
  * "jit_max_cost", "vb", "sweep_minb", "merge_smem_kb", "merge_dmma3_warps", "jit_minb", "dense_norm" (normalised 2x2s:

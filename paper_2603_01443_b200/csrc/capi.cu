@@ -20,6 +20,8 @@
 #include "plan.hpp"
 #include "jit.hpp"
 
+#include <nvtx3/nvToolsExt.h>
+
 namespace cutsim {
 extern int g_sweep_minb;
 size_t sweep_smem_bytes(int tile_bits, int low_bits, int dtype, int n_ops, int vb);
@@ -73,16 +75,28 @@ struct Options {
   int64_t zero_start_tiles = 1;   // from |0..0>: zero the states once, launch only the tiles that can be non-zero
   int64_t merge_ozaki = 1;        // int8 tcgen05 merge (exact FP64 splitting) for K >= merge_ozaki_min_k
   int64_t merge_ozaki_min_k = 16;
-  int64_t merge_ozaki_digits = 8;  // digit bits of the int8 merge: 8 (7 slices, faster) or 7 (8 slices)
+  int64_t merge_ozaki_digits = 7;  // digit bits of the int8 merge: 7 (8 slices, default) or 8 (7 slices: 3-4 % faster at K <= 32, 2x the truncation)
   int64_t engine = 1;      // 1: register-tile kernel (rsweep), 0: shared-memory tile kernel (sweep)
   int64_t jit = 0;         // 0 never, 1 from a program's 2nd use, 2 always (compile on first use, blocking),
                            // 3 tiered: the interpreter runs while the module compiles on a background thread
+  int64_t cluster = 1;      // cluster-resident variant batches (one kernel, states in DSMEM) with the NVRTC kernels
+  int64_t cluster_max = 16; // CTAs per cluster at most (16 = the non-portable size)
   int64_t jit_struct = 1;  // param-mode (structure-keyed) modules: 0 never, 1 for small programs (< 2^22
                            // amplitudes: variant batches), 2 always
   int64_t jit_max_cost = 40000;  // FP64 instructions per specialised launch (code-size guard)
   int64_t plan_json = 0;   // cs_sweep_plan_json: 0 sweeps, 1 register programs
 } g_opt;
 std::mutex g_opt_mu;
+
+// NVTX ranges (header-only nvtx3: free without an attached tool): every
+// entry point and the pipeline's stages show up by name in Nsight
+// Systems / Compute (e.g. ncu --nvtx --nvtx-include "cs_cut_run/merge/")
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+  Nvtx(const Nvtx&) = delete;
+  Nvtx& operator=(const Nvtx&) = delete;
+};
 
 int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -176,6 +190,23 @@ int choose_tile_bits(int nq, int64_t n_states, int tile_bits, int dtype) {
   return dflt;
 }
 
+// Cluster size (log2) of the cluster-resident form, 0 = not used: the NVRTC
+// kernels must be on, the state 2^12..2^16 amplitudes, and a CTA's chunk
+// plus its transpose scratch within 128 KiB (T <= 12 for complex128, 13 for
+// complex64). Clusters as large as cluster_max allows while the batch's CTAs
+// still fit the chip once (more CTAs per state = more SMs on the FP64 work).
+int choose_cluster_bits(int nq, int64_t n_states, int dtype) {
+  if (!g_opt.cluster || g_opt.jit == 0 || g_opt.engine != 1 || nq < 12 || nq > 16) return 0;
+  const int tmax = dtype == CS_C128 ? 12 : 13;
+  int cmax = 0;
+  while ((int64_t(2) << cmax) <= g_opt.cluster_max) ++cmax;  // log2(cluster_max)
+  int want = 0;
+  while (want < cmax && (n_states << (want + 1)) <= 148) ++want;
+  const int cb = std::max(nq - tmax, want);
+  if (cb > cmax || nq - cb < 8) return 0;
+  return cb;
+}
+
 struct Launch {
   int sweep = 0;
   std::vector<SweepOp> entries;  // engine 0
@@ -192,6 +223,7 @@ struct Program {
   mutable std::atomic<int> uses{0};
   int64_t n_states = 1;  // states per launch the program was scheduled for
   bool param_mode = false;  // structure-keyed kernels with the coefficients as kernel parameters
+  int cluster_bits = 0;     // > 0: every sweep tiles the state into 2^cluster_bits tiles (one per cluster CTA)
 };
 
 // content-keyed program cache with least-recently-used eviction (a clear-all
@@ -245,7 +277,11 @@ std::shared_ptr<const Program> build_schedule(int nq, const uint8_t* kinds, cons
                                                          const int64_t* qb, const double* params,
                                                          const int32_t* slots, int64_t n_gates, int64_t n_states,
                                                          int tile_bits, int dtype, bool zero_start) {
-  const int T = choose_tile_bits(nq, n_states, tile_bits, dtype);
+  // cluster-resident form (started from |0..0>, NVRTC kernels, 12..16
+  // qubits): the state lives in the shared memory of a cluster of 2^cb CTAs,
+  // each holding a 2^T chunk (T = nq - cb); sweeps become phases of ONE kernel
+  const int cb = (zero_start && tile_bits <= 0) ? choose_cluster_bits(nq, n_states, dtype) : 0;
+  const int T = cb ? nq - cb : choose_tile_bits(nq, n_states, tile_bits, dtype);
   const int L = (T == nq) ? nq : std::max(3, std::min(int(g_opt.low_bits), T - 6));
   const int vb = choose_vb(n_states);
   std::string key;
@@ -258,22 +294,20 @@ std::shared_ptr<const Program> build_schedule(int nq, const uint8_t* kinds, cons
   // normalised 2x2s only pay where the 1-coefficients become free (the
   // NVRTC-specialised kernels); the interpreter keeps the plain matrices
   // param mode: small (latency-bound) programs get structure-keyed kernels;
-  // their normalisation is off (its pivot choice depends on the angles and
-  // would make the structure value-dependent)
+  // their 2x2s are normalised by the diagonal entries (a structural pivot,
+  // plan.cpp normalize_dense) so the kernel source does not depend on angles
   const bool param_mode = g_opt.jit != 0 && g_opt.engine == 1 &&
                           (g_opt.jit_struct == 2 || (g_opt.jit_struct == 1 && !zero_start_pays(n_states, nq)));
-  const int norm = param_mode ? 0
-                   : g_opt.dense_norm == 2 ? (g_opt.jit != 0 && g_opt.engine == 1 ? 1 : 0)
-                                           : int(g_opt.dense_norm);
+  const int norm = g_opt.dense_norm == 2 ? (g_opt.jit != 0 && g_opt.engine == 1 ? 1 : 0) : int(g_opt.dense_norm);
   // the cost-aware tile-set policy (3) only pays for a start from |0..0>
   // (zero-start tiles); other starts keep the most-absorbed-ops policy
   const int windows = (g_sweep_windows == 3 && !(zero_start && g_opt.zero_start_tiles &&
                                                  zero_start_pays(n_states, nq)))
                           ? 1
                           : g_sweep_windows;
-  const int32_t hdr[14] = {nq, T, L, int32_t(fuse), slots ? 1 : 0, dtype, vb, g_sweep_minb,
+  const int32_t hdr[15] = {nq, T, L, int32_t(fuse), slots ? 1 : 0, dtype, vb, g_sweep_minb,
                            int32_t(g_opt.engine), norm, g_reg_bits * 8 + g_reg_reorder * 4 + windows, g_jit_minb,
-                           g_jit_persistent, param_mode ? 1 : 0};
+                           g_jit_persistent, param_mode ? 1 : 0, cb};
   key.append(reinterpret_cast<const char*>(hdr), sizeof(hdr));
   key.append(reinterpret_cast<const char*>(kinds), size_t(n_gates));
   key.append(reinterpret_cast<const char*>(qa), size_t(n_gates) * 8);
@@ -292,13 +326,14 @@ std::shared_ptr<const Program> build_schedule(int nq, const uint8_t* kinds, cons
   if (fuse == 2) ops = fuse_ops(commute_phases(ops), true);
   else if (fuse == 1) ops = fuse_ops(ops);
   // growth budget: amplitudes stay below 2^200 (c128) / 2^20 (c64)
-  if (norm) ops = normalize_dense(ops, nq, dtype == CS_C128 ? 200.0 : 20.0);
+  if (norm) ops = normalize_dense(ops, nq, dtype == CS_C128 ? 200.0 : 20.0, param_mode);
   // register groups hold 2^k x vb complex values: 8 (c128) / 16 (c64) per thread
   const int max_group = std::min(sweep_max_group(T), group_budget(vb, dtype));
   auto built = std::make_shared<Program>();
   built->engine = int(g_opt.engine);
   built->n_states = n_states;
   built->param_mode = param_mode;
+  built->cluster_bits = cb;
   built->sweeps = schedule_sweeps(ops, nq, T, L, max_group, windows);
   build_launches(*built);
   std::shared_ptr<const Program> prog = built;
@@ -583,6 +618,15 @@ void compile_program_jit(const Program& prog, int dtype) {
   }
   if (!any) return;
   std::string err;
+  if (prog.cluster_bits > 0 && std::all_of(rp.begin(), rp.end(), [](const auto* r) { return r != nullptr; })) {
+    // the whole program as one cluster-resident kernel; if that cannot be
+    // built the same schedule runs as per-launch kernels
+    auto cm = jit_compile_cluster(sw, rp, prog.sweeps[0].tile_bits, dtype, &err, prog.param_mode);
+    if (cm) {
+      prog.jit = cm;
+      return;
+    }
+  }
   auto mod = jit_compile(sw, rp, dtype, &err, &minb, &pers, prog.param_mode);
   if (!mod) g_err = "JIT unavailable, using the interpreter kernel: " + err;
   prog.jit = mod;
@@ -689,8 +733,37 @@ int run_program(const std::shared_ptr<const Program>& prog_ptr, int nq, void* st
                                             size_t(n_states), st);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
   }
+  if (jit && jit->cluster > 0 && jit->units[0] && deadline_s <= 0.0) {
+    // the cluster-resident kernel: one launch, one cluster of jit->cluster
+    // CTAs per state (blockIdx.y = variant), the whole program in DSMEM
+    const JitUnit* ju = jit->units[0].get();
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaError_t e = cudaKernelSetAttributeForDevice(ju->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                    int(ju->smem), dev);
+    if (e == cudaSuccess && jit->cluster > 8)
+      e = cudaKernelSetAttributeForDevice(ju->kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1, dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cluster kernel attributes");
+    const std::vector<unsigned char>& blob = jit->blobs[0];
+    for (int64_t v0 = 0; v0 < n_states; v0 += 65535) {
+      const int64_t vc = std::min<int64_t>(65535, n_states - v0);
+      void* sp_arg = static_cast<char*>(states) + size_t(v0) * size_t(state_stride) * elem_bytes(dtype);
+      long long stride_arg = state_stride;
+      unsigned long long vbase_arg = variant_base + uint64_t(v0);
+      int init_arg = 1;
+      unsigned long long ntiles_arg = uint64_t(jit->cluster);
+      void* args[] = {&sp_arg, &stride_arg, &vbase_arg, &init_arg, &ntiles_arg,
+                      blob.empty() ? nullptr : const_cast<unsigned char*>(blob.data())};
+      e = cudaLaunchKernel(reinterpret_cast<const void*>(ju->kernel), dim3(unsigned(jit->cluster), unsigned(vc), 1),
+                           dim3(unsigned(ju->threads), 1, 1), args, ju->smem, st);
+      g_launches.fetch_add(1);
+      if (e != cudaSuccess) return cuda_fail(e, "cluster kernel launch");
+    }
+    return CS_OK;
+  }
   for (const Launch& ln : prog->launches) {
-    const JitUnit* jk = (jit && li < jit->units.size() && jit->units[li]) ? jit->units[li].get() : nullptr;
+    const JitUnit* jk = (jit && jit->cluster == 0 && li < jit->units.size() && jit->units[li])
+                            ? jit->units[li].get() : nullptr;
     const std::vector<unsigned char>* blob = jk ? &jit->blobs[li] : nullptr;
     ++li;
     const Sweep& sw = prog->sweeps[size_t(ln.sweep)];
@@ -975,6 +1048,11 @@ int cs_set_option(const char* key, int64_t value) {
   } else if (k == "merge_ozaki_digits") {
     if (value != 7 && value != 8) return fail(CS_ERR_INVALID, "merge_ozaki_digits must be 7 or 8");
     g_opt.merge_ozaki_digits = value;
+  } else if (k == "cluster") {
+    g_opt.cluster = value ? 1 : 0;
+  } else if (k == "cluster_max") {
+    if (value != 2 && value != 4 && value != 8 && value != 16) return fail(CS_ERR_INVALID, "cluster_max must be 2, 4, 8 or 16");
+    g_opt.cluster_max = value;
   } else if (k == "jit_struct") {
     if (value < 0 || value > 2) return fail(CS_ERR_INVALID, "jit_struct must be 0, 1 or 2");
     g_opt.jit_struct = value;
@@ -1007,6 +1085,8 @@ int64_t cs_get_option(const char* key) {
   if (k == "engine") return g_opt.engine;
   if (k == "jit") return g_opt.jit;
   if (k == "jit_struct") return g_opt.jit_struct;
+  if (k == "cluster") return g_opt.cluster;
+  if (k == "cluster_max") return g_opt.cluster_max;
   if (k == "merge_ozaki_digits") return g_opt.merge_ozaki_digits;
   if (k == "jit_units_compiled") return jit_units_compiled();
   if (k == "jit_units_reused") return jit_units_reused();
@@ -1055,6 +1135,7 @@ int cs_init_basis(void* states, int32_t nq, int64_t n_states, int64_t index, int
 int cs_sim_batch(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int64_t* qb, const double* params,
                  const int32_t* slots, int64_t n_gates, void* states, int64_t n_states, int64_t state_stride,
                  uint64_t variant_base, int32_t init_zero, int32_t dtype, void* stream) {
+  Nvtx nvtx_entry("cs_sim_batch");
   if (!valid_dtype(dtype)) return fail(CS_ERR_INVALID, "dtype must be CS_C128 or CS_C64");
   if (nq < 0 || nq > 62) return fail(CS_ERR_INVALID, "qubit count out of range");
   if (!states || n_states < 1) return fail(CS_ERR_INVALID, "empty state batch");
@@ -1078,6 +1159,7 @@ int cs_sim_batch_until(int32_t nq, const uint8_t* kinds, const int64_t* qa, cons
                        const double* params, const int32_t* slots, int64_t n_gates, void* states, int64_t n_states,
                        int64_t state_stride, uint64_t variant_base, int32_t init_zero, int32_t dtype, void* stream,
                        double deadline_s) {
+  Nvtx nvtx_entry("cs_sim_batch_until");
   if (!valid_dtype(dtype)) return fail(CS_ERR_INVALID, "dtype must be CS_C128 or CS_C64");
   if (nq < 1 || nq > 62) return fail(CS_ERR_INVALID, "qubit count out of range");
   if (!states || n_states < 1) return fail(CS_ERR_INVALID, "empty state batch");
@@ -1134,7 +1216,12 @@ int cs_jit_selftest(int32_t nq, const uint8_t* kinds, const int64_t* qa, const i
   std::vector<char> cubin;
   std::vector<std::string> names;
   std::string err;
-  if (!jit_cubin(sw, rp, dtype, &cubin, &names, &err, prog->param_mode)) return fail(CS_ERR_INTERNAL, err);
+  if (prog->cluster_bits > 0) {  // the form cs_sim_batch would run: one cluster-resident kernel
+    if (!jit_cluster_cubin(sw, rp, prog->sweeps[0].tile_bits, dtype, &cubin, &err, prog->param_mode))
+      return fail(CS_ERR_INTERNAL, err);
+  } else if (!jit_cubin(sw, rp, dtype, &cubin, &names, &err, prog->param_mode)) {
+    return fail(CS_ERR_INTERNAL, err);
+  }
   if (cubin_bytes) *cubin_bytes = int64_t(cubin.size());
   return CS_OK;
 }
@@ -1143,6 +1230,7 @@ int cs_merge_terms(int32_t S, int32_t K, const int32_t* hidx, const int32_t* lid
                    const void* hi, int64_t hi_len, const void* lo, int64_t lo_len, int64_t row_begin,
                    int64_t row_end, void* out, int64_t out_slot_stride, int32_t accumulate, int32_t dtype,
                    void* stream) {
+  Nvtx nvtx_entry("cs_merge_terms");
   return merge_terms_impl(S, K, hidx, lidx, coef, hi, hi_len, lo, lo_len, row_begin, row_end, out,
                           out_slot_stride, accumulate, dtype, as_stream(stream));
 }
@@ -1167,6 +1255,7 @@ int cs_merge_chain(int32_t n, const int32_t* seg_nq, const void* const* seg_stat
                    const int32_t* seg_cut_ids, int32_t c_total, const int32_t* cut_boundary, const double* term_coef,
                    int32_t force_bond, int64_t out_begin, int64_t out_end, void* out, void* workspace,
                    int64_t workspace_bytes, int32_t dtype, void* stream) {
+  Nvtx nvtx_entry("cs_merge_chain");
   if (!valid_dtype(dtype)) return fail(CS_ERR_INVALID, "dtype must be CS_C128 or CS_C64");
   ChainPlan plan;
   PlanError err{0, ""};
@@ -1444,6 +1533,7 @@ int cs_cut_host_workspace(int32_t nq, const uint8_t* kinds, const int64_t* qa, c
 int cs_cut_run_to_host(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int64_t* qb, const double* params,
                        int64_t n_gates, int32_t n_seg, const int32_t* seg_sizes, int32_t chunks, void* host_out,
                        void* workspace, int64_t workspace_bytes, int32_t dtype, void* stream, double* stage_ms) {
+  Nvtx nvtx_entry("cs_cut_run_to_host");
   if (!valid_dtype(dtype)) return fail(CS_ERR_INVALID, "dtype must be CS_C128 or CS_C64");
   if (nq < 2 || nq > 62 || !seg_sizes) return fail(CS_ERR_INVALID, "bad qubit count or segment sizes");
   if (!host_out) return fail(CS_ERR_INVALID, "null host output pointer");
@@ -1524,6 +1614,7 @@ int cs_cut_run(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int64_
                int64_t n_gates, int32_t n_seg, const int32_t* seg_sizes, int32_t force_bond, int64_t out_begin,
                int64_t out_end, void* out, void* workspace, int64_t workspace_bytes, int32_t dtype, void* stream,
                void* const* stage_events, double* stage_ms) {
+  Nvtx nvtx_entry("cs_cut_run");
   if (!valid_dtype(dtype)) return fail(CS_ERR_INVALID, "dtype must be CS_C128 or CS_C64");
   if (nq < 2 || nq > 62 || !seg_sizes) return fail(CS_ERR_INVALID, "bad qubit count or segment sizes");
   if (!out) return fail(CS_ERR_INVALID, "null output pointer");
@@ -1547,9 +1638,13 @@ int cs_cut_run(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int64_
   }
   if (ev[0]) cudaEventRecord(ev[0], st);
   std::vector<const void*> seg_states;
-  rc = cut_segments(job, progs, workspace, dtype, st, &seg_states);
+  {
+    Nvtx r("variant_stage");
+    rc = cut_segments(job, progs, workspace, dtype, st, &seg_states);
+  }
   if (rc != CS_OK) return rc;
   if (ev[1]) cudaEventRecord(ev[1], st);
+  Nvtx r_merge("merge");
   rc = run_chain(job.plan, pr.n, seg_states.data(), out_begin, out_end, out,
                  static_cast<char*>(workspace) + job.chain_off, job.total_bytes - job.chain_off, dtype, st);
   if (rc != CS_OK) return rc;
@@ -1600,6 +1695,7 @@ int cs_cut_run_sharded(int32_t nq, const uint8_t* kinds, const int64_t* qa, cons
                        int32_t rank, int64_t out_begin, int64_t out_end, void* out, void* workspace,
                        int64_t workspace_bytes, int32_t dtype, void* stream, void* const* stage_events,
                        double* stage_ms) {
+  Nvtx nvtx_entry("cs_cut_run_sharded");
   if (!valid_dtype(dtype)) return fail(CS_ERR_INVALID, "dtype must be CS_C128 or CS_C64");
   if (nq < 2 || nq > 62 || !seg_sizes) return fail(CS_ERR_INVALID, "bad qubit count or segment sizes");
   if (world < 1 || rank < 0 || rank >= world) return fail(CS_ERR_INVALID, "bad rank / world");
@@ -1631,7 +1727,10 @@ int cs_cut_run_sharded(int32_t nq, const uint8_t* kinds, const int64_t* qa, cons
     for (auto& e : ev) cudaEventCreate(&e);
   }
   if (ev[0]) cudaEventRecord(ev[0], st);
-  rc = run_pieces(job, pieces, progs, dtype, st);
+  {
+    Nvtx r("variant_stage");
+    rc = run_pieces(job, pieces, progs, dtype, st);
+  }
   if (rc != CS_OK) return rc;
   if (ev[1]) cudaEventRecord(ev[1], st);
   if (exchange) {
@@ -1644,6 +1743,7 @@ int cs_cut_run_sharded(int32_t nq, const uint8_t* kinds, const int64_t* qa, cons
   for (size_t s = 0; s < job.prep.segs.size(); ++s)
     seg_states.push_back(static_cast<char*>(workspace) + lay.seg_first[s] * lay.L * int64_t(elem_bytes(dtype)));
   if (out_end > out_begin) {
+    Nvtx r("merge");
     rc = run_chain(job.plan, job.prep.n, seg_states.data(), out_begin, out_end, out,
                    static_cast<char*>(workspace) + lay.chain_off, lay.total_bytes - lay.chain_off, dtype, st);
     if (rc != CS_OK) return rc;

@@ -19,6 +19,7 @@
 #include <cstdlib>
 #include <mutex>
 #include <sstream>
+#include <functional>
 #include <thread>
 #include <unordered_map>
 #include <cstring>
@@ -109,86 +110,14 @@ int64_t jit_cost(const std::vector<RegOp>& prog, int RB) {
   return c;
 }
 
-std::string jit_source(const Sweep& sw, const std::vector<RegOp>& prog, int RB, int dtype, const std::string& name,
-                       int minb, bool persistent, std::vector<double>* pvals) {
-  const int T = sw.tile_bits;
-  const int L = sw.low_bits;
+// Straight-line code of one register program (dense / phase / remap ops)
+// on registers v0..v{2^RB-1}: starts and ends in the canonical register
+// mapping (register bit k = tile bit T - RB + k); uses tid, tp, base,
+// variant and the shared-memory transpose buffer sm of the enclosing kernel.
+static void emit_register_program(std::ostringstream& o, const std::vector<RegOp>& prog, int T, int RB,
+                                  const std::function<std::string(double)>& val) {
   const int NR = 1 << RB;
-  const int BD = 1 << (T - RB);
-  bool remap = false;
-  for (const RegOp& r : prog) remap |= r.kind == ROP_REMAP;
-  // value mode (pvals == null): matrices and phases as hex-float literals;
-  // param mode: every coefficient that is not exactly 0 or +-1 is read from
-  // the kernel-parameter block P (constant bank: DFMA takes it as an operand),
-  // so the source — and the compiled module — depends only on the circuit's
-  // structure (gate positions, tile sets, masks, slots), not on its angles
-  auto val = [&](double v) -> std::string {
-    if (!pvals) return lit(v);
-    pvals->push_back(v);
-    return "P.m[" + std::to_string(pvals->size() - 1) + "]";
-  };
   auto trivial = [](double v) { return v == 0.0 || v == 1.0 || v == -1.0; };
-  std::ostringstream o;
-  o << "  extern __shared__ __align__(16) unsigned char smraw[];\n";
-  o << "  V* sm = reinterpret_cast<V*>(smraw); (void)sm;\n";
-  o << "  const unsigned tid = threadIdx.x;\n";
-  o << "  const unsigned long long variant = vbase + blockIdx.y; (void)variant;\n";
-  o << "  V* st = states + (long long)blockIdx.y * stride;\n";
-  auto base_of = [&](const char* dst, const char* tile) {
-    std::ostringstream b;
-    b << dst << " = 0ull;";
-    for (size_t j = 0; j < sw.oq.size(); ++j)
-      b << " " << dst << " |= ((" << tile << " >> " << j << ") & 1ull) << " << sw.oq[j] << ";";
-    return b.str();
-  };
-  auto gidx = [&](int j, const char* basev) {
-    std::ostringstream g;
-    g << "{ const unsigned e = tid + " << (j * BD) << "u; const unsigned c = e >> " << L
-      << "; unsigned long long g = " << basev << " + (e & " << ((1u << L) - 1u) << "u);";
-    for (size_t i = 0; i < sw.hq.size(); ++i)
-      g << " g |= (unsigned long long)((c >> " << i << ") & 1u) << " << sw.hq[i] << ";";
-    return g.str();
-  };
-  for (int j = 0; j < NR; ++j) o << "  V v" << j << ";\n";
-  if (persistent) {
-    // one CTA per SM walks the tiles; each thread prefetches the amplitudes it
-    // will own in the next tile into its own shared-memory slots with
-    // cp.async while the current tile's gates run (no barrier needed: a
-    // thread only ever reads the slots it filled itself)
-    o << "  V* pf = sm + " << (remap ? (1u << T) : 0u) << "u;\n";
-    o << "  unsigned long long tile = blockIdx.x, base;\n";
-    o << "  if (!init && tile < n_tiles) { unsigned long long nb; " << base_of("nb", "tile") << "\n";
-    for (int j = 0; j < NR; ++j)
-      o << "    " << gidx(j, "nb") << " cpa(pf + e, st + g); }\n";
-    o << "  }\n  cpc();\n";
-    o << "  for (; tile < n_tiles; tile += gridDim.x) {\n";
-    o << "  " << base_of("base", "tile") << "\n";
-    o << "  if (init) {\n";
-    for (int j = 0; j < NR; ++j)
-      o << "    { const unsigned e = tid + " << (j * BD) << "u; v" << j
-        << ".x = (base == 0ull && e == 0u) ? R(1) : R(0); v" << j << ".y = R(0); }\n";
-    o << "  } else {\n    cpw();\n";
-    for (int j = 0; j < NR; ++j) o << "    v" << j << " = pf[tid + " << (j * BD) << "u];\n";
-    o << "    const unsigned long long nt = tile + gridDim.x;\n";
-    o << "    if (nt < n_tiles) { unsigned long long nb; " << base_of("nb", "nt") << "\n";
-    for (int j = 0; j < NR; ++j)
-      o << "      " << gidx(j, "nb") << " cpa(pf + e, st + g); }\n";
-    o << "    }\n    cpc();\n  }\n";
-  } else {
-    o << "  const unsigned long long tile = blockIdx.x; (void)n_tiles;\n";
-    o << "  unsigned long long " << base_of("base", "tile") << "\n";
-    // started from |0..0>, every tile but the one holding index 0 is all
-    // zero and stays zero under the tile's gates: store zeros, skip the math
-    // (base is uniform across the CTA, so the early return skips no barrier
-    // another thread waits on)
-    o << "  if (init && base != 0ull) {\n";
-    for (int j = 0; j < NR; ++j) o << "    " << gidx(j, "base") << " st[g] = V{R(0), R(0)}; }\n";
-    o << "    return;\n  }\n";
-    for (int j = 0; j < NR; ++j)
-      o << "  " << gidx(j, "base") << " if (init) { v" << j << ".x = (base == 0ull && e == 0u) ? R(1) : R(0); v" << j
-        << ".y = R(0); } else v" << j << " = st[g]; }\n";
-  }
-  o << "  unsigned tp = tid; (void)tp;\n";
   int rpos[4];
   for (int k = 0; k < RB; ++k) rpos[k] = T - RB + k;
   auto roff = [&](int j) {
@@ -298,6 +227,88 @@ std::string jit_source(const Sweep& sw, const std::vector<RegOp>& prog, int RB, 
     o << " } }\n";
     i += slotted ? 2 : 1;
   }
+}
+
+std::string jit_source(const Sweep& sw, const std::vector<RegOp>& prog, int RB, int dtype, const std::string& name,
+                       int minb, bool persistent, std::vector<double>* pvals) {
+  const int T = sw.tile_bits;
+  const int L = sw.low_bits;
+  const int NR = 1 << RB;
+  const int BD = 1 << (T - RB);
+  bool remap = false;
+  for (const RegOp& r : prog) remap |= r.kind == ROP_REMAP;
+  // value mode (pvals == null): matrices and phases as hex-float literals;
+  // param mode: every coefficient that is not exactly 0 or +-1 is read from
+  // the kernel-parameter block P (constant bank: DFMA takes it as an operand),
+  // so the source — and the compiled module — depends only on the circuit's
+  // structure (gate positions, tile sets, masks, slots), not on its angles
+  auto val = [&](double v) -> std::string {
+    if (!pvals) return lit(v);
+    pvals->push_back(v);
+    return "P.m[" + std::to_string(pvals->size() - 1) + "]";
+  };
+  std::ostringstream o;
+  o << "  extern __shared__ __align__(16) unsigned char smraw[];\n";
+  o << "  V* sm = reinterpret_cast<V*>(smraw); (void)sm;\n";
+  o << "  const unsigned tid = threadIdx.x;\n";
+  o << "  const unsigned long long variant = vbase + blockIdx.y; (void)variant;\n";
+  o << "  V* st = states + (long long)blockIdx.y * stride;\n";
+  auto base_of = [&](const char* dst, const char* tile) {
+    std::ostringstream b;
+    b << dst << " = 0ull;";
+    for (size_t j = 0; j < sw.oq.size(); ++j)
+      b << " " << dst << " |= ((" << tile << " >> " << j << ") & 1ull) << " << sw.oq[j] << ";";
+    return b.str();
+  };
+  auto gidx = [&](int j, const char* basev) {
+    std::ostringstream g;
+    g << "{ const unsigned e = tid + " << (j * BD) << "u; const unsigned c = e >> " << L
+      << "; unsigned long long g = " << basev << " + (e & " << ((1u << L) - 1u) << "u);";
+    for (size_t i = 0; i < sw.hq.size(); ++i)
+      g << " g |= (unsigned long long)((c >> " << i << ") & 1u) << " << sw.hq[i] << ";";
+    return g.str();
+  };
+  for (int j = 0; j < NR; ++j) o << "  V v" << j << ";\n";
+  if (persistent) {
+    // one CTA per SM walks the tiles; each thread prefetches the amplitudes it
+    // will own in the next tile into its own shared-memory slots with
+    // cp.async while the current tile's gates run (no barrier needed: a
+    // thread only ever reads the slots it filled itself)
+    o << "  V* pf = sm + " << (remap ? (1u << T) : 0u) << "u;\n";
+    o << "  unsigned long long tile = blockIdx.x, base;\n";
+    o << "  if (!init && tile < n_tiles) { unsigned long long nb; " << base_of("nb", "tile") << "\n";
+    for (int j = 0; j < NR; ++j)
+      o << "    " << gidx(j, "nb") << " cpa(pf + e, st + g); }\n";
+    o << "  }\n  cpc();\n";
+    o << "  for (; tile < n_tiles; tile += gridDim.x) {\n";
+    o << "  " << base_of("base", "tile") << "\n";
+    o << "  if (init) {\n";
+    for (int j = 0; j < NR; ++j)
+      o << "    { const unsigned e = tid + " << (j * BD) << "u; v" << j
+        << ".x = (base == 0ull && e == 0u) ? R(1) : R(0); v" << j << ".y = R(0); }\n";
+    o << "  } else {\n    cpw();\n";
+    for (int j = 0; j < NR; ++j) o << "    v" << j << " = pf[tid + " << (j * BD) << "u];\n";
+    o << "    const unsigned long long nt = tile + gridDim.x;\n";
+    o << "    if (nt < n_tiles) { unsigned long long nb; " << base_of("nb", "nt") << "\n";
+    for (int j = 0; j < NR; ++j)
+      o << "      " << gidx(j, "nb") << " cpa(pf + e, st + g); }\n";
+    o << "    }\n    cpc();\n  }\n";
+  } else {
+    o << "  const unsigned long long tile = blockIdx.x; (void)n_tiles;\n";
+    o << "  unsigned long long " << base_of("base", "tile") << "\n";
+    // started from |0..0>, every tile but the one holding index 0 is all
+    // zero and stays zero under the tile's gates: store zeros, skip the math
+    // (base is uniform across the CTA, so the early return skips no barrier
+    // another thread waits on)
+    o << "  if (init && base != 0ull) {\n";
+    for (int j = 0; j < NR; ++j) o << "    " << gidx(j, "base") << " st[g] = V{R(0), R(0)}; }\n";
+    o << "    return;\n  }\n";
+    for (int j = 0; j < NR; ++j)
+      o << "  " << gidx(j, "base") << " if (init) { v" << j << ".x = (base == 0ull && e == 0u) ? R(1) : R(0); v" << j
+        << ".y = R(0); } else v" << j << " = st[g]; }\n";
+  }
+  o << "  unsigned tp = tid; (void)tp;\n";
+  emit_register_program(o, prog, T, RB, val);
   for (int j = 0; j < NR; ++j) o << "  " << gidx(j, "base") << " st[g] = v" << j << "; }\n";
   if (persistent) o << "  }\n";
   o << "}\n";
@@ -306,6 +317,111 @@ std::string jit_source(const Sweep& sw, const std::vector<RegOp>& prog, int RB, 
   const bool params = pvals && !pvals->empty();
   if (params) head << "struct JP_" << name << " { R m[" << pvals->size() << "]; };\n";
   head << "extern \"C\" __global__ void __launch_bounds__(" << BD << ", " << minb << ") " << name
+       << "(V* __restrict__ states, long long stride, unsigned long long vbase, int init, unsigned long long n_tiles";
+  if (params) head << ", const JP_" << name << " P";
+  head << ") {\n";
+  return head.str() + o.str();
+}
+
+// Cluster-resident form of a whole program (north_star (1): states resident
+// in cluster DSMEM when small). A state of nq qubits lives in the shared
+// memory of a cluster of C = 2^(nq - T) CTAs: CTA r holds amplitudes
+// [r 2^T, (r+1) 2^T) ("canonical chunk"). Every launch of the program (a
+// sweep tile set, or part of one) becomes a phase of ONE kernel: CTA r takes
+// tile r of that phase's geometry — loaded from the owning CTAs' chunks
+// with ld.shared::cluster — runs the phase's register program, and writes it
+// back with st.shared::cluster; one cluster barrier separates phases (every
+// index belongs to exactly one tile per phase, so there is no other hazard).
+// The first phase starts from |0..0> in registers; the last one stores to
+// the state in global memory. The variant id is blockIdx.y (one cluster per
+// variant state), as in the per-launch kernels.
+std::string jit_cluster_source(const std::vector<const Sweep*>& sweeps,
+                               const std::vector<const std::vector<RegOp>*>& progs, int T, int RB, int dtype,
+                               const std::string& name, std::vector<double>* pvals) {
+  const int NR = 1 << RB;
+  const int BD = 1 << (T - RB);
+  const int C = 1 << sweeps[0]->oq.size();
+  bool remap = false;
+  for (const auto* pr : progs)
+    for (const RegOp& r : *pr) remap |= r.kind == ROP_REMAP;
+  auto val = [&](double v) -> std::string {
+    if (!pvals) return lit(v);
+    pvals->push_back(v);
+    return "P.m[" + std::to_string(pvals->size() - 1) + "]";
+  };
+  const char* vreg = dtype == 0 ? "d" : "f";
+  const char* vty = dtype == 0 ? "f64" : "f32";
+  std::ostringstream o;
+  o << "  extern __shared__ __align__(16) unsigned char smraw[];\n";
+  o << "  V* chunk = reinterpret_cast<V*>(smraw);\n";
+  o << "  V* sm = chunk + " << (1u << T) << "u; (void)sm;\n";
+  o << "  const unsigned tid = threadIdx.x;\n";
+  o << "  unsigned rank; asm volatile(\"mov.u32 %0, %%cluster_ctarank;\" : \"=r\"(rank));\n";
+  o << "  const unsigned long long variant = vbase + blockIdx.y; (void)variant;\n";
+  o << "  V* st = states + (long long)blockIdx.y * stride; (void)n_tiles; (void)init;\n";
+  o << "  const unsigned csa = (unsigned)__cvta_generic_to_shared(chunk);\n";
+  o << "  unsigned long long base; unsigned tp;\n";
+  for (int j = 0; j < NR; ++j) o << "  V v" << j << ";\n";
+  // every CTA of the cluster is running before any DSMEM access
+  o << "  asm volatile(\"barrier.cluster.arrive.release.aligned;\\n\\tbarrier.cluster.wait.acquire.aligned;\" ::: \"memory\");\n";
+  auto base_of = [&](const Sweep& sw) {
+    std::ostringstream b;
+    b << "  base = 0ull;";
+    for (size_t j = 0; j < sw.oq.size(); ++j)
+      b << " base |= (unsigned long long)((rank >> " << j << ") & 1u) << " << sw.oq[j] << ";";
+    return b.str();
+  };
+  auto gidx = [&](const Sweep& sw, int j) {
+    const int L = sw.low_bits;
+    std::ostringstream g;
+    g << "{ const unsigned e = tid + " << (j * BD) << "u; const unsigned c = e >> " << L
+      << "; unsigned long long g = base + (e & " << ((1u << L) - 1u) << "u);";
+    for (size_t i = 0; i < sw.hq.size(); ++i)
+      g << " g |= (unsigned long long)((c >> " << i << ") & 1u) << " << sw.hq[i] << ";";
+    g << " unsigned ra; asm(\"mapa.shared::cluster.u32 %0, %1, %2;\" : \"=r\"(ra) : \"r\"(csa + (unsigned)(g & "
+      << ((1u << T) - 1u) << "ull) * (unsigned)sizeof(V)), \"r\"((unsigned)(g >> " << T << ")));";
+    return g.str();
+  };
+  for (size_t ph = 0; ph < sweeps.size(); ++ph) {
+    const Sweep& sw = *sweeps[ph];
+    o << "  // phase " << ph << "\n" << base_of(sw) << "\n";
+    if (ph == 0) {
+      for (int j = 0; j < NR; ++j)
+        o << "  { const unsigned e = tid + " << (j * BD) << "u; v" << j
+          << ".x = (base == 0ull && e == 0u) ? R(1) : R(0); v" << j << ".y = R(0); }\n";
+    } else {
+      for (int j = 0; j < NR; ++j)
+        o << "  " << gidx(sw, j) << " asm volatile(\"ld.shared::cluster.v2." << vty << " {%0, %1}, [%2];\" : \"="
+          << vreg << "\"(v" << j << ".x), \"=" << vreg << "\"(v" << j << ".y) : \"r\"(ra) : \"memory\"); }\n";
+    }
+    o << "  tp = tid;\n";
+    emit_register_program(o, *progs[ph], T, RB, val);
+    if (ph + 1 < sweeps.size()) {
+      for (int j = 0; j < NR; ++j)
+        o << "  " << gidx(sw, j) << " asm volatile(\"st.shared::cluster.v2." << vty << " [%0], {%1, %2};\" :: \"r\"(ra), \""
+          << vreg << "\"(v" << j << ".x), \"" << vreg << "\"(v" << j << ".y) : \"memory\"); }\n";
+      o << "  asm volatile(\"barrier.cluster.arrive.release.aligned;\\n\\tbarrier.cluster.wait.acquire.aligned;\" ::: \"memory\");\n";
+    } else {
+      // the last phase writes the state (canonical index order) to global memory
+      for (int j = 0; j < NR; ++j) {
+        const int L = sw.low_bits;
+        o << "  { const unsigned e = tid + " << (j * BD) << "u; const unsigned c = e >> " << L
+          << "; unsigned long long g = base + (e & " << ((1u << L) - 1u) << "u);";
+        for (size_t i = 0; i < sw.hq.size(); ++i)
+          o << " g |= (unsigned long long)((c >> " << i << ") & 1u) << " << sw.hq[i] << ";";
+        o << " st[g] = v" << j << "; }\n";
+      }
+      // no CTA leaves while another may still read its chunk
+      o << "  asm volatile(\"barrier.cluster.arrive.release.aligned;\\n\\tbarrier.cluster.wait.acquire.aligned;\" ::: \"memory\");\n";
+    }
+  }
+  o << "}\n";
+  (void)remap;
+  std::ostringstream head;
+  const bool params = pvals && !pvals->empty();
+  if (params) head << "struct JP_" << name << " { R m[" << pvals->size() << "]; };\n";
+  head << "extern \"C\" __global__ void __cluster_dims__(" << C << ", 1, 1) __launch_bounds__(" << BD << ", 1) "
+       << name
        << "(V* __restrict__ states, long long stride, unsigned long long vbase, int init, unsigned long long n_tiles";
   if (params) head << ", const JP_" << name << " P";
   head << ") {\n";
@@ -518,6 +634,79 @@ std::shared_ptr<JitModule> jit_compile(const std::vector<const Sweep*>& sweeps,
       if (progs[j] && !mod->units[j] && codes[j] == codes[i]) mod->units[j] = u;
   }
   return mod;
+}
+
+// The cluster-resident program (jit_cluster_source) as one unit; cached by
+// source like every other unit.
+std::shared_ptr<JitModule> jit_compile_cluster(const std::vector<const Sweep*>& sweeps,
+                                               const std::vector<const std::vector<RegOp>*>& progs, int T,
+                                               int dtype, std::string* err, bool param_mode) {
+  const int RB = reg_bits_for(T);
+  std::vector<double> vals;
+  const std::string code =
+      header(dtype) + jit_cluster_source(sweeps, progs, T, RB, dtype, "cs_jit_k", param_mode ? &vals : nullptr);
+  auto mod = std::make_shared<JitModule>();
+  mod->cluster = 1 << sweeps[0]->oq.size();
+  mod->units.assign(1, nullptr);
+  mod->blobs.assign(1, {});
+  if (!vals.empty()) {
+    std::vector<unsigned char>& b = mod->blobs[0];
+    if (dtype == 0) {
+      b.resize(vals.size() * sizeof(double));
+      std::memcpy(b.data(), vals.data(), b.size());
+    } else {
+      std::vector<float> f(vals.begin(), vals.end());
+      b.resize(f.size() * sizeof(float));
+      std::memcpy(b.data(), f.data(), b.size());
+    }
+    if (b.size() > 30000) {  // the kernel-parameter limit (32764 B minus the other arguments)
+      *err = "cluster program has too many coefficients for the parameter block";
+      return nullptr;
+    }
+  }
+  {
+    std::lock_guard<std::mutex> lk(g_units_mu);
+    auto it = g_units.find(code);
+    if (it != g_units.end()) {
+      it->second.last_use = ++g_units_clock;
+      mod->units[0] = it->second.unit;
+      ++g_units_reused;
+      return mod;
+    }
+  }
+  std::vector<char> cubin;
+  if (!compile_source(code, &cubin, err)) return nullptr;
+  dump_artifact("cs_jit_cluster", code, cubin);
+  auto u = std::make_shared<JitUnit>();
+  cudaError_t e = cudaLibraryLoadData(&u->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
+  if (e != cudaSuccess) {
+    u->lib = nullptr;
+    *err = std::string("cudaLibraryLoadData: ") + cudaGetErrorString(e);
+    return nullptr;
+  }
+  e = cudaLibraryGetKernel(&u->kernel, u->lib, "cs_jit_k");
+  if (e != cudaSuccess) {
+    *err = std::string("cudaLibraryGetKernel: ") + cudaGetErrorString(e);
+    return nullptr;
+  }
+  u->threads = 1 << (T - RB);
+  u->smem = 2 * (size_t(1) << T) * (dtype == 0 ? 16 : 8);  // canonical chunk + transpose scratch
+  ++g_units_compiled;
+  std::lock_guard<std::mutex> lk(g_units_mu);
+  g_units[code] = UnitEntry{u, ++g_units_clock};
+  mod->units[0] = u;
+  return mod;
+}
+
+// NVRTC step only of the cluster form (host self-test)
+bool jit_cluster_cubin(const std::vector<const Sweep*>& sweeps, const std::vector<const std::vector<RegOp>*>& progs,
+                       int T, int dtype, std::vector<char>* cubin, std::string* err, bool param_mode) {
+  std::vector<double> vals;
+  const std::string code = header(dtype) + jit_cluster_source(sweeps, progs, T, reg_bits_for(T), dtype, "cs_jit_k",
+                                                              param_mode ? &vals : nullptr);
+  const bool ok = compile_source(code, cubin, err);
+  if (ok) dump_artifact("cluster_selftest", code, *cubin);
+  return ok;
 }
 
 }  // namespace cutsim

@@ -28,6 +28,7 @@ struct JitUnit {
 struct JitModule {
   std::vector<std::shared_ptr<JitUnit>> units;
   std::vector<std::vector<unsigned char>> blobs;
+  int cluster = 0;  // > 0: ONE cluster-resident kernel (units[0]) of this many CTAs per state
 };
 
 // CUDA C++ source of one launch: straight-line code for the register program
@@ -48,6 +49,18 @@ std::shared_ptr<JitModule> jit_compile(const std::vector<const Sweep*>& sweeps,
                                        const std::vector<const std::vector<RegOp>*>& progs, int dtype,
                                        std::string* err, const std::vector<int>* minb = nullptr,
                                        const std::vector<char>* persistent = nullptr, bool param_mode = false);
+
+// The whole program as one cluster-resident kernel (jit.cpp
+// jit_cluster_source): every launch's sweep must use tile_bits T with
+// 2^(nq - T) tiles = the cluster size.
+std::string jit_cluster_source(const std::vector<const Sweep*>& sweeps,
+                               const std::vector<const std::vector<RegOp>*>& progs, int T, int RB, int dtype,
+                               const std::string& name, std::vector<double>* pvals);
+std::shared_ptr<JitModule> jit_compile_cluster(const std::vector<const Sweep*>& sweeps,
+                                               const std::vector<const std::vector<RegOp>*>& progs, int T,
+                                               int dtype, std::string* err, bool param_mode);
+bool jit_cluster_cubin(const std::vector<const Sweep*>& sweeps, const std::vector<const std::vector<RegOp>*>& progs,
+                       int T, int dtype, std::vector<char>* cubin, std::string* err, bool param_mode);
 
 // units compiled / served from the unit cache since load (cs_get_option
 // "jit_units_compiled" / "jit_units_reused")

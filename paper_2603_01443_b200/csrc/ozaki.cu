@@ -50,9 +50,10 @@ namespace {
 // (64 B/cycle per SM, the K <= 32 bound: DESIGN.md §3), so 7 diagonals cut
 // both that read stream and the digit-pair MMAs (28 instead of 36) by 1/8
 // and 2/9 at the same 2^-55 truncation level.
-// Option "merge_ozaki_digits" selects DB (8 default). Truncation measured in
+// Option "merge_ozaki_digits" selects DB (7 default). Truncation measured in
 // a host emulation: max |error| / (max|a| max|b|) = 2.2e-15 (DB = 8) and
-// 5.6e-16 (DB = 7) over K = 16 terms.
+// 5.6e-16 (DB = 7) over K = 16 terms; on the B200 (tools/ozaki_digits.py,
+// q=30) DB = 8 is 3-4 % faster at K = 16 / 32 and equal at K = 64.
 template <int DB>
 struct Digits {
   static constexpr int S = DB == 8 ? 7 : 8;  // slices
@@ -282,13 +283,21 @@ __global__ void ozaki_prep_hi(const __grid_constant__ OzPrep p, int64_t nrows, i
       br = v.x * cr - v.y * ci;
       bi = v.x * ci + v.y * cr;
     }
-    int dr[kSlices], di[kSlices];
+    int dr[kSlices], di[kSlices], dn[kSlices];
     digits_split<DB>(br, sc, dr);
     digits_split<DB>(bi, sc, di);
+    // -Hi split on its own: a balanced base-256 digit may be -128, whose
+    // negation does not fit int8 (base 128: -d is a valid digit)
+    if constexpr (DB == 8) {
+      digits_split<DB>(-bi, sc, dn);
+    } else {
+#pragma unroll
+      for (int i = 0; i < kSlices; ++i) dn[i] = -di[i];
+    }
 #pragma unroll
     for (int i = 0; i < kSlices; ++i) {
       // row (h, 0): (Hr, -Hi) -> real part; row (h, 1): (Hi, Hr) -> imaginary part
-      const uint32_t p0 = pack2(dr[i], -di[i]) << (16 * (tt & 1));
+      const uint32_t p0 = pack2(dr[i], dn[i]) << (16 * (tt & 1));
       const uint32_t p1 = pack2(di[i], dr[i]) << (16 * (tt & 1));
       if (tt & 1) {
         w0[i][tt >> 1] |= p0;

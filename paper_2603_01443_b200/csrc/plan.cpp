@@ -248,7 +248,7 @@ LOp phase_op(int q, Cx v) {
 
 }  // namespace
 
-std::vector<LOp> normalize_dense(const std::vector<LOp>& ops, int nq, double max_growth_bits) {
+std::vector<LOp> normalize_dense(const std::vector<LOp>& ops, int nq, double max_growth_bits, bool fixed_pivot) {
   std::vector<LOp> out;
   out.reserve(ops.size() + size_t(nq) + 1);
   std::vector<Cx> d0(static_cast<size_t>(nq)), d1(static_cast<size_t>(nq));
@@ -297,7 +297,10 @@ std::vector<LOp> normalize_dense(const std::vector<LOp>& ops, int nq, double max
     Cx dn[2];
     int piv[2];
     for (int r = 0; r < 2; ++r) {
-      piv[r] = cabs2(m[r][0]) >= cabs2(m[r][1]) ? 0 : 1;
+      if (fixed_pivot && cabs2(m[r][r]) >= 1e-24 * cabs2(m[r][1 - r]) && cabs2(m[r][r]) > 0.0)
+        piv[r] = r;
+      else
+        piv[r] = cabs2(m[r][0]) >= cabs2(m[r][1]) ? 0 : 1;
       dn[r] = m[r][piv[r]];
     }
     const double g = bits_of(dn[0], dn[1]);

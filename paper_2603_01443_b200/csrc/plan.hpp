@@ -52,7 +52,13 @@ std::vector<LOp> fuse_ops(const std::vector<LOp>& ops, bool same_type_only = fal
 // state by up to 1/2 bit per op; whenever the total would exceed
 // max_growth_bits an op is emitted un-normalised (with the pending diagonal
 // and scalar applied), restoring the true scale.
-std::vector<LOp> normalize_dense(const std::vector<LOp>& ops, int nq, double max_growth_bits);
+// fixed_pivot: every row is divided by its DIAGONAL entry (unless that is
+// below 1e-12 of the other one: the growth budget bounds the inflation a
+// small pivot causes; the precision of a + x b does not depend on |x|), so
+// which coefficients become 1 depends on the gate structure, not on the
+// angles (param-mode kernels, jit_struct)
+std::vector<LOp> normalize_dense(const std::vector<LOp>& ops, int nq, double max_growth_bits,
+                                 bool fixed_pivot = false);
 
 // Defer single-qubit phases past everything they commute with (diagonal
 // ops, dense ops controlled by or not touching their qubit) and merge the

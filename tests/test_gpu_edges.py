@@ -209,7 +209,8 @@ def test_reference_variant_loop_runs_one_batch_per_family(cb):
     for f, sts in zip(subs.segments, states):
         for b, sv in enumerate(sts):
             alone = cb.simulate(cb.Circuit.from_table(f.num_qubits, f.variant_table(b)))
-            assert np.array_equal(sv.amps, alone.amps)
+            # one batched program vs a single-state one (other tiling): equal to rounding
+            assert np.abs(sv.amps - alone.amps).max() < 1e-14
     merged = cb.merge(cb.merge_input_from(subs, states)).amps
     assert np.abs(merged - ref_state(circ)).max() < TOL
     again = cb.simulate(fam.circuits[1])  # a second request: a new pass, a fresh state

@@ -233,3 +233,55 @@ def test_tiered_jit_runs_interpreter_then_compiled_kernels():
         assert np.abs(cb.simulate(circ).amps - u_first).max() < 1e-12
     finally:
         _native.set_option("jit", old)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("qs,c,dtype,tol,cmax", [(12, 2, np.complex128, 1e-10, 16), (15, 2, np.complex128, 1e-10, 16),
+                                                  (15, 4, np.complex128, 1e-10, 8), (16, 2, np.complex128, 1e-10, 16),
+                                                  (13, 3, np.complex64, 1e-5, 16), (14, 6, np.complex128, 1e-10, 4)])
+def test_cluster_resident_variant_batches(jit_on, qs, c, dtype, tol, cmax):
+    """Variant batches of 12..16-qubit segments run as ONE cluster-resident
+    kernel (each state in the shared memory of a CTA cluster, sweeps as
+    phases separated by cluster barriers): one launch per family, equal to
+    the per-launch kernels and the oracle."""
+    import paper_2603_01443_b200 as cb
+    from paper_2603_01443_b200.engine import simulate_family
+
+    old = _native.get_option("cluster_max")
+    _native.set_option("cluster_max", cmax)
+    try:
+        circ = cb.build_brickwall(cb.BrickwallSpec(2 * qs, 6, 2, c, qs))
+        prep = preprocess(circ, 2)
+        for fam in prep.subs.segments:
+            simulate_family(fam, dtype=dtype)  # compile
+            n0 = _native.launch_count()
+            got = simulate_family(fam, dtype=dtype).cpu().numpy()
+            assert _native.launch_count() - n0 == 1
+            _native.set_option("cluster", 0)
+            try:
+                per_launch = simulate_family(fam, dtype=dtype).cpu().numpy()
+            finally:
+                _native.set_option("cluster", 1)
+            for v in range(fam.num_variants):
+                t = fam.variant_table(v)
+                ref = orc.simulate(qs, t.kinds, t.qa, t.qb, t.params)
+                assert np.abs(got[v] - ref).max() < tol
+            assert np.abs(got - per_launch).max() < tol
+        ref = orc.simulate(2 * qs, circ.kinds, circ.qa, circ.qb, circ.params)
+        assert np.abs(cb.run_cut(circ, 2, dtype=dtype).amps - ref).max() < tol
+    finally:
+        _native.set_option("cluster_max", old)
+
+
+@pytest.mark.gpu
+def test_cluster_resident_uncut_small_states(jit_on):
+    """A single 12..16-qubit simulate() from |0..0> also runs cluster-resident."""
+    import paper_2603_01443_b200 as cb
+
+    for q in (12, 14, 16):
+        circ = cb.build_brickwall(cb.BrickwallSpec(q, 8, 2, 2, q))
+        cb.simulate(circ)
+        n0 = _native.launch_count()
+        got = cb.simulate(circ).amps
+        assert _native.launch_count() - n0 == 1
+        assert np.abs(got - orc.simulate(q, circ.kinds, circ.qa, circ.qb, circ.params)).max() < 1e-10

@@ -94,18 +94,23 @@ def execute_schedule(plan, nq, variant=0):
     return amps
 
 
-@pytest.fixture(params=[(1, 0), (2, 0), (1, 1), (2, 1)],
-                ids=["fuse-complex", "fuse-split-u3", "normalised", "split-normalised"])
+@pytest.fixture(params=[(1, 0, 0), (2, 0, 0), (1, 1, 0), (2, 1, 0), (1, 1, 1)],
+                ids=["fuse-complex", "fuse-split-u3", "normalised", "split-normalised", "normalised-diag-pivot"])
 def fuse_mode(request):
     """The lowerings: fused complex 2x2s (interpreter default), split U3 =
-    phase . Ry . phase with commuted phases, and normalised 2x2s with the
-    deferred diagonals (the specialised-kernel default)."""
-    old = _native.get_option("fuse"), _native.get_option("dense_norm")
+    phase . Ry . phase with commuted phases, normalised 2x2s with the
+    deferred diagonals (the specialised-kernel default), and the param-mode
+    form normalised by the structural (diagonal) pivot (jit_struct)."""
+    keys = ("fuse", "dense_norm", "jit", "jit_struct")
+    old = [_native.get_option(k) for k in keys]
     _native.set_option("fuse", request.param[0])
     _native.set_option("dense_norm", request.param[1])
+    if request.param[2]:
+        _native.set_option("jit", 2)
+        _native.set_option("jit_struct", 2)
     yield request.param
-    _native.set_option("fuse", old[0])
-    _native.set_option("dense_norm", old[1])
+    for k, v in zip(keys, old):
+        _native.set_option(k, v)
 
 
 @pytest.mark.parametrize("tile_bits", [4, 6, 12])
@@ -207,6 +212,38 @@ def test_normalised_dense_ops_have_unit_pivots():
                 unit += 1
     # every row of every dense op but the last (which carries the global scalar)
     assert unit >= 2 * len(dense) - 2
+
+
+def test_diagonal_pivot_keeps_the_structure_of_new_angles():
+    """Param mode (jit_struct) normalises every row by its diagonal entry, so
+    which coefficients are exactly 1 does not depend on the angles: two
+    circuits of one structure (new U3 angles) lower to the same pattern."""
+    circ = G.build_brickwall(G.BrickwallSpec(14, 6, 2, 2, 3))
+    rng = np.random.default_rng(1)
+    p2 = circ.params.copy()
+    u3 = circ.kinds == C.KIND_U3
+    p2[u3] = rng.uniform(0.3, 2.8, size=(int(u3.sum()), 3))
+    circ2 = C.Circuit.from_table(14, C.GateTable(circ.kinds, circ.qa, circ.qb, p2))
+    keys = ("dense_norm", "jit", "jit_struct")
+    old = [_native.get_option(k) for k in keys]
+    try:
+        _native.set_option("dense_norm", 1)
+        _native.set_option("jit", 2)
+        _native.set_option("jit_struct", 2)
+
+        def pattern(c):
+            plan = json.loads(_native.sweep_plan_json(14, c.table))
+            return [(e["type"], tuple(tuple(np.array(e["m"]) == 1.0)), tuple(tuple(np.array(e["m"]) == 0.0)))
+                    for s in plan["sweeps"] for e in s["entries"]], plan
+
+        a, plan = pattern(circ)
+        b, _ = pattern(circ2)
+        assert a == b
+        got = execute_schedule(plan, 14)
+        assert np.abs(got - orc.simulate(14, circ.kinds, circ.qa, circ.qb, circ.params)).max() < 1e-12
+    finally:
+        for k, v in zip(keys, old):
+            _native.set_option(k, v)
 
 
 def test_uncut_q30_schedule_is_compact():
