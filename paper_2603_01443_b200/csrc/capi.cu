@@ -192,12 +192,15 @@ int choose_tile_bits(int nq, int64_t n_states, int tile_bits, int dtype) {
 
 // Cluster size (log2) of the cluster-resident form, 0 = not used: the NVRTC
 // kernels must be on, the state 2^12..2^16 amplitudes, and a CTA's chunk
-// plus its transpose scratch within 128 KiB (T <= 12 for complex128, 13 for
+// plus its transpose scratch within 64 KiB (T <= 11 for complex128, 12 for
 // complex64). Clusters as large as cluster_max allows while the batch's CTAs
 // still fit the chip once (more CTAs per state = more SMs on the FP64 work).
 int choose_cluster_bits(int nq, int64_t n_states, int dtype) {
   if (!g_opt.cluster || g_opt.jit == 0 || g_opt.engine != 1 || nq < 12 || nq > 16) return 0;
-  const int tmax = dtype == CS_C128 ? 12 : 13;
+  // chunks of 2^11 amplitudes (32 KiB complex128: 8 amplitudes per thread,
+  // 128 registers); 2^12-amplitude chunks (16 per thread, ~220 registers,
+  // one 8-warp CTA per SM) measured 2-3x slower than the per-launch kernels
+  const int tmax = dtype == CS_C128 ? 11 : 12;
   int cmax = 0;
   while ((int64_t(2) << cmax) <= g_opt.cluster_max) ++cmax;  // log2(cluster_max)
   int want = 0;

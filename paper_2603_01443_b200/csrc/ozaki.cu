@@ -494,6 +494,11 @@ __global__ void __launch_bounds__(oz_threads<UNIT>(), UNIT ? 2 : 1) ozaki_merge_
 #pragma unroll
         for (int j = 0; j < 8; ++j) asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(src + j * p.W));
       }
+      // the 8 row scales of this warp's h rows, fetched before the wait so
+      // their load latency hides under the MMA instead of the epilogue
+      double sbv[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) sbv[j] = __ldg(p.sb + hb * kHB + hl_base + j);
       mbar_wait(tfull + g, n & 1);
       ++n;
       tc_after_sync();
@@ -513,10 +518,9 @@ __global__ void __launch_bounds__(oz_threads<UNIT>(), UNIT ? 2 : 1) ozaki_merge_
         }
         const int hl0 = hl_base + 4 * hc;
         double2* dst = p.out + (hb * kHB + hl0) * p.W + l;
-        const double* sbp = p.sb + hb * kHB + hl0;
 #pragma unroll
         for (int j = 0; j < 4; ++j, dst += p.W) {
-          const double s = sl * __ldg(sbp + j);
+          const double s = sl * sbv[4 * hc + j];
           double v2[2];
 #pragma unroll
           for (int v = 0; v < 2; ++v) {

@@ -106,8 +106,15 @@ def _cut_once(circuit: Circuit, n: int, *, max_qubits: int, deadline: float | No
         from .engine import StateVec
 
         states = []
-        for fam in subs.segments:
-            batch = simulate_family(fam, deadline=deadline, max_qubits=max_qubits)
+        if deadline is None:
+            # every family in one batched launch sequence, families concurrently
+            # on side streams (pipeline.simulate_families)
+            from .pipeline import simulate_families
+
+            batches = simulate_families(subs.segments, max_qubits=max_qubits)
+        else:
+            batches = [simulate_family(fam, deadline=deadline, max_qubits=max_qubits) for fam in subs.segments]
+        for fam, batch in zip(subs.segments, batches):
             states.append([StateVec(fam.num_qubits, device=batch[v]) for v in range(fam.num_variants)])
     else:
         states = [[simulate(c, max_qubits=max_qubits, deadline=deadline) for c in fam.circuits]

@@ -65,10 +65,20 @@ class ChainSpec:
         return np.array([COEFF_TERM0.real, COEFF_TERM0.imag, COEFF_TERM1.real, COEFF_TERM1.imag])
 
     def plan(self, dtype=np.complex128, force_bond: int = -1):
-        """(workspace_bytes, bond, q_low) — host-only."""
-        return _native.chain_plan(self.n, self.seg_nq, self.seg_ncuts, self.seg_cut_ids, self.c_total,
-                                  self.cut_boundary, self.term_coef(), force_bond,
-                                  _device.code_of(dtype))
+        """(workspace_bytes, bond, q_low) — host-only; memoised per spec
+        (the spec is an immutable value)."""
+        key = (np.dtype(dtype).str, force_bond)
+        got = _CHAIN_PLANS.get((self, key))
+        if got is None:
+            got = _native.chain_plan(self.n, self.seg_nq, self.seg_ncuts, self.seg_cut_ids, self.c_total,
+                                     self.cut_boundary, self.term_coef(), force_bond, _device.code_of(dtype))
+            if len(_CHAIN_PLANS) > 4096:
+                _CHAIN_PLANS.clear()
+            _CHAIN_PLANS[(self, key)] = got
+        return got
+
+
+_CHAIN_PLANS: dict = {}
 
 
 @dataclass
@@ -118,9 +128,13 @@ def merge_input_from(subcircuits, states: list[list[StateVec]]) -> MergeInput:
     plan = subcircuits.plan
     chain = None
     # the chain plan is valid only for the decomposition's own table/coefficients
-    if (np.array_equal(subcircuits.merge_table, merge_table_of(plan))
-            and np.array_equal(subcircuits.coeffs, coefficients_of(plan.c_total))):
-        chain = ChainSpec.from_plan(plan)
+    # (the canonical ones are memoised on the plan: the comparison is cheap)
+    canon = getattr(plan, "_canonical", None)
+    if canon is None:
+        canon = (merge_table_of(plan), coefficients_of(plan.c_total), ChainSpec.from_plan(plan))
+        object.__setattr__(plan, "_canonical", canon)
+    if np.array_equal(subcircuits.merge_table, canon[0]) and np.array_equal(subcircuits.coeffs, canon[1]):
+        chain = canon[2]
     return MergeInput(
         segment_states=states,
         coeffs=subcircuits.coeffs,

@@ -53,12 +53,16 @@ def preprocess(circuit: Circuit, n: int) -> Prepared:
 
 
 def simulate_segments(prep: Prepared, *, dtype=np.complex128, max_qubits=DEFAULT_MAX_QUBITS):
-    """Device batches [2^{c_i}, 2^{q_i}] of every segment's variants (t_sub).
+    """Device batches [2^{c_i}, 2^{q_i}] of every segment's variants (t_sub)."""
+    return simulate_families(prep.subs.segments, dtype=dtype, max_qubits=max_qubits)
+
+
+def simulate_families(fams, *, dtype=np.complex128, max_qubits=DEFAULT_MAX_QUBITS):
+    """Device batches [2^{c_i}, 2^{q_i}] of the given segment families.
 
     Segments are independent, so each family runs on its own side stream
     (forked from and joined back into the current stream): the short,
     latency-bound sweep chains of different segments overlap on the GPU."""
-    fams = prep.subs.segments
     if len(fams) == 1:
         return [simulate_family(fams[0], dtype=dtype, max_qubits=max_qubits)]
     t = _device.torch()

@@ -267,8 +267,10 @@ def test_cluster_resident_variant_batches(jit_on, qs, c, dtype, tol, cmax):
                 ref = orc.simulate(qs, t.kinds, t.qa, t.qb, t.params)
                 assert np.abs(got[v] - ref).max() < tol
             assert np.abs(got - per_launch).max() < tol
-        ref = orc.simulate(2 * qs, circ.kinds, circ.qa, circ.qb, circ.params)
-        assert np.abs(cb.run_cut(circ, 2, dtype=dtype).amps - ref).max() < tol
+        from paper_2603_01443_b200 import engine
+
+        cut = cb.run_cut(circ, 2, dtype=dtype, max_qubits=32)
+        assert engine.max_abs_diff(cut, cb.simulate(circ, dtype=dtype, max_qubits=32)) < tol
     finally:
         _native.set_option("cluster_max", old)
 
