@@ -237,8 +237,8 @@ def test_tiered_jit_runs_interpreter_then_compiled_kernels():
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("qs,c,dtype,tol,cmax", [(12, 2, np.complex128, 1e-10, 16), (15, 2, np.complex128, 1e-10, 16),
-                                                  (15, 4, np.complex128, 1e-10, 8), (16, 2, np.complex128, 1e-10, 16),
-                                                  (13, 3, np.complex64, 1e-5, 16), (14, 6, np.complex128, 1e-10, 4)])
+                                                  (15, 4, np.complex128, 1e-10, 16), (16, 2, np.complex64, 1e-5, 16),
+                                                  (13, 3, np.complex64, 1e-5, 16), (14, 6, np.complex128, 1e-10, 8)])
 def test_cluster_resident_variant_batches(jit_on, qs, c, dtype, tol, cmax):
     """Variant batches of 12..16-qubit segments run as ONE cluster-resident
     kernel (each state in the shared memory of a CTA cluster, sweeps as

@@ -12,6 +12,8 @@ import paper_2603_01443_b200 as cb  # noqa: E402
 from paper_2603_01443_b200 import _native  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "cfg4a"
+if len(sys.argv) > 2:
+    _native.set_option("reg_bits", int(sys.argv[2]))
 _native.set_option("jit", 2)
 spec = cb.BASELINE_CONFIGS[name]
 circ = cb.build_brickwall(spec)
@@ -28,5 +30,5 @@ for cl, cmax in ((0, 16), (1, 4), (1, 8), (1, 16)):
         ts.append(evs[0].elapsed_time(evs[1]) * 1e3)
     n0 = _native.launch_count()
     cb.run_cut(circ, spec.n, out=out, max_qubits=spec.q)
-    print(f"{name} cluster={cl} cluster_max={cmax}: variant stage median {np.median(ts):.1f} us "
+    print(f"{name} reg_bits={_native.get_option('reg_bits')} cluster={cl} cluster_max={cmax}: variant stage median {np.median(ts):.1f} us "
           f"(min {min(ts):.1f}), launches/step {_native.launch_count() - n0}", flush=True)
