@@ -22,14 +22,21 @@ def torch():
     return _torch
 
 
+_CUDA_OK = False
+
+
 def require_cuda():
+    global _CUDA_OK
     t = torch()
+    if _CUDA_OK:  # a visible device stays visible for the life of the process
+        return t
     if not t.cuda.is_available():
         raise NativeUnavailableError(
             "no CUDA device is visible; the cut pipeline runs only on the sm_100a kernels "
             "(there is no CPU fallback)"
         )
     _native.load()
+    _CUDA_OK = True
     return t
 
 
@@ -48,9 +55,12 @@ def torch_dtype(dtype):
 
 
 def stream_ptr(stream=None) -> int:
+    if stream is not None:
+        return int(stream.cuda_stream)
+    # torch's current stream of the current device without building a Stream
+    # object (the API path calls this per native call)
     t = torch()
-    s = stream if stream is not None else t.cuda.current_stream()
-    return int(s.cuda_stream)
+    return int(t._C._cuda_getCurrentRawStream(t._C._cuda_getDevice()))
 
 
 _TOTAL = {}

@@ -255,7 +255,7 @@ class SegmentFamily:
         sequence (`simulate_batch`) and each variant's state is handed out
         once, as a row of that batch (so merge() reads the batch in place);
         asking for a variant again starts a new pass — every call returns a
-        fresh state, as the reference's simulate() does."""
+        fresh state, as the reference's simulate() does. Returns (batch, b)."""
         key = np.dtype(dtype).str
         batch, left = self._pending.get(key, (None, None))
         if batch is None or b not in left:
@@ -266,7 +266,7 @@ class SegmentFamily:
             self._pending[key] = (batch, left)
         else:
             self._pending.pop(key, None)
-        return batch[b]
+        return batch, b
 
     @property
     def num_cuts(self) -> int:
@@ -390,6 +390,17 @@ def _segment_family(circuit: Circuit, plan: CutPlan, seg: int, cut_pos: np.ndarr
                          np.array(patch, dtype=np.int64), tuple(adj))
 
 
+def _canonical_tables(plan: CutPlan):
+    """Fresh copies of the plan's merge table and coefficients (callers may
+    mutate a SubcircuitSet's arrays); the originals are computed once per plan
+    and kept on it (merging.merge_input_from compares against them)."""
+    canon = getattr(plan, "_canonical_tc", None)
+    if canon is None:
+        canon = (merge_table_of(plan), coefficients_of(plan.c_total))
+        object.__setattr__(plan, "_canonical_tc", canon)
+    return canon[0].copy(), canon[1].copy()
+
+
 def merge_table_of(plan: CutPlan) -> np.ndarray:
     ms = np.arange(1 << plan.c_total, dtype=np.int64)
     table = np.zeros((plan.n, ms.size), dtype=np.int64)
@@ -428,11 +439,12 @@ def decompose(circuit: Circuit, plan: CutPlan) -> SubcircuitSet:
         if nt is not None and [int(v) for v in nt[0][:, 0]] != [bg.position for bg in plan.boundary_gates]:
             nt = None  # a plan that is not this circuit's own: follow it literally
     if nt is not None:
-        return SubcircuitSet(plan, _families_from_tables(plan, nt), merge_table_of(plan),
-                             coefficients_of(plan.c_total))
+        table, coeffs = _canonical_tables(plan)
+        return SubcircuitSet(plan, _families_from_tables(plan, nt), table, coeffs)
     cut_pos = np.array([bg.position for bg in plan.boundary_gates], dtype=np.int64)
     owner = seg_of[circuit.qa] if circuit.gate_count else np.zeros(0, np.int64)
     owner = owner.copy()
     owner[cut_pos] = -1
     segments = [_segment_family(circuit, plan, seg, cut_pos, owner) for seg in range(plan.n)]
-    return SubcircuitSet(plan, segments, merge_table_of(plan), coefficients_of(plan.c_total))
+    table, coeffs = _canonical_tables(plan)
+    return SubcircuitSet(plan, segments, table, coeffs)

@@ -39,11 +39,12 @@ class StateVec:
     take the device tensor (uploading the host array when it is newer).
     """
 
-    __slots__ = ("num_qubits", "_host", "_dev", "_owner", "dtype", "_keep")
+    __slots__ = ("num_qubits", "_host", "_dev", "_owner", "dtype", "_keep", "_row_of")
 
-    def __init__(self, num_qubits: int, amps=None, *, device=None, dtype=None):
+    def __init__(self, num_qubits: int, amps=None, *, device=None, dtype=None, row_of=None):
         self.num_qubits = int(num_qubits)
         self._keep = None
+        self._row_of = row_of  # (family batch, row) when device is that batch's row
         n = 1 << self.num_qubits
         if device is not None:
             if amps is not None:
@@ -116,6 +117,10 @@ class StateVec:
                 and self._host.flags.c_contiguous:
             _device.to_host(self._dev, out=self._host)
             self._owner = "both"
+
+    def on_device_only(self) -> bool:
+        """The device tensor is the current copy (no newer host amplitudes)."""
+        return self._owner in ("device", "both")
 
     @property
     def on_device(self) -> bool:
@@ -208,8 +213,8 @@ def simulate(circuit: Circuit, *, max_qubits: int = DEFAULT_MAX_QUBITS, deadline
     origin = getattr(circuit, "_origin", None)
     if origin is not None and deadline is None:
         fam, b = origin
-        row = fam.claim_state(b, dtype, lambda: simulate_family(fam, dtype=dtype, max_qubits=max_qubits))
-        return StateVec(circuit.num_qubits, device=row)
+        batch, row = fam.claim_state(b, dtype, lambda: simulate_family(fam, dtype=dtype, max_qubits=max_qubits))
+        return StateVec(circuit.num_qubits, device=batch[row], row_of=(batch, row))
     states = simulate_table(circuit.num_qubits, circuit.table, deadline=deadline, dtype=dtype)
     return StateVec(circuit.num_qubits, device=states[0])
 

@@ -115,7 +115,8 @@ def _cut_once(circuit: Circuit, n: int, *, max_qubits: int, deadline: float | No
         else:
             batches = [simulate_family(fam, deadline=deadline, max_qubits=max_qubits) for fam in subs.segments]
         for fam, batch in zip(subs.segments, batches):
-            states.append([StateVec(fam.num_qubits, device=batch[v]) for v in range(fam.num_variants)])
+            states.append([StateVec(fam.num_qubits, device=batch[v], row_of=(batch, v))
+                           for v in range(fam.num_variants)])
     else:
         states = [[simulate(c, max_qubits=max_qubits, deadline=deadline) for c in fam.circuits]
                   for fam in subs.segments]

@@ -129,12 +129,15 @@ def merge_input_from(subcircuits, states: list[list[StateVec]]) -> MergeInput:
     chain = None
     # the chain plan is valid only for the decomposition's own table/coefficients
     # (the canonical ones are memoised on the plan: the comparison is cheap)
-    canon = getattr(plan, "_canonical", None)
-    if canon is None:
-        canon = (merge_table_of(plan), coefficients_of(plan.c_total), ChainSpec.from_plan(plan))
-        object.__setattr__(plan, "_canonical", canon)
-    if np.array_equal(subcircuits.merge_table, canon[0]) and np.array_equal(subcircuits.coeffs, canon[1]):
-        chain = canon[2]
+    tc = getattr(plan, "_canonical_tc", None)
+    if tc is None:
+        tc = (merge_table_of(plan), coefficients_of(plan.c_total))
+        object.__setattr__(plan, "_canonical_tc", tc)
+    if np.array_equal(subcircuits.merge_table, tc[0]) and np.array_equal(subcircuits.coeffs, tc[1]):
+        chain = getattr(plan, "_chain_spec", None)
+        if chain is None:
+            chain = ChainSpec.from_plan(plan)
+            object.__setattr__(plan, "_chain_spec", chain)
     return MergeInput(
         segment_states=states,
         coeffs=subcircuits.coeffs,
@@ -153,6 +156,14 @@ def segment_batch(states: list[StateVec], dtype):
     place; anything else is stacked."""
     t = _device.torch()
     tdt = _device.torch_dtype(dtype)
+    # states handed out as the rows of one family batch (engine.simulate of
+    # decompose()'s variants, harness._cut_once) carry that batch: use it as is
+    rows = [getattr(sv, "_row_of", None) for sv in states]
+    b0 = rows[0][0] if rows[0] is not None else None
+    if (b0 is not None and b0.dtype == tdt and b0.shape[0] == len(states)
+            and all(r is not None and r[0] is b0 and r[1] == i and sv.on_device_only()
+                    for i, (r, sv) in enumerate(zip(rows, states)))):
+        return b0
     devs = [sv.device_tensor() for sv in states]
     n = 1 << states[0].num_qubits
     first = devs[0]

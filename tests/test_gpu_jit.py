@@ -277,10 +277,11 @@ def test_cluster_resident_variant_batches(jit_on, qs, c, dtype, tol, cmax):
 
 @pytest.mark.gpu
 def test_cluster_resident_uncut_small_states(jit_on):
-    """A single 12..16-qubit simulate() from |0..0> also runs cluster-resident."""
+    """A single 12..15-qubit simulate() from |0..0> also runs cluster-resident
+    (2^11-amplitude chunks: up to 16 CTAs per cluster)."""
     import paper_2603_01443_b200 as cb
 
-    for q in (12, 14, 16):
+    for q in (12, 14, 15):
         circ = cb.build_brickwall(cb.BrickwallSpec(q, 8, 2, 2, q))
         cb.simulate(circ)
         n0 = _native.launch_count()
