@@ -282,7 +282,7 @@ def test_cluster_resident_uncut_small_states(jit_on):
     import paper_2603_01443_b200 as cb
 
     for q in (12, 14, 15):
-        circ = cb.build_brickwall(cb.BrickwallSpec(q, 8, 2, 2, q))
+        circ = cb.build_brickwall(cb.BrickwallSpec(q, 8, 3 if q % 2 else 2, 2, q))
         cb.simulate(circ)
         n0 = _native.launch_count()
         got = cb.simulate(circ).amps
