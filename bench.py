@@ -522,8 +522,19 @@ def run_ours(args):
             # the e2e result is the same state: check the sampled amplitudes too
             host_np = host.numpy()
             e2e_parity = float(np.abs(host_np[idx] - got).max())
-            del hws
             d2h_gbs = pinned_d2h_gbs(torch, host, total, stream)
+            del host, host_np
+            # the reference returns a plain (pageable) numpy array: the same
+            # call into one (informational; its D2H goes through the driver's
+            # staging buffers)
+            pageable = np.empty(total, dtype=np.complex128)
+            pageable[:: 1 << 16] = 0  # touch a few pages; the copy faults in the rest
+            t0 = time.perf_counter()
+            run_cut_to_host(circ, n, pageable, workspace=hws, max_qubits=q)
+            torch.cuda.synchronize()
+            t_pageable = time.perf_counter() - t0
+            pageable_parity = float(np.abs(pageable[idx] - got).max())
+            del pageable, hws
             e2e = {"value": total / t_e2e, "unit": UNIT, "h2d_bytes_per_step": g_bytes,
                    "d2h_bytes_per_step": total * 16, "ms_per_step": t_e2e * 1e3, "steps": e_steps,
                    "path": "run_cut_to_host -> cs_cut_run_to_host (C-ABI, host buffer): chunked merge "
@@ -531,8 +542,11 @@ def run_ours(args):
                    "bound": {"kind": "pcie_d2h", "measured_copy_gbs": d2h_gbs,
                              "achieved_gbs": total * 16 / t_e2e / 1e9,
                              "frac": total * 16 / t_e2e / 1e9 / d2h_gbs},
-                   "max_abs_vs_device_result": e2e_parity}
-            del host
+                   "max_abs_vs_device_result": e2e_parity,
+                   "pageable_numpy": {"ms": t_pageable * 1e3, "value": total / t_pageable,
+                                      "max_abs_vs_device_result": pageable_parity,
+                                      "note": "one call into a freshly allocated pageable numpy array (the "
+                                              "reference's return type), first-touch page faults included"}}
         elif world > 1:
             ews = torch.empty(max(shard_workspace_bytes(circ, n, world), 1), dtype=torch.uint8, device="cuda")
             host = torch.empty(end - begin, dtype=torch.complex128, pin_memory=True)
