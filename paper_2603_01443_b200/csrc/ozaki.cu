@@ -525,17 +525,26 @@ __global__ void __launch_bounds__(oz_threads<UNIT>(), UNIT ? 2 : 1) ozaki_merge_
 #pragma unroll
           for (int v = 0; v < 2; ++v) {
             const int c = 2 * j + v;
+            // q0, q1 are produced with the int64 -> double bias 0x4338000000000000
+            // (1.5 * 2^52) already folded into the 64-bit addend of the
+            // IMAD.WIDE: bias_ext(x) = 2^32 (0x43380000 + (x >> 31)) + (uint32)x
+            // = bias + sign-extended x, one IADD3 (+ SHF) for the high word
+            // instead of a separate 64-bit add per value
+            auto bias_ext = [](int x) {
+              const unsigned hi = unsigned(x >> 31) + 0x43380000u;
+              return static_cast<long long>((static_cast<unsigned long long>(hi) << 32) | unsigned(x));
+            };
             long long q0, q1;
             if constexpr (kDigitBits == 8) {
               // base 256, 7 diagonals (|D_p| < 2^24): Q0 = D_0 2^24 + D_1 2^16
               // + D_2 2^8 + D_3, Q1 = D_4 2^16 + D_5 2^8 + D_6 (|Q0| < 2^49,
               // |Q1| < 2^41: exact in int64 and in a double); product =
               // 2^-38 (Q0 + 2^-24 Q1) sa sb
-              const long long a0 = (static_cast<long long>(int(d[hc][0][c])) << 8) + int(d[hc][1][c]);
-              const long long a1 = (static_cast<long long>(int(d[hc][2][c])) << 8) + int(d[hc][3][c]);
-              const long long a2 = (static_cast<long long>(int(d[hc][4][c])) << 8) + int(d[hc][5][c]);
-              q0 = (a0 << 16) + a1;
-              q1 = (a2 << 8) + int(d[hc][6][c]);
+              const long long a0 = static_cast<long long>(int(d[hc][0][c])) * 256 + int(d[hc][1][c]);
+              const long long a1 = static_cast<long long>(int(d[hc][2][c])) * 256 + int(d[hc][3][c]);
+              const long long a2 = static_cast<long long>(int(d[hc][4][c])) * 256 + int(d[hc][5][c]);
+              q0 = a0 * 65536 + a1 + 0x4338000000000000LL;
+              q1 = a2 * 256 + bias_ext(int(d[hc][6][c]));
             } else {
               // base 128, 8 diagonals: P_m = 128 D_2m + D_2m+1 (|D_p| < 2^23:
               // exact in int32), Q0 = 2^14 P_0 + P_1, Q1 = 2^14 P_2 + P_3;
@@ -544,12 +553,12 @@ __global__ void __launch_bounds__(oz_threads<UNIT>(), UNIT ? 2 : 1) ozaki_merge_
               const int p1 = int(d[hc][2][c]) * 128 + int(d[hc][3][c]);
               const int p2 = int(d[hc][4][c]) * 128 + int(d[hc][5][c]);
               const int p3 = int(d[hc][kSlices - 2][c]) * 128 + int(d[hc][kSlices - 1][c]);
-              q0 = (static_cast<long long>(p0) << 14) + p1;
-              q1 = (static_cast<long long>(p2) << 14) + p3;
+              q0 = static_cast<long long>(p0) * 16384 + bias_ext(p1);
+              q1 = static_cast<long long>(p2) * 16384 + bias_ext(p3);
             }
-            // int64 -> double with the 1.5 * 2^52 bias (|q| < 2^51)
-            const double f0 = __longlong_as_double(q0 + 0x4338000000000000LL) - 0x1.8p52;
-            const double f1 = __longlong_as_double(q1 + 0x4338000000000000LL) - 0x1.8p52;
+            // int64 -> double: the bias is in q already (|q - bias| < 2^51)
+            const double f0 = __longlong_as_double(q0) - 0x1.8p52;
+            const double f1 = __longlong_as_double(q1) - 0x1.8p52;
             v2[v] = fma(f1, kDigitBits == 8 ? 0x1p-24 : 0x1p-28, f0) * s;
           }
           double2 val = make_double2(v2[0], v2[1]);
