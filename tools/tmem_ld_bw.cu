@@ -142,8 +142,9 @@ void run(int warps, int sms) {
   double avg = 0;
   for (int i = 0; i < sms; ++i) avg += double(h[i]);
   avg /= sms;
-  const int bytes_per_ld = MODE == 1 ? 16 * 32 * 4 * 2 : (MODE == 2 ? 32 * 32 * 16 : 32 * 32 * MODE);
-  // 16x256b.x4: 16 lanes x 256 bit x 4 = 2 KiB per warp instruction
+  // 32x32b.xN: 32 lanes x N columns x 4 B per warp instruction; 16x256b.x4:
+  // 16 lanes x 32 B x 4 = 2 KiB; mode 2: two 32x32b.x8 per wait
+  const int bytes_per_ld = MODE == 1 ? 16 * 32 * 4 : (MODE == 2 ? 32 * 4 * 16 : 32 * 4 * MODE);
   const double bytes = double(bytes_per_ld) * rounds * warps;
   printf("mode %-3d warps %2d  %8.1f cycles  %7.1f B/cycle/SM\n", MODE, warps, avg, bytes / avg);
   free(h);
