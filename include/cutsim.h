@@ -66,7 +66,9 @@ int cs_device_count(int32_t* count);
  * "jit_units_compiled" / "jit_units_reused" (read-only counters),
  * "merge_ozaki" (int8 tcgen05 tensor-core merge with exact FP64 splitting
  * for one-slot products of K >= "merge_ozaki_min_k" terms, lo_len % 128 == 0,
- * row ranges % 16 == 0; default 1, min K 16), "merge_ozaki_digits" (7: 8
+ * row ranges % 16 == 0, outputs * K >= 2^"merge_ozaki_min_work" (default
+ * 27: smaller products run faster on the FP64 kernels); default 1, min K
+ * 16), "merge_ozaki_digits" (7: 8
  * balanced base-128 digits per operand, 8 int32 diagonals per output,
  * truncation ~6e-16 of max|a| max|b| — default; 8: 7 base-256 digits, 7
  * diagonals, ~1e-15, 3-4 % faster at K <= 32), "cluster" (cluster-resident
@@ -106,6 +108,19 @@ int cs_sim_batch(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int6
                  const double* params, const int32_t* slots, int64_t n_gates, void* states,
                  int64_t n_states, int64_t state_stride, uint64_t variant_base, int32_t init_zero,
                  int32_t dtype, void* stream);
+
+/* Every segment family of one decomposition in ONE call: family f has
+ * nq[f] qubits, gate_count[f] consecutive rows of the concatenated tables
+ * (kinds/qa/qb/params/slots, the layout cs_cut_tables writes) and
+ * n_states[f] variant states (variant ids 0..n_states[f]-1, contiguous at
+ * states[f], stride 2^nq[f]), all started from |0..0>. Families run
+ * concurrently on the library's side streams forked from / joined into
+ * `stream`. Replaces the per-variant simulate() loop of the reference's
+ * harness (harness.py:136-139) for a whole SubcircuitSet
+ * (pipeline.simulate_families). */
+int cs_sim_families(int32_t n_fam, const int32_t* nq, const int64_t* gate_count, const uint8_t* kinds,
+                    const int64_t* qa, const int64_t* qb, const double* params, const int32_t* slots,
+                    void* const* states, const int64_t* n_states, int32_t dtype, void* stream);
 
 /* cs_sim_batch with a cooperative budget (the reference's `deadline`,
  * engine.py:142-155): deadline_s is CLOCK_MONOTONIC seconds (Python's

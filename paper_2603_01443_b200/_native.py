@@ -50,6 +50,7 @@ SIGNATURES = {
     "cs_launch_count": (_i64, []),
     "cs_jit_wait": (ctypes.c_int, [ctypes.c_double]),
     "cs_init_basis": (ctypes.c_int, [_vp, _i32, _i64, _i64, _i32, _vp]),
+    "cs_sim_families": (ctypes.c_int, [_i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp]),
     "cs_sim_batch": (ctypes.c_int, [_i32, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _i64, _i64, _u64, _i32,
                                     _i32, _vp]),
     "cs_sim_batch_until": (ctypes.c_int, [_i32, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _i64, _i64, _u64, _i32,
@@ -247,7 +248,7 @@ def cut_tables(nq, table, sizes):
     k, qa, qb, prm = _table_args(table)
     sz = c_i32(sizes)
     n = len(sz)
-    n2 = int(np.count_nonzero((k == 5) | (k == 6)))
+    n2 = int(np.count_nonzero(k >= 5))  # CX = 5, CZ = 6, U3 = 7 (a bound is enough)
     gcap = len(k) + 4 * n2 + 1
     ccap = n2 + 1
     cuts = np.empty((ccap, 4), np.int64)

@@ -185,6 +185,14 @@ class GateTable:
         if not (self.qa.shape[0] == g and self.qb.shape[0] == g):
             raise ValidationError("gate table columns differ in length")
 
+    @classmethod
+    def trusted(cls, kinds, qa, qb, params) -> "GateTable":
+        """Columns already of the kernel dtypes, contiguous and equally long
+        (the C++ planner's output): no conversion pass."""
+        t = cls.__new__(cls)
+        t.kinds, t.qa, t.qb, t.params = kinds, qa, qb, params
+        return t
+
     def __len__(self) -> int:
         return int(self.kinds.shape[0])
 

@@ -8,6 +8,10 @@
 #include <deque>
 #include <thread>
 #include <chrono>
+#include <cstdlib>
+#include <csignal>
+#include <execinfo.h>
+#include <unistd.h>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -55,6 +59,24 @@ using namespace cutsim;
 
 namespace {
 
+// Debug aid (env CUTSIM_SEGV_TRACE=1 at load): a SIGSEGV prints the native
+// backtrace of the faulting thread to stderr before the default action.
+void segv_trace(int sig) {
+  void* fr[64];
+  const int n = backtrace(fr, 64);
+  const char msg[] = "libcutsim: fatal signal, native backtrace:\n";
+  (void)!write(2, msg, sizeof msg - 1);
+  backtrace_symbols_fd(fr, n, 2);
+  signal(sig, SIG_DFL);
+  raise(sig);
+}
+struct SegvTraceInstaller {
+  SegvTraceInstaller() {
+    const char* e = std::getenv("CUTSIM_SEGV_TRACE");
+    if (e && *e == '1') signal(SIGSEGV, segv_trace);
+  }
+} g_segv_trace_installer;
+
 thread_local std::string g_err;
 std::atomic<int64_t> g_launches{0};
 
@@ -75,6 +97,7 @@ struct Options {
   int64_t zero_start_tiles = 1;   // from |0..0>: zero the states once, launch only the tiles that can be non-zero
   int64_t merge_ozaki = 1;        // int8 tcgen05 merge (exact FP64 splitting) for K >= merge_ozaki_min_k
   int64_t merge_ozaki_min_k = 16;
+  int64_t merge_ozaki_min_work = 27;  // log2 of outputs * K below which the FP64 kernels run
   int64_t merge_ozaki_digits = 7;  // digit bits of the int8 merge: 7 (8 slices, default) or 8 (7 slices: 3-4 % faster at K <= 32, 2x the truncation)
   int64_t engine = 1;      // 1: register-tile kernel (rsweep), 0: shared-memory tile kernel (sweep)
   int64_t jit = 0;         // 0 never, 1 from a program's 2nd use, 2 always (compile on first use, blocking),
@@ -378,8 +401,13 @@ bool dmma3_eligible(int K, int dtype, int64_t lo_len) {
 }
 
 // merge_ozaki: the int8 tcgen05 kernel (ozaki.cu) for K >= merge_ozaki_min_k
+// and the product is big enough to amortise its two digit-prep launches:
+// outputs * K >= 2^merge_ozaki_min_work (tools/merge_small_q.py: at 2^20
+// outputs the FP64 kernels win every K <= 64, at 2^22 K <= 16, from 2^24 on
+// the int8 kernel wins from K = 16)
 bool ozaki_eligible(int K, int dtype, int64_t lo_len, int64_t nrows) {
   return g_opt.merge_ozaki && dtype == CS_C128 && K >= g_opt.merge_ozaki_min_k &&
+         double(nrows) * double(lo_len) * double(K) >= std::ldexp(1.0, int(g_opt.merge_ozaki_min_work)) &&
          merge_ozaki_supported(K, lo_len, nrows);
 }
 
@@ -643,6 +671,7 @@ struct JitQueue {
   std::deque<std::pair<std::shared_ptr<const Program>, int>> q;
   int busy = 0;
   bool started = false;
+  bool stopping = false;  // process exit: no new jobs (drain_jit_queue)
 };
 // never destroyed: the detached worker waits on cv for the life of the
 // process, and destroying a condition variable with a waiter blocks exit
@@ -654,7 +683,8 @@ void jit_worker(int device) {
     std::pair<std::shared_ptr<const Program>, int> job;
     {
       std::unique_lock<std::mutex> lk(g_jitq.mu);
-      g_jitq.cv.wait(lk, [] { return !g_jitq.q.empty(); });
+      g_jitq.cv.wait(lk, [] { return !g_jitq.q.empty() || g_jitq.stopping; });
+      if (g_jitq.stopping) return;
       job = std::move(g_jitq.q.front());
       g_jitq.q.pop_front();
       ++g_jitq.busy;
@@ -669,11 +699,29 @@ void jit_worker(int device) {
   }
 }
 
+// At process exit: drop the queued programs and wait for the one being
+// compiled, so the worker never runs inside (or after) the destruction of
+// the unit cache, NVRTC and the CUDA context it uses — a process that exited
+// mid-compile crashed inside nvrtcCompileProgram (CUTSIM_SEGV_TRACE
+// backtrace). Exit handlers and library destructors run in reverse order of
+// registration, so this is registered after NVRTC (and the builtins library
+// its first compile loads) is loaded: jit_warm_nvrtc() first.
+void drain_jit_queue() {
+  std::unique_lock<std::mutex> lk(g_jitq.mu);
+  g_jitq.q.clear();
+  g_jitq.stopping = true;
+  g_jitq.cv.notify_all();
+  g_jitq.idle_cv.wait_for(lk, std::chrono::seconds(60), [] { return g_jitq.busy == 0; });
+}
+
 void enqueue_jit(std::shared_ptr<const Program> prog, int dtype) {
   std::lock_guard<std::mutex> lk(g_jitq.mu);
+  if (g_jitq.stopping) return;
   if (!g_jitq.started) {
     int dev = 0;
     cudaGetDevice(&dev);
+    jit_warm_nvrtc();  // once per process, ~0.1 s: see drain_jit_queue
+    std::atexit(drain_jit_queue);
     std::thread(jit_worker, dev).detach();
     g_jitq.started = true;
   }
@@ -739,14 +787,18 @@ int run_program(const std::shared_ptr<const Program>& prog_ptr, int nq, void* st
   if (jit && jit->cluster > 0 && jit->units[0] && deadline_s <= 0.0) {
     // the cluster-resident kernel: one launch, one cluster of jit->cluster
     // CTAs per state (blockIdx.y = variant), the whole program in DSMEM
-    const JitUnit* ju = jit->units[0].get();
+    JitUnit* ju = jit->units[0].get();
     int dev = 0;
     cudaGetDevice(&dev);
-    cudaError_t e = cudaKernelSetAttributeForDevice(ju->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                    int(ju->smem), dev);
-    if (e == cudaSuccess && jit->cluster > 8)
-      e = cudaKernelSetAttributeForDevice(ju->kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1, dev);
-    if (e != cudaSuccess) return cuda_fail(e, "cluster kernel attributes");
+    cudaError_t e = cudaSuccess;
+    const uint64_t bit = uint64_t(1) << (dev & 63);
+    if (!(ju->attrs_set.load(std::memory_order_relaxed) & bit)) {
+      e = cudaKernelSetAttributeForDevice(ju->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ju->smem), dev);
+      if (e == cudaSuccess && jit->cluster > 8)
+        e = cudaKernelSetAttributeForDevice(ju->kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1, dev);
+      if (e != cudaSuccess) return cuda_fail(e, "cluster kernel attributes");
+      ju->attrs_set.fetch_or(bit);
+    }
     const std::vector<unsigned char>& blob = jit->blobs[0];
     for (int64_t v0 = 0; v0 < n_states; v0 += 65535) {
       const int64_t vc = std::min<int64_t>(65535, n_states - v0);
@@ -765,8 +817,8 @@ int run_program(const std::shared_ptr<const Program>& prog_ptr, int nq, void* st
     return CS_OK;
   }
   for (const Launch& ln : prog->launches) {
-    const JitUnit* jk = (jit && jit->cluster == 0 && li < jit->units.size() && jit->units[li])
-                            ? jit->units[li].get() : nullptr;
+    JitUnit* jk = (jit && jit->cluster == 0 && li < jit->units.size() && jit->units[li])
+                      ? jit->units[li].get() : nullptr;
     const std::vector<unsigned char>* blob = jk ? &jit->blobs[li] : nullptr;
     ++li;
     const Sweep& sw = prog->sweeps[size_t(ln.sweep)];
@@ -791,8 +843,12 @@ int run_program(const std::shared_ptr<const Program>& prog_ptr, int nq, void* st
         if (jk->smem > 48 * 1024) {
           int dev = 0;
           cudaGetDevice(&dev);
-          e = cudaKernelSetAttributeForDevice(jk->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              int(jk->smem), dev);
+          const uint64_t bit = uint64_t(1) << (dev & 63);
+          if (!(jk->attrs_set.load(std::memory_order_relaxed) & bit)) {
+            e = cudaKernelSetAttributeForDevice(jk->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                int(jk->smem), dev);
+            if (e == cudaSuccess) jk->attrs_set.fetch_or(bit);
+          }
         }
         if (e == cudaSuccess)
           e = cudaLaunchKernel(reinterpret_cast<const void*>(jk->kernel),
@@ -1038,6 +1094,9 @@ int cs_set_option(const char* key, int64_t value) {
   } else if (k == "merge_ozaki") {
     if (value < 0 || value > 2) return fail(CS_ERR_INVALID, "merge_ozaki must be 0, 1 or 2");
     g_opt.merge_ozaki = value;
+  } else if (k == "merge_ozaki_min_work") {
+    if (value < 0 || value > 62) return fail(CS_ERR_INVALID, "merge_ozaki_min_work must be 0..62");
+    g_opt.merge_ozaki_min_work = value;
   } else if (k == "merge_ozaki_min_k") {
     if (value != 8 && value != 16 && value != 32 && value != 64)
       return fail(CS_ERR_INVALID, "merge_ozaki_min_k must be 8, 16, 32 or 64");
@@ -1098,6 +1157,7 @@ int64_t cs_get_option(const char* key) {
   if (k == "merge_ozaki") return g_opt.merge_ozaki;
   if (k == "zero_start_tiles") return g_opt.zero_start_tiles;
   if (k == "merge_ozaki_min_k") return g_opt.merge_ozaki_min_k;
+  if (k == "merge_ozaki_min_work") return g_opt.merge_ozaki_min_work;
   if (k == "merge_smem_kb") return g_opt.merge_smem_kb;
   if (k == "merge_dmma3_warps") return g_opt.merge_dmma3_warps;
   if (k == "jit_minb") return g_jit_minb;
@@ -1156,6 +1216,50 @@ int cs_sim_batch(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int6
     return fail(pe.code, pe.msg);
   }
   return run_program(prog, nq, states, n_states, state_stride, variant_base, init_zero, dtype, st);
+}
+
+int cs_sim_families(int32_t n_fam, const int32_t* nq, const int64_t* gate_count, const uint8_t* kinds,
+                    const int64_t* qa, const int64_t* qb, const double* params, const int32_t* slots,
+                    void* const* states, const int64_t* n_states, int32_t dtype, void* stream) {
+  Nvtx nvtx_entry("cs_sim_families");
+  if (!valid_dtype(dtype)) return fail(CS_ERR_INVALID, "dtype must be CS_C128 or CS_C64");
+  if (n_fam < 1 || !nq || !gate_count || !states || !n_states) return fail(CS_ERR_INVALID, "empty family list");
+  std::vector<std::shared_ptr<const Program>> progs(static_cast<size_t>(n_fam));
+  int64_t g0 = 0;
+  for (int f = 0; f < n_fam; ++f) {
+    const int64_t m = gate_count[f];
+    if (nq[f] < 1 || nq[f] > 62) return fail(CS_ERR_INVALID, "qubit count out of range");
+    if (!states[f] || n_states[f] < 1) return fail(CS_ERR_INVALID, "empty state batch");
+    if (m < 0 || (m > 0 && (!kinds || !qa || !qb))) return fail(CS_ERR_INVALID, "bad gate table");
+    try {
+      progs[size_t(f)] = build_schedule(nq[f], kinds + g0, qa + g0, qb + g0, params ? params + 3 * g0 : nullptr,
+                                        slots ? slots + g0 : nullptr, m, n_states[f], 0, dtype, true);
+    } catch (const PlanError& pe) {
+      return fail(pe.code, pe.msg);
+    }
+    g0 += m;
+  }
+  cudaStream_t st = as_stream(stream);
+  cudaEvent_t fork = nullptr;
+  if (n_fam > 1) {
+    cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
+    cudaEventRecord(fork, st);
+  }
+  int rc = CS_OK;
+  for (int f = 0; f < n_fam && rc == CS_OK; ++f) {
+    cudaStream_t ss = fork ? side_stream(f % 4) : st;
+    if (fork) cudaStreamWaitEvent(ss, fork, 0);
+    rc = run_program(progs[size_t(f)], nq[f], states[f], n_states[f], int64_t(1) << nq[f], 0, 1, dtype, ss);
+    if (ss != st) {
+      cudaEvent_t done = nullptr;
+      cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
+      cudaEventRecord(done, ss);
+      cudaStreamWaitEvent(st, done, 0);
+      cudaEventDestroy(done);
+    }
+  }
+  if (fork) cudaEventDestroy(fork);
+  return rc;
 }
 
 int cs_sim_batch_until(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int64_t* qb,

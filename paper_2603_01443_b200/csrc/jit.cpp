@@ -483,6 +483,19 @@ static void dump_artifact(const std::string& name, const std::string& code, cons
   }
 }
 
+// Load NVRTC and run one trivial compile (which loads its builtins library)
+// on the calling thread. The tiered compiler calls it before registering its
+// exit-time drain, so that drain runs before the destructors of every library
+// a compile uses (exit handlers run in reverse registration order).
+bool jit_warm_nvrtc() {
+  static const bool ok = [] {
+    std::vector<char> cubin;
+    std::string err;
+    return compile_source("extern \"C\" __global__ void cs_warm() {}\n", &cubin, &err);
+  }();
+  return ok;
+}
+
 int g_jit_persistent = 0;  // prefetching persistent kernels for streaming sweeps (measured slower: opt-in)
 int g_jit_minb = 2;  // __launch_bounds__ min blocks per SM of the streaming (many-tile) kernels
 

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <atomic>
 #include <memory>
 #include <string>
 #include <vector>
@@ -20,6 +21,9 @@ struct JitUnit {
   size_t smem = 0;
   int threads = 0;
   bool persistent = false;  // one CTA per SM walking the tiles, next tile prefetched
+  // devices whose launch attributes (dynamic smem, cluster size) are set: one
+  // bit per device, so the per-launch path makes no attribute calls
+  std::atomic<uint64_t> attrs_set{0};
   ~JitUnit();
 };
 
@@ -61,6 +65,10 @@ std::shared_ptr<JitModule> jit_compile_cluster(const std::vector<const Sweep*>& 
                                                int dtype, std::string* err, bool param_mode);
 bool jit_cluster_cubin(const std::vector<const Sweep*>& sweeps, const std::vector<const std::vector<RegOp>*>& progs,
                        int T, int dtype, std::vector<char>* cubin, std::string* err, bool param_mode);
+
+// NVRTC loaded and one trivial compile done on this thread (libraries a
+// compile needs are loaded); false when NVRTC is unavailable
+bool jit_warm_nvrtc();
 
 // units compiled / served from the unit cache since load (cs_get_option
 // "jit_units_compiled" / "jit_units_reused")

@@ -1034,6 +1034,15 @@ CutPrep cut_prepare(int nq, const uint8_t* kinds, const int64_t* qa, const int64
     SegmentPlan sp;
     sp.nq = sizes[s];
     sp.first = first;
+    {
+      // upper bound of this segment's rows: its share of the gates plus 3 per cut
+      const size_t cap = size_t(G) * size_t(sizes[s]) / size_t(nq) + size_t(G) / 8 + 3 * prep.cut_pos.size() + 16;
+      sp.kinds.reserve(cap);
+      sp.qa.reserve(cap);
+      sp.qb.reserve(cap);
+      sp.params.reserve(3 * cap);
+      sp.slots.reserve(cap);
+    }
     auto put = [&](uint8_t k, int64_t a, int64_t b, const double* p, int32_t slot) {
       sp.kinds.push_back(k);
       sp.qa.push_back(a);

@@ -152,22 +152,26 @@ def _native_tables(circuit: Circuit, sizes):
 
 
 def _plan_from_tables(circuit: Circuit, sizes: tuple[int, ...], nt) -> CutPlan:
+    # plain Python over the (few) cuts: this is on the drop-in API's t_pre path
     n = len(sizes)
-    cuts = nt[0]
-    boundary_gates = tuple(BoundaryGate(int(p), int(b), int(x), int(y)) for p, b, x, y in cuts.tolist())
-    counts = np.bincount(cuts[:, 1], minlength=n - 1).astype(np.int64)
-    c_i = np.zeros(n, dtype=np.int64)
-    c_i[:-1] += counts
-    c_i[1:] += counts
+    rows = nt[0].tolist()
+    boundary_gates = tuple(map(BoundaryGate._make, rows))
+    counts = [0] * (n - 1)
+    for r in rows:
+        counts[r[1]] += 1
+    c_i = [0] * n
+    for b, cnt in enumerate(counts):
+        c_i[b] += cnt
+        c_i[b + 1] += cnt
     plan = CutPlan(
         n=n,
         segment_sizes=sizes,
-        segment_of=tuple(int(v) for v in np.repeat(np.arange(n), sizes)),
+        segment_of=tuple(i for i, sz in enumerate(sizes) for _ in range(sz)),
         boundary_gates=boundary_gates,
-        c_per_boundary=tuple(int(v) for v in counts),
-        c_i=tuple(int(v) for v in c_i),
-        c_total=int(counts.sum()),
-        c_max=int(c_i.max()),
+        c_per_boundary=tuple(counts),
+        c_i=tuple(c_i),
+        c_total=len(rows),
+        c_max=max(c_i),
     )
     # decompose() reuses the tables for the same circuit (identity of its columns)
     object.__setattr__(plan, "_tables", (circuit.table.kinds, nt))
@@ -177,16 +181,25 @@ def _plan_from_tables(circuit: Circuit, sizes: tuple[int, ...], nt) -> CutPlan:
 def _families_from_tables(plan: CutPlan, nt) -> list[SegmentFamily]:
     _cuts, counts, k, a, b, p, sl, cid = nt
     fams = []
-    g0 = c0 = 0
-    firsts = plan.first_qubit
+    g0 = c0 = first = 0
+    cnt = counts.tolist()
+    cids = cid.tolist()
     for seg in range(plan.n):
-        m, nc = int(counts[seg, 0]), int(counts[seg, 1])
+        m, nc = cnt[seg]
         slots = sl[g0:g0 + m]
+        # every adjacent cut patches exactly one gate: patch[slot] = its row
         idx = np.flatnonzero(slots >= 0)
-        patch = idx[np.argsort(slots[idx], kind="stable")].astype(np.int64)
-        fams.append(SegmentFamily(seg, firsts[seg], plan.segment_sizes[seg],
-                                  GateTable(k[g0:g0 + m], a[g0:g0 + m], b[g0:g0 + m], p[g0:g0 + m]),
-                                  slots, patch, tuple(int(v) for v in cid[c0:c0 + nc])))
+        patch = np.empty(idx.size, np.int64)
+        patch[slots[idx]] = idx
+        tab = GateTable.trusted(k[g0:g0 + m], a[g0:g0 + m], b[g0:g0 + m], p[g0:g0 + m])
+        size = plan.segment_sizes[seg]
+        fam = SegmentFamily(seg, first, size, tab, slots, patch, tuple(cids[c0:c0 + nc]))
+        first += size
+        # where the template sits in the C++ planner's concatenated tables:
+        # pipeline.simulate_families runs all families of one decomposition
+        # in one native call straight from them (while the template is unchanged)
+        fam._src = (nt, g0, m, tab.kinds, slots)
+        fams.append(fam)
         g0 += m
         c0 += nc
     return fams
@@ -245,6 +258,7 @@ class SegmentFamily:
     def __post_init__(self):
         self.circuits = _VariantCircuits(self)
         self._pending = {}  # dtype -> (device batch, variants not yet handed out)
+        self._src = None  # (planner tables, first row, rows, kinds view, slots) when from the C++ planner
 
     def claim_state(self, b: int, dtype, simulate_batch):
         """Variant b's state from one batched simulation of the whole family.
@@ -401,7 +415,24 @@ def _canonical_tables(plan: CutPlan):
     return canon[0].copy(), canon[1].copy()
 
 
+_TABLES_MEMO: dict = {}
+
+
 def merge_table_of(plan: CutPlan) -> np.ndarray:
+    """r_i(m) for every segment and term (a fresh array; the values depend
+    only on n and the cuts' boundaries, so they are memoised on those)."""
+    key = (plan.n, tuple(bg.boundary for bg in plan.boundary_gates))
+    got = _TABLES_MEMO.get(key)
+    if got is None:
+        got = _merge_table(plan)
+        got.flags.writeable = False
+        if len(_TABLES_MEMO) > 1024:
+            _TABLES_MEMO.clear()
+        _TABLES_MEMO[key] = got
+    return got.copy()
+
+
+def _merge_table(plan: CutPlan) -> np.ndarray:
     ms = np.arange(1 << plan.c_total, dtype=np.int64)
     table = np.zeros((plan.n, ms.size), dtype=np.int64)
     for seg, cuts in enumerate(plan.adjacent_cuts()):
@@ -412,7 +443,17 @@ def merge_table_of(plan: CutPlan) -> np.ndarray:
 
 def coefficients_of(c_total: int) -> np.ndarray:
     """alpha_m = t0^(c - popcount m) * t1^(popcount m), by exact repeated
-    products (the factors are dyadic, so no rounding occurs)."""
+    products (the factors are dyadic, so no rounding occurs). Memoised per
+    c_total; a fresh array is returned."""
+    got = _TABLES_MEMO.get(("coef", c_total))
+    if got is None:
+        got = _coefficients(c_total)
+        got.flags.writeable = False
+        _TABLES_MEMO[("coef", c_total)] = got
+    return got.copy()
+
+
+def _coefficients(c_total: int) -> np.ndarray:
     ms = np.arange(1 << c_total, dtype=np.int64)
     ones = np.zeros(ms.size, dtype=np.int64)
     for j in range(c_total):

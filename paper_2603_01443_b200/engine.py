@@ -69,13 +69,35 @@ class StateVec:
             self._owner = "host"
             self.dtype = np.complex64 if arr.dtype == np.complex64 else np.complex128
 
+    @classmethod
+    def batch_row(cls, num_qubits: int, batch, row: int, dtype) -> "StateVec":
+        """Row ``row`` of a device family batch [2^c, 2^num_qubits] (trusted
+        shape: built by the library itself). The row tensor is materialised on
+        first use, so handing out a family's states costs no torch calls."""
+        sv = cls.__new__(cls)
+        sv.num_qubits = num_qubits
+        sv._keep = None
+        sv._row_of = (batch, row)
+        sv._dev = None
+        sv._host = None
+        sv._owner = "device"
+        sv.dtype = dtype
+        return sv
+
+    def _devt(self):
+        d = self._dev
+        if d is None and self._row_of is not None:
+            b, v = self._row_of
+            d = self._dev = b[v]
+        return d
+
     # -- host view ---------------------------------------------------------
     @property
     def amps(self) -> np.ndarray:
         if self._owner == "device":
             if self._host is None or self._host.dtype != self.dtype:
                 self._host = np.empty(1 << self.num_qubits, dtype=self.dtype)
-            _device.to_host(self._dev, out=self._host)
+            _device.to_host(self._devt(), out=self._host)
             self._owner = "host"
         return self._host
 
@@ -96,16 +118,17 @@ class StateVec:
             if src.dtype not in (np.complex128, np.complex64):
                 src = src.astype(np.complex128)
             t = _device.torch()
-            if self._dev is None or str(self._dev.dtype) != str(_device.torch_dtype(src.dtype)):
+            dev = self._devt()
+            if dev is None or str(dev.dtype) != str(_device.torch_dtype(src.dtype)):
                 self._dev = _device.from_host(src)
             else:
-                self._dev.copy_(t.from_numpy(np.ascontiguousarray(src)))
+                dev.copy_(t.from_numpy(np.ascontiguousarray(src)))
             self.dtype = src.dtype.type
             if for_write:
                 self._owner = "device"
         elif for_write:
             self._owner = "device"
-        return self._dev
+        return self._devt()
 
     def _sync_handed_out(self) -> None:
         """The reference's apply_gate mutates ``amps`` in place
@@ -115,7 +138,7 @@ class StateVec:
         are then current ("both")."""
         if self._host is not None and self._host.dtype == self.dtype and self._host.flags.writeable \
                 and self._host.flags.c_contiguous:
-            _device.to_host(self._dev, out=self._host)
+            _device.to_host(self._devt(), out=self._host)
             self._owner = "both"
 
     def on_device_only(self) -> bool:
@@ -214,7 +237,7 @@ def simulate(circuit: Circuit, *, max_qubits: int = DEFAULT_MAX_QUBITS, deadline
     if origin is not None and deadline is None:
         fam, b = origin
         batch, row = fam.claim_state(b, dtype, lambda: simulate_family(fam, dtype=dtype, max_qubits=max_qubits))
-        return StateVec(circuit.num_qubits, device=batch[row], row_of=(batch, row))
+        return StateVec.batch_row(circuit.num_qubits, batch, row, np.dtype(dtype).type)
     states = simulate_table(circuit.num_qubits, circuit.table, deadline=deadline, dtype=dtype)
     return StateVec(circuit.num_qubits, device=states[0])
 

@@ -16,6 +16,8 @@ from __future__ import annotations
 
 import gc
 import math
+
+import numpy as np
 import time
 from dataclasses import dataclass, field
 from io import StringIO
@@ -115,8 +117,8 @@ def _cut_once(circuit: Circuit, n: int, *, max_qubits: int, deadline: float | No
         else:
             batches = [simulate_family(fam, deadline=deadline, max_qubits=max_qubits) for fam in subs.segments]
         for fam, batch in zip(subs.segments, batches):
-            states.append([StateVec(fam.num_qubits, device=batch[v], row_of=(batch, v))
-                           for v in range(fam.num_variants)])
+            nq, dt = fam.num_qubits, np.complex128
+            states.append([StateVec.batch_row(nq, batch, v, dt) for v in range(fam.num_variants)])
     else:
         states = [[simulate(c, max_qubits=max_qubits, deadline=deadline) for c in fam.circuits]
                   for fam in subs.segments]

@@ -104,21 +104,26 @@ class MergeInput:
         if len(self.coeffs) != m_count:
             raise ValidationError(f"coefficient count {len(self.coeffs)} != table width {m_count}")
         total = 0
+        if m_count:  # one reduction per bound for the whole table
+            tmax = table.max(axis=1).tolist()
+            tmin = table.min(axis=1).tolist()
         for seg, states in enumerate(self.segment_states):
             if not states:
                 raise ValidationError(f"segment {seg} has no states")
-            sizes = {sv.num_qubits for sv in states}
-            if len(sizes) != 1:
-                raise ValidationError(f"segment {seg} mixes qubit counts {sizes}")
+            nq0 = states[0].num_qubits
+            for sv in states:
+                if sv.num_qubits != nq0:
+                    raise ValidationError(f"segment {seg} mixes qubit counts "
+                                          f"{ {x.num_qubits for x in states} }")
             count = len(states)
             if count & (count - 1):
                 raise ValidationError(f"segment {seg} must hold a power-of-two state count, got {count}")
-            if m_count and (int(table[seg].max()) >= count or int(table[seg].min()) < 0):
+            if m_count and (tmax[seg] >= count or tmin[seg] < 0):
                 raise ValidationError(
-                    f"merge table references state {int(table[seg].max())} but segment {seg} "
+                    f"merge table references state {tmax[seg]} but segment {seg} "
                     f"holds {count}"
                 )
-            total += states[0].num_qubits
+            total += nq0
         if total != self.num_qubits:
             raise ValidationError(f"segment qubit counts sum to {total}, expected {self.num_qubits}")
 
@@ -208,16 +213,48 @@ def merge_terms_device(hi, lo, hidx, lidx, coef, *, S=1, rows=None, out=None, dt
     return out
 
 
+_CHAIN_ARGS: dict = {}
+_CHAIN_WS: dict = {}
+
+
+def _chain_args(chain: ChainSpec):
+    """The chain's ctypes arguments (arrays kept alive with their addresses);
+    memoised per spec, an immutable value."""
+    got = _CHAIN_ARGS.get(chain)
+    if got is None:
+        arrs = (_native.c_i32(chain.seg_nq), _native.c_i32(chain.seg_ncuts),
+                _native.c_i32(chain.seg_cut_ids if chain.seg_cut_ids else [0]),
+                _native.c_i32(chain.cut_boundary if chain.cut_boundary else [0]), _native.c_f64(chain.term_coef()))
+        got = (arrs, tuple(_native.ptr(a) for a in arrs))
+        if len(_CHAIN_ARGS) > 4096:
+            _CHAIN_ARGS.clear()
+        _CHAIN_ARGS[chain] = got
+    return got[1]
+
+
+def _chain_workspace(nbytes: int, stream=None):
+    """Chain workspace per (device, stream), grown on demand and reused:
+    merges on one stream are ordered, so reuse never races."""
+    t = _device.torch()
+    key = (t.cuda.current_device(), _device.stream_ptr(stream))
+    ws = _CHAIN_WS.get(key)
+    if ws is None or ws.numel() < nbytes:
+        ws = t.empty(max(nbytes, 256), dtype=t.uint8, device="cuda")
+        if len(_CHAIN_WS) > 64:
+            _CHAIN_WS.clear()
+        _CHAIN_WS[key] = ws
+    return ws
+
+
 def merge_chain_device(chain: ChainSpec, seg_batches, *, dtype=np.complex128, out=None,
                        out_range=None, workspace=None, force_bond: int = -1, stream=None):
     """Chain-contracted reconstruction of amplitudes [begin, end) on the device.
     seg_batches[j] is the [2^{c_j}, 2^{q_j}] device batch of segment j."""
-    t = _device.torch()
     q = chain.num_qubits
     begin, end = (0, 1 << q) if out_range is None else out_range
     ws_bytes, _bond, _qlow = chain.plan(dtype, force_bond)
     if workspace is None or workspace.numel() < ws_bytes:
-        workspace = t.empty(max(ws_bytes, 1), dtype=t.uint8, device="cuda")
+        workspace = _chain_workspace(ws_bytes, stream)
     if not (0 <= begin <= end <= (1 << q)):
         raise ValidationError(f"output range [{begin}, {end}) outside [0, 2^{q})")
     if out is None:
@@ -231,14 +268,10 @@ def merge_chain_device(chain: ChainSpec, seg_batches, *, dtype=np.complex128, ou
         if b.dtype != tdt or b.device.type != "cuda":
             raise ValidationError(f"segment {j} batch must be a CUDA tensor of {tdt}, got {b.dtype} on {b.device}")
     ptrs = np.array([b.data_ptr() for b in seg_batches], dtype=np.uint64)
-    nq = _native.c_i32(chain.seg_nq)
-    nc = _native.c_i32(chain.seg_ncuts)
-    ids = _native.c_i32(chain.seg_cut_ids if chain.seg_cut_ids else [0])
-    bnd = _native.c_i32(chain.cut_boundary if chain.cut_boundary else [0])
-    tc = _native.c_f64(chain.term_coef())
+    p_nq, p_nc, p_ids, p_bnd, p_tc = _chain_args(chain)
     _native.check(
-        _native.load().cs_merge_chain(chain.n, _native.ptr(nq), _native.ptr(ptrs), _native.ptr(nc),
-                                      _native.ptr(ids), chain.c_total, _native.ptr(bnd), _native.ptr(tc),
+        _native.load().cs_merge_chain(chain.n, p_nq, _native.ptr(ptrs), p_nc,
+                                      p_ids, chain.c_total, p_bnd, p_tc,
                                       force_bond, begin, end, out.data_ptr(), workspace.data_ptr(),
                                       workspace.numel(), _device.code_of(dtype),
                                       _device.stream_ptr(stream)),

@@ -16,7 +16,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from . import _device
+from . import _device, _native
 from .circuits import Circuit
 from .cutting import decompose, plan_cut
 from .engine import DEFAULT_MAX_QUBITS, StateVec, check_capacity, simulate_family
@@ -65,6 +65,9 @@ def simulate_families(fams, *, dtype=np.complex128, max_qubits=DEFAULT_MAX_QUBIT
     latency-bound sweep chains of different segments overlap on the GPU."""
     if len(fams) == 1:
         return [simulate_family(fams[0], dtype=dtype, max_qubits=max_qubits)]
+    fast = _simulate_families_native(fams, dtype, max_qubits)
+    if fast is not None:
+        return fast
     t = _device.torch()
     main = t.cuda.current_stream()
     fork = t.cuda.Event()
@@ -81,6 +84,39 @@ def simulate_families(fams, *, dtype=np.complex128, max_qubits=DEFAULT_MAX_QUBIT
     for ev, o in zip(joins, outs):
         main.wait_event(ev)
         o.record_stream(main)
+    return outs
+
+
+def _simulate_families_native(fams, dtype, max_qubits):
+    """All families of one C++-planned decomposition in ONE native call
+    (cs_sim_families: schedules, side streams and joins inside libcutsim),
+    reading the templates straight from the planner's concatenated tables.
+    None when the families are not such a set (or a template was replaced)."""
+    src0 = getattr(fams[0], "_src", None)
+    if src0 is None:
+        return None
+    nt = src0[0]
+    g = 0
+    for f in fams:
+        src = f._src
+        if src is None or src[0] is not nt or src[1] != g or f.template.kinds is not src[3] or f.slots is not src[4]:
+            return None
+        g += src[2]
+    for f in fams:
+        check_capacity(f.num_qubits, max_qubits)
+    _device.require_cuda()
+    t = _device.torch()
+    tdt = _device.torch_dtype(dtype)
+    outs = [t.empty((f.num_variants, 1 << f.num_qubits), dtype=tdt, device="cuda") for f in fams]
+    _cuts, _counts, k, a, b, p, sl, _cid = nt
+    nq = np.array([f.num_qubits for f in fams], np.int32)
+    gc = np.array([f._src[2] for f in fams], np.int64)
+    ns = np.array([f.num_variants for f in fams], np.int64)
+    ptrs = np.array([o.data_ptr() for o in outs], np.uint64)
+    ptr = _native.ptr
+    _native.check(_native.load().cs_sim_families(len(fams), ptr(nq), ptr(gc), ptr(k), ptr(a), ptr(b), ptr(p),
+                                                 ptr(sl), ptr(ptrs), ptr(ns), _device.code_of(dtype),
+                                                 _device.stream_ptr()), "cs_sim_families")
     return outs
 
 

@@ -38,9 +38,11 @@ def reference(hi, lo, hidx, lidx, coef, S, rows):
 def run(torch, native, hi, lo, hidx, lidx, coef, S=1, rows=None, ozaki=1, out=None, accumulate=False, digits=8):
     from paper_2603_01443_b200.merging import merge_terms_device
 
-    old = native.get_option("merge_ozaki"), native.get_option("merge_ozaki_digits")
+    old = native.get_option("merge_ozaki"), native.get_option("merge_ozaki_digits"), \
+        native.get_option("merge_ozaki_min_work")
     native.set_option("merge_ozaki", ozaki)
     native.set_option("merge_ozaki_digits", digits)
+    native.set_option("merge_ozaki_min_work", 0)  # these products are small: take the int8 kernel anyway
     try:
         res = merge_terms_device(torch.as_tensor(hi, device="cuda"), torch.as_tensor(lo, device="cuda"),
                                  hidx, lidx, coef, S=S, rows=rows, out=out, accumulate=accumulate)
@@ -49,6 +51,7 @@ def run(torch, native, hi, lo, hidx, lidx, coef, S=1, rows=None, ozaki=1, out=No
     finally:
         native.set_option("merge_ozaki", old[0])
         native.set_option("merge_ozaki_digits", old[1])
+        native.set_option("merge_ozaki_min_work", old[2])
 
 
 CASES = [  # (K, S, H, W, rows)
