@@ -195,34 +195,55 @@ struct OzPrep {
 };
 
 // ---------------------------------------------------------------------------
-// digit preparation: A (the lo side), one thread per (l, k-step)
-// adig layout: [l_tile][ks][slice][4096 B canonical block]; sa[l] = 2^(e_l + kSaShift)
+// digit preparation. Four adjacent lanes share one (row, k-step): the row
+// maximum is reduced over the lanes with shuffles, and lane `sub` splits
+// terms 4 sub .. 4 sub + 3 of the k-step (bytes 8 sub .. 8 sub + 7 of the
+// row's 32-byte k-step: the first 16 at the block row, the last 16 one
+// 128-byte K-chunk further). Four times the threads of one lane per row —
+// at small q each side is only a few thousand rows and the single-lane form
+// was latency bound (q=24 K=16: 8 + 12 us ahead of a 63 us merge kernel).
 // ---------------------------------------------------------------------------
+constexpr int kPrepLanes = 4;
+
+__device__ __forceinline__ uint32_t lane_chunk_off(int sub) { return sub < 2 ? 8u * sub : 128u + 8u * (sub - 2); }
+
+// A (the lo side). adig layout: [l_tile][ks][slice][4096 B canonical block];
+// sa[l] = 2^(e_l + kSaShift)
 template <int KS, int DB>
 __global__ void ozaki_prep_lo(const __grid_constant__ OzPrep p, int8_t* adig, double* sa) {
   OZ_DIGIT_CONSTS
-  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (idx >= p.lo_len * KS) return;
-  const int ks = int(idx / p.lo_len);
-  const int64_t l = idx - int64_t(ks) * p.lo_len;
+  const int64_t gidx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int sub = int(gidx & (kPrepLanes - 1));
+  const int64_t idx = gidx / kPrepLanes;
+  const bool live = idx < p.lo_len * KS;  // the 4 lanes of a group agree; no early exit before the shuffles
+  const int ks = live ? int(idx / p.lo_len) : 0;
+  const int64_t l = live ? idx - int64_t(ks) * p.lo_len : 0;
   const double2* lo = p.lo;
   const int K = p.K;
   double mx = 0.0;
-  bool finite = true;
-  for (int t = 0; t < K; ++t) {
-    const double2 v = __ldg(lo + int64_t(p.lidx[t]) * p.lo_len + l);
-    finite &= isfinite(v.x) && isfinite(v.y);
-    mx = fmax(mx, fmax(fabs(v.x), fabs(v.y)));
+  int finite = 1;
+  if (live) {
+    for (int t = sub; t < K; t += kPrepLanes) {
+      const double2 v = __ldg(lo + int64_t(p.lidx[t]) * p.lo_len + l);
+      finite &= isfinite(v.x) && isfinite(v.y);
+      mx = fmax(mx, fmax(fabs(v.x), fabs(v.y)));
+    }
   }
+#pragma unroll
+  for (int o = 1; o < kPrepLanes; o <<= 1) {
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    finite &= __shfl_xor_sync(0xffffffffu, finite, o);
+  }
+  if (!live) return;
   const int e = row_exponent(finite ? mx : 0.0);
   // a NaN/Inf operand makes the whole output column NaN (as the FP64 kernels
   // propagate it) instead of saturated digits turning it into a finite value
-  if (ks == 0) sa[l] = finite ? ldexp(1.0, e + kSaShift) : __longlong_as_double(0x7ff8000000000000ll);
+  if (ks == 0 && sub == 0) sa[l] = finite ? ldexp(1.0, e + kSaShift) : __longlong_as_double(0x7ff8000000000000ll);
   const double sc = digit_scale<DB>(e);
-  uint32_t w[kSlices][8];
+  uint32_t w[kSlices][2];
 #pragma unroll
-  for (int tt = 0; tt < 16; ++tt) {
-    const int t = 16 * ks + tt;
+  for (int tt = 0; tt < 4; ++tt) {
+    const int t = 16 * ks + 4 * sub + tt;
     double2 v = make_double2(0.0, 0.0);
     if (t < K) v = __ldg(lo + int64_t(p.lidx[t]) * p.lo_len + l);
     int dr[kSlices], di[kSlices];
@@ -230,52 +251,56 @@ __global__ void ozaki_prep_lo(const __grid_constant__ OzPrep p, int8_t* adig, do
     digits_split<DB>(v.y, sc, di);
 #pragma unroll
     for (int i = 0; i < kSlices; ++i) {
-      // bytes 2tt, 2tt + 1 of the row's 32-byte k-step: (re, im)
+      // bytes 2tt, 2tt + 1 of this lane's 8 bytes: (re, im)
       const uint32_t pr = pack2(dr[i], di[i]) << (16 * (tt & 1));
       if (tt & 1) w[i][tt >> 1] |= pr;
       else w[i][tt >> 1] = pr;
     }
   }
-  int8_t* base = adig + (l >> 7) * int64_t(KS * kSlices * kABlock) + cm_row_off(int(l & 127));
+  int8_t* base = adig + (l >> 7) * int64_t(KS * kSlices * kABlock) + cm_row_off(int(l & 127)) + lane_chunk_off(sub);
 #pragma unroll
-  for (int i = 0; i < kSlices; ++i) {
-    int8_t* blk = base + (ks * kSlices + i) * kABlock;
-    *reinterpret_cast<uint4*>(blk) = make_uint4(w[i][0], w[i][1], w[i][2], w[i][3]);
-    *reinterpret_cast<uint4*>(blk + 128) = make_uint4(w[i][4], w[i][5], w[i][6], w[i][7]);
-  }
+  for (int i = 0; i < kSlices; ++i)
+    *reinterpret_cast<uint2*>(base + (ks * kSlices + i) * kABlock) = make_uint2(w[i][0], w[i][1]);
 }
 
-// ---------------------------------------------------------------------------
-// digit preparation: B (the hi side with the coefficients), one thread per
-// (h, k-step); bdig layout: [h_block][ks][slice][1024 B canonical block],
-// row r = 2 (h % 16) + v; sb[h] = 2^e_h
-// ---------------------------------------------------------------------------
+// B (the hi side with the coefficients). bdig layout: [h_block][ks][slice]
+// [1024 B canonical block], row r = 2 (h % 16) + v; sb[h] = 2^e_h
 template <int KS, int DB>
 __global__ void ozaki_prep_hi(const __grid_constant__ OzPrep p, int64_t nrows, int8_t* bdig, double* sb) {
   OZ_DIGIT_CONSTS
-  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (idx >= nrows * KS) return;
-  const int ks = int(idx / nrows);
-  const int64_t hr = idx - int64_t(ks) * nrows;
+  const int64_t gidx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int sub = int(gidx & (kPrepLanes - 1));
+  const int64_t idx = gidx / kPrepLanes;
+  const bool live = idx < nrows * KS;
+  const int ks = live ? int(idx / nrows) : 0;
+  const int64_t hr = live ? idx - int64_t(ks) * nrows : 0;
   const int64_t h = p.row_begin + hr;
   const double2* hi = p.hi;
   const int K = p.K;
   double mx = 0.0;
-  bool finite = true;
-  for (int t = 0; t < K; ++t) {
-    const double2 v = __ldg(hi + int64_t(p.hidx[t]) * p.hi_len + h);
-    const double cr = p.coef[t].x, ci = p.coef[t].y;
-    const double br = v.x * cr - v.y * ci, bi = v.x * ci + v.y * cr;
-    finite &= isfinite(br) && isfinite(bi);
-    mx = fmax(mx, fmax(fabs(br), fabs(bi)));
+  int finite = 1;
+  if (live) {
+    for (int t = sub; t < K; t += kPrepLanes) {
+      const double2 v = __ldg(hi + int64_t(p.hidx[t]) * p.hi_len + h);
+      const double cr = p.coef[t].x, ci = p.coef[t].y;
+      const double br = v.x * cr - v.y * ci, bi = v.x * ci + v.y * cr;
+      finite &= isfinite(br) && isfinite(bi);
+      mx = fmax(mx, fmax(fabs(br), fabs(bi)));
+    }
   }
-  const int e = row_exponent(finite ? mx : 0.0);
-  if (ks == 0) sb[hr] = finite ? ldexp(1.0, e) : __longlong_as_double(0x7ff8000000000000ll);
-  const double sc = digit_scale<DB>(e);
-  uint32_t w0[kSlices][8], w1[kSlices][8];
 #pragma unroll
-  for (int tt = 0; tt < 16; ++tt) {
-    const int t = 16 * ks + tt;
+  for (int o = 1; o < kPrepLanes; o <<= 1) {
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    finite &= __shfl_xor_sync(0xffffffffu, finite, o);
+  }
+  if (!live) return;
+  const int e = row_exponent(finite ? mx : 0.0);
+  if (ks == 0 && sub == 0) sb[hr] = finite ? ldexp(1.0, e) : __longlong_as_double(0x7ff8000000000000ll);
+  const double sc = digit_scale<DB>(e);
+  uint32_t w0[kSlices][2], w1[kSlices][2];
+#pragma unroll
+  for (int tt = 0; tt < 4; ++tt) {
+    const int t = 16 * ks + 4 * sub + tt;
     double br = 0.0, bi = 0.0;
     if (t < K) {
       const double2 v = __ldg(hi + int64_t(p.hidx[t]) * p.hi_len + h);
@@ -309,16 +334,12 @@ __global__ void ozaki_prep_hi(const __grid_constant__ OzPrep p, int64_t nrows, i
     }
   }
   const int hl = int(hr & (kHB - 1));
-  int8_t* base = bdig + (hr / kHB) * int64_t(KS * kSlices * kBBlock);
+  int8_t* base = bdig + (hr / kHB) * int64_t(KS * kSlices * kBBlock) + lane_chunk_off(sub);
 #pragma unroll
   for (int i = 0; i < kSlices; ++i) {
     int8_t* blk = base + (ks * kSlices + i) * kBBlock;
-    int8_t* r0 = blk + cm_row_off(2 * hl);
-    int8_t* r1 = blk + cm_row_off(2 * hl + 1);
-    *reinterpret_cast<uint4*>(r0) = make_uint4(w0[i][0], w0[i][1], w0[i][2], w0[i][3]);
-    *reinterpret_cast<uint4*>(r0 + 128) = make_uint4(w0[i][4], w0[i][5], w0[i][6], w0[i][7]);
-    *reinterpret_cast<uint4*>(r1) = make_uint4(w1[i][0], w1[i][1], w1[i][2], w1[i][3]);
-    *reinterpret_cast<uint4*>(r1 + 128) = make_uint4(w1[i][4], w1[i][5], w1[i][6], w1[i][7]);
+    *reinterpret_cast<uint2*>(blk + cm_row_off(2 * hl)) = make_uint2(w0[i][0], w0[i][1]);
+    *reinterpret_cast<uint2*>(blk + cm_row_off(2 * hl + 1)) = make_uint2(w1[i][0], w1[i][1]);
   }
 }
 
@@ -369,22 +390,28 @@ struct TileWalk {
 template <bool UNIT>
 constexpr int oz_threads() { return 64 + 32 * (UNIT ? kEpiWarps / 2 : kEpiWarps); }
 
+// A digit buffers in shared memory: two (the next work unit's l-tile digits
+// load while the current unit's MMAs run) where they fit next to the B ring
+template <int KS, bool UNIT>
+constexpr int oz_abufs() { return (!UNIT && KS <= 2) ? 2 : 1; }
+
 template <int KS, int NST, bool ACC, bool UNIT, int DB>
 __global__ void __launch_bounds__(oz_threads<UNIT>(), UNIT ? 2 : 1) ozaki_merge_kernel(const __grid_constant__ OzParams p) {
   OZ_DIGIT_CONSTS
   constexpr int NBUF = UNIT ? 1 : 2;  // TMEM accumulators (= epilogue groups)
+  constexpr int NA = oz_abufs<KS, UNIT>();
   constexpr uint32_t TCOLS = 256 * NBUF;
   constexpr uint32_t A_BYTES = KS * kSlices * kABlock;
   constexpr uint32_t B_BYTES = KS * kSlices * kBBlock;
   extern __shared__ __align__(1024) uint8_t smem[];
-  int8_t* sA = reinterpret_cast<int8_t*>(smem);
-  int8_t* sB = reinterpret_cast<int8_t*>(smem + A_BYTES);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + A_BYTES + NST * B_BYTES);
+  int8_t* sA = reinterpret_cast<int8_t*>(smem);  // [NA]
+  int8_t* sB = reinterpret_cast<int8_t*>(smem + NA * A_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NA * A_BYTES + NST * B_BYTES);
   uint64_t* full = bars;             // [NST]
   uint64_t* empty = bars + NST;      // [NST]
-  uint64_t* afull = bars + 2 * NST;
-  uint64_t* aempty = afull + 1;
-  uint64_t* tfull = aempty + 1;      // [2]
+  uint64_t* afull = bars + 2 * NST;  // [NA]
+  uint64_t* aempty = afull + NA;     // [NA]
+  uint64_t* tfull = aempty + NA;     // [2]
   uint64_t* tempty = tfull + 2;      // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -398,8 +425,10 @@ __global__ void __launch_bounds__(oz_threads<UNIT>(), UNIT ? 2 : 1) ozaki_merge_
       mbar_init(full + s, 1);
       mbar_init(empty + s, 1);
     }
-    mbar_init(afull, 1);
-    mbar_init(aempty, 1);
+    for (int a = 0; a < NA; ++a) {
+      mbar_init(afull + a, 1);
+      mbar_init(aempty + a, 1);
+    }
     for (int b = 0; b < NBUF; ++b) {
       mbar_init(tfull + b, 1);
       mbar_init(tempty + b, kEpiWarps / 2);
@@ -419,16 +448,16 @@ __global__ void __launch_bounds__(oz_threads<UNIT>(), UNIT ? 2 : 1) ozaki_merge_
   if (warp == 0) {
     {
       int64_t cur = -1;
-      uint32_t aph = 0;
+      int uc = -1;  // work units (A loads) so far
       int it = 0;
       for (TileWalk w(p); w.valid(); w.next(), ++it) {
         const int64_t lt = w.lt, hb = w.hb;
         if (lt != cur) {
-          if (cur >= 0) {
-            mbar_wait(aempty, aph);
-            aph ^= 1;
-          }
-          bulk_load(sA, p.adig + lt * A_BYTES, A_BYTES, afull);
+          ++uc;
+          const int ab = uc % NA;
+          // buffer ab was last filled for unit uc - NA: wait for its MMAs
+          if (uc >= NA) mbar_wait(aempty + ab, ((uc / NA) - 1) & 1);
+          bulk_load(sA + ab * A_BYTES, p.adig + lt * A_BYTES, A_BYTES, afull + ab);
           cur = lt;
         }
         const int st = it % NST;
@@ -440,15 +469,18 @@ __global__ void __launch_bounds__(oz_threads<UNIT>(), UNIT ? 2 : 1) ozaki_merge_
   } else if (warp == 1) {
     {
       int64_t cur = -1;
-      uint32_t aph = 0;
+      int uc = -1;
       int it = 0;
-      const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
+      uint32_t a0 = smem_u32(sA);
+      const uint32_t b0 = smem_u32(sB);
       for (TileWalk w(p); w.valid(); w.next(), ++it) {
         const int64_t lt = w.lt;
         if (lt != cur) {
-          if (cur >= 0) mma_commit(aempty);
-          mbar_wait(afull, aph);
-          aph ^= 1;
+          // the previous unit's MMAs release its A buffer when they complete
+          if (uc >= 0) mma_commit(aempty + (uc % NA));
+          ++uc;
+          mbar_wait(afull + (uc % NA), (uc / NA) & 1);
+          a0 = smem_u32(sA + (uc % NA) * A_BYTES);
           cur = lt;
         }
         const int st = it % NST;
@@ -578,10 +610,10 @@ __global__ void __launch_bounds__(oz_threads<UNIT>(), UNIT ? 2 : 1) ozaki_merge_
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TCOLS));
 }
 
-template <int KS, int NST, int DB>
+template <int KS, int NST, int DB, bool UNIT>
 constexpr size_t oz_smem() {
   constexpr int kSlices = Digits<DB>::S;
-  return size_t(KS) * kSlices * kABlock + size_t(NST) * KS * kSlices * kBBlock + 256;
+  return size_t(oz_abufs<KS, UNIT>()) * KS * kSlices * kABlock + size_t(NST) * KS * kSlices * kBBlock + 256;
 }
 
 // digit workspace per stream (grow-only; merges on different streams may overlap)
@@ -640,8 +672,8 @@ cudaError_t run_ozaki(const MergeParams& mp, int64_t nrows, void* out, int accum
     pp.lidx[t] = mp.lidx[t];
     pp.coef[t] = make_double2(mp.coef[2 * t], mp.coef[2 * t + 1]);
   }
-  ozaki_prep_lo<KS, DB><<<unsigned((W * KS + 127) / 128), 128, 0, stream>>>(pp, adig, sa);
-  ozaki_prep_hi<KS, DB><<<unsigned((nrows * KS + 127) / 128), 128, 0, stream>>>(pp, nrows, bdig, sb);
+  ozaki_prep_lo<KS, DB><<<unsigned((W * KS * kPrepLanes + 127) / 128), 128, 0, stream>>>(pp, adig, sa);
+  ozaki_prep_hi<KS, DB><<<unsigned((nrows * KS * kPrepLanes + 127) / 128), 128, 0, stream>>>(pp, nrows, bdig, sb);
   OzParams op;
   op.adig = adig;
   op.bdig = bdig;
@@ -670,7 +702,7 @@ cudaError_t run_ozaki(const MergeParams& mp, int64_t nrows, void* out, int accum
   // persistent: at least ~116 KB of shared memory so that exactly one CTA
   // (and one 512-column TMEM allocation) lives on each SM; unit CTAs: two
   // per SM (256 TMEM columns each)
-  const size_t smem = UNIT ? oz_smem<KS, NST, DB>() : std::max<size_t>(oz_smem<KS, NST, DB>(), 116 * 1024);
+  const size_t smem = UNIT ? oz_smem<KS, NST, DB, UNIT>() : std::max<size_t>(oz_smem<KS, NST, DB, UNIT>(), 116 * 1024);
   constexpr int inst = ((KS == 1 ? 0 : KS == 2 ? 1 : 2) * 2 + (UNIT ? 1 : 0)) * 2 + (DB == 8 ? 1 : 0);
   const uint64_t bit = uint64_t(1) << (dev & 63);
   if (!(g_oz_configured[inst].load() & bit)) {
