@@ -1218,6 +1218,39 @@ int cs_sim_batch(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int6
   return run_program(prog, nq, states, n_states, state_stride, variant_base, init_zero, dtype, st);
 }
 
+// Run n independent launch sequences concurrently: items 1..n-1 on the
+// library's side streams (forked from `st` by one event, joined back into
+// it), item 0 on `st` itself, launched last so every item starts together.
+// Keeping one item on `st` saves it the fork and join hops (cfg4a variant
+// stage: family batches 28-30 us each, 43 us both through two side streams).
+extern "C++" {
+template <typename F>
+int run_forked(int n, cudaStream_t st, F&& launch) {
+  if (n <= 1) return n == 1 ? launch(0, st) : CS_OK;
+  cudaEvent_t fork = nullptr;
+  cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
+  cudaEventRecord(fork, st);
+  int rc = CS_OK;
+  std::vector<cudaEvent_t> done;
+  for (int i = 1; i < n && rc == CS_OK; ++i) {
+    cudaStream_t ss = side_stream((i - 1) % 4);
+    cudaStreamWaitEvent(ss, fork, 0);
+    rc = launch(i, ss);
+    cudaEvent_t d = nullptr;
+    cudaEventCreateWithFlags(&d, cudaEventDisableTiming);
+    cudaEventRecord(d, ss);
+    done.push_back(d);
+  }
+  if (rc == CS_OK) rc = launch(0, st);
+  for (cudaEvent_t d : done) {
+    cudaStreamWaitEvent(st, d, 0);
+    cudaEventDestroy(d);
+  }
+  cudaEventDestroy(fork);
+  return rc;
+}
+}  // extern "C++"
+
 int cs_sim_families(int32_t n_fam, const int32_t* nq, const int64_t* gate_count, const uint8_t* kinds,
                     const int64_t* qa, const int64_t* qb, const double* params, const int32_t* slots,
                     void* const* states, const int64_t* n_states, int32_t dtype, void* stream) {
@@ -1239,27 +1272,9 @@ int cs_sim_families(int32_t n_fam, const int32_t* nq, const int64_t* gate_count,
     }
     g0 += m;
   }
-  cudaStream_t st = as_stream(stream);
-  cudaEvent_t fork = nullptr;
-  if (n_fam > 1) {
-    cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
-    cudaEventRecord(fork, st);
-  }
-  int rc = CS_OK;
-  for (int f = 0; f < n_fam && rc == CS_OK; ++f) {
-    cudaStream_t ss = fork ? side_stream(f % 4) : st;
-    if (fork) cudaStreamWaitEvent(ss, fork, 0);
-    rc = run_program(progs[size_t(f)], nq[f], states[f], n_states[f], int64_t(1) << nq[f], 0, 1, dtype, ss);
-    if (ss != st) {
-      cudaEvent_t done = nullptr;
-      cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
-      cudaEventRecord(done, ss);
-      cudaStreamWaitEvent(st, done, 0);
-      cudaEventDestroy(done);
-    }
-  }
-  if (fork) cudaEventDestroy(fork);
-  return rc;
+  return run_forked(n_fam, as_stream(stream), [&](int f, cudaStream_t ss) {
+    return run_program(progs[size_t(f)], nq[f], states[f], n_states[f], int64_t(1) << nq[f], 0, 1, dtype, ss);
+  });
 }
 
 int cs_sim_batch_until(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int64_t* qb,
@@ -1484,29 +1499,12 @@ int piece_programs(const CutJob& job, const std::vector<Piece>& pieces, int dtyp
 // forked from / joined into `st` (segments are independent).
 int run_pieces(const CutJob& job, const std::vector<Piece>& pieces,
                const std::vector<std::shared_ptr<const Program>>& progs, int dtype, cudaStream_t st) {
-  cudaEvent_t fork = nullptr;
-  if (pieces.size() > 1) {
-    cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
-    cudaEventRecord(fork, st);
-  }
-  int rc = CS_OK;
-  for (size_t i = 0; i < pieces.size(); ++i) {
-    const Piece& pc = pieces[i];
+  return run_forked(int(pieces.size()), st, [&](int i, cudaStream_t ss) {
+    const Piece& pc = pieces[size_t(i)];
     const SegmentPlan& sp = job.prep.segs[size_t(pc.seg)];
-    cudaStream_t ss = fork ? side_stream(int(i % 4)) : st;
-    if (fork) cudaStreamWaitEvent(ss, fork, 0);
-    rc = run_program(progs[i], sp.nq, pc.dst, pc.v1 - pc.v0, int64_t(1) << sp.nq, uint64_t(pc.v0), 1, dtype, ss);
-    if (rc != CS_OK) break;
-    if (ss != st) {
-      cudaEvent_t done = nullptr;
-      cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
-      cudaEventRecord(done, ss);
-      cudaStreamWaitEvent(st, done, 0);
-      cudaEventDestroy(done);
-    }
-  }
-  if (fork) cudaEventDestroy(fork);
-  return rc;
+    return run_program(progs[size_t(i)], sp.nq, pc.dst, pc.v1 - pc.v0, int64_t(1) << sp.nq, uint64_t(pc.v0), 1, dtype,
+                       ss);
+  });
 }
 
 // The single-GPU pieces: every segment's whole family at its workspace slot.
