@@ -761,12 +761,13 @@ def measure_int8(q, out, stream):
         _native.set_option("merge_ozaki", 1)
         t = res["int8_tcgen05"] / 1e3
         res_all[f"K{K}"] = {"ms": res["int8_tcgen05"], "fp64_dmma_3m_ms": res["fp64_dmma_3m"],
-                            "out_gbs": 16.0 * total / t / 1e9, "hbm_frac_out": 16.0 * total / t / 1e9 / 6548.2,
+                            "out_gbs": 16.0 * total / t / 1e9, "hbm_frac_out": 16.0 * total / t / 1e9 / load_peaks()[0],
                             "fp64_tflops_alg": 8.0 * K * total / t / 1e12}
         del hi, lo
     res_all["note"] = ("q=30 rank-K product out[h][l] = sum_t c_t hi_t[h] lo_t[l] (n=2 merge with K cut terms) "
-                       "into the 16 GiB output: int8 tcgen05.mma with 8 base-128 digits per FP64 operand "
-                       "(max|d| vs DFMA ~1e-16) vs the FP64 tensor-core 3M kernel; 8K flop per output algorithmic")
+                       "into the 16 GiB output: int8 tcgen05.mma with 7 balanced base-256 digits per FP64 operand "
+                       "(max|d| vs DFMA ~1e-15 of max|out|) vs the FP64 tensor-core 3M kernel; 8K flop per output "
+                       "algorithmic; hbm_frac_out against the measured copy peak")
     return res_all
 
 

@@ -68,10 +68,10 @@ int cs_device_count(int32_t* count);
  * for one-slot products of K >= "merge_ozaki_min_k" terms, lo_len % 128 == 0,
  * row ranges % 16 == 0, outputs * K >= 2^"merge_ozaki_min_work" (default
  * 27: smaller products run faster on the FP64 kernels); default 1, min K
- * 16), "merge_ozaki_digits" (7: 8
- * balanced base-128 digits per operand, 8 int32 diagonals per output,
- * truncation ~6e-16 of max|a| max|b| — default; 8: 7 base-256 digits, 7
- * diagonals, ~1e-15, 3-4 % faster at K <= 32), "cluster" (cluster-resident
+ * 16), "merge_ozaki_digits" (8: 7
+ * balanced base-256 digits per operand, 7 int32 diagonals per output,
+ * truncation ~1e-15 of max|out| — default, q=30 K=16 in 3.0 ms; 7: 8
+ * base-128 digits, 8 diagonals, ~6e-16, 8 % slower at K = 16), "cluster" (cluster-resident
  * variant batches: one NVRTC kernel per program, the 2^12..2^16-amplitude
  * states in the distributed shared memory of a CTA cluster; default 1),
  * "cluster_max" (CTAs per cluster at most: 2..16, default 16),

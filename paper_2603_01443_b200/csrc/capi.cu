@@ -98,7 +98,7 @@ struct Options {
   int64_t merge_ozaki = 1;        // int8 tcgen05 merge (exact FP64 splitting) for K >= merge_ozaki_min_k
   int64_t merge_ozaki_min_k = 16;
   int64_t merge_ozaki_min_work = 27;  // log2 of outputs * K below which the FP64 kernels run
-  int64_t merge_ozaki_digits = 7;  // digit bits of the int8 merge: 7 (8 slices, default) or 8 (7 slices: 3-4 % faster at K <= 32, 2x the truncation)
+  int64_t merge_ozaki_digits = 8;  // digit bits of the int8 merge: 8 (7 base-256 slices, default: q=30 K=16 3.0 vs 3.27 ms) or 7 (8 base-128 slices, half the truncation)
   int64_t engine = 1;      // 1: register-tile kernel (rsweep), 0: shared-memory tile kernel (sweep)
   int64_t jit = 0;         // 0 never, 1 from a program's 2nd use, 2 always (compile on first use, blocking),
                            // 3 tiered: the interpreter runs while the module compiles on a background thread

@@ -9,12 +9,14 @@
 //   B[(h,0)] = (Hr_0, -Hi_0, ...)  -> Re out,   B[(h,1)] = (Hi_0, Hr_0, ...) -> Im out.
 // Every row of A (per l) and every pair of rows of B (per h) is scaled by a
 // power of two 2^-e so its entries are <= 1/2 in magnitude, rounded to
-// 56-bit fixed point (2^-57 of the row maximum) and split into S = 8
-// balanced base-128 digits (int8, |d| <= 65). Digit products of equal
-// weight i + j = p ("diagonal p") accumulate exactly in int32:
-//   D_p = sum_{i+j=p} A_i B_j^T,      out = 2^(e_l + e_h) sum_p 2^-7(p+2) D_p
-// keeping p <= S-1 (the dropped terms are < 2^-56 relative to the row/column
-// maxima: the rounding level of a K-term FP64 dot product).
+// fixed point and split into S balanced int8 digits: by default S = 7
+// base-256 digits (55-bit fixed point), or S = 8 base-128 digits (56-bit;
+// option merge_ozaki_digits = 7). Digit products of equal weight i + j = p
+// ("diagonal p") accumulate exactly in int32:
+//   D_p = sum_{i+j=p} A_i B_j^T,   out = 2^(e_l + e_h) sum_p B^-(p+2) D_p
+// keeping p <= S-1 (the dropped terms are ~2^-55 / 2^-56 relative to the
+// row/column maxima: the rounding level of a K-term FP64 dot product;
+// measured max|d| / max|out| 1.1e-15 / 5.7e-16 at K = 16).
 //
 // Diagonal stacking: the B digit slices of one h block are stacked along N
 // (slice j = rows 32j..32j+31), so ONE MMA per A slice i,
@@ -46,14 +48,14 @@ namespace {
 
 // Digit base 2^kDigitBits: 8 -> 7 balanced base-256 digits (|d| <= 128,
 // top digit <= 65), 7 int32 diagonals per output; 7 -> 8 base-128 digits, 8
-// diagonals. The epilogue reads every diagonal of every output from TMEM
-// (64 B/cycle per SM, the K <= 32 bound: DESIGN.md §3), so 7 diagonals cut
-// both that read stream and the digit-pair MMAs (28 instead of 36) by 1/8
-// and 2/9 at the same 2^-55 truncation level.
-// Option "merge_ozaki_digits" selects DB (7 default). Truncation measured in
+// diagonals. 7 diagonals cut the epilogue's TMEM reads and the digit-pair
+// MMAs (28 instead of 36) by 1/8 and 2/9 at twice the truncation.
+// Option "merge_ozaki_digits" selects DB (8 default). Truncation measured in
 // a host emulation: max |error| / (max|a| max|b|) = 2.2e-15 (DB = 8) and
-// 5.6e-16 (DB = 7) over K = 16 terms; on the B200 (tools/ozaki_digits.py,
-// q=30) DB = 8 is 3-4 % faster at K = 16 / 32 and equal at K = 64.
+// 5.6e-16 (DB = 7) over K = 16 terms; on the B200 (tools/ozaki_ab.py, q=30,
+// with the base-256 digit pairs combined in int32 for K <= 32): DB = 8 K=16
+// 3.01 vs 3.27 ms, K=32 4.64 vs 4.89, K=64 7.54 vs 7.69, q=32 K=16 14.0 vs
+// 14.75 ms.
 template <int DB>
 struct Digits {
   static constexpr int S = DB == 8 ? 7 : 8;  // slices
@@ -572,11 +574,21 @@ __global__ void __launch_bounds__(oz_threads<UNIT>(), UNIT ? 2 : 1) ozaki_merge_
               // + D_2 2^8 + D_3, Q1 = D_4 2^16 + D_5 2^8 + D_6 (|Q0| < 2^49,
               // |Q1| < 2^41: exact in int64 and in a double); product =
               // 2^-38 (Q0 + 2^-24 Q1) sa sb
-              const long long a0 = static_cast<long long>(int(d[hc][0][c])) * 256 + int(d[hc][1][c]);
-              const long long a1 = static_cast<long long>(int(d[hc][2][c])) * 256 + int(d[hc][3][c]);
-              const long long a2 = static_cast<long long>(int(d[hc][4][c])) * 256 + int(d[hc][5][c]);
-              q0 = a0 * 65536 + a1 + 0x4338000000000000LL;
-              q1 = a2 * 256 + bias_ext(int(d[hc][6][c]));
+              if constexpr (KS <= 2) {
+                // K <= 32: |D_p| <= 7 * 64 * 2^14 < 2^22.9, so the digit
+                // pairs D_2m 2^8 + D_2m+1 stay exact in int32 (one IMAD each)
+                const int a0 = int(d[hc][0][c]) * 256 + int(d[hc][1][c]);
+                const int a1 = int(d[hc][2][c]) * 256 + int(d[hc][3][c]);
+                const int a2 = int(d[hc][4][c]) * 256 + int(d[hc][5][c]);
+                q0 = static_cast<long long>(a0) * 65536 + bias_ext(a1);
+                q1 = static_cast<long long>(a2) * 256 + bias_ext(int(d[hc][6][c]));
+              } else {
+                const long long a0 = static_cast<long long>(int(d[hc][0][c])) * 256 + int(d[hc][1][c]);
+                const long long a1 = static_cast<long long>(int(d[hc][2][c])) * 256 + int(d[hc][3][c]);
+                const long long a2 = static_cast<long long>(int(d[hc][4][c])) * 256 + int(d[hc][5][c]);
+                q0 = a0 * 65536 + a1 + 0x4338000000000000LL;
+                q1 = a2 * 256 + bias_ext(int(d[hc][6][c]));
+              }
             } else {
               // base 128, 8 diagonals: P_m = 128 D_2m + D_2m+1 (|D_p| < 2^23:
               // exact in int32), Q0 = 2^14 P_0 + P_1, Q1 = 2^14 P_2 + P_3;

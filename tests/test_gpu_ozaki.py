@@ -1,5 +1,5 @@
 """The int8 tensor-core merge (csrc/ozaki.cu: tcgen05.mma kind::i8, exact
-FP64 splitting into 8 base-128 digits) against numpy and against the FP64
+FP64 splitting into 7 base-256 digits by default, or 8 base-128 digits) against numpy and against the FP64
 DFMA kernel: every instantiated K (16, 32, 64) and chunked K (48, 128, 200),
 row ranges (output shards), several slots, accumulate, all-zero and badly
 scaled rows, ineligible shapes falling back to the FP64 kernels, and a
