@@ -95,7 +95,7 @@ struct Options {
   int64_t merge_smem_kb = 96;  // staged-row budget per CTA of the tensor-core merge
   int64_t merge_dmma = 2;  // FP64 tensor-core merge: 1 = four real GEMMs, 2 = three (3M)
   int64_t zero_start_tiles = 1;   // from |0..0>: zero the states once, launch only the tiles that can be non-zero
-  int64_t merge_ozaki = 1;        // int8 tcgen05 merge (exact FP64 splitting) for K >= merge_ozaki_min_k
+  int64_t merge_ozaki = 1;        // int8 tcgen05 merge (exact FP64 splitting) for K >= merge_ozaki_min_k: 1 auto (unit CTAs for K <= 16, else persistent), 2 unit CTAs, 3 persistent; 0 off
   int64_t merge_ozaki_min_k = 16;
   int64_t merge_ozaki_min_work = 27;  // log2 of outputs * K below which the FP64 kernels run
   int64_t merge_ozaki_digits = 8;  // digit bits of the int8 merge: 8 (7 base-256 slices, default: q=30 K=16 3.0 vs 3.27 ms) or 7 (8 base-128 slices, half the truncation)
@@ -442,7 +442,11 @@ int merge_launch_one(int S, int Kc, const int32_t* hidx, const int32_t* lidx, co
         po.coef[2 * t + 1] = coef[2 * src + 1];
       }
       void* o = static_cast<char*>(out) + size_t(s) * size_t(out_slot_stride) * elem_bytes(dtype);
-      cudaError_t e = launch_merge_ozaki(po, row_end - row_begin, o, accumulate, sm_count(), g_opt.merge_ozaki == 2,
+      // short-lived unit CTAs (two per SM) for K <= 16, the persistent
+      // kernel above (tools/ozaki_ab.py merge_ozaki=2,3: q=30 K=16 2.94 vs
+      // 3.04 ms, K=32 4.40 vs 4.25 ms)
+      const bool unit = g_opt.merge_ozaki == 2 || (g_opt.merge_ozaki == 1 && Kc <= 16);
+      cudaError_t e = launch_merge_ozaki(po, row_end - row_begin, o, accumulate, sm_count(), unit,
                                          stream, int(g_opt.merge_ozaki_digits));
       g_launches.fetch_add(3);
       if (e != cudaSuccess) return cuda_fail(e, "merge_ozaki launch");
@@ -1092,7 +1096,7 @@ int cs_set_option(const char* key, int64_t value) {
   } else if (k == "zero_start_tiles") {
     g_opt.zero_start_tiles = value ? 1 : 0;
   } else if (k == "merge_ozaki") {
-    if (value < 0 || value > 2) return fail(CS_ERR_INVALID, "merge_ozaki must be 0, 1 or 2");
+    if (value < 0 || value > 3) return fail(CS_ERR_INVALID, "merge_ozaki must be 0, 1, 2 or 3");
     g_opt.merge_ozaki = value;
   } else if (k == "merge_ozaki_min_work") {
     if (value < 0 || value > 62) return fail(CS_ERR_INVALID, "merge_ozaki_min_work must be 0..62");

@@ -61,7 +61,7 @@ CASES = [  # (K, S, H, W, rows)
 
 
 @pytest.mark.parametrize("digits", [8, 7], ids=["base256", "base128"])
-@pytest.mark.parametrize("mode", [1, 2], ids=["persistent", "unit-ctas"])
+@pytest.mark.parametrize("mode", [3, 2, 1], ids=["persistent", "unit-ctas", "auto"])
 @pytest.mark.parametrize("K,S,H,W,rows", CASES)
 def test_ozaki_vs_numpy_and_dfma(dev, K, S, H, W, rows, mode, digits):
     torch, native = dev
@@ -98,7 +98,7 @@ def test_ozaki_vs_numpy_and_dfma(dev, K, S, H, W, rows, mode, digits):
     assert launches >= 3 * S * min(chunks, 2)
 
 
-@pytest.mark.parametrize("mode", [1, 2], ids=["persistent", "unit-ctas"])
+@pytest.mark.parametrize("mode", [3, 2, 1], ids=["persistent", "unit-ctas", "auto"])
 def test_ozaki_accumulate(dev, mode):
     torch, native = dev
     rng = np.random.default_rng(5)
@@ -133,7 +133,7 @@ def test_ineligible_shapes_fall_back(dev, H, W, rows):
     assert np.abs(got - want).max() <= 1e-13 * np.abs(want).max()
 
 
-@pytest.mark.parametrize("mode", [1, 2], ids=["persistent", "unit-ctas"])
+@pytest.mark.parametrize("mode", [3, 2, 1], ids=["persistent", "unit-ctas", "auto"])
 def test_ozaki_large_product_vs_dfma(dev, mode):
     """q = 28 (14 | 14), K = 16: 4 GiB state, every tile of a full-size grid."""
     torch, native = dev
@@ -159,7 +159,7 @@ def test_ozaki_large_product_vs_dfma(dev, mode):
     assert diff <= 1e-15 * scale * K, (diff, scale)
 
 
-@pytest.mark.parametrize("mode", [1, 2], ids=["persistent", "unit-ctas"])
+@pytest.mark.parametrize("mode", [3, 2, 1], ids=["persistent", "unit-ctas", "auto"])
 def test_ozaki_propagates_non_finite(dev, mode):
     """A NaN or Inf operand gives NaN outputs in its row/column (as the FP64
     kernels do), never a finite value made of saturated digits."""
