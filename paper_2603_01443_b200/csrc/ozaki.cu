@@ -583,11 +583,13 @@ __global__ void __launch_bounds__(oz_threads<UNIT>(), UNIT ? 2 : 1) ozaki_merge_
                 q0 = static_cast<long long>(a0) * 65536 + bias_ext(a1);
                 q1 = static_cast<long long>(a2) * 256 + bias_ext(int(d[hc][6][c]));
               } else {
-                const long long a0 = static_cast<long long>(int(d[hc][0][c])) * 256 + int(d[hc][1][c]);
-                const long long a1 = static_cast<long long>(int(d[hc][2][c])) * 256 + int(d[hc][3][c]);
-                const long long a2 = static_cast<long long>(int(d[hc][4][c])) * 256 + int(d[hc][5][c]);
-                q0 = a0 * 65536 + a1 + 0x4338000000000000LL;
-                q1 = a2 * 256 + bias_ext(int(d[hc][6][c]));
+                // K = 64: |D_p| < 2^23.7, a digit pair may overflow int32;
+                // Horner chains of 32 x 32 -> 64-bit multiply-adds (one
+                // IMAD.WIDE per diagonal) on the biased low diagonal
+                auto wide = [](int x, int m, long long acc) { return static_cast<long long>(x) * m + acc; };
+                q0 = wide(int(d[hc][0][c]), 1 << 24,
+                          wide(int(d[hc][1][c]), 1 << 16, wide(int(d[hc][2][c]), 1 << 8, bias_ext(int(d[hc][3][c])))));
+                q1 = wide(int(d[hc][4][c]), 1 << 16, wide(int(d[hc][5][c]), 1 << 8, bias_ext(int(d[hc][6][c]))));
               }
             } else {
               // base 128, 8 diagonals: P_m = 128 D_2m + D_2m+1 (|D_p| < 2^23:
