@@ -288,3 +288,60 @@ def test_cluster_resident_uncut_small_states(jit_on):
         got = cb.simulate(circ).amps
         assert _native.launch_count() - n0 == 1
         assert np.abs(got - orc.simulate(q, circ.kinds, circ.qa, circ.qb, circ.params)).max() < 1e-10
+
+
+@pytest.mark.gpu
+def test_process_exits_cleanly_while_the_background_compiler_runs():
+    """jit = 3 queues NVRTC compiles on a background thread; a process that
+    exits while one is in flight used to crash inside nvrtcCompileProgram
+    (NVRTC's destructors ran before the library's exit drain). Each child
+    enqueues compiles of never-seen circuits and exits at once."""
+    import subprocess
+    import sys
+    import os
+
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys; sys.path.insert(0, %r)\n"
+            "import paper_2603_01443_b200 as cb\n"
+            "from paper_2603_01443_b200 import _native\n"
+            "_native.set_option('jit', 3)\n"
+            "for s in range(3):\n"
+            "    cb.run_cut(cb.build_brickwall(cb.BrickwallSpec(16, 6, 2, 2, 900 + 7 * s + int(sys.argv[1]))), 2)\n"
+            "print('done')\n") % root
+    for run in range(3):
+        r = subprocess.run([sys.executable, "-c", code, str(run)], capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0 and "done" in r.stdout, (r.returncode, r.stderr[-2000:])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("q,n,c", [(12, 3, 4), (16, 4, 5), (14, 2, 3)])
+def test_sim_families_one_call_matches_per_family(jit_on, q, n, c):
+    """cs_sim_families (every family of a decomposition in one native call,
+    read from the planner's tables, families on forked streams) equals one
+    simulate_family call per family; a family whose template was replaced
+    takes the per-family path."""
+    import torch
+
+    from paper_2603_01443_b200.cutting import GateTable
+    from paper_2603_01443_b200.engine import simulate_family
+    from paper_2603_01443_b200.pipeline import _simulate_families_native, simulate_families
+
+    circ = G.build_brickwall(G.BrickwallSpec(q, 5, n, c, 3))
+    fams = preprocess(circ, n).subs.segments
+    one = _simulate_families_native(fams, np.complex128, 30)
+    assert one is not None and len(one) == n
+    each = [simulate_family(f) for f in fams]
+    torch.cuda.synchronize()
+    for a, b in zip(one, each):
+        assert a.shape == b.shape and torch.equal(a, b)
+    t = fams[1].template
+    fams[1].template = GateTable(t.kinds.copy(), t.qa, t.qb, t.params)
+    assert _simulate_families_native(fams, np.complex128, 30) is None
+    again = simulate_families(fams)
+    torch.cuda.synchronize()
+    for a, b in zip(again, each):
+        assert torch.equal(a, b)
