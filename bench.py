@@ -546,7 +546,8 @@ def run_ours(args):
                    "pageable_numpy": {"ms": t_pageable * 1e3, "value": total / t_pageable,
                                       "max_abs_vs_device_result": pageable_parity,
                                       "note": "one call into a freshly allocated pageable numpy array (the "
-                                              "reference's return type), first-touch page faults included"}}
+                                              "reference's return type), first-touch page faults included; "
+                                              "pinned staging ring + 16 host copy threads (cs_copy_to_host)"}}
         elif world > 1:
             ews = torch.empty(max(shard_workspace_bytes(circ, n, world), 1), dtype=torch.uint8, device="cuda")
             host = torch.empty(end - begin, dtype=torch.complex128, pin_memory=True)

@@ -204,6 +204,14 @@ int cs_cut_run(int32_t nq, const uint8_t* kinds, const int64_t* qa, const int64_
                int32_t force_bond, int64_t out_begin, int64_t out_end, void* out, void* workspace,
                int64_t workspace_bytes, int32_t dtype, void* stream, void* const* stage_events,
                double* stage_ms);
+/* Copy `bytes` of device memory to host memory and return when the host copy
+ * is complete (after the work queued on `stream`). A pinned destination is
+ * one cudaMemcpyAsync; a pageable one (e.g. a numpy array) goes through a
+ * ring of pinned staging buffers drained by a pool of host threads, near the
+ * PCIe rate instead of the driver's pageable path. Replaces the host copy
+ * behind the reference's numpy results (StateVec.amps, engine.py:30-45). */
+int cs_copy_to_host(void* host, const void* device, int64_t bytes, void* stream);
+
 /* The same pipeline delivering the full 2^nq state into HOST memory
  * (host_out: 2^nq amplitudes, ideally pinned) — the reference API's contract
  * of a host-resident result. The merge runs in `chunks` row ranges into two

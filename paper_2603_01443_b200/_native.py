@@ -50,6 +50,7 @@ SIGNATURES = {
     "cs_launch_count": (_i64, []),
     "cs_jit_wait": (ctypes.c_int, [ctypes.c_double]),
     "cs_init_basis": (ctypes.c_int, [_vp, _i32, _i64, _i64, _i32, _vp]),
+    "cs_copy_to_host": (ctypes.c_int, [_vp, _vp, _i64, _vp]),
     "cs_sim_families": (ctypes.c_int, [_i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp]),
     "cs_sim_batch": (ctypes.c_int, [_i32, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _i64, _i64, _u64, _i32,
                                     _i32, _vp]),
