@@ -1907,6 +1907,9 @@ int cs_copy_to_host(void* host, const void* device, int64_t bytes, void* stream)
     e = writer.write(static_cast<char*>(host), static_cast<const char*>(device), size_t(bytes), ready);
     if (e == cudaSuccess) e = writer.finish();
   }
+  // no staging copy may still be in flight when the ring is next used
+  const cudaError_t se = cudaStreamSynchronize(copy_stream());
+  if (e == cudaSuccess) e = se;
   cudaEventDestroy(ready);
   return e == cudaSuccess ? CS_OK : cuda_fail(e, "staged device to host copy");
 }
