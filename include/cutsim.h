@@ -67,8 +67,9 @@ int cs_device_count(int32_t* count);
  * "merge_ozaki" (int8 tcgen05 tensor-core merge with exact FP64 splitting
  * for one-slot products of K >= "merge_ozaki_min_k" terms, lo_len % 128 == 0,
  * row ranges % 16 == 0, outputs * K >= 2^"merge_ozaki_min_work" (default
- * 27: smaller products run faster on the FP64 kernels); 1 = default: short-
- * lived unit CTAs for K <= 16 and the persistent kernel above, 2 = unit CTAs,
+ * 24: smaller products run faster on the FP64 kernels); 1 = default: short-
+ * lived unit CTAs for K <= 16 and >= 2^27 outputs, the persistent kernel
+ * otherwise, 2 = unit CTAs,
  * 3 = persistent, 0 = off; min K 16), "merge_ozaki_digits" (8: 7
  * balanced base-256 digits per operand, 7 int32 diagonals per output,
  * truncation ~1e-15 of max|out| — default, q=30 K=16 in 3.0 ms; 7: 8

@@ -97,7 +97,7 @@ struct Options {
   int64_t zero_start_tiles = 1;   // from |0..0>: zero the states once, launch only the tiles that can be non-zero
   int64_t merge_ozaki = 1;        // int8 tcgen05 merge (exact FP64 splitting) for K >= merge_ozaki_min_k: 1 auto (unit CTAs for K <= 16, else persistent), 2 unit CTAs, 3 persistent; 0 off
   int64_t merge_ozaki_min_k = 16;
-  int64_t merge_ozaki_min_work = 27;  // log2 of outputs * K below which the FP64 kernels run
+  int64_t merge_ozaki_min_work = 24;  // log2 of outputs * K below which the FP64 kernels run
   int64_t merge_ozaki_digits = 8;  // digit bits of the int8 merge: 8 (7 base-256 slices, default: q=30 K=16 3.0 vs 3.27 ms) or 7 (8 base-128 slices, half the truncation)
   int64_t engine = 1;      // 1: register-tile kernel (rsweep), 0: shared-memory tile kernel (sweep)
   int64_t jit = 0;         // 0 never, 1 from a program's 2nd use, 2 always (compile on first use, blocking),
@@ -401,10 +401,10 @@ bool dmma3_eligible(int K, int dtype, int64_t lo_len) {
 }
 
 // merge_ozaki: the int8 tcgen05 kernel (ozaki.cu) for K >= merge_ozaki_min_k
-// and the product is big enough to amortise its two digit-prep launches:
-// outputs * K >= 2^merge_ozaki_min_work (tools/merge_small_q.py: at 2^20
-// outputs the FP64 kernels win every K <= 64, at 2^22 K <= 16, from 2^24 on
-// the int8 kernel wins from K = 16)
+// and the product is big enough to amortise its digit-prep launch:
+// outputs * K >= 2^merge_ozaki_min_work (tools/merge_small_q.py, one
+// combined 4-lane prep launch: q=20 K=16 16 vs 15 us FP64, K=64 23 vs 35;
+// q=22 K=16 27 vs 34; q=24 K=16 61 vs 95; K = 8 stays on the FP64 kernels)
 bool ozaki_eligible(int K, int dtype, int64_t lo_len, int64_t nrows) {
   return g_opt.merge_ozaki && dtype == CS_C128 && K >= g_opt.merge_ozaki_min_k &&
          double(nrows) * double(lo_len) * double(K) >= std::ldexp(1.0, int(g_opt.merge_ozaki_min_work)) &&
@@ -442,10 +442,12 @@ int merge_launch_one(int S, int Kc, const int32_t* hidx, const int32_t* lidx, co
         po.coef[2 * t + 1] = coef[2 * src + 1];
       }
       void* o = static_cast<char*>(out) + size_t(s) * size_t(out_slot_stride) * elem_bytes(dtype);
-      // short-lived unit CTAs (two per SM) for K <= 16, the persistent
-      // kernel above (tools/ozaki_ab.py merge_ozaki=2,3: q=30 K=16 2.94 vs
-      // 3.04 ms, K=32 4.40 vs 4.25 ms)
-      const bool unit = g_opt.merge_ozaki == 2 || (g_opt.merge_ozaki == 1 && Kc <= 16);
+      // short-lived unit CTAs (two per SM) for K <= 16 and >= 2^27 outputs,
+      // the persistent kernel otherwise (tools/ozaki_ab.py merge_ozaki=2,3:
+      // K=16 at q=30 2.97 vs 3.23 ms, q=28 0.74 vs 0.76, q=26 0.215 vs
+      // 0.204, q=24 71 vs 64 us; K=32 at q=30 4.40 vs 4.25 ms)
+      const bool unit = g_opt.merge_ozaki == 2 ||
+                        (g_opt.merge_ozaki == 1 && Kc <= 16 && double(row_end - row_begin) * double(lo_len) >= 0x1p27);
       cudaError_t e = launch_merge_ozaki(po, row_end - row_begin, o, accumulate, sm_count(), unit,
                                          stream, int(g_opt.merge_ozaki_digits));
       g_launches.fetch_add(3);

@@ -212,9 +212,8 @@ __device__ __forceinline__ uint32_t lane_chunk_off(int sub) { return sub < 2 ? 8
 // A (the lo side). adig layout: [l_tile][ks][slice][4096 B canonical block];
 // sa[l] = 2^(e_l + kSaShift)
 template <int KS, int DB>
-__global__ void ozaki_prep_lo(const __grid_constant__ OzPrep p, int8_t* adig, double* sa) {
+__device__ __forceinline__ void ozaki_prep_lo(const OzPrep& p, int64_t gidx, int8_t* adig, double* sa) {
   OZ_DIGIT_CONSTS
-  const int64_t gidx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const int sub = int(gidx & (kPrepLanes - 1));
   const int64_t idx = gidx / kPrepLanes;
   const bool live = idx < p.lo_len * KS;  // the 4 lanes of a group agree; no early exit before the shuffles
@@ -268,9 +267,8 @@ __global__ void ozaki_prep_lo(const __grid_constant__ OzPrep p, int8_t* adig, do
 // B (the hi side with the coefficients). bdig layout: [h_block][ks][slice]
 // [1024 B canonical block], row r = 2 (h % 16) + v; sb[h] = 2^e_h
 template <int KS, int DB>
-__global__ void ozaki_prep_hi(const __grid_constant__ OzPrep p, int64_t nrows, int8_t* bdig, double* sb) {
+__device__ __forceinline__ void ozaki_prep_hi(const OzPrep& p, int64_t gidx, int64_t nrows, int8_t* bdig, double* sb) {
   OZ_DIGIT_CONSTS
-  const int64_t gidx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const int sub = int(gidx & (kPrepLanes - 1));
   const int64_t idx = gidx / kPrepLanes;
   const bool live = idx < nrows * KS;
@@ -343,6 +341,17 @@ __global__ void ozaki_prep_hi(const __grid_constant__ OzPrep p, int64_t nrows, i
     *reinterpret_cast<uint2*>(blk + cm_row_off(2 * hl)) = make_uint2(w0[i][0], w0[i][1]);
     *reinterpret_cast<uint2*>(blk + cm_row_off(2 * hl + 1)) = make_uint2(w1[i][0], w1[i][1]);
   }
+}
+
+// both sides in one launch: blocks [0, lo_blocks) the lo rows, the rest the
+// hi rows (independent work; one launch and no serialisation between them)
+template <int KS, int DB>
+__global__ void __launch_bounds__(128) ozaki_prep(const __grid_constant__ OzPrep p, int64_t nrows, int64_t lo_blocks,
+                                                 int8_t* adig, double* sa, int8_t* bdig, double* sb) {
+  if (int64_t(blockIdx.x) < lo_blocks)
+    ozaki_prep_lo<KS, DB>(p, int64_t(blockIdx.x) * blockDim.x + threadIdx.x, adig, sa);
+  else
+    ozaki_prep_hi<KS, DB>(p, (int64_t(blockIdx.x) - lo_blocks) * blockDim.x + threadIdx.x, nrows, bdig, sb);
 }
 
 struct OzParams {
@@ -686,8 +695,9 @@ cudaError_t run_ozaki(const MergeParams& mp, int64_t nrows, void* out, int accum
     pp.lidx[t] = mp.lidx[t];
     pp.coef[t] = make_double2(mp.coef[2 * t], mp.coef[2 * t + 1]);
   }
-  ozaki_prep_lo<KS, DB><<<unsigned((W * KS * kPrepLanes + 127) / 128), 128, 0, stream>>>(pp, adig, sa);
-  ozaki_prep_hi<KS, DB><<<unsigned((nrows * KS * kPrepLanes + 127) / 128), 128, 0, stream>>>(pp, nrows, bdig, sb);
+  const int64_t lo_blocks = (W * KS * kPrepLanes + 127) / 128;
+  const int64_t hi_blocks = (nrows * KS * kPrepLanes + 127) / 128;
+  ozaki_prep<KS, DB><<<unsigned(lo_blocks + hi_blocks), 128, 0, stream>>>(pp, nrows, lo_blocks, adig, sa, bdig, sb);
   OzParams op;
   op.adig = adig;
   op.bdig = bdig;

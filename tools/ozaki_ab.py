@@ -31,7 +31,10 @@ def timed(fn, reps=8):
 
 
 peak = 6455.6e9
-for q, Ks in ((30, (16, 32, 64)), (32, (16,))):
+CASES = ((30, (16, 32, 64)), (32, (16,)))
+if os.environ.get("OZ_CASES"):  # e.g. OZ_CASES="24:16,26:16,28:16"
+    CASES = tuple((int(a), (int(b),)) for a, b in (c.split(":") for c in os.environ["OZ_CASES"].split(",")))
+for q, Ks in CASES:
     out = torch.empty(1 << q, dtype=torch.complex128, device="cuda")
     g = torch.Generator(device="cuda").manual_seed(0)
     for K in Ks:
@@ -53,7 +56,7 @@ for q, Ks in ((30, (16, 32, 64)), (32, (16,))):
                 errs[c] = (out[: 1 << 26] - ref).abs().max().item() / ref.abs().max().item()
         floor = 16 * (1 << q) / peak * 1e3
         print(f"q={q} K={K} | " + " | ".join(
-            ",".join(f"{n}={v}" for (n, _), v in zip(opts, c)) + f": {best[c]:.3f} ms ({floor / best[c] * 100:.1f}%) err {errs[c]:.1e}"
+            ",".join(f"{n}={v}" for (n, _), v in zip(opts, c)) + f": {best[c]:.4f} ms ({floor / best[c] * 100:.1f}%) err {errs[c]:.1e}"
             for c in combos), flush=True)
         del hi, lo
     del out
