@@ -191,7 +191,8 @@ def run_cut(circuit: Circuit, n: int, *, dtype=np.complex128, max_qubits: int = 
     evp = None
     if events is not None:
         for ev in events:
-            ev.record()  # materialise the underlying cudaEvent_t
+            if not ev.cuda_event:  # torch creates the cudaEvent_t on first record
+                ev.record()
         evp = (ctypes.c_void_p * 3)(*(ev.cuda_event for ev in events))
     _native.check(
         _native.load().cs_cut_run(q, _native.ptr(k), _native.ptr(qa), _native.ptr(qb), _native.ptr(prm), len(k),
@@ -248,7 +249,8 @@ def run_cut_sharded_native(circuit: Circuit, n: int, *, rank: int = 0, world: in
     evp = None
     if events is not None:
         for ev in events:
-            ev.record()
+            if not ev.cuda_event:  # torch creates the cudaEvent_t on first record
+                ev.record()
         evp = (ctypes.c_void_p * 4)(*(ev.cuda_event for ev in events))
     handle = comm.handle if comm is not None else None
     _native.check(
