@@ -38,8 +38,6 @@ _LAW = "reference CPU cost law: "
 KNOWN: dict[str, str] = {
     "TestMeasuredInvariants::test_merge_time_slope_in_cut_count":
         _LAW + "log2 t_merge vs c_total slope ~1 at q=14 (GPU merge of a 2^14 state is launch-bound, flat in c)",
-    "TestMeasuredInvariants::test_sub_faster_than_orig_inside_threshold":
-        _LAW + "t_sub < t_orig at q=16 (both ~0.2 ms of launch latency on the GPU)",
     "TestMeasuredInvariants::test_heatmap_sign_extremes":
         _LAW + "cutting wins at q=20, c=1 (GPU uncut q=20 takes ~0.25 ms, below the cut path's host work)",
     "TestMeasuredInvariants::test_depth_sweep_slope_stability":
@@ -63,6 +61,8 @@ KNOWN: dict[str, str] = {
 def pytest_collection_modifyitems(config, items):
     import pytest
 
+    if os.environ.get("CUTSIM_REFSUITE_NOSKIP") == "1":  # diagnostics: run the KNOWN tests too
+        return
     for item in items:
         for suffix, why in KNOWN.items():
             if item.nodeid.endswith(suffix):
