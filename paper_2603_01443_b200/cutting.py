@@ -198,7 +198,7 @@ def _families_from_tables(plan: CutPlan, nt) -> list[SegmentFamily]:
         # where the template sits in the C++ planner's concatenated tables:
         # pipeline.simulate_families runs all families of one decomposition
         # in one native call straight from them (while the template is unchanged)
-        fam._src = (nt, g0, m, tab.kinds, slots)
+        fam._src = (nt, g0, m, tab, (tab.kinds, tab.qa, tab.qb, tab.params), slots)
         fams.append(fam)
         g0 += m
         c0 += nc
@@ -258,7 +258,7 @@ class SegmentFamily:
     def __post_init__(self):
         self.circuits = _VariantCircuits(self)
         self._pending = {}  # dtype -> (device batch, variants not yet handed out)
-        self._src = None  # (planner tables, first row, rows, kinds view, slots) when from the C++ planner
+        self._src = None  # (planner tables, first row, rows, template, its columns, slots) from the C++ planner
 
     def claim_state(self, b: int, dtype, simulate_batch):
         """Variant b's state from one batched simulation of the whole family.

@@ -98,9 +98,14 @@ def _simulate_families_native(fams, dtype, max_qubits):
     nt = src0[0]
     g = 0
     for f in fams:
-        src = f._src
-        if src is None or src[0] is not nt or src[1] != g or f.template.kinds is not src[3] or f.slots is not src[4]:
+        src = getattr(f, "_src", None)
+        if src is None or src[0] is not nt or src[1] != g or f.slots is not src[5]:
             return None
+        t_ = f.template
+        cols = src[4]
+        if t_ is not src[3] or t_.kinds is not cols[0] or t_.qa is not cols[1] or t_.qb is not cols[2] \
+                or t_.params is not cols[3]:
+            return None  # the template (or a column of it) was replaced: not the planner's tables any more
         g += src[2]
     for f in fams:
         check_capacity(f.num_qubits, max_qubits)
