@@ -700,14 +700,17 @@ def measure_uncut(cb, circ, q, stream, peak):
     _native.jit_wait(600)
     cb.simulate(circ, max_qubits=q)
     torch.cuda.synchronize()
-    u0 = torch.cuda.Event(enable_timing=True)
-    u1 = torch.cuda.Event(enable_timing=True)
-    u0.record(stream)
-    sv = cb.simulate(circ, max_qubits=q)
-    u1.record(stream)
-    u1.synchronize()
-    ms = u0.elapsed_time(u1)
-    del sv
+    runs = []
+    for _ in range(3):  # median of three (a single run caught a 2.8x outlier once)
+        u0 = torch.cuda.Event(enable_timing=True)
+        u1 = torch.cuda.Event(enable_timing=True)
+        u0.record(stream)
+        sv = cb.simulate(circ, max_qubits=q)
+        u1.record(stream)
+        u1.synchronize()
+        runs.append(u0.elapsed_time(u1))
+        del sv
+    ms = float(np.median(runs))
     # started from |0..0>, sweep k launches only its 2^z_k tiles that can be
     # non-zero (the state is zeroed once: 16 B per amplitude written), so the
     # algorithmic traffic is 32 B per amplitude of the launched tiles
