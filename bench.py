@@ -619,6 +619,7 @@ def run_ours(args):
             if world > 1 else "1 GPU", "bond": bond,
             "stage_ms": stage,
             "stage_ms_sync": stage_sync,
+            "variant_stage": variant_stage_rates(prep0, stage),
             "parity": parity,
             "cold": cold,
             "uncut_ms": uncut["ms"] if uncut else None,
@@ -687,6 +688,21 @@ def measure_cold(cb, spec, out, workspace, steps):
                     "has not seen, timed on the host wall clock around a synchronised run_cut: C++ "
                     "preprocess, sweep schedules, and the variant stage on the interpreter kernel while the "
                     "circuit's NVRTC modules compile in the background (jit = 3)"}
+
+
+def variant_stage_rates(prep, stage):
+    """The subcircuit stage's own rates (on-chip work, not
+    an HBM item): gate applications (variant states x template gates, cut
+    insertions included) and amplitude updates (x 2^q_i) per second of the
+    steady-state stage time."""
+    if not stage or not stage.get("sub"):
+        return None
+    t = stage["sub"] / 1e3
+    gates = sum(f.num_variants * len(f.template) for f in prep.subs.segments)
+    amps = sum(f.num_variants * len(f.template) * (1 << f.num_qubits) for f in prep.subs.segments)
+    states = sum(f.num_variants for f in prep.subs.segments)
+    return {"us": stage["sub"] * 1e3, "variant_states": states, "gate_applications_per_s": gates / t,
+            "amplitude_updates_per_s": amps / t}
 
 
 def measure_uncut(cb, circ, q, stream, peak):
