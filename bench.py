@@ -268,7 +268,7 @@ def run_cpu_leg(args):
         r = cpu_step(spec, 1, frac)
         whole = frac >= 1.0
         res["cpu_baseline"] = {
-            "value": r["value"], "unit": UNIT, "cores": 1, "kind": "port",
+            "value": r["value"], "unit": UNIT, "cores": 1, "host_cpus": os.cpu_count(), "kind": "port",
             "sample": (f"one full step of the reference algorithm on 1 host thread (its protocol, "
                        f"engine.py:4-7): preprocess, all subcircuit states, the whole merge "
                        f"(zero-fill + one RMW pass per term, {r['rows_total']} rows); nothing extrapolated"
@@ -317,7 +317,7 @@ def run_reference(args):
         "stage_ms": {"pre": 1e3 * float(np.mean([s["t_pre"] for s in steps])),
                      "sub": 1e3 * float(np.mean([s["t_sub"] for s in steps])),
                      "merge": 1e3 * float(np.mean([s["t_merge"] for s in steps]))},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "host_cpus": os.cpu_count(), "kind": "port",
                          "sample": sample, "wall_s": wall},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
