@@ -268,7 +268,7 @@ def run_cpu_leg(args):
         r = cpu_step(spec, 1, frac)
         whole = frac >= 1.0
         res["cpu_baseline"] = {
-            "value": r["value"], "unit": UNIT, "cores": 1, "host_cpus": os.cpu_count(), "kind": "port",
+            "value": r["value"], "unit": UNIT, "cores": 1, "kind": "port",
             "sample": (f"one full step of the reference algorithm on 1 host thread (its protocol, "
                        f"engine.py:4-7): preprocess, all subcircuit states, the whole merge "
                        f"(zero-fill + one RMW pass per term, {r['rows_total']} rows); nothing extrapolated"
