@@ -312,6 +312,29 @@ def test_compute_entry_points_fail_loudly_without_gpu():
         engine.simulate(C.Circuit(2, [C.h(0)]))
 
 
+def test_family_fast_path_needs_the_planner_tables_and_fails_loudly_without_gpu():
+    """pipeline.simulate_families runs a C++-planned decomposition's families
+    in one native call only while every template column is still the
+    planner's own array (identity, not equality); without a GPU that path
+    raises instead of falling back."""
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2603_01443_b200 import generators as G
+    from paper_2603_01443_b200.cutting import decompose, plan_cut
+    from paper_2603_01443_b200.pipeline import _simulate_families_native
+
+    circ = G.build_brickwall(G.BrickwallSpec(12, 4, 2, 2, 0))
+    fams = decompose(circ, plan_cut(circ, 2)).segments
+    with pytest.raises(NativeUnavailableError):
+        _simulate_families_native(fams, np.complex128, 30)
+    fams[1].template.qa = fams[1].template.qa.copy()  # same values, not the planner's array
+    assert _simulate_families_native(fams, np.complex128, 30) is None
+    fams2 = decompose(circ, plan_cut(circ, 2)).segments
+    assert _simulate_families_native(fams2[1:], np.complex128, 30) is None  # not from the first row
+
+
 def execute_reg_programs(plan, nq, variant=0):
     """Interpret the register-tile programs (rsweep kernel input) on a full
     numpy state: tile bit b is qubit b (< L) or hq[b - L]; register bit k is
