@@ -76,7 +76,10 @@ int cs_device_count(int32_t* count);
  * base-128 digits, 8 diagonals, ~6e-16, 8 % slower at K = 16), "cluster" (cluster-resident
  * variant batches: one NVRTC kernel per program, the 2^12..2^16-amplitude
  * states in the distributed shared memory of a CTA cluster; default 1),
- * "cluster_max" (CTAs per cluster at most: 2..16, default 16),
+ * "cluster_max" (CTAs per cluster at most: 2..16, default 16), "cluster_loop"
+ * (the ahead-of-time cluster kernel that reads the program as an op stream,
+ * cluster.cu: 1 = default, while a new program's NVRTC cluster kernel
+ * compiles (it replaces the per-launch interpreter there); 2 = always; 0 = off),
  * "zero_start_tiles" (simulations
  * from |0..0> zero the states once and launch only the tiles that can be
  * non-zero; default 1),

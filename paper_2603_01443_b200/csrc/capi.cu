@@ -23,6 +23,7 @@
 #include "ops.hpp"
 #include "plan.hpp"
 #include "jit.hpp"
+#include "cluster.hpp"
 
 #include <nvtx3/nvToolsExt.h>
 
@@ -104,6 +105,7 @@ struct Options {
                            // 3 tiered: the interpreter runs while the module compiles on a background thread
   int64_t cluster = 1;      // cluster-resident variant batches (one kernel, states in DSMEM) with the NVRTC kernels
   int64_t cluster_max = 16; // CTAs per cluster at most (16 = the non-portable size)
+  int64_t cluster_loop = 1; // cluster.cu's op-stream kernel: 1 = until the NVRTC cluster kernel is compiled, 2 = always
   int64_t jit_struct = 1;  // param-mode (structure-keyed) modules: 0 never, 1 for small programs (< 2^22
                            // amplitudes: variant batches), 2 always
   int64_t jit_max_cost = 40000;  // FP64 instructions per specialised launch (code-size guard)
@@ -250,6 +252,9 @@ struct Program {
   int64_t n_states = 1;  // states per launch the program was scheduled for
   bool param_mode = false;  // structure-keyed kernels with the coefficients as kernel parameters
   int cluster_bits = 0;     // > 0: every sweep tiles the state into 2^cluster_bits tiles (one per cluster CTA)
+  // cluster_loop: the program as an op stream for cluster.cu's
+  // ahead-of-time kernel (null: the NVRTC cluster kernel / per-launch form)
+  std::unique_ptr<ClusterBlob> cloop;
 };
 
 // content-keyed program cache with least-recently-used eviction (a clear-all
@@ -331,9 +336,9 @@ std::shared_ptr<const Program> build_schedule(int nq, const uint8_t* kinds, cons
                                                  zero_start_pays(n_states, nq)))
                           ? 1
                           : g_sweep_windows;
-  const int32_t hdr[15] = {nq, T, L, int32_t(fuse), slots ? 1 : 0, dtype, vb, g_sweep_minb,
+  const int32_t hdr[16] = {nq, T, L, int32_t(fuse), slots ? 1 : 0, dtype, vb, g_sweep_minb,
                            int32_t(g_opt.engine), norm, g_reg_bits * 8 + g_reg_reorder * 4 + windows, g_jit_minb,
-                           g_jit_persistent, param_mode ? 1 : 0, cb};
+                           g_jit_persistent, param_mode ? 1 : 0, cb, int32_t(g_opt.cluster_loop)};
   key.append(reinterpret_cast<const char*>(hdr), sizeof(hdr));
   key.append(reinterpret_cast<const char*>(kinds), size_t(n_gates));
   key.append(reinterpret_cast<const char*>(qa), size_t(n_gates) * 8);
@@ -362,6 +367,17 @@ std::shared_ptr<const Program> build_schedule(int nq, const uint8_t* kinds, cons
   built->cluster_bits = cb;
   built->sweeps = schedule_sweeps(ops, nq, T, L, max_group, windows);
   build_launches(*built);
+  if (cb > 0 && g_opt.cluster_loop && built->engine == 1) {
+    std::vector<const Sweep*> sw;
+    std::vector<const std::vector<RegOp>*> rp;
+    for (const Launch& ln : built->launches) {
+      sw.push_back(&built->sweeps[size_t(ln.sweep)]);
+      rp.push_back(&ln.reg);
+    }
+    auto cl = std::make_unique<ClusterBlob>();
+    std::string why;
+    if (cluster_blob_build(sw, rp, T, dtype, cl.get(), &why)) built->cloop = std::move(cl);
+  }
   std::shared_ptr<const Program> prog = built;
   std::lock_guard<std::mutex> lk(g_cache_mu);
   if (g_cache.size() >= kProgramCacheCap) {
@@ -759,6 +775,8 @@ std::shared_ptr<JitModule> program_jit(const std::shared_ptr<const Program>& pp,
   return prog.jit;
 }
 
+std::mutex g_cluster_launch_mu;  // launch_cluster_prog's static parameter blocks
+
 // deadline_s > 0: CLOCK_MONOTONIC seconds (Python's time.monotonic()); the
 // stream is synchronised after every launch and CS_ERR_TIMEOUT returned once
 // it has passed (the reference's cooperative budget, engine.py:142-155)
@@ -766,7 +784,25 @@ int run_program(const std::shared_ptr<const Program>& prog_ptr, int nq, void* st
                 int64_t state_stride, uint64_t variant_base, int init_zero, int dtype, cudaStream_t st,
                 double deadline_s = 0.0) {
   const Program* prog = prog_ptr.get();
+  // cluster-resident op-stream kernel (cluster.cu): no NVRTC, one launch.
+  // cluster_loop 1: the first tier while the NVRTC cluster kernel compiles
+  // (it replaces the per-launch interpreter there); 2: always
+  auto run_cloop = [&]() -> int {
+    std::lock_guard<std::mutex> lk(g_cluster_launch_mu);
+    for (int64_t v0 = 0; v0 < n_states; v0 += 65535) {
+      const int64_t vc = std::min<int64_t>(65535, n_states - v0);
+      void* sp = static_cast<char*>(states) + size_t(v0) * size_t(state_stride) * elem_bytes(dtype);
+      const cudaError_t e =
+          launch_cluster_prog(*prog->cloop, sp, state_stride, variant_base + uint64_t(v0), uint32_t(vc), st);
+      g_launches.fetch_add(1);
+      if (e != cudaSuccess) return cuda_fail(e, "cluster program launch");
+    }
+    return CS_OK;
+  };
+  const bool cloop_ok = prog->cloop && deadline_s <= 0.0;
+  if (cloop_ok && g_opt.cluster_loop == 2) return run_cloop();
   std::shared_ptr<JitModule> jit = program_jit(prog_ptr, dtype);
+  if (cloop_ok && !jit) return run_cloop();
   static SweepParams p;
   static RegParams rp;
   static std::mutex pm;
@@ -1118,6 +1154,9 @@ int cs_set_option(const char* key, int64_t value) {
     g_opt.merge_ozaki_digits = value;
   } else if (k == "cluster") {
     g_opt.cluster = value ? 1 : 0;
+  } else if (k == "cluster_loop") {
+    if (value < 0 || value > 2) return fail(CS_ERR_INVALID, "cluster_loop must be 0, 1 or 2");
+    g_opt.cluster_loop = value;
   } else if (k == "cluster_max") {
     if (value != 2 && value != 4 && value != 8 && value != 16) return fail(CS_ERR_INVALID, "cluster_max must be 2, 4, 8 or 16");
     g_opt.cluster_max = value;
@@ -1155,6 +1194,7 @@ int64_t cs_get_option(const char* key) {
   if (k == "jit_struct") return g_opt.jit_struct;
   if (k == "cluster") return g_opt.cluster;
   if (k == "cluster_max") return g_opt.cluster_max;
+  if (k == "cluster_loop") return g_opt.cluster_loop;
   if (k == "merge_ozaki_digits") return g_opt.merge_ozaki_digits;
   if (k == "jit_units_compiled") return jit_units_compiled();
   if (k == "jit_units_reused") return jit_units_reused();
