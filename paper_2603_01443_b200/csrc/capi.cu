@@ -288,9 +288,18 @@ void build_launches(Program& prog) {
       l.sweep = int(s);
       l.entries.assign(sw.entries.begin() + long(i0), sw.entries.begin() + long(i1));
       if (prog.engine == 1) {
-        Sweep part = sw;
-        part.entries = l.entries;
-        l.reg = reg_program(part, reg_bits_for(sw.tile_bits));
+        if (i0 == 0 && i1 == sw.entries.size()) {
+          l.reg = reg_program(sw, reg_bits_for(sw.tile_bits));
+        } else {
+          Sweep part;
+          part.tile_bits = sw.tile_bits;
+          part.low_bits = sw.low_bits;
+          part.hq = sw.hq;
+          part.oq = sw.oq;
+          part.zero_tiles_log2 = sw.zero_tiles_log2;
+          part.entries = l.entries;
+          l.reg = reg_program(part, reg_bits_for(sw.tile_bits));
+        }
       }
       prog.launches.push_back(std::move(l));
       i0 = i1;

@@ -824,15 +824,6 @@ namespace {
 // diagonal does not touch the dense target; two dense ops when neither
 // target is a qubit (target or control) of the other. Tile-local masks
 // only: outside-tile bits are constants within a tile.
-bool commutes(const SweepOp& a, const SweepOp& b) {
-  const bool da = a.type == OP_DENSE, db = b.type == OP_DENSE;
-  if (!da && !db) return true;
-  if (da && !db) return ((b.lmask >> a.target) & 1u) == 0;
-  if (!da && db) return ((a.lmask >> b.target) & 1u) == 0;
-  if (a.target == b.target) return false;
-  return ((b.lmask >> a.target) & 1u) == 0 && ((a.lmask >> b.target) & 1u) == 0;
-}
-
 // The sweep's ops (a slotted op = two consecutive entries) in an order that
 // needs fewer register remaps: list scheduling over the commutation DAG that
 // prefers any ready op whose dense target is already a register bit, and on
@@ -840,16 +831,50 @@ bool commutes(const SweepOp& a, const SweepOp& b) {
 // program order. Returns entry-index starts of the units in the new order.
 std::vector<size_t> reorder_for_registers(const std::vector<SweepOp>& E, int RB, const int* rpos0, int T) {
   std::vector<size_t> start;
+  start.reserve(E.size());
   for (size_t i = 0; i < E.size(); i += (E[i].slot >= 0 ? 2 : 1)) start.push_back(i);
   const size_t n = start.size();
-  std::vector<std::vector<int>> succ(n);
-  std::vector<int> npred(n, 0);
-  for (size_t j = 0; j < n; ++j)
-    for (size_t i = 0; i < j; ++i)
-      if (!commutes(E[start[i]], E[start[j]])) {
-        succ[i].push_back(int(j));
-        ++npred[j];
-      }
+  // Dependence edges with the same transitive closure as "i < j do not
+  // commute" (commutes() above), found per tile bit instead of over all
+  // pairs: a dense op acts as X on its target and Z on its controls, a
+  // diagonal op as Z on its bits; two ops conflict iff one's X bit is the
+  // other's X or Z bit. Per bit, an op depends on the bit's last X op and,
+  // if it is X there, on the Z ops since. Readiness under list scheduling
+  // is that of the full relation (every dropped edge is implied by a chain).
+  std::vector<uint64_t> pairs;
+  pairs.reserve(n * 4);
+  std::vector<int> npred(n, 0), soff(n + 1, 0);
+  int last_x[32];
+  std::vector<int> zs[32];
+  for (int b = 0; b < 32; ++b) last_x[b] = -1;
+  auto edge = [&](int i, size_t j) {
+    pairs.push_back(uint64_t(i) << 32 | uint64_t(j));
+    ++soff[size_t(i) + 1];
+    ++npred[j];
+  };
+  for (size_t j = 0; j < n; ++j) {
+    const SweepOp& e = E[start[j]];
+    const bool dense = e.type == OP_DENSE;
+    uint32_t zmask = e.lmask & 0xffffffffu;
+    if (dense) {
+      const int t = e.target;
+      if (last_x[t] >= 0) edge(last_x[t], j);
+      for (int i : zs[t]) edge(i, j);
+      zmask &= ~(1u << t);
+    }
+    for (uint32_t m = zmask; m; m &= m - 1) {
+      const int b = __builtin_ctz(m);
+      if (last_x[b] >= 0) edge(last_x[b], j);
+    }
+    if (dense) {
+      last_x[e.target] = int(j);
+      zs[e.target].clear();
+    }
+    for (uint32_t m = zmask; m; m &= m - 1) zs[__builtin_ctz(m)].push_back(int(j));
+  }
+  for (size_t i = 0; i < n; ++i) soff[i + 1] += soff[i];
+  std::vector<int> succ(pairs.size()), fill(soff.begin(), soff.end() - 1);
+  for (uint64_t pr : pairs) succ[size_t(fill[size_t(pr >> 32)]++)] = int(pr & 0xffffffffu);
   std::vector<char> done(n, 0);
   std::vector<size_t> order;
   order.reserve(n);
@@ -858,7 +883,7 @@ std::vector<size_t> reorder_for_registers(const std::vector<SweepOp>& E, int RB,
   auto take = [&](size_t u) {
     done[u] = 1;
     order.push_back(start[u]);
-    for (int v : succ[u]) --npred[v];
+    for (int s = soff[u]; s < soff[u + 1]; ++s) --npred[size_t(succ[size_t(s)])];
   };
   while (order.size() < n) {
     bool progress = true;
@@ -907,9 +932,11 @@ std::vector<RegOp> reg_program(const Sweep& sw, int RB) {
   for (int k = 0; k < RB; ++k) map.rpos[k] = T - RB + k;
   map.build();
   std::vector<RegOp> out;
+  out.reserve(sw.entries.size() + 16);
   // optionally reorder the sweep's commuting ops so fewer remaps are needed
   std::vector<SweepOp> reordered;
   if (g_reg_reorder) {
+    reordered.reserve(sw.entries.size());
     const std::vector<size_t> order = reorder_for_registers(sw.entries, RB, map.rpos, T);
     for (size_t st : order) {
       reordered.push_back(sw.entries[st]);
