@@ -1188,15 +1188,25 @@ static cudaError_t launch_rsweep_cap(const RegParamsT<CAP>& p, int rb, uint32_t 
   }
 }
 
+// The launch copies the whole parameter block, so its host cost grows with
+// the capacity (32 KiB at kMaxRegOps: ~15 us more per launch than 4 KiB,
+// tools/sub_host_split.py): launch through the smallest capacity tier that
+// holds the program.
+template <typename R, int CAP>
+static cudaError_t launch_rsweep_tier(const RegParams& p, int rb, uint32_t n_tiles, uint32_t n_states,
+                                      cudaStream_t stream) {
+  static RegParamsT<CAP> ps;  // launch copies it; callers hold capi's lock
+  std::memcpy(&ps, &p, offsetof(RegParams, ops));
+  std::memcpy(ps.ops, p.ops, sizeof(RegOp) * size_t(p.n_ops));
+  return launch_rsweep_cap<R, CAP>(ps, rb, n_tiles, n_states, stream);
+}
+
 template <typename R>
 static cudaError_t launch_rsweep_t(const RegParams& p, int rb, uint32_t n_tiles, uint32_t n_states,
                                    cudaStream_t stream) {
-  if (p.n_ops <= kSmallOps) {
-    static RegParamsSmall ps;  // launch copies it; callers hold capi's lock
-    std::memcpy(&ps, &p, offsetof(RegParams, ops));
-    std::memcpy(ps.ops, p.ops, sizeof(RegOp) * size_t(p.n_ops));
-    return launch_rsweep_cap<R, kSmallOps>(ps, rb, n_tiles, n_states, stream);
-  }
+  if (p.n_ops <= kSmallOps) return launch_rsweep_tier<R, kSmallOps>(p, rb, n_tiles, n_states, stream);
+  if (p.n_ops <= kMidRegOps) return launch_rsweep_tier<R, kMidRegOps>(p, rb, n_tiles, n_states, stream);
+  if (p.n_ops <= kLargeRegOps) return launch_rsweep_tier<R, kLargeRegOps>(p, rb, n_tiles, n_states, stream);
   return launch_rsweep_cap<R, kMaxRegOps>(p, rb, n_tiles, n_states, stream);
 }
 

@@ -78,6 +78,8 @@ struct alignas(16) RegOp {
 };
 static_assert(sizeof(RegOp) == 96, "RegOp layout");
 constexpr int kMaxRegOps = 320;        // RegParams under the 32 KiB param limit
+constexpr int kMidRegOps = 96;         // launch tiers between kSmallOps and kMaxRegOps (9 / 17 KiB)
+constexpr int kLargeRegOps = 176;
 
 template <int CAP>
 struct RegParamsT {
