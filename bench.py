@@ -728,12 +728,17 @@ def measure_uncut(cb, circ, q, stream, peak):
         del sv
     ms = float(np.median(runs))
     # started from |0..0>, sweep k launches only its 2^z_k tiles that can be
-    # non-zero (the state is zeroed once: 16 B per amplitude written), so the
-    # algorithmic traffic is 32 B per amplitude of the launched tiles
+    # non-zero and writes them whole (16 B per amplitude); it reads only the
+    # amplitudes whose tile-local qubits some earlier sweep held (zero_skip:
+    # a fraction 2^-popcount(zl_k) of the launched ones; the first sweep starts
+    # in registers), and the state is zeroed first (16 B per amplitude) only
+    # when the sweeps do not hold every qubit
     plan = json.loads(_native.sweep_plan_json(q, circ.table))
     sparse = _native.get_option("zero_start_tiles") == 1
-    n_dense = amps_swept = dense_amps = 0
-    for sw in plan["sweeps"]:
+    skip = sparse and _native.get_option("zero_skip") == 1
+    n_dense = amps_swept = amps_read = dense_amps = 0
+    held = 0
+    for k, sw in enumerate(plan["sweeps"]):
         ents, i, nd = sw["entries"], 0, 0
         while i < len(ents):  # a slotted op occupies two entries
             nd += ents[i]["type"] == 0
@@ -741,18 +746,24 @@ def measure_uncut(cb, circ, q, stream, peak):
         amps = (1 << (sw["z"] if sparse else q - sw["T"])) << sw["T"]
         n_dense += nd
         amps_swept += amps
+        amps_read += 0 if k == 0 else (amps >> bin(sw["zl"]).count("1") if skip else amps)
         dense_amps += nd * amps
+        for g in list(range(sw["L"])) + list(sw["hq"]):
+            held |= 1 << g
     t = ms / 1e3
     total = 1 << q
-    traffic = 32.0 * amps_swept + (16.0 * total if sparse else 0.0)
+    zeroed = sparse and not (skip and held == total - 1)
+    traffic = 16.0 * (amps_swept + amps_read) + (16.0 * total if zeroed else 0.0)
     return {"ms": ms, "sweeps": len(plan["sweeps"]), "dense_ops": n_dense,
             "sweeps_full_equivalent": amps_swept / total,
             "hbm_gbs": traffic / t / 1e9, "hbm_frac": traffic / t / 1e9 / peak,
             "fp64_tflops_executed": 8.0 * dense_amps / t / 1e12,
             "fp64_frac_of_dfma_peak": 8.0 * dense_amps / t / 1e12 / DFMA_PEAK_TF,
             "fp64_tflops_algorithmic_info": 16.0 * dense_amps / t / 1e12,
-            "note": "HBM: 32 B/amplitude per launched tile per sweep (read+write) + the 16 B/amplitude zeroing "
-                    "(only the tiles that can be non-zero from |0..0> launch). FP64 executed: the normalised "
+            "reads_full_equivalent": amps_read / total, "zeroing_pass": zeroed,
+            "note": "HBM: 16 B/amplitude written per launched tile per sweep + 16 B/amplitude read where the "
+                    "tile-local qubits were held by an earlier sweep (only the tiles that can be non-zero from "
+                    "|0..0> launch; no zeroing pass when the sweeps hold every qubit). FP64 executed: the normalised "
                     "2x2s run 4 DFMA (8 flop) per amplitude per dense op, against the 36.5 TF/s DFMA peak "
                     "measured with tools/fp64_peak.cu (ncu: FP64 pipe 92.8 % on the support-completing sweep, "
                     "profiles/r01_uncut_sweep12_ncu_full.json); the algorithmic 16 flop/amplitude/op figure "

@@ -82,7 +82,10 @@ int cs_device_count(int32_t* count);
  * compiles (it replaces the per-launch interpreter there); 2 = always; 0 = off),
  * "zero_start_tiles" (simulations
  * from |0..0> zero the states once and launch only the tiles that can be
- * non-zero; default 1),
+ * non-zero; default 1), "zero_skip" (with zero-start tiles and the register-tile
+ * kernels: a sweep does not load the amplitudes its tile-local zero mask marks as
+ * still 0, and the zeroing pass is dropped when the sweeps hold every qubit;
+ * default 1),
  * "jit_max_cost", "vb", "sweep_minb", "merge_smem_kb", "merge_dmma3_warps", "jit_minb", "dense_norm" (normalised 2x2s:
  * 0 off, 1 on, 2 = with the NVRTC kernels), "reg_bits", "plan_json" (tuning /
  * testing). */

@@ -96,6 +96,7 @@ struct Options {
   int64_t merge_smem_kb = 96;  // staged-row budget per CTA of the tensor-core merge
   int64_t merge_dmma = 2;  // FP64 tensor-core merge: 1 = four real GEMMs, 2 = three (3M)
   int64_t zero_start_tiles = 1;   // from |0..0>: zero the states once, launch only the tiles that can be non-zero
+  int64_t zero_skip = 1;  // with zero-start tiles: skip loads of still-zero amplitudes, and the zeroing when the sweeps hold every qubit
   int64_t merge_ozaki = 1;        // int8 tcgen05 merge (exact FP64 splitting) for K >= merge_ozaki_min_k: 1 auto (unit CTAs for K <= 16, else persistent), 2 unit CTAs, 3 persistent; 0 off
   int64_t merge_ozaki_min_k = 16;
   int64_t merge_ozaki_min_work = 24;  // log2 of outputs * K below which the FP64 kernels run
@@ -252,6 +253,10 @@ struct Program {
   int64_t n_states = 1;  // states per launch the program was scheduled for
   bool param_mode = false;  // structure-keyed kernels with the coefficients as kernel parameters
   int cluster_bits = 0;     // > 0: every sweep tiles the state into 2^cluster_bits tiles (one per cluster CTA)
+  // the sweeps' tiles together hold every qubit: a start from |0..0> with
+  // zero-start tiles writes every amplitude and never reads one before it
+  // was written (Sweep::zero_local_mask), so the states need no zeroing
+  bool covers_all_qubits = false;
   // cluster_loop: the program as an op stream for cluster.cu's
   // ahead-of-time kernel (null: the NVRTC cluster kernel / per-launch form)
   std::unique_ptr<ClusterBlob> cloop;
@@ -375,6 +380,14 @@ std::shared_ptr<const Program> build_schedule(int nq, const uint8_t* kinds, cons
   built->param_mode = param_mode;
   built->cluster_bits = cb;
   built->sweeps = schedule_sweeps(ops, nq, T, L, max_group, windows);
+  {
+    uint64_t held = 0;
+    for (const Sweep& sw : built->sweeps) {
+      for (int q = 0; q < sw.low_bits; ++q) held |= 1ull << q;
+      for (int q : sw.hq) held |= 1ull << q;
+    }
+    built->covers_all_qubits = held == (nq >= 64 ? ~0ull : (1ull << nq) - 1ull);
+  }
   build_launches(*built);
   if (cb > 0 && g_opt.cluster_loop && built->engine == 1) {
     std::vector<const Sweep*> sw;
@@ -826,7 +839,12 @@ int run_program(const std::shared_ptr<const Program>& prog_ptr, int nq, void* st
                         const Sweep& s0 = prog->sweeps[size_t(l.sweep)];
                         return s0.zero_tiles_log2 < nq - s0.tile_bits;
                       });
-  if (sparse) {
+  // with the register-tile kernels, a sweep skips the loads of amplitudes its
+  // zero_local_mask marks as still 0; when the sweeps hold every qubit, every
+  // amplitude is then written before it is read and the zeroing pass (16 B
+  // per amplitude) goes (cfg4a uncut: 2.6 ms of HBM writes)
+  const bool skip_zero_loads = sparse && prog->engine == 1 && g_opt.zero_skip;
+  if (sparse && !(skip_zero_loads && prog->covers_all_qubits)) {
     // exactly the states (the caller may keep other data between strided states)
     const size_t eb = elem_bytes(dtype);
     cudaError_t e = state_stride == (int64_t(1) << nq)
@@ -867,9 +885,15 @@ int run_program(const std::shared_ptr<const Program>& prog_ptr, int nq, void* st
     }
     return CS_OK;
   }
+  int prev_sweep = -1;
   for (const Launch& ln : prog->launches) {
     JitUnit* jk = (jit && jit->cluster == 0 && li < jit->units.size() && jit->units[li])
                       ? jit->units[li].get() : nullptr;
+    // only the first launch of a sweep sees the sweep's known-zero amplitudes
+    const uint32_t zmask =
+        (skip_zero_loads && !(first && init_zero) && ln.sweep != prev_sweep)
+            ? prog->sweeps[size_t(ln.sweep)].zero_local_mask : 0u;
+    prev_sweep = ln.sweep;
     const std::vector<unsigned char>* blob = jk ? &jit->blobs[li] : nullptr;
     ++li;
     const Sweep& sw = prog->sweeps[size_t(ln.sweep)];
@@ -887,8 +911,9 @@ int run_program(const std::shared_ptr<const Program>& prog_ptr, int nq, void* st
         unsigned long long vbase_arg = variant_base + uint64_t(v0);
         int init_arg = (first && init_zero) ? 1 : 0;
         unsigned long long ntiles_arg = n_tiles;
-        // param mode: the launch's coefficients travel as the 6th argument
-        void* args[] = {&sp_arg, &stride_arg, &vbase_arg, &init_arg, &ntiles_arg,
+        unsigned zmask_arg = zmask;
+        // param mode: the launch's coefficients travel as the 7th argument
+        void* args[] = {&sp_arg, &stride_arg, &vbase_arg, &init_arg, &ntiles_arg, &zmask_arg,
                         blob && !blob->empty() ? const_cast<unsigned char*>(blob->data()) : nullptr};
         e = cudaSuccess;
         if (jk->smem > 48 * 1024) {
@@ -919,6 +944,7 @@ int run_program(const std::shared_ptr<const Program>& prog_ptr, int nq, void* st
         rp.n_ops = int32_t(ln.reg.size());
         rp.init_basis = (first && init_zero) ? 1 : 0;
         rp.n_states = int32_t(vc);
+        rp.zmask = zmask;
         for (size_t j = 0; j < sw.hq.size() && j < size_t(kMaxTileBits); ++j) rp.hq[j] = int8_t(sw.hq[j]);
         for (size_t j = 0; j < sw.oq.size() && j < 64; ++j) rp.oq[j] = int8_t(sw.oq[j]);
         if (!ln.reg.empty()) std::memcpy(rp.ops, ln.reg.data(), sizeof(RegOp) * ln.reg.size());
@@ -1142,6 +1168,8 @@ int cs_set_option(const char* key, int64_t value) {
     g_opt.merge_dmma3_warps = value;
   } else if (k == "zero_start_tiles") {
     g_opt.zero_start_tiles = value ? 1 : 0;
+  } else if (k == "zero_skip") {
+    g_opt.zero_skip = value ? 1 : 0;
   } else if (k == "merge_ozaki") {
     if (value < 0 || value > 3) return fail(CS_ERR_INVALID, "merge_ozaki must be 0, 1, 2 or 3");
     g_opt.merge_ozaki = value;
@@ -1211,6 +1239,7 @@ int64_t cs_get_option(const char* key) {
   if (k == "merge_dmma") return g_opt.merge_dmma;
   if (k == "merge_ozaki") return g_opt.merge_ozaki;
   if (k == "zero_start_tiles") return g_opt.zero_start_tiles;
+  if (k == "zero_skip") return g_opt.zero_skip;
   if (k == "merge_ozaki_min_k") return g_opt.merge_ozaki_min_k;
   if (k == "merge_ozaki_min_work") return g_opt.merge_ozaki_min_work;
   if (k == "merge_smem_kb") return g_opt.merge_smem_kb;

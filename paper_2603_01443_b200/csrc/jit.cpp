@@ -278,7 +278,7 @@ std::string jit_source(const Sweep& sw, const std::vector<RegOp>& prog, int RB, 
     o << "  unsigned long long tile = blockIdx.x, base;\n";
     o << "  if (!init && tile < n_tiles) { unsigned long long nb; " << base_of("nb", "tile") << "\n";
     for (int j = 0; j < NR; ++j)
-      o << "    " << gidx(j, "nb") << " cpa(pf + e, st + g); }\n";
+      o << "    " << gidx(j, "nb") << " if (!(e & zmask)) cpa(pf + e, st + g); }\n";
     o << "  }\n  cpc();\n";
     o << "  for (; tile < n_tiles; tile += gridDim.x) {\n";
     o << "  " << base_of("base", "tile") << "\n";
@@ -287,11 +287,13 @@ std::string jit_source(const Sweep& sw, const std::vector<RegOp>& prog, int RB, 
       o << "    { const unsigned e = tid + " << (j * BD) << "u; v" << j
         << ".x = (base == 0ull && e == 0u) ? R(1) : R(0); v" << j << ".y = R(0); }\n";
     o << "  } else {\n    cpw();\n";
-    for (int j = 0; j < NR; ++j) o << "    v" << j << " = pf[tid + " << (j * BD) << "u];\n";
+    for (int j = 0; j < NR; ++j)
+      o << "    v" << j << " = ((tid + " << (j * BD) << "u) & zmask) ? V{R(0), R(0)} : pf[tid + " << (j * BD)
+        << "u];\n";
     o << "    const unsigned long long nt = tile + gridDim.x;\n";
     o << "    if (nt < n_tiles) { unsigned long long nb; " << base_of("nb", "nt") << "\n";
     for (int j = 0; j < NR; ++j)
-      o << "      " << gidx(j, "nb") << " cpa(pf + e, st + g); }\n";
+      o << "      " << gidx(j, "nb") << " if (!(e & zmask)) cpa(pf + e, st + g); }\n";
     o << "    }\n    cpc();\n  }\n";
   } else {
     o << "  const unsigned long long tile = blockIdx.x; (void)n_tiles;\n";
@@ -305,7 +307,7 @@ std::string jit_source(const Sweep& sw, const std::vector<RegOp>& prog, int RB, 
     o << "    return;\n  }\n";
     for (int j = 0; j < NR; ++j)
       o << "  " << gidx(j, "base") << " if (init) { v" << j << ".x = (base == 0ull && e == 0u) ? R(1) : R(0); v" << j
-        << ".y = R(0); } else v" << j << " = st[g]; }\n";
+        << ".y = R(0); } else v" << j << " = (e & zmask) ? V{R(0), R(0)} : st[g]; }\n";
   }
   o << "  unsigned tp = tid; (void)tp;\n";
   emit_register_program(o, prog, T, RB, val);
@@ -316,8 +318,11 @@ std::string jit_source(const Sweep& sw, const std::vector<RegOp>& prog, int RB, 
   std::ostringstream head;
   const bool params = pvals && !pvals->empty();
   if (params) head << "struct JP_" << name << " { R m[" << pvals->size() << "]; };\n";
+  // zmask: tile-local bits whose amplitudes are known 0 in a start from
+  // |0..0> (Sweep::zero_local_mask; 0 otherwise): not loaded
   head << "extern \"C\" __global__ void __launch_bounds__(" << BD << ", " << minb << ") " << name
-       << "(V* __restrict__ states, long long stride, unsigned long long vbase, int init, unsigned long long n_tiles";
+       << "(V* __restrict__ states, long long stride, unsigned long long vbase, int init, unsigned long long n_tiles"
+       << ", unsigned zmask";
   if (params) head << ", const JP_" << name << " P";
   head << ") {\n";
   return head.str() + o.str();

@@ -430,6 +430,9 @@ __global__ void __launch_bounds__(512) rsweep_kernel(const __grid_constant__ Reg
     if (p.init_basis) {
       v[j].x = (base == 0 && e == 0) ? R(1) : R(0);
       v[j].y = R(0);
+    } else if (e & p.zmask) {
+      v[j].x = R(0);
+      v[j].y = R(0);
     } else {
       v[j] = st[int64_t(base) + chunkoff[e >> L] + (e & lowmask)];
     }

@@ -86,7 +86,8 @@ struct RegParamsT {
   void* states;
   int64_t stride;
   uint64_t variant_base;
-  int32_t tile_bits, low_bits, n_high, n_out, n_ops, init_basis, n_states, pad;
+  int32_t tile_bits, low_bits, n_high, n_out, n_ops, init_basis, n_states;
+  uint32_t zmask;           // tile-local bits whose amplitudes are known 0 (Sweep::zero_local_mask): not loaded
   int8_t hq[kMaxTileBits];
   int8_t oq[64];
   RegOp ops[CAP];

@@ -480,6 +480,10 @@ static void order_tiles_for_zero_start(std::vector<Sweep>& sweeps) {
     int m = 0;
     for (int q : sw.oq) m += int((support >> q) & 1ull);
     sw.zero_tiles_log2 = m;
+    uint32_t zm = 0;
+    for (int q = 0; q < sw.low_bits; ++q) zm |= uint32_t(!((support >> q) & 1ull)) << q;
+    for (size_t j = 0; j < sw.hq.size(); ++j) zm |= uint32_t(!((support >> sw.hq[j]) & 1ull)) << (sw.low_bits + int(j));
+    sw.zero_local_mask = zm;
     for (int q = 0; q < sw.low_bits; ++q) support |= 1ull << q;
     for (int q : sw.hq) support |= 1ull << q;
   }
@@ -744,7 +748,7 @@ std::string sweeps_to_json(const std::vector<Sweep>& sweeps, int nq) {
     for (size_t i = 0; i < sw.hq.size(); ++i) os << (i ? "," : "") << sw.hq[i];
     os << "],\"oq\":[";
     for (size_t i = 0; i < sw.oq.size(); ++i) os << (i ? "," : "") << sw.oq[i];
-    os << "],\"z\":" << sw.zero_tiles_log2 << ",\"entries\":[";
+    os << "],\"z\":" << sw.zero_tiles_log2 << ",\"zl\":" << sw.zero_local_mask << ",\"entries\":[";
     for (size_t i = 0; i < sw.entries.size(); ++i) {
       const SweepOp& e = sw.entries[i];
       os << (i ? "," : "") << "{\"type\":" << e.type << ",\"target\":" << e.target

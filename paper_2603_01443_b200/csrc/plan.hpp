@@ -75,6 +75,11 @@ struct Sweep {
   // sweep held in its tile first (a dense op never moves amplitude across
   // tiles, so a qubit no earlier sweep held is still 0 everywhere)
   int zero_tiles_log2 = 0;
+  // tile-local index bits ([0, L): qubit q; L + j: hq[j]) whose qubit no
+  // earlier sweep held: started from |0..0>, every amplitude with one of them
+  // set is still 0 when this sweep runs, so its load can be skipped (and the
+  // state need not be zeroed first when the sweeps together hold every qubit)
+  uint32_t zero_local_mask = 0;
   std::vector<SweepOp> entries;  // slotted ops take two consecutive entries
 };
 

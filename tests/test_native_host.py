@@ -51,19 +51,38 @@ def test_options_round_trip_and_errors():
     assert "unknown option" in _native.last_error()
 
 
-def execute_schedule(plan, nq, variant=0):
+def execute_schedule(plan, nq, variant=0, garbage=False):
     """Interpret the exported sweep schedule on a full numpy state. Before
     every sweep, check the zero-start tile bound the kernels rely on: every
-    non-zero amplitude lies in a tile t < 2^z (tile-id bit j <-> qubit oq[j])."""
+    non-zero amplitude lies in a tile t < 2^z (tile-id bit j <-> qubit oq[j]).
+    garbage=True models the kernels without the zeroing pass: memory starts
+    as NaN, the first sweep's launched tile starts from |0..0>, and every
+    later sweep reads an amplitude of its launched tiles as 0 when its
+    tile-local index has a bit of the sweep's zero_local_mask ("zl") set —
+    the result must still be finite and exact."""
     amps = orc.zero_state(nq)
     idx = np.arange(1 << nq, dtype=np.int64)
-    for sw in plan["sweeps"]:
+    if garbage:
+        amps[:] = np.nan
+    for k, sw in enumerate(plan["sweeps"]):
         high = 0
         for q in sw["oq"][sw["z"]:]:
             high |= 1 << q
-        assert not np.any((idx[np.abs(amps) > 0] & high) != 0), "amplitude outside the zero-start tiles"
         L, hq = sw["L"], sw["hq"]
         glob = list(range(L)) + list(hq)
+        if garbage:
+            launched = (idx & high) == 0
+            if k == 0:
+                amps[launched] = 0
+                amps[0] = 1
+            else:
+                zq = 0
+                for p, q in enumerate(glob):
+                    if (sw["zl"] >> p) & 1:
+                        zq |= 1 << q
+                amps[launched & ((idx & zq) != 0)] = 0
+        else:
+            assert not np.any((idx[np.abs(amps) > 0] & high) != 0), "amplitude outside the zero-start tiles"
         ents = sw["entries"]
         i = 0
         while i < len(ents):
@@ -144,6 +163,31 @@ def test_cost_aware_zero_start_schedule_reproduces_oracle():
     assert plan3["sweeps"][0]["z"] == 0 and any(sw["z"] < q - sw["T"] for sw in plan3["sweeps"][1:])
     assert plan3 != plan1
     got = execute_schedule(plan3, q)
+    ref = orc.simulate(q, circ.kinds, circ.qa, circ.qb, circ.params)
+    assert np.abs(got - ref).max() < 1e-12
+
+
+@pytest.mark.parametrize("q,d,n,c,seed,tile_bits", [(22, 4, 2, 2, 5, 0), (16, 5, 2, 3, 1, 8), (15, 6, 3, 4, 2, 6),
+                                                    (14, 3, 2, 2, 0, 4)])
+def test_zero_start_without_zeroing_reproduces_oracle(q, d, n, c, seed, tile_bits):
+    """The register-tile kernels skip the zeroing pass when the sweeps hold
+    every qubit: each sweep loads as 0 the amplitudes whose tile-local index
+    has a bit of its zero_local_mask (a qubit no earlier sweep held) and never
+    reads a tile outside 2^z. Executed here on NaN-initialised memory, the
+    schedule still gives the oracle's state, and the masks are what the
+    support implies."""
+    circ = G.build_brickwall(G.BrickwallSpec(q, d, n, c, seed))
+    plan = json.loads(_native.sweep_plan_json(q, circ.table, tile_bits=tile_bits))
+    held = 0
+    for sw in plan["sweeps"]:
+        glob = list(range(sw["L"])) + list(sw["hq"])
+        assert sw["zl"] == sum(1 << p for p, g in enumerate(glob) if not (held >> g) & 1)
+        for g in glob:
+            held |= 1 << g
+    assert held == (1 << q) - 1
+    assert any(sw["zl"] for sw in plan["sweeps"][1:])
+    got = execute_schedule(plan, q, garbage=True)
+    assert np.all(np.isfinite(got))
     ref = orc.simulate(q, circ.kinds, circ.qa, circ.qb, circ.params)
     assert np.abs(got - ref).max() < 1e-12
 
