@@ -71,13 +71,14 @@ def load_dram_pct():
     """ncu's dram throughput (% of its DRAM peak) for the committed capture of
     the same merge launch, for reading `frac` (which is against the measured
     read+write copy rate) next to the DRAM-peak view."""
-    path = os.path.join(ROOT, "profiles", "r01_ncu_full.json")
-    try:
-        with open(path) as fh:
-            d = json.load(fh)
-        return float(d["merge_kernel"][0]["gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"])
-    except (OSError, ValueError, KeyError, IndexError, TypeError):
-        return None
+    for name in ("r02_ncu_full.json", "r01_ncu_full.json"):
+        try:
+            with open(os.path.join(ROOT, "profiles", name)) as fh:
+                d = json.load(fh)
+            return float(d["merge_kernel"][0]["gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"])
+        except (OSError, ValueError, KeyError, IndexError, TypeError):
+            continue
+    return None
 
 
 class ClockSampler:
