@@ -354,10 +354,18 @@ def run_ours(args):
                                                 run_cut_to_host, shard_workspace_bytes)
 
     world, rank, local = dist_env()
+    emulated = None
+    if args.emulate_shard:
+        if world > 1:
+            raise SystemExit("--emulate-shard is a single-process mode")
+        rank, world = (int(x) for x in args.emulate_shard.split("/"))
+        if not 0 <= rank < world:
+            raise SystemExit("--emulate-shard R/W needs 0 <= R < W")
+        emulated = f"{rank}/{world}"
     torch.cuda.set_device(local)
     dist = None
     comm = None
-    if world > 1:
+    if world > 1 and not emulated:
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -383,7 +391,7 @@ def run_ours(args):
     q, n = spec.q, spec.n
     total = 1 << q
     if (16 << q) // world > 150 * 2**30:
-        if rank == 0:
+        if rank == 0 or emulated:
             print(json.dumps({"metric": METRIC, "unavailable": f"{args.workload} needs {16 << q >> 30} GiB of "
                               f"output: run it on >= {(16 << q) // (150 * 2**30) + 1} GPUs"}), flush=True)
         return 0
@@ -584,15 +592,17 @@ def run_ours(args):
 
             for _ in range(max(1, min(args.warmup, 2))):
                 e2e_step()
-            dist.barrier()
+            if dist:
+                dist.barrier()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             for _ in range(e_steps):
                 e2e_step()
             t_rank = (time.perf_counter() - t0) / e_steps
-            tt = torch.tensor([t_rank], device="cuda", dtype=torch.float64)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            t_rank = float(tt.item())
+            if dist:
+                tt = torch.tensor([t_rank], device="cuda", dtype=torch.float64)
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                t_rank = float(tt.item())
             e2e = {"value": total / t_rank, "unit": UNIT, "h2d_bytes_per_step": g_bytes * world,
                    "d2h_bytes_per_step": total * 16, "ms_per_step": t_rank * 1e3, "steps": e_steps,
                    "path": (f"cs_cut_run_sharded on {world} ranks (variant chunk, in-place NCCL all-gather, "
@@ -603,7 +613,7 @@ def run_ours(args):
     # ---- the CPU leg (subprocess): oracle amplitudes for the parity check
     # and, at N = 1, the 1-thread reference-algorithm baseline
     parity, cpu = None, None
-    if rank == 0:
+    if rank == 0 or emulated:
         import tempfile
 
         with tempfile.TemporaryDirectory() as td:
@@ -622,9 +632,10 @@ def run_ours(args):
             except Exception as exc:  # noqa: BLE001
                 parity = {"max_abs": None, "samples": int(idx.size), "ok": False, "error": str(exc)[-500:]}
 
-    if rank == 0:
+    if rank == 0 or emulated:
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1 if emulated else world,
+            "emulated_shard": emulated, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded U3 brick-wall, SURVEY.md §8(d)); output resident in HBM",
@@ -633,7 +644,11 @@ def run_ours(args):
                             if comm is not None or world == 1 else
                             f"output rows sharded over {world} GPU(s), every rank simulates all variants "
                             "(native NCCL exchange unavailable on this node)")
-            if world > 1 else "1 GPU", "bond": bond,
+            if world > 1 and not emulated else
+            (f"EMULATED: this one GPU computed rank {emulated}'s share (output rows [{begin}, {end})) of the "
+             "sharded job and simulated every variant itself; value = 2^q / this rank's time, i.e. what the "
+             "job would do if every rank took as long and the exchange were free -- not a scaling measurement"
+             if emulated else "1 GPU"), "bond": bond,
             "stage_ms": stage,
             "stage_ms_sync": stage_sync,
             "variant_stage": variant_stage_rates(prep0, stage),
@@ -848,6 +863,9 @@ def main():
     ap.add_argument("--no-cold", action="store_true")
     ap.add_argument("--no-jit", action="store_true", help="interpreter sweep kernels only")
     # internal: the cpu_baseline leg, run as a subprocess of the GPU arm
+    ap.add_argument("--emulate-shard", default=None, metavar="R/W",
+                    help="one GPU computes rank R's share of a W-GPU job through the sharded call (no exchange: "
+                         "it simulates every variant itself); the line is labelled, not a scaling measurement")
     ap.add_argument("--cpu-leg", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--samples-in", default=None, help=argparse.SUPPRESS)
     ap.add_argument("--time-cpu", action="store_true", help=argparse.SUPPRESS)
