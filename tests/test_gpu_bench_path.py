@@ -136,3 +136,27 @@ def test_cfg4a_host_buffer_leg(cb):
     dev = engine.gather(cb.run_cut(circ, 2), idx)
     assert np.array_equal(got, dev)
     del host
+
+
+def test_bench_emulated_shard_line():
+    """bench.py's N > 1 code path on one GPU (`--emulate-shard R/W`): rank 5 of
+    8 of cfg4a through cs_cut_shard_plan + cs_cut_run_sharded on its rows
+    (reference merging.py:156-186, rows [begin, end)); the line is labelled,
+    carries its own oracle parity check and exits 0 only if that passed."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--emulate-shard", "5/8", "--steps", "2",
+                          "--warmup", "3", "--no-e2e", "--no-cpu", "--samples", "1024"],
+                         capture_output=True, text=True, timeout=600, cwd=root)
+    assert res.returncode == 0, res.stderr[-2000:]
+    line = json.loads([ln for ln in res.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["emulated_shard"] == "5/8" and line["n_gpus"] == 1
+    assert line["parallelism"].startswith("EMULATED")
+    assert line["parity"]["ok"] and line["parity"]["max_abs"] <= 1e-10
+    assert line["roofline"]["per_rank"] is True
+    # an eighth of the 16 GiB output plus the subcircuit states
+    assert (16 << 30) // 8 <= line["roofline"]["algorithmic_bytes_per_launch"] < (16 << 30) // 8 + (1 << 24)
